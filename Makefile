@@ -1,0 +1,42 @@
+# Product build: sm_100a CUDA kernels + C-ABI -> paper_2306_16926_b200/libosp_b200.so
+# (in-tree, so it travels to the GPU box with gpurun and is what tests/bench load).
+#
+#   make            -> library + oracle/liboracle.so
+#   make ref        -> oracle/_ref/ (needs /root/reference; test infrastructure)
+
+NVCC ?= nvcc
+PKG := paper_2306_16926_b200
+CSRC := $(PKG)/csrc
+LIB := $(PKG)/libosp_b200.so
+
+ARCH := -gencode arch=compute_100a,code=sm_100a
+# --fmad=false: no FMA contraction anywhere (bit-exact fp32/fp64 rounding)
+NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcompiler -Wall \
+           -Iinclude -I$(CSRC) --expt-relaxed-constexpr -Xptxas -warn-spills
+
+CU_SRCS := $(CSRC)/kernels/stage.cu $(CSRC)/kernels/resolve.cu $(CSRC)/kernels/elementwise.cu \
+           $(CSRC)/capi/osp_capi.cu
+CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
+HDRS := include/osp_c.h $(CSRC)/osp_internal.h $(CSRC)/kernels/common.cuh
+
+.PHONY: all lib oracle ref clean
+
+all: lib oracle
+
+lib: $(LIB)
+
+build/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@
+
+$(LIB): $(CU_OBJS)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -Xlinker -soname,libosp_b200.so
+
+oracle:
+	$(MAKE) -s -C oracle liboracle.so
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(LIB)

@@ -1,0 +1,319 @@
+"""OSP sync+LGP step benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+A step is one OSP iteration of the synchronization hot path for N_w = 8 logical
+workers over the ResNet-50 layout (BASELINE.json configs[1]): stage 1 (barrier:
+RS aggregate/apply/pull + LGP partial), the 4 ICS chunks (aggregate/apply/LGP
+correct), and the resolution (PGP -> certified rank -> next GIB). Inputs are the
+reference synthetic deltas (runner.cpp:312-321, seed 11), resident in HBM; the
+two delta sets alternate between steps and total 2 x 818 MB (> L2, so no flush is
+needed). One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import shutil
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "OSP sync+LGP step params/sec and HBM GB/s at 1/2/4/8 B200 vs roofline"
+UNIT = "params/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--layout", default="resnet50")
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--budget-frac", type=float, default=0.5)
+    ap.add_argument("--chunks", type=int, default=4)
+    ap.add_argument("--seed", type=int, default=11)
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=3)
+    return ap.parse_args()
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---- clocks during the timed region -------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+        self._t = None
+
+    def start(self):
+        if not shutil.which("nvidia-smi"):
+            return
+        self.proc = subprocess.Popen(
+            ["nvidia-smi", f"--id={self.dev}", f"--query-gpu={self.FIELDS}",
+             "--format=csv,noheader,nounits", "-lms", "100"],
+            stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self._t:
+            self._t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, parts[5:9]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---- CPU baseline (reference engine on the host) ---------------------------------
+
+def run_reference_cpu(layout: str, workers: int, budget_frac: float, chunks: int, seed: int,
+                      iters: int, warmup: int, threads: int):
+    """Time the UNMODIFIED reference engine (oracle/_ref/ref_driver) on host cores."""
+    from paper_2306_16926_b200 import layouts
+    drv = os.path.join(REPO, "oracle", "_ref", "ref_driver")
+    counts = layouts.get(layout)
+    path = os.path.join("/tmp", f"osp_layers_{layout}.txt")
+    with open(path, "w") as f:
+        f.write(",".join(map(str, counts)))
+    if os.path.exists(drv):
+        cmd = [drv, "bench", "--layers-file", path, "--workers", str(workers), "--budget-frac",
+               str(budget_frac), "--chunks", str(chunks), "--seed", str(seed), "--iters",
+               str(iters), "--warmup", str(warmup), "--threads", str(threads)]
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+        if res.returncode == 0:
+            d = json.loads(res.stdout.strip().splitlines()[-1])
+            return {"value": d["params_per_s"], "unit": UNIT, "cores": threads,
+                    "kind": "reference", "ms_per_step": d["median_ms"],
+                    "sample": (f"reference pslab OspWorker/OspServer engine (oracle/_ref, g++ -O3), "
+                               f"{layout} layout, {workers} workers, budget {budget_frac} x model, "
+                               f"{chunks} chunks, median of {iters} steps after {warmup} warm-up; "
+                               f"synth delta generation excluded")}
+    # fallback: the C restatement (oracle/osp_oracle.c), single thread
+    import numpy as np
+    from oracle import oracle
+    M = sum(counts)
+    G = np.zeros(M, np.float32)
+    P = np.zeros((workers, M), np.float32)
+    flags = np.zeros(len(counts), np.uint8)
+    order = np.zeros(0, np.int32)
+    budget = int(budget_frac * M * 4)
+    times = []
+    for it in range(warmup + iters):
+        X = np.stack([oracle.synth_delta(seed, w, it, M) for w in range(workers)])
+        t0 = time.perf_counter()
+        r = oracle.step(counts, 4, [1.0 / workers] * workers, X, G, P, flags, order, chunks, budget)
+        t1 = time.perf_counter()
+        flags, order = r["flags_out"], r["order_out"]
+        if it >= warmup:
+            times.append(t1 - t0)
+    med = statistics.median(times)
+    return {"value": M / med, "unit": UNIT, "cores": 1, "kind": "port", "ms_per_step": med * 1e3,
+            "sample": f"C restatement (oracle/osp_oracle.c), {layout}, {workers} workers, "
+                      f"median of {iters} steps"}
+
+
+def reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    t0 = time.time()
+    cb = run_reference_cpu(args.layout, args.workers, args.budget_frac, args.chunks, args.seed,
+                           max(1, args.steps if args.steps <= 5 else 5), max(1, min(args.warmup, 2)),
+                           threads)
+    from paper_2306_16926_b200 import layouts
+    M = sum(layouts.get(args.layout))
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
+            "config": {"workload": f"{args.layout}-size OSP step", "params": M,
+                       "workers": args.workers, "budget_frac": args.budget_frac,
+                       "chunks": args.chunks},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": round(time.time() - t0, 2)}
+    print(json.dumps(line), flush=True)
+
+
+# ---- the B200 arm ---------------------------------------------------------------
+
+def b200_single(args):
+    import numpy as np
+    import torch
+
+    from paper_2306_16926_b200 import layouts, osp
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    counts = layouts.get(args.layout)
+    N, M, L = args.workers, sum(counts), len(counts)
+    model_bytes = M * 4
+    budget = int(args.budget_frac * model_bytes)
+    part = osp.Partition(counts)
+    grp = osp.OspGroup(part, N, [1.0 / N] * N, n_chunks=args.chunks, tile_elems=args.tile)
+    X = [osp.synth_deltas(args.seed, N, i, M) for i in range(2)]
+    grp.set_budget(budget)
+    stream = torch.cuda.current_stream()
+
+    def step(k, evs=None):
+        x = X[k % 2]
+        if evs is not None:
+            evs[0].record(stream)
+        grp.stage1(x)
+        if evs is not None:
+            evs[1].record(stream)
+        for c in range(args.chunks):
+            grp.stage2_chunk(c, x)
+        if evs is not None:
+            evs[2].record(stream)
+        grp.resolve(x)
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    tag0 = grp.read_gib()["tag"]  # GIB used by the first timed step
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(dev)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for k in range(K):
+        step(args.warmup + k, evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = start.elapsed_time(end)
+    ms_step = total_ms / K
+    s1 = [evs[k][0].elapsed_time(evs[k][1]) for k in range(K)]
+    s2 = [evs[k][1].elapsed_time(evs[k][2]) for k in range(K)]
+    # u of each timed step = deferred bytes of the GIB it split with (tags tag0..)
+    deferred = grp.deferred_history(tag0, K).astype(np.float64)
+    u = deferred / model_bytes
+    # algorithmic bytes: stage 1 = 4M[(2N+2) - u]; step adds 4M u (2N+2)
+    b_s1 = [4.0 * M * ((2 * N + 2) - uk) for uk in u]
+    b_step = [4.0 * M * ((2 * N + 2) + uk * (2 * N + 1)) for uk in u]
+    s1_avg = sum(s1) / K
+    ach_s1 = (sum(b_s1) / K) / (s1_avg * 1e-3) / 1e9
+    ach_step = (sum(b_step) / K) / (ms_step * 1e-3) / 1e9
+    peak, peak_kind = measured_peaks()
+    stats = grp.stats()
+    launches_per_step = 1 + args.chunks + 3  # stage1, chunk kernels, resolve(pass1, fallback, pass2)
+
+    # ---- e2e through the C-ABI with host buffers (pinned), H2D + step + D2H of the GIB
+    host = [x.cpu().pin_memory() for x in X]
+    e2e_ms = []
+    for k in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        grp.step_host(host[k % 2])
+        t1 = time.perf_counter()
+        if k > 0:
+            e2e_ms.append((t1 - t0) * 1e3)
+    e2e_step = statistics.median(e2e_ms)
+    gib_bytes = 8 + (L + 7) // 8
+
+    line = {
+        "metric": METRIC, "value": M / (ms_step * 1e-3), "unit": UNIT, "n_gpus": 1,
+        "steps": K, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
+        "config": {"workload": f"{args.layout}-size OSP sync+LGP step (BASELINE configs[1])",
+                   "params": M, "layers": L, "workers": N, "budget_frac": args.budget_frac,
+                   "chunks": args.chunks, "deltas": "reference synth generator, seed "
+                   f"{args.seed}, 2 sets alternating (1.6 GB > L2, no flush)",
+                   "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU"},
+        "hbm_gbs_step": ach_step,
+        "roofline": {"bound": "hbm", "kernel": "k_stage1 (barrier: RS agg/apply + LGP)",
+                     "achieved": ach_s1, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": ach_s1 / peak, "traffic": None,
+                     "alg_bytes_per_launch": sum(b_s1) / K, "avg_launch_ms": s1_avg,
+                     "step_frac": ach_step / peak},
+        "breakdown_ms": {"stage1": s1_avg, "stage2_chunks": sum(s2) / K,
+                         "resolve": ms_step - s1_avg - sum(s2) / K},
+        "u_mean": float(u.mean()),
+        "e2e": {"value": M / (e2e_step * 1e-3), "unit": UNIT, "ms_per_step": e2e_step,
+                "h2d_bytes_per_step": N * M * 4, "d2h_bytes_per_step": gib_bytes,
+                "path": "osp_group_step_host (C-ABI, pinned host deltas)"},
+        "gpu_launches": launches_per_step * K,
+        "certificate": stats,
+        "clocks": clk,
+    }
+    if not args.no_cpu_baseline:
+        try:
+            cb = run_reference_cpu(args.layout, N, args.budget_frac, args.chunks, args.seed,
+                                   args.cpu_iters, 1, 1)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # reported, not fatal
+            line["cpu_baseline"] = {"error": str(e)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    if world > 1 or args.gpus > 1:
+        from paper_2306_16926_b200 import dist_bench
+        dist_bench.run(args, METRIC, UNIT)
+        return
+    b200_single(args)
+
+
+if __name__ == "__main__":
+    main()

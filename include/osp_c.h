@@ -1,0 +1,250 @@
+/*
+ * osp_c.h — C-ABI of the B200-native OSP sync path (drop-in boundary).
+ *
+ * Plain C: opaque handles, plain pointers and sizes, status codes. No
+ * exceptions and no torch types cross this boundary. Vectors are DEVICE
+ * pointers (fp32, flat over a layer partition) unless a parameter says host.
+ * Every device operation is stream-ordered on the `stream` argument
+ * (a cudaStream_t passed as void*; NULL = legacy default stream).
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/proj, file:line). The reference has no FFI: its boundary is
+ * the C++ library API in include/pslab/{param,importance,protocol,tuning}.hpp
+ * and learner.hpp:77. The C++ façade in include/pslab/ (this repo) re-exposes
+ * that API on top of these functions, rethrowing the matching pslab::Error
+ * subclass from the status code.
+ */
+#ifndef OSP_C_H
+#define OSP_C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OSP_ABI_VERSION 1
+/* Workers per aggregation call / group (kernel-parameter weights table). */
+#define OSP_MAX_WORKERS 64
+
+/* Status codes, 1:1 with the pslab::Error hierarchy (errors.hpp:11-69). */
+typedef enum osp_status {
+    OSP_OK = 0,
+    OSP_ERR_PARTITION = 1, /* PartitionError */
+    OSP_ERR_SHAPE = 2,     /* ShapeError */
+    OSP_ERR_LAYER = 3,     /* LayerError */
+    OSP_ERR_PARSE = 4,     /* ParseError */
+    OSP_ERR_CONFIG = 5,    /* ConfigError */
+    OSP_ERR_FORMAT = 6,    /* FormatError */
+    OSP_ERR_PROTOCOL = 7,  /* ProtocolError */
+    OSP_ERR_NUMERIC = 8,   /* NumericError */
+    OSP_ERR_CUDA = 20,     /* CUDA runtime / launch failure (no reference analogue) */
+    OSP_ERR_INVALID = 21   /* null handle or pointer, unsupported size */
+} osp_status;
+
+/* Thread-local message of the last failing call on this thread. */
+const char* osp_last_error(void);
+const char* osp_status_name(osp_status s);
+int osp_abi_version(void);
+/* Device the library runs on (cudaGetDevice) and its SM count. */
+osp_status osp_device_info(int* device, int* sm_count, int* cc_major, int* cc_minor);
+
+/* ------------------------------------------------------------------------
+ * Partition — LayerPartition::make / make_partition (param.hpp:19-46,
+ * param.cpp:8-42). Layer ids dense from 0, offsets contiguous in id order.
+ * A device mirror of offsets/counts is kept for the kernels.
+ * ---------------------------------------------------------------------- */
+typedef struct osp_partition osp_partition;
+
+osp_status osp_partition_create(const uint64_t* layer_counts /*host*/, uint64_t n_layers,
+                                uint32_t bytes_per_element, osp_partition** out);
+void osp_partition_destroy(osp_partition* p);
+uint64_t osp_partition_layer_count(const osp_partition* p);
+uint64_t osp_partition_total_count(const osp_partition* p);
+uint64_t osp_partition_total_bytes(const osp_partition* p);
+uint32_t osp_partition_bytes_per_element(const osp_partition* p);
+/* LayerPartition::layer (param.cpp:31-37): LayerError when out of range. */
+osp_status osp_partition_layer(const osp_partition* p, int64_t id, uint64_t* offset,
+                               uint64_t* count);
+
+/* ------------------------------------------------------------------------
+ * Device buffers (the façade's storage; the Python side uses torch).
+ * ---------------------------------------------------------------------- */
+osp_status osp_device_alloc(uint64_t bytes, void** out);
+osp_status osp_device_free(void* ptr);
+osp_status osp_memcpy_h2d(void* dst, const void* src, uint64_t bytes, void* stream);
+osp_status osp_memcpy_d2h(void* dst, const void* src, uint64_t bytes, void* stream);
+osp_status osp_memcpy_d2d(void* dst, const void* src, uint64_t bytes, void* stream);
+osp_status osp_memset(void* dst, int value, uint64_t bytes, void* stream);
+osp_status osp_stream_sync(void* stream);
+
+/* ------------------------------------------------------------------------
+ * Element-wise primitives (one kernel each).
+ * ---------------------------------------------------------------------- */
+
+/* aggregate_layer (protocol.cpp:9-30): out[e] = float(sum_w w_k*(double)x_k[e] / sum w),
+ * fp64 mul then add in ascending worker order, no FMA. contribs is a HOST array
+ * of n_workers device pointers; weights is a host array. ProtocolError if
+ * n_workers < 1 or the weights do not sum > 0. */
+osp_status osp_aggregate_layer(const float* const* contribs, int n_workers,
+                               const double* weights, uint64_t n, float* out, void* stream);
+
+/* OspServer::finish_layer (protocol.cpp:292-307) for a set of layers in one
+ * launch: agg = aggregate(contribs), global += agg. contribs are HOST arrays of
+ * n_workers device pointers, each to a FLAT vector over the partition; layer_ids
+ * (host) selects the layers. agg_out (flat, may be NULL) receives the aggregate. */
+osp_status osp_aggregate_apply_layers(const osp_partition* part, const float* const* contribs,
+                                      int n_workers, const double* weights,
+                                      const int32_t* layer_ids, int64_t n_ids, float* global,
+                                      float* agg_out, void* stream);
+
+/* apply_delta (param.cpp:127-150): p[i] = p[i] + scale*d[i] (fp32 mul, then add). */
+osp_status osp_apply_delta(float* p, const float* d, uint64_t n, float scale, void* stream);
+
+/* sgd_delta (learner.cpp:391-398): out = float(-lr * (double)g). ConfigError if lr <= 0. */
+osp_status osp_sgd_delta(const float* grad, uint64_t n, double lr, float* out, void* stream);
+
+/* Synthetic delta source (runner.cpp:312-321, rng.hpp:16-61): elements
+ * [first, first+n) of float(uniform(-1e-3, 1e-3)) drawn from
+ * Rng(derive_seed(seed, kSynthGrad=6, worker, iteration)). */
+osp_status osp_synth_delta(uint64_t seed, uint64_t worker, uint64_t iteration, uint64_t first,
+                           uint64_t n, float* out, void* stream);
+/* Same stream, n_workers rows of a [n_workers][ld] block in one launch. */
+osp_status osp_synth_deltas(uint64_t seed, int n_workers, uint64_t iteration, uint64_t n,
+                            float* out, uint64_t ld, void* stream);
+
+/* lgp_partial (protocol.cpp:69-97) on flat vectors. ics_flags (HOST, one byte per
+ * layer): 0 = the layer takes the global delta (p += 1.0f*global_delta),
+ * 1 = local estimate (base = p; p += local_delta). base is written on flagged
+ * layers only. */
+osp_status osp_lgp_partial(const osp_partition* part, float* params, const float* global_delta,
+                           const float* local_delta, const uint8_t* ics_flags, float* base,
+                           void* stream);
+
+/* lgp_correct (protocol.cpp:99-116): p = base + global_delta on the listed
+ * layers (HOST ids). */
+osp_status osp_lgp_correct(const osp_partition* part, float* params, const float* base,
+                           const float* global_delta, const int32_t* layer_ids, int64_t n_ids,
+                           void* stream);
+
+/* pgp_layer_importance (importance.cpp:11-28), reference-exact: scores (HOST,
+ * n_layers doubles) bit-identical to the sequential double sum. One CTA per
+ * layer, summed in ascending element order. */
+osp_status osp_pgp_layer_importance(const osp_partition* part, const float* params,
+                                    const float* grads, double* scores_host, void* stream);
+
+/* rank_layers (importance.cpp:30-40) + build_gib (:42-59) on HOST scores, run as
+ * the single-CTA device kernel of the group path. order_host: all layer ids
+ * ascending by (score, id); ics_flags_host: prefix rule under budget_bytes. */
+osp_status osp_rank_and_gib(const osp_partition* part, const double* scores_host,
+                            uint64_t budget_bytes, int32_t* order_host, uint8_t* ics_flags_host,
+                            void* stream);
+
+/* split_for_sync (protocol.cpp:122-166) index lists (payload copies are not
+ * made: the device path works on segment lists). HOST in/out. rs_ids gets the
+ * RS layer ids ascending; chunk_of[l] the compacted chunk of each deferred layer
+ * (-1 for RS); *n_used the number of non-empty chunks. ConfigError if
+ * n_chunks < 1, ShapeError if ics_flags does not cover the partition. */
+osp_status osp_split_for_sync(const osp_partition* part, const uint8_t* ics_flags,
+                              const int32_t* ics_order, int64_t n_order, int n_chunks,
+                              int32_t* rs_ids, int64_t* n_rs, int32_t* chunk_of, int* n_used);
+
+/* GIB wire format (importance.cpp:61-117): tag u32 LE, L u32 LE, ceil(L/8)
+ * bitmap bytes, bit k%8 of byte k/8 marks layer k deferred. HOST buffers. */
+uint64_t osp_gib_encoded_size(uint64_t n_layers);
+osp_status osp_gib_encode(uint32_t tag, uint64_t n_layers, const uint8_t* ics_flags,
+                          uint8_t* out, uint64_t out_len);
+/* FormatError on truncation. flags_cap bounds the decoded bitmap. */
+osp_status osp_gib_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint32_t* n_layers,
+                          uint8_t* ics_flags, uint64_t flags_cap);
+
+/* compute_umax / tune_sgu (tuning.cpp:8-48), host scalar logic. */
+osp_status osp_compute_umax(double bandwidth_bps, double latency_s, double loss_rate,
+                            double t_c_seconds, int n_workers, uint64_t model_bytes,
+                            int eq5_literal, uint64_t* out);
+typedef struct osp_sgu_schedule {
+    uint64_t u_max;
+    int has_initial_loss;
+    double initial_loss;
+    uint64_t current_budget;
+    uint64_t epoch;
+} osp_sgu_schedule;
+osp_status osp_tune_sgu(osp_sgu_schedule* sched, uint64_t epoch_index, double epoch_loss,
+                        uint64_t* budget_out);
+
+/* ------------------------------------------------------------------------
+ * Group: the batched fast path for N co-resident logical workers + the PS on
+ * one GPU (OspWorker x N + OspServer in the synchronous fresh-GIB regime,
+ * protocol.cpp:172-447). Device state: global vector G [M], worker params
+ * P [N][ldP], per-tile PGP partials, current GIB, ICS order and chunk lists.
+ *
+ * Iteration i:  stage1 (barrier: RS aggregate/apply/pull + LGP partial on ICS)
+ *               stage2_chunk(c) for c < n_chunks (ICS aggregate/apply/correct)
+ *               resolve (PGP -> certified rank -> GIB tag i+1 -> next lists)
+ * Deltas are [N][ld] fp32 on the device (ld >= M). With sgd_lr > 0 they are raw
+ * gradients and delta = float(-lr*(double)g) is fused into the load.
+ * ---------------------------------------------------------------------- */
+typedef struct osp_group osp_group;
+
+typedef struct osp_group_config {
+    int n_workers;            /* N, 1..OSP_MAX_WORKERS */
+    const double* weights;    /* HOST, N subset weights (OspServer weights) */
+    int n_chunks;             /* ICS chunk slots per iteration (>= 1) */
+    uint32_t tile_elems;      /* 0 = default (power of two, >= 1024) */
+    double sgd_lr;            /* 0 = inputs are deltas; > 0 fuse sgd_delta */
+} osp_group_config;
+
+/* init_params: DEVICE pointer to M floats (P0), or NULL for zeros. Every worker
+ * and the server start from it (runner.cpp:214-231). */
+osp_status osp_group_create(const osp_partition* part, const osp_group_config* cfg,
+                            const float* init_params, void* stream, osp_group** out);
+void osp_group_destroy(osp_group* g);
+
+/* Deferred-byte budget used by the NEXT resolve (budget_for_epoch(epoch(i+1)),
+ * protocol.cpp:396-405, 446-451). Stream-ordered. */
+osp_status osp_group_set_budget(osp_group* g, uint64_t budget_bytes, void* stream);
+/* Overwrite the current GIB (flags HOST [L], rank-ordered ICS ids HOST).
+ * Mirrors OspWorker::on_gib_update (protocol.cpp:252-256). */
+osp_status osp_group_set_gib(osp_group* g, const uint8_t* ics_flags, const int32_t* ics_order,
+                             int64_t n_order, uint32_t tag, void* stream);
+
+osp_status osp_group_stage1(osp_group* g, const float* deltas, uint64_t ld, void* stream);
+osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, uint64_t ld,
+                                  void* stream);
+osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream);
+/* stage1 + every chunk + resolve. */
+osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream);
+/* End-to-end step from HOST (pinned or pageable) deltas: H2D copy of the N rows
+ * into the group's staging buffer, the step, and a D2H read of the encoded next
+ * GIB into gib_out (osp_gib_encoded_size(L) bytes, may be NULL). Synchronous. */
+osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,
+                               uint8_t* gib_out, void* stream);
+
+/* Device pointers into the group state (valid until destroy). */
+float* osp_group_global(osp_group* g);
+float* osp_group_worker_params(osp_group* g, uint64_t* ld);
+double* osp_group_scores(osp_group* g);
+/* HOST snapshot of the current GIB / rank order / chunk map (synchronises
+ * `stream`). Any pointer may be NULL. chunk_of: [L], -1 for RS layers. */
+osp_status osp_group_read_gib(osp_group* g, uint8_t* ics_flags, int32_t* ics_order,
+                              int64_t* n_order, int32_t* chunk_of, int* n_used_chunks,
+                              uint32_t* tag, uint64_t* deferred_bytes, void* stream);
+/* Counters: iterations resolved, layers that needed the exact sequential PGP
+ * fallback (certificate failures), and resolves that used it. */
+osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fallback_layers,
+                           uint64_t* fallback_resolves, void* stream);
+/* Deferred (ICS) bytes of the GIBs with tags first_tag .. first_tag+n-1 (a
+ * device ring of the last 1024 resolutions): the u of each iteration for the
+ * algorithmic-byte accounting, without a host sync inside a timed loop. */
+osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, uint64_t* out,
+                                      void* stream);
+/* Tile geometry (for roofline accounting and tests). */
+osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,
+                              int* grid_blocks, int* block_threads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* OSP_C_H */

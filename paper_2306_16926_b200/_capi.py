@@ -1,0 +1,118 @@
+"""ctypes binding of the C-ABI (include/osp_c.h) — the only way Python reaches
+the CUDA path. Loading fails loudly when the in-tree library is missing: there
+is no CPU fallback anywhere in the product.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libosp_b200.so")
+
+c_void_p = ctypes.c_void_p
+c_int = ctypes.c_int
+c_u32 = ctypes.c_uint32
+c_u64 = ctypes.c_uint64
+c_i64 = ctypes.c_int64
+c_dbl = ctypes.c_double
+c_float = ctypes.c_float
+P = ctypes.POINTER
+
+
+class osp_group_config(ctypes.Structure):
+    _fields_ = [("n_workers", c_int), ("weights", P(c_dbl)), ("n_chunks", c_int),
+                ("tile_elems", c_u32), ("sgd_lr", c_dbl)]
+
+
+class osp_sgu_schedule(ctypes.Structure):
+    _fields_ = [("u_max", c_u64), ("has_initial_loss", c_int), ("initial_loss", c_dbl),
+                ("current_budget", c_u64), ("epoch", c_u64)]
+
+
+# name -> (restype, argtypes)
+_SIGS = {
+    "osp_last_error": (ctypes.c_char_p, []),
+    "osp_status_name": (ctypes.c_char_p, [c_int]),
+    "osp_abi_version": (c_int, []),
+    "osp_device_info": (c_int, [P(c_int), P(c_int), P(c_int), P(c_int)]),
+    "osp_partition_create": (c_int, [P(c_u64), c_u64, c_u32, P(c_void_p)]),
+    "osp_partition_destroy": (None, [c_void_p]),
+    "osp_partition_layer_count": (c_u64, [c_void_p]),
+    "osp_partition_total_count": (c_u64, [c_void_p]),
+    "osp_partition_total_bytes": (c_u64, [c_void_p]),
+    "osp_partition_bytes_per_element": (c_u32, [c_void_p]),
+    "osp_partition_layer": (c_int, [c_void_p, c_i64, P(c_u64), P(c_u64)]),
+    "osp_device_alloc": (c_int, [c_u64, P(c_void_p)]),
+    "osp_device_free": (c_int, [c_void_p]),
+    "osp_memcpy_h2d": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_memcpy_d2h": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_memcpy_d2d": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_memset": (c_int, [c_void_p, c_int, c_u64, c_void_p]),
+    "osp_stream_sync": (c_int, [c_void_p]),
+    "osp_aggregate_layer": (c_int, [P(c_void_p), c_int, P(c_dbl), c_u64, c_void_p, c_void_p]),
+    "osp_aggregate_apply_layers": (c_int, [c_void_p, P(c_void_p), c_int, P(c_dbl),
+                                           P(ctypes.c_int32), c_i64, c_void_p, c_void_p,
+                                           c_void_p]),
+    "osp_apply_delta": (c_int, [c_void_p, c_void_p, c_u64, c_float, c_void_p]),
+    "osp_sgd_delta": (c_int, [c_void_p, c_u64, c_dbl, c_void_p, c_void_p]),
+    "osp_synth_delta": (c_int, [c_u64, c_u64, c_u64, c_u64, c_u64, c_void_p, c_void_p]),
+    "osp_synth_deltas": (c_int, [c_u64, c_int, c_u64, c_u64, c_void_p, c_u64, c_void_p]),
+    "osp_lgp_partial": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(ctypes.c_uint8),
+                                c_void_p, c_void_p]),
+    "osp_lgp_correct": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(ctypes.c_int32),
+                                c_i64, c_void_p]),
+    "osp_pgp_layer_importance": (c_int, [c_void_p, c_void_p, c_void_p, P(c_dbl), c_void_p]),
+    "osp_rank_and_gib": (c_int, [c_void_p, P(c_dbl), c_u64, P(ctypes.c_int32),
+                                 P(ctypes.c_uint8), c_void_p]),
+    "osp_split_for_sync": (c_int, [c_void_p, P(ctypes.c_uint8), P(ctypes.c_int32), c_i64,
+                                   c_int, P(ctypes.c_int32), P(c_i64), P(ctypes.c_int32),
+                                   P(c_int)]),
+    "osp_gib_encoded_size": (c_u64, [c_u64]),
+    "osp_gib_encode": (c_int, [c_u32, c_u64, P(ctypes.c_uint8), P(ctypes.c_uint8), c_u64]),
+    "osp_gib_decode": (c_int, [P(ctypes.c_uint8), c_u64, P(c_u32), P(c_u32), P(ctypes.c_uint8),
+                               c_u64]),
+    "osp_compute_umax": (c_int, [c_dbl, c_dbl, c_dbl, c_dbl, c_int, c_u64, c_int, P(c_u64)]),
+    "osp_tune_sgu": (c_int, [P(osp_sgu_schedule), c_u64, c_dbl, P(c_u64)]),
+    "osp_group_create": (c_int, [c_void_p, P(osp_group_config), c_void_p, c_void_p,
+                                 P(c_void_p)]),
+    "osp_group_destroy": (None, [c_void_p]),
+    "osp_group_set_budget": (c_int, [c_void_p, c_u64, c_void_p]),
+    "osp_group_set_gib": (c_int, [c_void_p, P(ctypes.c_uint8), P(ctypes.c_int32), c_i64, c_u32,
+                                  c_void_p]),
+    "osp_group_stage1": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_group_stage2_chunk": (c_int, [c_void_p, c_int, c_void_p, c_u64, c_void_p]),
+    "osp_group_resolve": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_group_step": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_group_step_host": (c_int, [c_void_p, c_void_p, c_u64, P(ctypes.c_uint8), c_void_p]),
+    "osp_group_global": (c_void_p, [c_void_p]),
+    "osp_group_worker_params": (c_void_p, [c_void_p, P(c_u64)]),
+    "osp_group_scores": (c_void_p, [c_void_p]),
+    "osp_group_read_gib": (c_int, [c_void_p, P(ctypes.c_uint8), P(ctypes.c_int32), P(c_i64),
+                                   P(ctypes.c_int32), P(c_int), P(c_u32), P(c_u64), c_void_p]),
+    "osp_group_stats": (c_int, [c_void_p, P(c_u64), P(c_u64), P(c_u64), c_void_p]),
+    "osp_group_deferred_history": (c_int, [c_void_p, c_u32, c_int, P(c_u64), c_void_p]),
+    "osp_group_geometry": (c_int, [c_void_p, P(c_u32), P(c_u64), P(c_int), P(c_int)]),
+}
+
+EXPORTED = sorted(_SIGS)
+
+_lib = None
+
+
+def load(path: str = LIB_PATH):
+    """Load the in-tree CUDA library; raises if it was not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} is missing: build it with `make lib` (or __graft_entry__.build()). "
+            "The OSP sync path has no CPU fallback.")
+    lib = ctypes.CDLL(path)
+    for name, (res, args) in _SIGS.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib

@@ -1,0 +1,849 @@
+// C-ABI implementation (include/osp_c.h): handles, validation with the
+// reference's error classes, and the launch sequences. No exception crosses
+// this boundary; every failure sets a thread-local message and returns a status.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../osp_internal.h"
+
+namespace osp {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+osp_status fail(osp_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+osp_status cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return OSP_ERR_CUDA;
+}
+
+int sm_count() {
+    static int cached = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+            cached = 148;
+    });
+    return cached;
+}
+
+AggParams make_agg_params(int n, const double* weights, double sgd_lr) {
+    AggParams ap{};
+    ap.n = n;
+    double total = 0.0;
+    for (int w = 0; w < n; ++w) {
+        ap.w[w] = weights[w];
+        total += weights[w];  // protocol.cpp:14-15, ascending
+    }
+    ap.total = total;
+    ap.divide = total == 1.0 ? 0 : 1;
+    ap.sgd = sgd_lr > 0 ? 1 : 0;
+    ap.neg_lr = -sgd_lr;
+    return ap;
+}
+
+}  // namespace osp
+
+using namespace osp;
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+
+struct osp_partition {
+    std::vector<uint64_t> counts;
+    std::vector<uint64_t> offsets;
+    uint64_t total = 0;
+    uint32_t bpe = 4;
+    uint64_t* d_offsets = nullptr;
+    uint64_t* d_counts = nullptr;
+};
+
+struct osp_group {
+    const osp_partition* part = nullptr;
+    int N = 0;
+    int n_chunks = 1;
+    double sgd_lr = 0.0;
+    std::vector<double> weights;
+    AggParams ap{};
+    GroupView v{};
+    int grid = 1;
+    int blocks_per_sm = 1;
+    // owned device buffers
+    std::vector<void*> owned;
+    int* d_order_tmp = nullptr;
+    float* d_staging = nullptr;
+};
+
+namespace {
+
+template <typename T>
+osp_status dalloc(osp_group* g, T** out, size_t count) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    g->owned.push_back(p);
+    *out = static_cast<T*>(p);
+    return OSP_OK;
+}
+
+#define OSP_TRY(expr)                      \
+    do {                                   \
+        osp_status s_ = (expr);            \
+        if (s_ != OSP_OK) return s_;       \
+    } while (0)
+
+osp_status check_weights(int n, const double* weights) {
+    if (n < 1) return fail(OSP_ERR_PROTOCOL, "aggregation needs one contribution per worker");
+    if (n > OSP_MAX_WORKERS)
+        return fail(OSP_ERR_INVALID, "more than OSP_MAX_WORKERS (" +
+                                         std::to_string(OSP_MAX_WORKERS) + ") workers");
+    if (!weights) return fail(OSP_ERR_INVALID, "null weights");
+    double tw = 0.0;
+    for (int w = 0; w < n; ++w) tw += weights[w];
+    if (!(tw > 0.0)) return fail(OSP_ERR_PROTOCOL, "aggregation weights must sum > 0");
+    return OSP_OK;
+}
+
+// Device segment table from host (offset, count[, flag]) lists; freed stream-ordered.
+struct SegTable {
+    uint64_t* off = nullptr;
+    uint64_t* cnt = nullptr;
+    uint8_t* flag = nullptr;
+    cudaStream_t s = nullptr;
+    ~SegTable() {
+        if (off) cudaFreeAsync(off, s);
+        if (cnt) cudaFreeAsync(cnt, s);
+        if (flag) cudaFreeAsync(flag, s);
+    }
+};
+
+osp_status upload_segments(SegTable& t, const std::vector<uint64_t>& off,
+                           const std::vector<uint64_t>& cnt, const std::vector<uint8_t>* flag,
+                           cudaStream_t s) {
+    t.s = s;
+    const size_t n = std::max<size_t>(off.size(), 1);
+    OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t.off), n * 8, s));
+    OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t.cnt), n * 8, s));
+    if (!off.empty()) {
+        OSP_CUDA(cudaMemcpyAsync(t.off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s));
+        OSP_CUDA(cudaMemcpyAsync(t.cnt, cnt.data(), cnt.size() * 8, cudaMemcpyHostToDevice, s));
+    }
+    if (flag) {
+        OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t.flag), n, s));
+        if (!flag->empty())
+            OSP_CUDA(cudaMemcpyAsync(t.flag, flag->data(), flag->size(), cudaMemcpyHostToDevice, s));
+    }
+    return OSP_OK;
+}
+
+void put_u32le(uint8_t* p, uint32_t v) {
+    p[0] = v & 0xff;
+    p[1] = (v >> 8) & 0xff;
+    p[2] = (v >> 16) & 0xff;
+    p[3] = (v >> 24) & 0xff;
+}
+
+uint32_t get_u32le(const uint8_t* p) {
+    return uint32_t(p[0]) | (uint32_t(p[1]) << 8) | (uint32_t(p[2]) << 16) | (uint32_t(p[3]) << 24);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* osp_last_error(void) { return g_last_error.c_str(); }
+
+const char* osp_status_name(osp_status s) {
+    switch (s) {
+        case OSP_OK: return "OK";
+        case OSP_ERR_PARTITION: return "PartitionError";
+        case OSP_ERR_SHAPE: return "ShapeError";
+        case OSP_ERR_LAYER: return "LayerError";
+        case OSP_ERR_PARSE: return "ParseError";
+        case OSP_ERR_CONFIG: return "ConfigError";
+        case OSP_ERR_FORMAT: return "FormatError";
+        case OSP_ERR_PROTOCOL: return "ProtocolError";
+        case OSP_ERR_NUMERIC: return "NumericError";
+        case OSP_ERR_CUDA: return "CudaError";
+        case OSP_ERR_INVALID: return "InvalidArgument";
+    }
+    return "Unknown";
+}
+
+int osp_abi_version(void) { return OSP_ABI_VERSION; }
+
+osp_status osp_device_info(int* device, int* sms, int* major, int* minor) {
+    int dev = 0;
+    OSP_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    OSP_CUDA(cudaGetDeviceProperties(&prop, dev));
+    if (device) *device = dev;
+    if (sms) *sms = prop.multiProcessorCount;
+    if (major) *major = prop.major;
+    if (minor) *minor = prop.minor;
+    return OSP_OK;
+}
+
+// ---- partition --------------------------------------------------------------
+
+osp_status osp_partition_create(const uint64_t* layer_counts, uint64_t n_layers,
+                                uint32_t bytes_per_element, osp_partition** out) {
+    if (!out) return fail(OSP_ERR_INVALID, "null output handle");
+    *out = nullptr;
+    if (n_layers == 0) return fail(OSP_ERR_PARTITION, "partition needs at least one layer");
+    if (bytes_per_element == 0) return fail(OSP_ERR_PARTITION, "bytes_per_element must be positive");
+    if (!layer_counts) return fail(OSP_ERR_INVALID, "null layer_counts");
+    auto* p = new (std::nothrow) osp_partition();
+    if (!p) return fail(OSP_ERR_INVALID, "out of host memory");
+    p->bpe = bytes_per_element;
+    p->counts.assign(layer_counts, layer_counts + n_layers);
+    p->offsets.resize(n_layers);
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n_layers; ++i) {
+        if (layer_counts[i] == 0) {
+            delete p;
+            return fail(OSP_ERR_PARTITION, "layer " + std::to_string(i) + " has zero elements");
+        }
+        p->offsets[i] = off;
+        off += layer_counts[i];
+    }
+    p->total = off;
+    cudaError_t e = cudaMalloc(&p->d_offsets, n_layers * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_counts, n_layers * 8);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_offsets, p->offsets.data(), n_layers * 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_counts, p->counts.data(), n_layers * 8, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        osp_partition_destroy(p);
+        return cuda_fail(e, "partition device mirror");
+    }
+    *out = p;
+    return OSP_OK;
+}
+
+void osp_partition_destroy(osp_partition* p) {
+    if (!p) return;
+    if (p->d_offsets) cudaFree(p->d_offsets);
+    if (p->d_counts) cudaFree(p->d_counts);
+    delete p;
+}
+
+uint64_t osp_partition_layer_count(const osp_partition* p) { return p ? p->counts.size() : 0; }
+uint64_t osp_partition_total_count(const osp_partition* p) { return p ? p->total : 0; }
+uint64_t osp_partition_total_bytes(const osp_partition* p) { return p ? p->total * p->bpe : 0; }
+uint32_t osp_partition_bytes_per_element(const osp_partition* p) { return p ? p->bpe : 0; }
+
+osp_status osp_partition_layer(const osp_partition* p, int64_t id, uint64_t* offset,
+                               uint64_t* count) {
+    if (!p) return fail(OSP_ERR_INVALID, "null partition");
+    if (id < 0 || static_cast<uint64_t>(id) >= p->counts.size())
+        return fail(OSP_ERR_LAYER, "layer id " + std::to_string(id) + " out of range (have " +
+                                       std::to_string(p->counts.size()) + " layers)");
+    if (offset) *offset = p->offsets[id];
+    if (count) *count = p->counts[id];
+    return OSP_OK;
+}
+
+// ---- buffers ----------------------------------------------------------------
+
+osp_status osp_device_alloc(uint64_t bytes, void** out) {
+    if (!out) return fail(OSP_ERR_INVALID, "null output");
+    OSP_CUDA(cudaMalloc(out, std::max<uint64_t>(bytes, 4)));
+    return OSP_OK;
+}
+osp_status osp_device_free(void* ptr) {
+    if (ptr) OSP_CUDA(cudaFree(ptr));
+    return OSP_OK;
+}
+osp_status osp_memcpy_h2d(void* dst, const void* src, uint64_t bytes, void* stream) {
+    if (bytes) OSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, as_stream(stream)));
+    return OSP_OK;
+}
+osp_status osp_memcpy_d2h(void* dst, const void* src, uint64_t bytes, void* stream) {
+    if (bytes) {
+        OSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, as_stream(stream)));
+        OSP_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    }
+    return OSP_OK;
+}
+osp_status osp_memcpy_d2d(void* dst, const void* src, uint64_t bytes, void* stream) {
+    if (bytes) OSP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, as_stream(stream)));
+    return OSP_OK;
+}
+osp_status osp_memset(void* dst, int value, uint64_t bytes, void* stream) {
+    if (bytes) OSP_CUDA(cudaMemsetAsync(dst, value, bytes, as_stream(stream)));
+    return OSP_OK;
+}
+osp_status osp_stream_sync(void* stream) {
+    OSP_CUDA(cudaStreamSynchronize(as_stream(stream)));
+    return OSP_OK;
+}
+
+// ---- element-wise primitives ------------------------------------------------
+
+osp_status osp_aggregate_layer(const float* const* contribs, int n_workers,
+                               const double* weights, uint64_t n, float* out, void* stream) {
+    OSP_TRY(check_weights(n_workers, weights));
+    if (!contribs || !out) return fail(OSP_ERR_INVALID, "null pointer");
+    for (int w = 0; w < n_workers; ++w)
+        if (!contribs[w] && n) return fail(OSP_ERR_INVALID, "null contribution");
+    AggParams ap = make_agg_params(n_workers, weights, 0.0);
+    OSP_CUDA(launch_aggregate_layer(contribs, ap, n, out, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_aggregate_apply_layers(const osp_partition* part, const float* const* contribs,
+                                      int n_workers, const double* weights,
+                                      const int32_t* layer_ids, int64_t n_ids, float* global,
+                                      float* agg_out, void* stream) {
+    if (!part) return fail(OSP_ERR_INVALID, "null partition");
+    OSP_TRY(check_weights(n_workers, weights));
+    if (n_ids > 65535) return fail(OSP_ERR_INVALID, "too many layers in one call");
+    std::vector<uint64_t> off, cnt;
+    for (int64_t i = 0; i < n_ids; ++i) {
+        uint64_t o = 0, c = 0;
+        OSP_TRY(osp_partition_layer(part, layer_ids[i], &o, &c));
+        off.push_back(o);
+        cnt.push_back(c);
+    }
+    if (off.empty()) return OSP_OK;
+    cudaStream_t s = as_stream(stream);
+    SegTable t;
+    OSP_TRY(upload_segments(t, off, cnt, nullptr, s));
+    AggParams ap = make_agg_params(n_workers, weights, 0.0);
+    OSP_CUDA(launch_aggregate_apply_segments(contribs, ap, t.off, t.cnt, static_cast<int>(off.size()),
+                                             global, agg_out, s));
+    return OSP_OK;
+}
+
+osp_status osp_apply_delta(float* p, const float* d, uint64_t n, float scale, void* stream) {
+    OSP_CUDA(launch_apply_delta(p, d, n, scale, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_sgd_delta(const float* grad, uint64_t n, double lr, float* out, void* stream) {
+    if (lr <= 0) return fail(OSP_ERR_CONFIG, "learning rate must be positive");
+    OSP_CUDA(launch_sgd_delta(grad, n, lr, out, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_synth_delta(uint64_t seed, uint64_t worker, uint64_t iteration, uint64_t first,
+                           uint64_t n, float* out, void* stream) {
+    OSP_CUDA(launch_synth(seed, 1, iteration, first, n, out, n, worker, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_synth_deltas(uint64_t seed, int n_workers, uint64_t iteration, uint64_t n,
+                            float* out, uint64_t ld, void* stream) {
+    if (n_workers < 0 || n_workers > 65535) return fail(OSP_ERR_INVALID, "bad worker count");
+    if (ld < n) return fail(OSP_ERR_SHAPE, "ld smaller than the vector length");
+    OSP_CUDA(launch_synth(seed, n_workers, iteration, 0, n, out, ld, 0, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_lgp_partial(const osp_partition* part, float* params, const float* global_delta,
+                           const float* local_delta, const uint8_t* ics_flags, float* base,
+                           void* stream) {
+    if (!part || !ics_flags) return fail(OSP_ERR_INVALID, "null argument");
+    const size_t L = part->counts.size();
+    std::vector<uint64_t> off(L), cnt(L);
+    std::vector<uint8_t> loc(L);
+    for (size_t l = 0; l < L; ++l) {
+        off[l] = part->offsets[l];
+        cnt[l] = part->counts[l];
+        loc[l] = ics_flags[l] ? 1 : 0;
+    }
+    if (L > 65535) return fail(OSP_ERR_INVALID, "too many layers in one call");
+    cudaStream_t s = as_stream(stream);
+    SegTable t;
+    OSP_TRY(upload_segments(t, off, cnt, &loc, s));
+    OSP_CUDA(launch_lgp_partial_segments(params, global_delta, local_delta, base, t.off, t.cnt, t.flag,
+                                         static_cast<int>(L), s));
+    return OSP_OK;
+}
+
+osp_status osp_lgp_correct(const osp_partition* part, float* params, const float* base,
+                           const float* global_delta, const int32_t* layer_ids, int64_t n_ids,
+                           void* stream) {
+    if (!part) return fail(OSP_ERR_INVALID, "null partition");
+    std::vector<uint64_t> off, cnt;
+    for (int64_t i = 0; i < n_ids; ++i) {
+        uint64_t o = 0, c = 0;
+        OSP_TRY(osp_partition_layer(part, layer_ids[i], &o, &c));
+        off.push_back(o);
+        cnt.push_back(c);
+    }
+    if (off.empty()) return OSP_OK;
+    if (off.size() > 65535) return fail(OSP_ERR_INVALID, "too many layers in one call");
+    cudaStream_t s = as_stream(stream);
+    SegTable t;
+    OSP_TRY(upload_segments(t, off, cnt, nullptr, s));
+    OSP_CUDA(launch_lgp_correct_segments(params, base, global_delta, t.off, t.cnt,
+                                         static_cast<int>(off.size()), s));
+    return OSP_OK;
+}
+
+osp_status osp_pgp_layer_importance(const osp_partition* part, const float* params,
+                                    const float* grads, double* scores_host, void* stream) {
+    if (!part || !scores_host) return fail(OSP_ERR_INVALID, "null argument");
+    const int L = static_cast<int>(part->counts.size());
+    cudaStream_t s = as_stream(stream);
+    double* d = nullptr;
+    OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&d), L * sizeof(double), s));
+    cudaError_t e = launch_pgp_exact(params, grads, part->d_offsets, part->d_counts, L, d, s);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(scores_host, d, L * sizeof(double), cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(d, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "pgp_layer_importance");
+    return OSP_OK;
+}
+
+osp_status osp_rank_and_gib(const osp_partition* part, const double* scores_host,
+                            uint64_t budget_bytes, int32_t* order_host, uint8_t* flags_host,
+                            void* stream) {
+    if (!part || !scores_host) return fail(OSP_ERR_INVALID, "null argument");
+    const int L = static_cast<int>(part->counts.size());
+    if (L > kMaxLayers)
+        return fail(OSP_ERR_INVALID, "more than " + std::to_string(kMaxLayers) + " layers");
+    cudaStream_t s = as_stream(stream);
+    double* ds = nullptr;
+    int* dord = nullptr;
+    uint8_t* dfl = nullptr;
+    OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ds), L * sizeof(double), s));
+    OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dord), L * sizeof(int), s));
+    OSP_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dfl), L, s));
+    cudaError_t e = cudaMemcpyAsync(ds, scores_host, L * sizeof(double), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess)
+        e = launch_rank_gib(ds, part->d_counts, part->bpe, L, budget_bytes, dord, dfl, s);
+    if (e == cudaSuccess && order_host)
+        e = cudaMemcpyAsync(order_host, dord, L * sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && flags_host)
+        e = cudaMemcpyAsync(flags_host, dfl, L, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(ds, s);
+    cudaFreeAsync(dord, s);
+    cudaFreeAsync(dfl, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "rank_and_gib");
+    return OSP_OK;
+}
+
+osp_status osp_split_for_sync(const osp_partition* part, const uint8_t* ics_flags,
+                              const int32_t* ics_order, int64_t n_order, int n_chunks,
+                              int32_t* rs_ids, int64_t* n_rs, int32_t* chunk_of, int* n_used) {
+    if (!part || !ics_flags) return fail(OSP_ERR_INVALID, "null argument");
+    if (n_chunks < 1) return fail(OSP_ERR_CONFIG, "need at least one chunk slot");
+    const int L = static_cast<int>(part->counts.size());
+    if (L > kMaxLayers)
+        return fail(OSP_ERR_INVALID, "more than " + std::to_string(kMaxLayers) + " layers");
+    // Scratch group view with one tile per layer; the device list builder
+    // (k_install -> finalize_lists, resolve.cu) does the index math.
+    std::vector<int> tb(L + 1);
+    for (int l = 0; l <= L; ++l) tb[l] = l;
+    std::vector<uint8_t> f(L);
+    for (int l = 0; l < L; ++l) f[l] = ics_flags[l] ? 1 : 0;
+    GroupView v{};
+    v.L = L;
+    v.T = 1 << 30;
+    v.NT = L;
+    v.n_chunks = n_chunks;
+    v.bpe = part->bpe;
+    v.offsets = part->d_offsets;
+    v.counts = part->d_counts;
+    std::vector<void*> tmp;
+    auto al = [&](auto** p, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(bytes, 8));
+        if (e == cudaSuccess) tmp.push_back(*p);
+        return e;
+    };
+    int* d_tb = nullptr;
+    int* d_order = nullptr;
+    cudaError_t e = al(&d_tb, (L + 1) * sizeof(int));
+    if (e == cudaSuccess) e = al(&d_order, std::max<int64_t>(n_order, 1) * sizeof(int));
+    if (e == cudaSuccess) e = al(&v.flags, L);
+    if (e == cudaSuccess) e = al(&v.ics_layers, L * sizeof(int));
+    if (e == cudaSuccess) e = al(&v.chunk_begin, (n_chunks + 1) * sizeof(int));
+    if (e == cudaSuccess) e = al(&v.ics_tile_prefix, (L + 1) * sizeof(int));
+    if (e == cudaSuccess) e = al(&v.meta, 8 * sizeof(int));
+    if (e == cudaSuccess) e = al(&v.meta64, 8 * sizeof(uint64_t));
+    if (e == cudaSuccess) e = al(&v.chunk_of, L * sizeof(int));
+    if (e == cudaSuccess) e = al(&v.gib_bytes, osp_gib_encoded_size(L));
+    v.tile_base = d_tb;
+    if (e == cudaSuccess) e = cudaMemcpy(d_tb, tb.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(v.flags, f.data(), L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && n_order > 0)
+        e = cudaMemcpy(d_order, ics_order, n_order * sizeof(int), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = launch_install_gib(v, d_order, static_cast<int>(n_order), 0, nullptr);
+    int meta[8] = {0};
+    std::vector<int32_t> co(L);
+    if (e == cudaSuccess) e = cudaMemcpy(meta, v.meta, sizeof meta, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(co.data(), v.chunk_of, L * 4, cudaMemcpyDeviceToHost);
+    for (void* p : tmp) cudaFree(p);
+    if (e != cudaSuccess) return cuda_fail(e, "split_for_sync");
+    int64_t nr = 0;
+    for (int l = 0; l < L; ++l) {
+        if (!f[l] && rs_ids) rs_ids[nr] = l;
+        if (!f[l]) ++nr;
+    }
+    if (n_rs) *n_rs = nr;
+    if (chunk_of) std::copy(co.begin(), co.end(), chunk_of);
+    if (n_used) *n_used = meta[META_N_USED];
+    return OSP_OK;
+}
+
+// ---- GIB wire format --------------------------------------------------------
+
+uint64_t osp_gib_encoded_size(uint64_t n_layers) { return 8 + (n_layers + 7) / 8; }
+
+osp_status osp_gib_encode(uint32_t tag, uint64_t n_layers, const uint8_t* ics_flags, uint8_t* out,
+                          uint64_t out_len) {
+    const uint64_t need = osp_gib_encoded_size(n_layers);
+    if (!out || out_len < need) return fail(OSP_ERR_INVALID, "gib output buffer too small");
+    std::memset(out, 0, need);
+    put_u32le(out, tag);
+    put_u32le(out + 4, static_cast<uint32_t>(n_layers));
+    for (uint64_t k = 0; k < n_layers; ++k)
+        if (ics_flags[k]) out[8 + k / 8] |= static_cast<uint8_t>(1u << (k % 8));
+    return OSP_OK;
+}
+
+osp_status osp_gib_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint32_t* n_layers,
+                          uint8_t* ics_flags, uint64_t flags_cap) {
+    if (len < 8)
+        return fail(OSP_ERR_FORMAT, "gib buffer truncated: " + std::to_string(len) + " bytes");
+    const uint32_t t = get_u32le(buf), L = get_u32le(buf + 4);
+    if (len < osp_gib_encoded_size(L))
+        return fail(OSP_ERR_FORMAT, "gib bitmap truncated: need " +
+                                        std::to_string(osp_gib_encoded_size(L)) + " bytes, have " +
+                                        std::to_string(len));
+    if (tag) *tag = t;
+    if (n_layers) *n_layers = L;
+    if (ics_flags) {
+        if (L > flags_cap) return fail(OSP_ERR_INVALID, "flags buffer too small");
+        for (uint64_t k = 0; k < L; ++k) ics_flags[k] = (buf[8 + k / 8] >> (k % 8)) & 1u;
+    }
+    return OSP_OK;
+}
+
+// ---- tuning (host scalar logic, tuning.cpp:8-48) ----------------------------
+
+osp_status osp_compute_umax(double bw, double latency_s, double loss_rate, double t_c,
+                            int n_workers, uint64_t model_bytes, int eq5_literal, uint64_t* out) {
+    if (bw <= 0) return fail(OSP_ERR_CONFIG, "bandwidth must be positive");
+    if (latency_s < 0) return fail(OSP_ERR_CONFIG, "latency must be non-negative");
+    if (loss_rate < 0 || loss_rate >= 1) return fail(OSP_ERR_CONFIG, "loss_rate must be in [0, 1)");
+    if (t_c < 0) return fail(OSP_ERR_CONFIG, "t_c must be non-negative");
+    if (n_workers < 1) return fail(OSP_ERR_CONFIG, "n_workers must be at least 1");
+    double raw = eq5_literal ? bw * (1.0 + loss_rate) * t_c / n_workers
+                             : bw * t_c / (n_workers * (1.0 + loss_rate));
+    double cap = 0.8 * static_cast<double>(model_bytes);
+    *out = static_cast<uint64_t>(std::floor(std::min(raw, cap)));
+    return OSP_OK;
+}
+
+osp_status osp_tune_sgu(osp_sgu_schedule* sched, uint64_t epoch_index, double epoch_loss,
+                        uint64_t* budget_out) {
+    if (!sched) return fail(OSP_ERR_INVALID, "null schedule");
+    if (epoch_index < 1) return fail(OSP_ERR_CONFIG, "epoch index is 1-based");
+    if (epoch_loss < 0) return fail(OSP_ERR_NUMERIC, "epoch loss must be non-negative");
+    sched->epoch = epoch_index;
+    if (epoch_index == 1) {
+        sched->initial_loss = epoch_loss;
+        sched->has_initial_loss = 1;
+        sched->current_budget = 0;
+        if (budget_out) *budget_out = 0;
+        return OSP_OK;
+    }
+    if (!sched->has_initial_loss)
+        return fail(OSP_ERR_PROTOCOL, "tune_sgu called for epoch " + std::to_string(epoch_index) +
+                                          " before epoch 1 recorded the reference loss");
+    const double ref = sched->initial_loss;
+    const double factor = ref <= 0.0 ? 1.0 : std::clamp(1.0 - epoch_loss / ref, 0.0, 1.0);
+    sched->current_budget =
+        static_cast<uint64_t>(std::floor(factor * static_cast<double>(sched->u_max)));
+    if (budget_out) *budget_out = sched->current_budget;
+    return OSP_OK;
+}
+
+// ---- group ------------------------------------------------------------------
+
+osp_status osp_group_create(const osp_partition* part, const osp_group_config* cfg,
+                            const float* init_params, void* stream, osp_group** out) {
+    if (!out || !part || !cfg) return fail(OSP_ERR_INVALID, "null argument");
+    *out = nullptr;
+    const int N = cfg->n_workers;
+    if (N < 1) return fail(OSP_ERR_CONFIG, "server needs worker weights");
+    if (N > OSP_MAX_WORKERS)
+        return fail(OSP_ERR_INVALID, "more than OSP_MAX_WORKERS workers per group");
+    if (!cfg->weights) return fail(OSP_ERR_INVALID, "null weights");
+    for (int w = 0; w < N; ++w)
+        if (cfg->weights[w] <= 0) return fail(OSP_ERR_CONFIG, "subset weight must be positive");
+    if (cfg->n_chunks < 1) return fail(OSP_ERR_CONFIG, "need at least one chunk slot");
+    if (cfg->sgd_lr < 0) return fail(OSP_ERR_CONFIG, "learning rate must be positive");
+    const uint64_t L = part->counts.size();
+    if (L > static_cast<uint64_t>(kMaxLayers))
+        return fail(OSP_ERR_INVALID, "more than " + std::to_string(kMaxLayers) + " layers");
+    uint32_t T = cfg->tile_elems ? cfg->tile_elems : 8192u;
+    if (T < 1024 || (T & (T - 1)))
+        return fail(OSP_ERR_INVALID, "tile_elems must be a power of two >= 1024");
+
+    auto* g = new (std::nothrow) osp_group();
+    if (!g) return fail(OSP_ERR_INVALID, "out of host memory");
+    auto cleanup = [&](osp_status s) {
+        osp_group_destroy(g);
+        return s;
+    };
+    g->part = part;
+    g->N = N;
+    g->n_chunks = cfg->n_chunks;
+    g->sgd_lr = cfg->sgd_lr;
+    g->weights.assign(cfg->weights, cfg->weights + N);
+    g->ap = make_agg_params(N, cfg->weights, cfg->sgd_lr);
+
+    // tile tables
+    std::vector<int> tile_base(L + 1), tile_layer;
+    uint64_t nt_total = 0;
+    for (uint64_t l = 0; l < L; ++l) {
+        tile_base[l] = static_cast<int>(nt_total);
+        const uint64_t nt = (part->counts[l] + T - 1) / T;
+        for (uint64_t k = 0; k < nt; ++k) tile_layer.push_back(static_cast<int>(l));
+        nt_total += nt;
+        if (nt_total > 0x7fffffffull) return cleanup(fail(OSP_ERR_INVALID, "too many tiles"));
+    }
+    tile_base[L] = static_cast<int>(nt_total);
+
+    GroupView& v = g->v;
+    v.L = static_cast<int>(L);
+    v.T = static_cast<int>(T);
+    v.NT = static_cast<int>(nt_total);
+    v.n_chunks = cfg->n_chunks;
+    v.bpe = part->bpe;
+    v.offsets = part->d_offsets;
+    v.counts = part->d_counts;
+    const uint64_t M = part->total;
+    v.ldP = (M + 3) & ~uint64_t(3);
+    int *d_tb = nullptr, *d_tl = nullptr;
+    osp_status st;
+    if ((st = dalloc(g, &d_tb, L + 1)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &d_tl, nt_total)) != OSP_OK) return cleanup(st);
+    v.tile_base = d_tb;
+    v.tile_layer = d_tl;
+    if ((st = dalloc(g, &v.G, M)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.P, v.ldP * N)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.partials, nt_total)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.flags, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.ics_layers, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.chunk_begin, cfg->n_chunks + 1)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.ics_tile_prefix, L + 1)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.meta, 8)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.meta64, 8)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.scores, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.exact, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.marked, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.chunk_of, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.gib_bytes, osp_gib_encoded_size(L))) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &g->d_order_tmp, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.hist, kHist)) != OSP_OK) return cleanup(st);
+
+    cudaStream_t s = as_stream(stream);
+    auto cu = [&](cudaError_t e, const char* what) -> osp_status {
+        return e == cudaSuccess ? OSP_OK : cuda_fail(e, what);
+    };
+    if ((st = cu(cudaMemcpyAsync(d_tb, tile_base.data(), (L + 1) * sizeof(int),
+                                 cudaMemcpyHostToDevice, s), "tile_base")) != OSP_OK)
+        return cleanup(st);
+    if ((st = cu(cudaMemcpyAsync(d_tl, tile_layer.data(), nt_total * sizeof(int),
+                                 cudaMemcpyHostToDevice, s), "tile_layer")) != OSP_OK)
+        return cleanup(st);
+    if (init_params) {
+        st = cu(cudaMemcpyAsync(v.G, init_params, M * 4, cudaMemcpyDeviceToDevice, s), "init G");
+        if (st == OSP_OK)
+            st = cu(cudaMemcpy2DAsync(v.P, v.ldP * 4, init_params, 0, M * 4, N,
+                                      cudaMemcpyDeviceToDevice, s), "init P");
+    } else {
+        st = cu(cudaMemsetAsync(v.G, 0, M * 4, s), "zero G");
+        if (st == OSP_OK) st = cu(cudaMemsetAsync(v.P, 0, v.ldP * N * 4, s), "zero P");
+    }
+    if (st != OSP_OK) return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.partials, 0, nt_total * 8, s), "partials")) != OSP_OK)
+        return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.flags, 0, L, s), "flags")) != OSP_OK) return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.marked, 0, L, s), "marked")) != OSP_OK) return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.meta, 0, 8 * sizeof(int), s), "meta")) != OSP_OK)
+        return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.meta64, 0, 8 * sizeof(uint64_t), s), "meta64")) != OSP_OK)
+        return cleanup(st);
+    // bootstrap GIB: nothing deferred, tag 0 (first_iteration_bootstrap, protocol.cpp:58-63)
+    if ((st = cu(launch_install_gib(v, g->d_order_tmp, 0, 0, s), "install bootstrap gib")) != OSP_OK)
+        return cleanup(st);
+    g->blocks_per_sm = stage_blocks_per_sm(N);
+    g->grid = sm_count() * g->blocks_per_sm;
+    if ((st = cu(cudaStreamSynchronize(s), "group create")) != OSP_OK) return cleanup(st);
+    *out = g;
+    return OSP_OK;
+}
+
+void osp_group_destroy(osp_group* g) {
+    if (!g) return;
+    cudaDeviceSynchronize();
+    for (void* p : g->owned) cudaFree(p);
+    if (g->d_staging) cudaFree(g->d_staging);
+    delete g;
+}
+
+osp_status osp_group_set_budget(osp_group* g, uint64_t budget, void* stream) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    OSP_CUDA(launch_set_budget(g->v, budget, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_group_set_gib(osp_group* g, const uint8_t* flags, const int32_t* order,
+                             int64_t n_order, uint32_t tag, void* stream) {
+    if (!g || !flags) return fail(OSP_ERR_INVALID, "null argument");
+    if (n_order < 0 || n_order > g->v.L)
+        return fail(OSP_ERR_INVALID, "rank order longer than the layer count");
+    cudaStream_t s = as_stream(stream);
+    std::vector<uint8_t> f(flags, flags + g->v.L);
+    for (auto& x : f) x = x ? 1 : 0;
+    OSP_CUDA(cudaMemcpyAsync(g->v.flags, f.data(), g->v.L, cudaMemcpyHostToDevice, s));
+    if (n_order > 0)
+        OSP_CUDA(cudaMemcpyAsync(g->d_order_tmp, order, n_order * sizeof(int32_t),
+                                 cudaMemcpyHostToDevice, s));
+    OSP_CUDA(launch_install_gib(g->v, g->d_order_tmp, static_cast<int>(n_order), tag, s));
+    OSP_CUDA(cudaStreamSynchronize(s));  // host vectors are released on return
+    return OSP_OK;
+}
+
+osp_status osp_group_stage1(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
+    if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    OSP_CUDA(launch_stage1(g->v, g->ap, deltas, ld, g->grid, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, uint64_t ld,
+                                  void* stream) {
+    if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
+    if (chunk < 0 || chunk >= g->n_chunks) return fail(OSP_ERR_INVALID, "chunk out of range");
+    if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, g->grid, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
+    OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_TRY(osp_group_stage1(g, deltas, ld, stream));
+    for (int c = 0; c < g->n_chunks; ++c) OSP_TRY(osp_group_stage2_chunk(g, c, deltas, ld, stream));
+    return osp_group_resolve(g, deltas, ld, stream);
+}
+
+osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,
+                               uint8_t* gib_out, void* stream) {
+    if (!g || !host_deltas) return fail(OSP_ERR_INVALID, "null argument");
+    const uint64_t M = g->part->total;
+    if (host_ld < M) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    cudaStream_t s = as_stream(stream);
+    if (!g->d_staging) OSP_CUDA(cudaMalloc(&g->d_staging, g->v.ldP * g->N * 4));
+    OSP_CUDA(cudaMemcpy2DAsync(g->d_staging, g->v.ldP * 4, host_deltas, host_ld * 4, M * 4, g->N,
+                               cudaMemcpyHostToDevice, s));
+    OSP_TRY(osp_group_step(g, g->d_staging, g->v.ldP, stream));
+    if (gib_out)
+        OSP_CUDA(cudaMemcpyAsync(gib_out, g->v.gib_bytes, osp_gib_encoded_size(g->v.L),
+                                 cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaStreamSynchronize(s));
+    return OSP_OK;
+}
+
+float* osp_group_global(osp_group* g) { return g ? g->v.G : nullptr; }
+float* osp_group_worker_params(osp_group* g, uint64_t* ld) {
+    if (!g) return nullptr;
+    if (ld) *ld = g->v.ldP;
+    return g->v.P;
+}
+double* osp_group_scores(osp_group* g) { return g ? g->v.scores : nullptr; }
+
+osp_status osp_group_read_gib(osp_group* g, uint8_t* flags, int32_t* order, int64_t* n_order,
+                              int32_t* chunk_of, int* n_used, uint32_t* tag, uint64_t* deferred,
+                              void* stream) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    cudaStream_t s = as_stream(stream);
+    int meta[8];
+    uint64_t meta64[8];
+    OSP_CUDA(cudaMemcpyAsync(meta, g->v.meta, sizeof meta, cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaMemcpyAsync(meta64, g->v.meta64, sizeof meta64, cudaMemcpyDeviceToHost, s));
+    if (flags) OSP_CUDA(cudaMemcpyAsync(flags, g->v.flags, g->v.L, cudaMemcpyDeviceToHost, s));
+    if (chunk_of)
+        OSP_CUDA(cudaMemcpyAsync(chunk_of, g->v.chunk_of, g->v.L * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> ord(g->v.L);
+    if (order) OSP_CUDA(cudaMemcpyAsync(ord.data(), g->v.ics_layers, g->v.L * 4,
+                                        cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaStreamSynchronize(s));
+    const int k = meta[META_N_ICS];
+    if (order) std::copy(ord.begin(), ord.begin() + k, order);
+    if (n_order) *n_order = k;
+    if (n_used) *n_used = meta[META_N_USED];
+    if (tag) *tag = static_cast<uint32_t>(meta64[META64_TAG]);
+    if (deferred) *deferred = meta64[META64_DEFERRED];
+    return OSP_OK;
+}
+
+osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fb_layers,
+                           uint64_t* fb_resolves, void* stream) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    uint64_t meta64[8];
+    cudaStream_t s = as_stream(stream);
+    OSP_CUDA(cudaMemcpyAsync(meta64, g->v.meta64, sizeof meta64, cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaStreamSynchronize(s));
+    if (resolved) *resolved = meta64[META64_RESOLVED];
+    if (fb_layers) *fb_layers = meta64[META64_FB_LAYERS];
+    if (fb_resolves) *fb_resolves = meta64[META64_FB_RESOLVES];
+    return OSP_OK;
+}
+
+osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, uint64_t* out,
+                                      void* stream) {
+    if (!g || !out) return fail(OSP_ERR_INVALID, "null argument");
+    if (n < 0 || n > kHist) return fail(OSP_ERR_INVALID, "history window out of range");
+    std::vector<uint64_t> h(kHist);
+    cudaStream_t s = as_stream(stream);
+    OSP_CUDA(cudaMemcpyAsync(h.data(), g->v.hist, kHist * 8, cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaStreamSynchronize(s));
+    for (int i = 0; i < n; ++i) out[i] = h[(first_tag + i) % kHist];
+    return OSP_OK;
+}
+
+osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,
+                              int* grid_blocks, int* block_threads) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    if (tile_elems) *tile_elems = static_cast<uint32_t>(g->v.T);
+    if (n_tiles) *n_tiles = static_cast<uint64_t>(g->v.NT);
+    if (grid_blocks) *grid_blocks = g->grid;
+    if (block_threads) *block_threads = kStageThreads;
+    return OSP_OK;
+}
+
+}  // extern "C"

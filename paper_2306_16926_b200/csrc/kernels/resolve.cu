@@ -1,0 +1,424 @@
+// Resolution of an iteration on the device (OspServer::check_resolution,
+// protocol.cpp:384-439): per-layer PGP (importance.cpp:11-28) -> rank
+// (importance.cpp:30-40) -> prefix-rule GIB (importance.cpp:42-59) -> the
+// rank-ordered ICS list, its byte-balanced chunk map (split_for_sync,
+// protocol.cpp:122-166) and the tile lists the next iteration's stage-2
+// kernels walk. One CTA; L <= kMaxLayers.
+//
+// Bit-exact ranking from a parallel sum (SURVEY.md §7 hard part 1). The
+// reference sums |g*p| sequentially in double; a parallel tree rounds
+// differently. Every term is exact in double and non-negative, so
+//   CPU:  |c - s| <= gamma(n-1) * s        (n = layer elements)
+//   GPU:  |s^ - s| <= gamma(D) * s          (D = adds on any term's path)
+// and c lies in [s^ - E, s^ + E] with E = s^ * u * (1.01 * (n - 1 + D) + 8)
+// (u = 2^-53; the slack absorbs gamma's second-order term and the rounding of
+// the interval ends). Layers whose interval touches another layer's interval
+// are "marked"; a second kernel recomputes their scores in the reference's
+// exact sequential order; the ranking is then redone with exact keys for the
+// marked layers. Unmarked intervals are disjoint from every other interval, so
+// the resulting order equals the reference's stable (score, id) order.
+// Exact zeros (s^ == 0 <=> every term is 0) are exact and never marked.
+
+#include "common.cuh"
+
+namespace osp {
+
+namespace {
+
+constexpr double kU = 1.1102230246251565404e-16;  // 2^-53
+
+// Depth of the stage kernels' per-tile reduction (stage.cu): per-thread
+// sequential terms (<= T/B + 8 with head/tail), 5 shuffle levels, then the
+// warps summed in order.
+__device__ __forceinline__ double tile_depth(int T) {
+    return static_cast<double>(T / kStageThreads + 8 + 5 + kStageThreads / 32);
+}
+
+struct Smem {
+    double* key;
+    double* rad;
+    double* a1;
+    double* a2;
+    int* sorted;
+    int* pos;
+    int* i1;
+    int* i2;
+    double* tmp;  // [kResolveThreads]
+    int* flag;    // [4]
+};
+
+__device__ Smem carve(char* base, int L) {
+    Smem s;
+    s.key = reinterpret_cast<double*>(base);
+    s.rad = s.key + L;
+    s.a1 = s.rad + L;
+    s.a2 = s.a1 + L;
+    s.tmp = s.a2 + L;
+    s.sorted = reinterpret_cast<int*>(s.tmp + kResolveThreads);
+    s.pos = s.sorted + L;
+    s.i1 = s.pos + L;
+    s.i2 = s.i1 + L;
+    s.flag = s.i2 + L;
+    return s;
+}
+
+size_t smem_bytes(int L) {
+    return static_cast<size_t>(L) * (4 * sizeof(double) + 4 * sizeof(int)) +
+           kResolveThreads * sizeof(double) + 4 * sizeof(int);
+}
+
+// Block-wide inclusive scan of a[0..n) in shared memory (commutative op).
+template <typename T, typename Op>
+__device__ void block_scan(T* a, int n, T ident, Op op, T* tmp) {
+    const int tid = threadIdx.x, B = blockDim.x;
+    const int per = (n + B - 1) / B;
+    const int b = min(n, tid * per), e = min(n, b + per);
+    T run = ident;
+    for (int i = b; i < e; ++i) {
+        run = op(run, a[i]);
+        a[i] = run;
+    }
+    tmp[tid] = run;
+    __syncthreads();
+    for (int o = 1; o < B; o <<= 1) {
+        T v = tid >= o ? tmp[tid - o] : ident;
+        __syncthreads();
+        tmp[tid] = op(tmp[tid], v);
+        __syncthreads();
+    }
+    const T pre = tid > 0 ? tmp[tid - 1] : ident;
+    for (int i = b; i < e; ++i) a[i] = op(pre, a[i]);
+    __syncthreads();
+}
+
+// Rank by (key, id): the reference's stable_sort by score with id tie-break.
+__device__ void rank_layers_block(const Smem& s, int L) {
+    for (int l = threadIdx.x; l < L; l += blockDim.x) {
+        const double kl = s.key[l];
+        int r = 0;
+        for (int j = 0; j < L; ++j) {
+            const double kj = s.key[j];
+            r += (kj < kl) || (kj == kl && j < l);
+        }
+        s.pos[l] = r;
+        s.sorted[r] = l;
+    }
+    __syncthreads();
+}
+
+// Given the ICS list ord[0..k) (rank order) and the inclusive byte prefix over
+// it in a1 (uint64 bit patterns), write flags, ICS list, compacted chunk map,
+// tile prefix, meta and the encoded GIB. Mirrors split_for_sync's chunking
+// (protocol.cpp:145-164): idx = min(n-1, cum*n/total) in u64, empty chunks dropped.
+__device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord, int k,
+                               uint32_t tag) {
+    const int tid = threadIdx.x, B = blockDim.x, L = g.L;
+    uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
+    const uint64_t total = k > 0 ? pre[k - 1] : 0;
+    const uint64_t nc = static_cast<uint64_t>(g.n_chunks);
+    // raw chunk index (i1) and chunk-start marks (i2, scanned to compacted ids)
+    for (int r = tid; r < k; r += B) {
+        const uint64_t bytes = g.counts[ord[r]] * static_cast<uint64_t>(g.bpe);
+        const uint64_t cum = pre[r] - bytes;
+        uint64_t idx = total == 0 ? 0 : (cum * nc) / total;
+        if (idx > nc - 1) idx = nc - 1;
+        s.i1[r] = static_cast<int>(idx);
+    }
+    for (int l = tid; l < L; l += B) {
+        g.flags[l] = 0;
+        g.chunk_of[l] = -1;
+    }
+    __syncthreads();
+    for (int r = tid; r < k; r += B) s.i2[r] = (r == 0 || s.i1[r] != s.i1[r - 1]) ? 1 : 0;
+    __syncthreads();
+    block_scan<int>(s.i2, k, 0, [](int a, int b) { return a + b; }, reinterpret_cast<int*>(s.tmp));
+    const int n_used = k > 0 ? s.i2[k - 1] : 0;
+    for (int r = tid; r < k; r += B) {
+        const int l = ord[r];
+        const int c = s.i2[r] - 1;
+        g.flags[l] = 1;
+        g.chunk_of[l] = c;
+        g.ics_layers[r] = l;
+        if (r == 0 || s.i2[r] != s.i2[r - 1]) g.chunk_begin[c] = r;
+    }
+    __syncthreads();
+    for (int r = tid; r < k; r += B) {
+        const int l = ord[r];
+        s.i1[r] = g.tile_base[l + 1] - g.tile_base[l];  // tiles of the layer
+    }
+    __syncthreads();
+    block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, reinterpret_cast<int*>(s.tmp));
+    for (int r = tid; r <= k; r += B) g.ics_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
+    if (tid == 0) {
+        g.chunk_begin[n_used] = k;
+        g.meta[META_N_ICS] = k;
+        g.meta[META_N_USED] = n_used;
+        g.meta64[META64_DEFERRED] = total;
+        g.meta64[META64_TAG] = tag;
+        if (g.hist) g.hist[tag % kHist] = total;
+        g.gib_bytes[0] = tag & 0xff;
+        g.gib_bytes[1] = (tag >> 8) & 0xff;
+        g.gib_bytes[2] = (tag >> 16) & 0xff;
+        g.gib_bytes[3] = (tag >> 24) & 0xff;
+        const uint32_t ul = static_cast<uint32_t>(L);
+        g.gib_bytes[4] = ul & 0xff;
+        g.gib_bytes[5] = (ul >> 8) & 0xff;
+        g.gib_bytes[6] = (ul >> 16) & 0xff;
+        g.gib_bytes[7] = (ul >> 24) & 0xff;
+    }
+    __syncthreads();
+    for (int byte = tid; byte < (L + 7) / 8; byte += B) {
+        uint8_t v = 0;
+        for (int b = 0; b < 8; ++b) {
+            const int l = byte * 8 + b;
+            if (l < L && g.flags[l]) v |= static_cast<uint8_t>(1u << b);
+        }
+        g.gib_bytes[8 + byte] = v;
+    }
+}
+
+__global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, int pass) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int L = g.L;
+    const Smem s = carve(smem_raw, L);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    if (pass == 2 && g.meta[META_NEED_FB] == 0) return;
+
+    if (pass == 1) {
+        // per-layer tree sum of the tile partials: lanes stride, fixed shuffle tree
+        for (int l = warp; l < L; l += nwarp) {
+            const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
+            double acc = 0.0;
+            for (int t = t0 + lane; t < t1; t += 32) acc = __dadd_rn(acc, g.partials[t]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+            if (lane == 0) {
+                const int nt = t1 - t0;
+                const double D = tile_depth(g.T) + (nt + 31) / 32 + 5 + 2;
+                const double n = static_cast<double>(g.counts[l]);
+                s.key[l] = acc;
+                s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
+                g.scores[l] = acc;
+            }
+        }
+    } else {
+        for (int l = tid; l < L; l += blockDim.x) {
+            if (g.marked[l]) {
+                s.key[l] = g.exact[l];
+                s.rad[l] = 0.0;
+            } else {
+                s.key[l] = g.scores[l];
+                s.rad[l] = 1.0;  // unused
+            }
+        }
+    }
+    __syncthreads();
+    rank_layers_block(s, L);
+
+    if (pass == 1) {
+        // certificate: interval overlap between any two layers -> mark both
+        for (int r = tid; r < L; r += blockDim.x) {
+            const int l = s.sorted[r];
+            s.a1[r] = s.key[l] + s.rad[l];                  // hi, prefix max
+            s.a2[L - 1 - r] = s.key[l] - s.rad[l];          // lo, reversed for suffix min
+        }
+        if (tid == 0) s.flag[0] = 0;
+        __syncthreads();
+        block_scan<double>(s.a1, L, -1.0, [](double a, double b) { return a > b ? a : b; }, s.tmp);
+        block_scan<double>(s.a2, L, 1e308, [](double a, double b) { return a < b ? a : b; }, s.tmp);
+        for (int r = tid; r < L; r += blockDim.x) {
+            const int l = s.sorted[r];
+            const double k = s.key[l], rd = s.rad[l];
+            const double hi = k + rd, lo = k - rd;
+            const double premax = r > 0 ? s.a1[r - 1] : -1.0;
+            const double sufmin = r < L - 1 ? s.a2[L - 2 - r] : 1e308;
+            const bool exact_zero = (k == 0.0);
+            const bool m = !exact_zero && (hi >= sufmin || lo <= premax);
+            g.marked[l] = m ? 1 : 0;
+            if (m) atomicAdd(&s.flag[0], 1);
+        }
+        __syncthreads();
+        if (s.flag[0] > 0) {
+            if (tid == 0) {
+                g.meta[META_NEED_FB] = 1;
+                g.meta64[META64_FB_LAYERS] += static_cast<uint64_t>(s.flag[0]);
+                g.meta64[META64_FB_RESOLVES] += 1;
+            }
+            return;
+        }
+        if (tid == 0) g.meta[META_NEED_FB] = 0;
+    }
+
+    // prefix rule: inclusive byte scan in rank order, k = #prefix <= budget
+    uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
+    for (int r = tid; r < L; r += blockDim.x)
+        pre[r] = g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
+    __syncthreads();
+    block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; },
+                         reinterpret_cast<uint64_t*>(s.tmp));
+    const uint64_t budget = g.meta64[META64_BUDGET];
+    if (tid == 0) s.flag[1] = 0;
+    __syncthreads();
+    int cnt = 0;
+    for (int r = tid; r < L; r += blockDim.x) cnt += pre[r] <= budget ? 1 : 0;
+    if (cnt) atomicAdd(&s.flag[1], cnt);
+    __syncthreads();
+    const int k = s.flag[1];
+    const uint32_t tag = static_cast<uint32_t>(g.meta64[META64_RESOLVED] + 1);
+    __syncthreads();
+    if (tid == 0) g.meta64[META64_RESOLVED] += 1;
+    finalize_lists(g, s, s.sorted, k, tag);
+}
+
+// Exact sequential PGP for marked layers (importance.cpp:20-25 order), with the
+// aggregated delta recomputed from the worker deltas exactly as the stages did.
+__global__ void k_fallback(GroupView g, AggParams ap, const float* __restrict__ X, uint64_t ldX) {
+    if (g.meta[META_NEED_FB] == 0) return;
+    const int l = blockIdx.x;
+    if (!g.marked[l]) return;
+    const int lane = threadIdx.x;
+    const uint64_t off = g.offsets[l], end = off + g.counts[l];
+    double sum = 0.0;
+    for (uint64_t b = off; b < end; b += 32) {
+        const uint64_t f = b + lane;
+        double t = 0.0;
+        if (f < end) {
+            double a = 0.0;
+            for (int w = 0; w < ap.n; ++w) {
+                float x = X[static_cast<uint64_t>(w) * ldX + f];
+                if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                a = agg_acc(a, ap.w[w], x);
+            }
+            t = pgp_term(agg_finish(ap, a), g.G[f]);
+        }
+        const int valid = static_cast<int>((end - b) < 32 ? (end - b) : 32);
+        for (int i = 0; i < valid; ++i) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, t, i));
+    }
+    if (lane == 0) g.exact[l] = sum;
+}
+
+// Install a host-provided GIB: g.flags already written; order (device) is the
+// rank list. Deferred order = order filtered by the bitmap, then missing
+// flagged ids ascending (split_for_sync, protocol.cpp:133-142).
+__global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const int* order,
+                                                             int n_order, uint32_t tag) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int L = g.L;
+    const Smem s = carve(smem_raw, L);
+    if (threadIdx.x == 0) {
+        int k = 0;
+        for (int l = 0; l < L; ++l) s.pos[l] = 0;  // seen
+        for (int i = 0; i < n_order; ++i) {
+            const int id = order[i];
+            if (id >= 0 && id < L && g.flags[id] && !s.pos[id]) {
+                s.sorted[k++] = id;
+                s.pos[id] = 1;
+            }
+        }
+        for (int l = 0; l < L; ++l)
+            if (g.flags[l] && !s.pos[l]) s.sorted[k++] = l;
+        s.flag[1] = k;
+        uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
+        uint64_t run = 0;
+        for (int r = 0; r < k; ++r) {
+            run += g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
+            pre[r] = run;
+        }
+        g.meta64[META64_RESOLVED] = tag;
+        g.meta[META_NEED_FB] = 0;
+    }
+    __syncthreads();
+    finalize_lists(g, s, s.sorted, s.flag[1], tag);
+}
+
+__global__ void k_set_budget(uint64_t* meta64, uint64_t budget) { meta64[META64_BUDGET] = budget; }
+
+// Per-function API: exact sequential PGP of (params, grads) per layer.
+__global__ void k_pgp_exact(const float* __restrict__ P, const float* __restrict__ Gr,
+                            const uint64_t* offsets, const uint64_t* counts, double* scores) {
+    const int l = blockIdx.x;
+    const int lane = threadIdx.x;
+    const uint64_t off = offsets[l], end = off + counts[l];
+    double sum = 0.0;
+    for (uint64_t b = off; b < end; b += 32) {
+        const uint64_t f = b + lane;
+        const double t = f < end ? pgp_term(Gr[f], P[f]) : 0.0;
+        const int valid = static_cast<int>((end - b) < 32 ? (end - b) : 32);
+        for (int i = 0; i < valid; ++i) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, t, i));
+    }
+    if (lane == 0) scores[l] = sum;
+}
+
+// Per-function API: rank + prefix-rule GIB of given scores.
+__global__ void __launch_bounds__(kResolveThreads) k_rank_gib(const double* scores,
+                                                              const uint64_t* counts, uint32_t bpe,
+                                                              int L, uint64_t budget, int* order,
+                                                              uint8_t* flags) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const Smem s = carve(smem_raw, L);
+    for (int l = threadIdx.x; l < L; l += blockDim.x) s.key[l] = scores[l];
+    __syncthreads();
+    rank_layers_block(s, L);
+    uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
+    for (int r = threadIdx.x; r < L; r += blockDim.x) pre[r] = counts[s.sorted[r]] * uint64_t(bpe);
+    __syncthreads();
+    block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; },
+                         reinterpret_cast<uint64_t*>(s.tmp));
+    for (int r = threadIdx.x; r < L; r += blockDim.x) {
+        order[r] = s.sorted[r];
+        flags[s.sorted[r]] = pre[r] <= budget ? 1 : 0;
+    }
+}
+
+cudaError_t set_smem(const void* fn, size_t bytes) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(bytes));
+}
+
+}  // namespace
+
+cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
+                           cudaStream_t st) {
+    const size_t sm = smem_bytes(g.L);
+    cudaError_t e = set_smem(reinterpret_cast<const void*>(k_resolve), sm);
+    if (e != cudaSuccess) return e;
+    k_resolve<<<1, kResolveThreads, sm, st>>>(g, 1);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_fallback<<<g.L, 32, 0, st>>>(g, ap, X, ldX);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    k_resolve<<<1, kResolveThreads, sm, st>>>(g, 2);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,
+                               cudaStream_t st) {
+    const size_t sm = smem_bytes(g.L);
+    cudaError_t e = set_smem(reinterpret_cast<const void*>(k_install), sm);
+    if (e != cudaSuccess) return e;
+    k_install<<<1, kResolveThreads, sm, st>>>(g, order, n_order, tag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t st) {
+    k_set_budget<<<1, 1, 0, st>>>(g.meta64, budget);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pgp_exact(const float* params, const float* grads, const uint64_t* offsets,
+                             const uint64_t* counts, int L, double* scores, cudaStream_t st) {
+    if (L < 1) return cudaSuccess;
+    k_pgp_exact<<<L, 32, 0, st>>>(params, grads, offsets, counts, scores);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_rank_gib(const double* scores, const uint64_t* counts, uint32_t bpe, int L,
+                            uint64_t budget, int* order, uint8_t* flags, cudaStream_t st) {
+    if (L < 1) return cudaSuccess;
+    const size_t sm = smem_bytes(L);
+    cudaError_t e = set_smem(reinterpret_cast<const void*>(k_rank_gib), sm);
+    if (e != cudaSuccess) return e;
+    k_rank_gib<<<1, kResolveThreads, sm, st>>>(scores, counts, bpe, L, budget, order, flags);
+    return cudaGetLastError();
+}
+
+}  // namespace osp

@@ -1,0 +1,125 @@
+// Internal declarations shared by the kernels and the C-ABI layer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "osp_c.h"
+
+namespace osp {
+
+// ---- error plumbing (C-ABI never throws) -----------------------------------
+void set_error(const std::string& msg);
+osp_status fail(osp_status s, const std::string& msg);
+osp_status cuda_fail(cudaError_t e, const char* what);
+
+#define OSP_CUDA(call)                                            \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) return ::osp::cuda_fail(e_, #call); \
+    } while (0)
+
+#define OSP_CHECK_LAUNCH(what)                                    \
+    do {                                                          \
+        cudaError_t e_ = cudaGetLastError();                      \
+        if (e_ != cudaSuccess) return ::osp::cuda_fail(e_, what); \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// ---- aggregation parameters (kernel argument, by value) ---------------------
+struct AggParams {
+    int n;                       // workers
+    int divide;                  // 0 when sum(weights) == 1.0 exactly (x / 1.0 == x)
+    int sgd;                     // inputs are gradients: x = float(-lr * (double)g)
+    double neg_lr;
+    double total;                // sum of weights, ascending (protocol.cpp:14-15)
+    double w[OSP_MAX_WORKERS];
+};
+
+AggParams make_agg_params(int n, const double* weights, double sgd_lr);
+
+// ---- group device view (kernel argument, by value) ---------------------------
+struct GroupView {
+    int L;                       // layers
+    int T;                       // tile elements (power of two)
+    int NT;                      // total tiles
+    int n_chunks;                // chunk slots
+    uint32_t bpe;
+    const uint64_t* offsets;     // [L]
+    const uint64_t* counts;      // [L]
+    const int* tile_base;        // [L+1] first global tile of each layer
+    const int* tile_layer;       // [NT]
+    float* G;                    // [M]
+    float* P;                    // [N][ldP]
+    uint64_t ldP;
+    double* partials;            // [NT] per-tile PGP partial sums
+    uint8_t* flags;              // [L] current GIB (1 = ICS)
+    int* ics_layers;             // [L] ICS layers, rank order (valid prefix n_ics)
+    int* chunk_begin;            // [n_chunks+1] into ics_layers, compacted chunks
+    int* ics_tile_prefix;        // [L+1] exclusive tile prefix along ics_layers
+    int* meta;                   // [8] n_ics, n_used_chunks, need_fallback, ...
+    uint64_t* meta64;            // [8] budget, tag, deferred_bytes, resolved, fb_layers, fb_resolves
+    double* scores;              // [L] approximate (tree) scores
+    double* exact;               // [L] exact sequential scores (fallback layers)
+    uint8_t* marked;             // [L] needs exact score
+    int* chunk_of;               // [L] compacted chunk or -1
+    uint8_t* gib_bytes;          // [8 + ceil(L/8)] encoded current GIB
+    uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
+};
+
+enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2 };
+enum Meta64Idx {
+    META64_BUDGET = 0,
+    META64_TAG = 1,
+    META64_DEFERRED = 2,
+    META64_RESOLVED = 3,
+    META64_FB_LAYERS = 4,
+    META64_FB_RESOLVES = 5
+};
+
+constexpr int kHist = 1024;
+constexpr int kMaxLayers = 4096;  // single-CTA resolve (resolve.cu)
+constexpr int kStageThreads = 256;
+constexpr int kResolveThreads = 1024;
+
+// ---- launchers (kernels/*.cu) ----------------------------------------------
+cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
+                          int grid, cudaStream_t s);
+cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
+                          int chunk, int grid, cudaStream_t s);
+cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
+                           cudaStream_t s);
+cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t s);
+// Rebuild device lists from g.flags + the given rank-ordered ICS ids (device).
+cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,
+                               cudaStream_t s);
+int stage_blocks_per_sm(int n_workers);
+
+cudaError_t launch_aggregate_layer(const float* const* contribs, const AggParams& ap, uint64_t n,
+                                   float* out, cudaStream_t s);
+cudaError_t launch_aggregate_apply_segments(const float* const* contribs, const AggParams& ap,
+                                            const uint64_t* seg_off, const uint64_t* seg_cnt,
+                                            int n_seg, float* global, float* agg_out,
+                                            cudaStream_t s);
+cudaError_t launch_apply_delta(float* p, const float* d, uint64_t n, float scale, cudaStream_t s);
+cudaError_t launch_sgd_delta(const float* g, uint64_t n, double lr, float* out, cudaStream_t s);
+cudaError_t launch_synth(uint64_t seed, int n_workers, uint64_t iteration, uint64_t first,
+                         uint64_t n, float* out, uint64_t ld, uint64_t worker0, cudaStream_t s);
+cudaError_t launch_lgp_partial_segments(float* p, const float* global_delta,
+                                        const float* local_delta, float* base,
+                                        const uint64_t* seg_off, const uint64_t* seg_cnt,
+                                        const uint8_t* seg_local, int n_seg, cudaStream_t s);
+cudaError_t launch_lgp_correct_segments(float* p, const float* base, const float* global_delta,
+                                        const uint64_t* seg_off, const uint64_t* seg_cnt,
+                                        int n_seg, cudaStream_t s);
+cudaError_t launch_pgp_exact(const float* params, const float* grads, const uint64_t* offsets,
+                             const uint64_t* counts, int L, double* scores, cudaStream_t s);
+cudaError_t launch_rank_gib(const double* scores, const uint64_t* counts, uint32_t bpe, int L,
+                            uint64_t budget, int* order, uint8_t* flags, cudaStream_t s);
+
+}  // namespace osp

@@ -1,0 +1,72 @@
+"""CPU-side checks of the drop-in boundary: the in-tree C-ABI library loads and
+exports every function include/osp_c.h declares (no compute without a GPU)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "osp_c.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = set(re.findall(r"\b(osp_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
+
+
+def test_header_declares_functions():
+    names = declared_functions()
+    assert "osp_group_step" in names and "osp_aggregate_layer" in names
+    assert len(names) >= 40
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2306_16926_b200 import _capi
+    assert os.path.exists(_capi.LIB_PATH), "run `make lib` first"
+    lib = ctypes.CDLL(_capi.LIB_PATH)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_covers_header():
+    from paper_2306_16926_b200 import _capi
+    assert set(declared_functions()) == set(_capi.EXPORTED)
+
+
+def test_host_only_entry_points_without_gpu():
+    """GIB codec and tuning are host logic; they run without a device."""
+    from paper_2306_16926_b200 import _capi
+    lib = _capi.load()
+    assert lib.osp_abi_version() == 1
+    assert lib.osp_gib_encoded_size(1000) == 133
+    assert lib.osp_status_name(7) == b"ProtocolError"
+    out = ctypes.c_uint64()
+    assert lib.osp_compute_umax(1.25e9, 0.0, 0.0, 0.1, 8, 100_000_000, 0, ctypes.byref(out)) == 0
+    assert out.value == 15_625_000
+
+
+def test_python_front_errors_without_gpu():
+    pytest.importorskip("torch")
+    from paper_2306_16926_b200 import osp
+    assert osp.gib_encode(42, [1] * 1000)[:4] == bytes([42, 0, 0, 0])
+    tag, flags = osp.gib_decode(osp.gib_encode(7, [1, 0, 0, 1, 0, 0, 0, 0]))
+    assert tag == 7 and list(flags) == [1, 0, 0, 1, 0, 0, 0, 0]
+    with pytest.raises(osp.FormatError):
+        osp.gib_decode(bytes([1, 2, 3]))
+    s = osp.SguSchedule(1000)
+    assert s.tune(1, 1.0) == 0
+    assert s.tune(7, 0.25) == 750
+    with pytest.raises(osp.ProtocolError):
+        osp.SguSchedule(10).tune(2, 0.5)
+    with pytest.raises(osp.ConfigError):
+        osp.SguSchedule(10).tune(0, 0.5)
+    with pytest.raises(osp.NumericError):
+        osp.SguSchedule(10).tune(1, -0.5)
+    assert osp.compute_umax(1.25e9, 0.1, 8, 1_000_000_000, loss_rate=0.25) == 12_500_000
+    assert osp.compute_umax(1.25e9, 0.1, 8, 1_000_000_000, loss_rate=0.25,
+                            eq5_literal=True) == 19_531_250
+    with pytest.raises(osp.ConfigError):
+        osp.compute_umax(-1.0, 0.1, 8, 100)

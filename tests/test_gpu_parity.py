@@ -1,0 +1,375 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference-engine goldens. Bit-exact for everything: masks, index lists, chunk
+maps, GIB bytes, aggregated/updated fp32 vectors. The only non-bit-exact
+quantity is the group's per-layer PGP score (a parallel tree sum, documented
+tolerance 1e-12 relative; the ranking built from it is certified exact)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle
+from osp_testlib import Golden
+
+pytestmark = pytest.mark.gpu
+
+SCORE_RTOL = 1e-12  # tree vs sequential fp64 sum of non-negative terms
+
+
+def bits(a):
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+@pytest.fixture(scope="module")
+def osp():
+    from paper_2306_16926_b200 import osp as m
+    m.lib()
+    return m
+
+
+def cuda(x):
+    return torch.as_tensor(np.ascontiguousarray(x), device="cuda")
+
+
+# ---- per-function primitives -------------------------------------------------
+
+def test_aggregate_hand_vectors(osp):
+    # test_protocol.cpp:21-40
+    a, b = cuda(np.float32([1, 3])), cuda(np.float32([3, 5]))
+    assert osp.aggregate_layer([a, b], [1.0, 1.0]).tolist() == [2, 4]
+    assert osp.aggregate_layer([a, b], [1.0, 3.0]).tolist() == [2.5, 4.5]
+    assert osp.aggregate_layer([a], [0.7]).tolist() == [1, 3]
+    with pytest.raises(osp.ProtocolError):
+        osp.aggregate_layer([a, cuda(np.float32([0, 0, 0]))], [1.0, 1.0])
+    with pytest.raises(osp.ProtocolError):
+        osp.aggregate_layer([a, b], [0.0, 0.0])
+
+
+def test_aggregate_random_bit_exact(osp):
+    # checks.cpp:220-264 (aggregation oracle): random weights and sizes
+    rng = np.random.default_rng(4242)
+    for _ in range(20):
+        n = int(rng.integers(1, 9))
+        size = int(rng.integers(1, 5000))
+        w = list(0.1 + rng.random(n))
+        xs = [rng.uniform(-2, 2, size).astype(np.float32) for _ in range(n)]
+        got = osp.aggregate_layer([cuda(x) for x in xs], w)
+        want = oracle.aggregate_layer(xs, w)
+        assert np.array_equal(bits(got), bits(want))
+
+
+def test_synth_delta_matches_reference_stream(osp, golden):
+    d = golden.get(0, "deltas")
+    if d is None:
+        pytest.skip("fixture without stored deltas")
+    got = osp.synth_deltas(golden.seed, golden.N, 0, golden.M)
+    assert np.array_equal(bits(got), bits(d))
+    win = osp.synth_delta(golden.seed, golden.N - 1, 0, 7, first=2) if golden.M > 9 else None
+    if win is not None:
+        assert np.array_equal(bits(win), bits(d[-1][2:9]))
+
+
+def test_synth_large_vs_oracle(osp):
+    n = 3_000_001
+    got = osp.synth_deltas(11, 3, 5, n)
+    for w in range(3):
+        assert np.array_equal(bits(got[w]), bits(oracle.synth_delta(11, w, 5, n)))
+
+
+def test_apply_and_sgd(osp):
+    # test_param.cpp:94-107, test_learner.cpp:203-218
+    p = cuda(np.float32([1, 1]))
+    d = cuda(np.float32([0.5, -0.5]))
+    osp.apply_delta(p, d, 1.0)
+    assert p.tolist() == [1.5, 0.5]
+    osp.apply_delta(p, d, 0.0)
+    assert p.tolist() == [1.5, 0.5]
+    with pytest.raises(osp.ShapeError):
+        osp.apply_delta(p, cuda(np.float32([1, 2, 3])), 1.0)
+    g = np.random.default_rng(1).normal(size=100_003).astype(np.float32)
+    assert np.array_equal(bits(osp.sgd_delta(cuda(g), 0.05)), bits(oracle.sgd_delta(g, 0.05)))
+    with pytest.raises(osp.ConfigError):
+        osp.sgd_delta(cuda(g), 0.0)
+
+
+def test_lgp_hand_vectors(osp):
+    # test_protocol.cpp:81-142
+    part = osp.Partition([2, 2])
+    p = cuda(np.float32([1, 1, 1, 1]))
+    gd = cuda(np.float32([0.1, -0.2, 0, 0]))
+    ld = cuda(np.float32([0, 0, 0.05, 0.05]))
+    base = torch.zeros(4, device="cuda")
+    osp.lgp_partial(part, p, gd, ld, [0, 1], base)
+    v = p.tolist()
+    assert v[0] == pytest.approx(1.1) and v[1] == pytest.approx(0.8)
+    assert v[2] == pytest.approx(1.05) and v[3] == pytest.approx(1.05)
+    osp.lgp_correct(part, p, base, cuda(np.float32([0, 0, 0.02, -0.01])), [1])
+    v = p.tolist()
+    assert v[2] == pytest.approx(1.02) and v[3] == pytest.approx(0.99)
+    # correcting with the local delta is an exact no-op (test_protocol.cpp:126-135)
+    part1 = osp.Partition([2])
+    q = cuda(np.float32([1, 1]))
+    loc = cuda(np.float32([0.3, -0.7]))
+    b1 = torch.zeros(2, device="cuda")
+    osp.lgp_partial(part1, q, torch.zeros(2, device="cuda"), loc, [1], b1)
+    before = q.clone()
+    osp.lgp_correct(part1, q, b1, loc, [0])
+    assert np.array_equal(bits(q), bits(before))
+    with pytest.raises(osp.LayerError):
+        osp.lgp_correct(part1, q, b1, loc, [5])
+
+
+def test_pgp_exact_vs_oracle(osp):
+    rng = np.random.default_rng(3)
+    counts = [1, 7, 300, 4096, 33, 100_000]
+    M = sum(counts)
+    p = rng.uniform(-1, 1, M).astype(np.float32)
+    g = rng.uniform(-1e-3, 1e-3, M).astype(np.float32)
+    part = osp.Partition(counts)
+    got = osp.pgp_layer_importance(part, cuda(p), cuda(g))
+    assert np.array_equal(bits(got), bits(oracle.pgp(counts, p, g)))
+    # test_importance.cpp:8-20
+    part2 = osp.Partition([2])
+    s = osp.pgp_layer_importance(part2, cuda(np.float32([1, -2])), cuda(np.float32([0.5, 0.25])))
+    assert s[0] == pytest.approx(1.0)
+
+
+def test_rank_gib_vs_oracle(osp):
+    # test_importance.cpp:39-87
+    part = osp.Partition([10, 15, 12])
+    order, flags = osp.rank_and_gib(part, [5.0, 1.0, 0.2], 100)
+    assert list(order) == [2, 1, 0] and list(flags) == [0, 0, 1]
+    _, flags = osp.rank_and_gib(part, [5.0, 1.0, 0.2], 0)
+    assert list(flags) == [0, 0, 0]
+    _, flags = osp.rank_and_gib(part, [5.0, 1.0, 0.2], part.total_bytes())
+    assert list(flags) == [1, 1, 1]
+    order, _ = osp.rank_and_gib(osp.Partition([1, 1, 1]), [1.0, 1.0, 1.0], 0)
+    assert list(order) == [0, 1, 2]
+    rng = np.random.default_rng(77)
+    for _ in range(30):
+        L = int(rng.integers(1, 600))
+        counts = rng.integers(1, 65, L)
+        scores = rng.uniform(0, 10, L)
+        scores[rng.integers(0, L, L // 4)] = 1.5  # ties
+        budget = int(rng.integers(0, int(counts.sum()) * 4 + 1))
+        part = osp.Partition(counts)
+        order, flags = osp.rank_and_gib(part, scores, budget)
+        assert np.array_equal(order, oracle.rank(scores))
+        assert np.array_equal(flags, oracle.build_gib(scores, counts, 4, budget))
+
+
+def test_split_vs_oracle(osp):
+    # test_protocol.cpp:42-79 and random
+    part = osp.Partition([4, 4, 4, 4])
+    rs, chunk_of, used = osp.split_for_sync(part, [0, 0, 1, 1], [3, 2], 2)
+    assert list(rs) == [0, 1] and used == 2 and chunk_of[3] == 0 and chunk_of[2] == 1
+    rs, chunk_of, used = osp.split_for_sync(osp.Partition([2, 2]), [0, 0], [], 4)
+    assert list(rs) == [0, 1] and used == 0
+    with pytest.raises(osp.ConfigError):
+        osp.split_for_sync(part, [0, 0, 0, 0], [], 0)
+    with pytest.raises(osp.ShapeError):
+        osp.split_for_sync(part, [0, 0], [], 1)
+    rng = np.random.default_rng(9)
+    for _ in range(40):
+        L = int(rng.integers(1, 300))
+        counts = rng.integers(1, 5000, L)
+        flags = (rng.random(L) < 0.5).astype(np.uint8)
+        perm = rng.permutation(L).astype(np.int32)
+        order = perm[: int(rng.integers(0, L + 1))]  # partial rank list: missing ids appended
+        nc = int(rng.integers(1, 9))
+        bpe = int(rng.choice([1, 4, 1000]))
+        p = osp.Partition(counts, bpe)
+        rs, co, used = osp.split_for_sync(p, flags, order, nc)
+        rs_o, co_o, used_o = oracle.split(counts, bpe, flags, order, nc)
+        assert np.array_equal(rs, rs_o) and np.array_equal(co, co_o) and used == used_o
+
+
+# ---- the group step against the reference-engine goldens ----------------------
+
+def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0):
+    part = osp.Partition(g.counts, g.bpe)
+    grp = osp.OspGroup(part, g.N, list(g.weights), n_chunks=g.n_chunks,
+                       init_params=cuda(g.p0), tile_elems=tile_elems)
+    for it in range(g.iters):
+        d = g.deltas(it)
+        X = torch.zeros((g.N, g.M + pad_ld), dtype=torch.float32, device="cuda")
+        X[:, : g.M] = cuda(d)
+        # the GIB this iteration splits with (tag it) must be what the group holds
+        st = grp.read_gib()
+        tag_in, flags_in = oracle.gib_decode(bytes(g.get(it, "gib_in")))
+        assert st["tag"] == tag_in
+        assert np.array_equal(st["flags"], flags_in)
+        assert np.array_equal(st["order"], g.get(it, "order_in"))
+        chunks_ref = Golden.decode_chunks(g.get(it, "chunks"))
+        assert st["n_used"] == len(chunks_ref)
+        for c, ids in enumerate(chunks_ref):
+            assert sorted(np.flatnonzero(st["chunk_of"] == c).tolist()) == ids
+        grp.set_budget(int(g.get(it, "budget")[0]))
+        grp.stage1(X)
+        st1 = g.get(it, "params_stage1")
+        P1 = grp.worker_params.cpu().numpy()
+        if st1 is not None:
+            assert np.array_equal(bits(P1), bits(st1)), f"stage-1 worker params, it {it}"
+        else:
+            assert np.array_equal(bits(P1[0]), bits(g.get(it, "params_stage1_w0")))
+            assert np.array_equal(bits(P1[-1]), bits(g.get(it, "params_stage1_wlast")))
+        for c in range(g.n_chunks):
+            grp.stage2_chunk(c, X)
+        grp.resolve(X)
+        G = grp.global_params.cpu().numpy()
+        assert np.array_equal(bits(G), bits(g.get(it, "global"))), f"global, it {it}"
+        assert int(g.get(it, "final_eq_global")[0]) == 1
+        P = grp.worker_params.cpu().numpy()
+        for w in range(g.N):
+            assert np.array_equal(bits(P[w]), bits(G)), f"worker {w} after corrections"
+        np.testing.assert_allclose(grp.scores.cpu().numpy(), g.get(it, "scores"), rtol=SCORE_RTOL,
+                                   atol=0)
+        nxt = grp.read_gib()
+        tag_out, flags_out = oracle.gib_decode(bytes(g.get(it, "gib_out")))
+        assert nxt["tag"] == tag_out == it + 1
+        assert np.array_equal(nxt["flags"], flags_out), f"GIB flags, it {it}"
+        assert np.array_equal(nxt["order"], g.get(it, "order_out")), f"ICS order, it {it}"
+    return grp
+
+
+def test_group_matches_reference_engine(osp, golden):
+    run_group_against_golden(osp, golden)
+
+
+def test_group_small_tiles_and_unaligned_rows(osp, golden):
+    # multi-tile layers, and rows whose stride breaks 16-byte alignment (scalar path)
+    run_group_against_golden(osp, golden, tile_elems=1024, pad_ld=1)
+
+
+# ---- the group step against the oracle at larger sizes ---------------------------
+
+def oracle_vs_group(osp, counts, N, weights, budget_frac, n_chunks, iters, seed, p0=None,
+                    sgd_lr=0.0, tile_elems=0):
+    counts = np.asarray(counts, dtype=np.uint64)
+    M = int(counts.sum())
+    bpe = 4
+    budget = int(budget_frac * M * bpe)
+    G = np.zeros(M, np.float32) if p0 is None else p0.copy()
+    P = np.tile(G, (N, 1))
+    part = osp.Partition(counts)
+    grp = osp.OspGroup(part, N, weights, n_chunks=n_chunks, init_params=cuda(G),
+                       sgd_lr=sgd_lr, tile_elems=tile_elems)
+    flags = np.zeros(len(counts), np.uint8)
+    order = np.zeros(0, np.int32)
+    X = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    for it in range(iters):
+        osp.synth_deltas(seed, N, it, M, out=X)
+        if sgd_lr > 0:
+            X.mul_(37.0)  # treat as raw gradients
+            deltas = np.stack([oracle.sgd_delta(X[w].cpu().numpy(), sgd_lr) for w in range(N)])
+        else:
+            deltas = X.cpu().numpy()
+        r = oracle.step(counts, bpe, weights, deltas, G, P, flags, order, n_chunks, budget)
+        grp.set_budget(budget)
+        grp.step(X)
+        assert np.array_equal(bits(grp.global_params), bits(G)), f"global, it {it}"
+        Pg = grp.worker_params.cpu().numpy()
+        for w in range(N):
+            assert np.array_equal(bits(Pg[w]), bits(P[w])), f"worker {w}, it {it}"
+        nxt = grp.read_gib()
+        assert np.array_equal(nxt["flags"], r["flags_out"]), f"flags, it {it}"
+        assert np.array_equal(nxt["order"], r["order_out"]), f"order, it {it}"
+        np.testing.assert_allclose(grp.scores.cpu().numpy(), r["scores"], rtol=SCORE_RTOL, atol=0)
+        flags, order = r["flags_out"], r["order_out"]
+    return grp
+
+
+def test_group_resnet50_layout_vs_oracle(osp):
+    from paper_2306_16926_b200 import layouts
+    grp = oracle_vs_group(osp, layouts.resnet50(), 8, [0.125] * 8, 0.5, 4, 3, seed=11)
+    assert grp.stats()["resolved"] == 3
+
+
+def test_group_odd_workers_unequal_weights(osp):
+    rng = np.random.default_rng(5)
+    counts = rng.integers(1, 20000, 57)
+    w = list(0.1 + rng.random(5))
+    p0 = rng.uniform(-1, 1, int(counts.sum())).astype(np.float32)
+    oracle_vs_group(osp, counts, 5, w, 0.6, 3, 4, seed=3, p0=p0, tile_elems=2048)
+
+
+def test_group_fused_sgd(osp):
+    rng = np.random.default_rng(8)
+    counts = rng.integers(1, 9000, 40)
+    oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 4, 3, seed=19, sgd_lr=0.05)
+
+
+def test_group_budget_edges(osp):
+    counts = [4096, 12, 70000, 1, 333, 8192, 5]
+    for frac in (0.0, 1.0, 0.33):
+        oracle_vs_group(osp, counts, 2, [0.5, 0.5], frac, 4, 3, seed=23)
+    oracle_vs_group(osp, counts, 1, [1.0], 0.7, 1, 3, seed=29)
+    oracle_vs_group(osp, counts, 3, [0.2, 0.3, 0.5], 0.9, 9, 3, seed=31)
+
+
+def test_certificate_fallback_on_exact_ties(osp):
+    """Two layers with identical contents tie exactly in the reference (stable
+    order by id); the tree sums cannot certify the order, so the exact
+    sequential fallback must run and reproduce the reference ranking."""
+    half = 50_000
+    counts = [half, half, 1000, half]
+    M = sum(counts)
+    N = 4
+    X = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    osp.synth_deltas(7, N, 0, M, out=X)
+    X[:, half: 2 * half] = X[:, :half]           # layer 1 == layer 0
+    X[:, 2 * half + 1000:] = X[:, :half]         # layer 3 == layer 0
+    part = osp.Partition(counts)
+    grp = osp.OspGroup(part, N, [0.25] * N, n_chunks=2)
+    G = np.zeros(M, np.float32)
+    P = np.zeros((N, M), np.float32)
+    budget = int(0.6 * M * 4)
+    r = oracle.step(counts, 4, [0.25] * N, X.cpu().numpy(), G, P, np.zeros(4, np.uint8),
+                    np.zeros(0, np.int32), 2, budget)
+    assert r["scores"][0] == r["scores"][1] == r["scores"][3]
+    grp.set_budget(budget)
+    grp.step(X)
+    nxt = grp.read_gib()
+    assert np.array_equal(nxt["flags"], r["flags_out"])
+    assert np.array_equal(nxt["order"], r["order_out"])
+    st = grp.stats()
+    assert st["fallback_resolves"] == 1 and st["fallback_layers"] >= 3
+
+
+def test_step_host_matches_device_step(osp):
+    from paper_2306_16926_b200 import layouts
+    counts = layouts.resnet50()[:40]
+    M = sum(counts)
+    N = 8
+    part = osp.Partition(counts)
+    a = osp.OspGroup(part, N, [0.125] * N, n_chunks=4)
+    b = osp.OspGroup(part, N, [0.125] * N, n_chunks=4)
+    for it in range(3):
+        X = osp.synth_deltas(11, N, it, M)
+        host = X.cpu().numpy()
+        a.set_budget(M * 2)
+        b.set_budget(M * 2)
+        a.step(X)
+        gib = b.step_host(host)
+        assert np.array_equal(bits(a.global_params), bits(b.global_params))
+        ra = a.read_gib()
+        assert gib == oracle.gib_encode(ra["tag"], ra["flags"])
+
+
+def test_group_errors(osp):
+    part = osp.Partition([10, 10])
+    with pytest.raises(osp.ConfigError):
+        osp.OspGroup(part, 2, [0.5, 0.5], n_chunks=0)
+    with pytest.raises(osp.ConfigError):
+        osp.OspGroup(part, 2, [0.5, -0.5])
+    grp = osp.OspGroup(part, 2, [0.5, 0.5])
+    with pytest.raises(osp.ShapeError):
+        grp.step(torch.zeros((2, 5), device="cuda"))
+    with pytest.raises(osp.PartitionError):
+        osp.Partition([3, 0])
+    with pytest.raises(osp.PartitionError):
+        osp.Partition([])
+    with pytest.raises(osp.LayerError):
+        part.layer(7)
