@@ -32,7 +32,7 @@ UNIT = "params/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--layout", default="resnet50")
@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--per-chunk", action="store_true", help="one stage-2 launch per ICS chunk")
     ap.add_argument("--cpu-iters", type=int, default=3)
     return ap.parse_args()
 
@@ -212,8 +213,11 @@ def b200_single(args):
         grp.stage1(x)
         if evs is not None:
             evs[1].record(stream)
-        for c in range(args.chunks):
-            grp.stage2_chunk(c, x)
+        if args.per_chunk:
+            for c in range(args.chunks):
+                grp.stage2_chunk(c, x)
+        else:
+            grp.stage2_all(x)
         if evs is not None:
             evs[2].record(stream)
         grp.resolve(x)
@@ -251,7 +255,7 @@ def b200_single(args):
     ach_step = (sum(b_step) / K) / (ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
     stats = grp.stats()
-    launches_per_step = 1 + args.chunks + 3  # stage1, chunk kernels, resolve(pass1, fallback, pass2)
+    launches_per_step = 1 + (args.chunks if args.per_chunk else 1) + 1  # stage1, stage2, resolve
 
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + step + D2H of the GIB
     host = [x.cpu().pin_memory() for x in X]

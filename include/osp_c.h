@@ -191,7 +191,7 @@ typedef struct osp_group_config {
     int n_workers;            /* N, 1..OSP_MAX_WORKERS */
     const double* weights;    /* HOST, N subset weights (OspServer weights) */
     int n_chunks;             /* ICS chunk slots per iteration (>= 1) */
-    uint32_t tile_elems;      /* 0 = default (power of two, >= 1024) */
+    uint32_t tile_elems;      /* elements per warp tile; 0 = default 1024 (power of two, 256..65536) */
     double sgd_lr;            /* 0 = inputs are deltas; > 0 fuse sgd_delta */
 } osp_group_config;
 
@@ -212,8 +212,13 @@ osp_status osp_group_set_gib(osp_group* g, const uint8_t* ics_flags, const int32
 osp_status osp_group_stage1(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, uint64_t ld,
                                   void* stream);
+/* Every ICS chunk of the iteration in ONE launch (identical results to calling
+ * stage2_chunk for c = 0..n_chunks-1 in order: chunks touch disjoint layers).
+ * The single-GPU step uses it; per-chunk launches remain for overlap with
+ * transfers (multi-GPU) and for the reference's message-by-message flow. */
+osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream);
-/* stage1 + every chunk + resolve. */
+/* stage1 + stage2_all + resolve. */
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 /* End-to-end step from HOST (pinned or pageable) deltas: H2D copy of the N rows
  * into the group's staging buffer, the step, and a D2H read of the encoded next

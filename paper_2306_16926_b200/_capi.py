@@ -82,6 +82,7 @@ _SIGS = {
                                   c_void_p]),
     "osp_group_stage1": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_stage2_chunk": (c_int, [c_void_p, c_int, c_void_p, c_u64, c_void_p]),
+    "osp_group_stage2_all": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_resolve": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_step": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_step_host": (c_int, [c_void_p, c_void_p, c_u64, P(ctypes.c_uint8), c_void_p]),

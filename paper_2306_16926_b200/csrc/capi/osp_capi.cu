@@ -602,9 +602,9 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     const uint64_t L = part->counts.size();
     if (L > static_cast<uint64_t>(kMaxLayers))
         return fail(OSP_ERR_INVALID, "more than " + std::to_string(kMaxLayers) + " layers");
-    uint32_t T = cfg->tile_elems ? cfg->tile_elems : 8192u;
-    if (T < 1024 || (T & (T - 1)))
-        return fail(OSP_ERR_INVALID, "tile_elems must be a power of two >= 1024");
+    uint32_t T = cfg->tile_elems ? cfg->tile_elems : kDefaultTile;
+    if (T < 256 || T > 65536 || (T & (T - 1)))
+        return fail(OSP_ERR_INVALID, "tile_elems must be a power of two in [256, 65536]");
 
     auto* g = new (std::nothrow) osp_group();
     if (!g) return fail(OSP_ERR_INVALID, "out of host memory");
@@ -663,6 +663,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &v.gib_bytes, osp_gib_encoded_size(L))) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &g->d_order_tmp, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.hist, kHist)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.sched, 8)) != OSP_OK) return cleanup(st);
 
     cudaStream_t s = as_stream(stream);
     auto cu = [&](cudaError_t e, const char* what) -> osp_status {
@@ -676,9 +677,9 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         return cleanup(st);
     if (init_params) {
         st = cu(cudaMemcpyAsync(v.G, init_params, M * 4, cudaMemcpyDeviceToDevice, s), "init G");
-        if (st == OSP_OK)
-            st = cu(cudaMemcpy2DAsync(v.P, v.ldP * 4, init_params, 0, M * 4, N,
-                                      cudaMemcpyDeviceToDevice, s), "init P");
+        for (int w = 0; w < N && st == OSP_OK; ++w)
+            st = cu(cudaMemcpyAsync(v.P + static_cast<uint64_t>(w) * v.ldP, init_params, M * 4,
+                                    cudaMemcpyDeviceToDevice, s), "init P");
     } else {
         st = cu(cudaMemsetAsync(v.G, 0, M * 4, s), "zero G");
         if (st == OSP_OK) st = cu(cudaMemsetAsync(v.P, 0, v.ldP * N * 4, s), "zero P");
@@ -688,6 +689,9 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.flags, 0, L, s), "flags")) != OSP_OK) return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.marked, 0, L, s), "marked")) != OSP_OK) return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.sched, 0, 8 * sizeof(int), s), "sched")) != OSP_OK)
+        return cleanup(st);
+    if ((st = cu(cudaMemsetAsync(v.hist, 0, kHist * 8, s), "hist")) != OSP_OK) return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.meta, 0, 8 * sizeof(int), s), "meta")) != OSP_OK)
         return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.meta64, 0, 8 * sizeof(uint64_t), s), "meta64")) != OSP_OK)
@@ -745,7 +749,14 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (chunk < 0 || chunk >= g->n_chunks) return fail(OSP_ERR_INVALID, "chunk out of range");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
-    OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, g->grid, as_stream(stream)));
+    OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, chunk + 1, g->grid, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
+    if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, 0, g->n_chunks, g->grid, as_stream(stream)));
     return OSP_OK;
 }
 
@@ -757,7 +768,7 @@ osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, voi
 
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     OSP_TRY(osp_group_stage1(g, deltas, ld, stream));
-    for (int c = 0; c < g->n_chunks; ++c) OSP_TRY(osp_group_stage2_chunk(g, c, deltas, ld, stream));
+    OSP_TRY(osp_group_stage2_all(g, deltas, ld, stream));
     return osp_group_resolve(g, deltas, ld, stream);
 }
 

@@ -3,7 +3,7 @@
 // (importance.cpp:30-40) -> prefix-rule GIB (importance.cpp:42-59) -> the
 // rank-ordered ICS list, its byte-balanced chunk map (split_for_sync,
 // protocol.cpp:122-166) and the tile lists the next iteration's stage-2
-// kernels walk. One CTA; L <= kMaxLayers.
+// kernels walk. One CTA of 1024 threads, one launch; L <= kMaxLayers.
 //
 // Bit-exact ranking from a parallel sum (SURVEY.md §7 hard part 1). The
 // reference sums |g*p| sequentially in double; a parallel tree rounds
@@ -13,26 +13,24 @@
 // and c lies in [s^ - E, s^ + E] with E = s^ * u * (1.01 * (n - 1 + D) + 8)
 // (u = 2^-53; the slack absorbs gamma's second-order term and the rounding of
 // the interval ends). Layers whose interval touches another layer's interval
-// are "marked"; a second kernel recomputes their scores in the reference's
-// exact sequential order; the ranking is then redone with exact keys for the
-// marked layers. Unmarked intervals are disjoint from every other interval, so
-// the resulting order equals the reference's stable (score, id) order.
-// Exact zeros (s^ == 0 <=> every term is 0) are exact and never marked.
+// are "marked"; their scores are recomputed in the reference's exact
+// sequential order (one warp per marked layer, inside this kernel), and the
+// ranking is redone with exact keys for them. Unmarked intervals are disjoint
+// from every other interval, so the resulting order equals the reference's
+// stable (score, id) order. Exact zeros (s^ == 0 <=> every term is 0) are
+// exact and never marked.
 
 #include "common.cuh"
 
 namespace osp {
-
 namespace {
 
 constexpr double kU = 1.1102230246251565404e-16;  // 2^-53
+constexpr int kWarps = kResolveThreads / 32;
 
-// Depth of the stage kernels' per-tile reduction (stage.cu): per-thread
-// sequential terms (<= T/B + 8 with head/tail), 5 shuffle levels, then the
-// warps summed in order.
-__device__ __forceinline__ double tile_depth(int T) {
-    return static_cast<double>(T / kStageThreads + 8 + 5 + kStageThreads / 32);
-}
+// Depth of the stage kernels' per-tile reduction (stage.cu): per-lane
+// sequential terms (<= T/32 + head/tail), then 5 shuffle levels.
+__device__ __forceinline__ double tile_depth(int T) { return static_cast<double>(T / 32 + 8 + 5); }
 
 struct Smem {
     double* key;
@@ -43,8 +41,8 @@ struct Smem {
     int* pos;
     int* i1;
     int* i2;
-    double* tmp;  // [kResolveThreads]
-    int* flag;    // [4]
+    double* wtot;  // [kWarps] scan scratch (8-byte slots)
+    int* flag;     // [8]
 };
 
 __device__ Smem carve(char* base, int L) {
@@ -53,8 +51,8 @@ __device__ Smem carve(char* base, int L) {
     s.rad = s.key + L;
     s.a1 = s.rad + L;
     s.a2 = s.a1 + L;
-    s.tmp = s.a2 + L;
-    s.sorted = reinterpret_cast<int*>(s.tmp + kResolveThreads);
+    s.wtot = s.a2 + L;
+    s.sorted = reinterpret_cast<int*>(s.wtot + kWarps);
     s.pos = s.sorted + L;
     s.i1 = s.pos + L;
     s.i2 = s.i1 + L;
@@ -64,30 +62,45 @@ __device__ Smem carve(char* base, int L) {
 
 size_t smem_bytes(int L) {
     return static_cast<size_t>(L) * (4 * sizeof(double) + 4 * sizeof(int)) +
-           kResolveThreads * sizeof(double) + 4 * sizeof(int);
+           kWarps * sizeof(double) + 8 * sizeof(int);
 }
 
-// Block-wide inclusive scan of a[0..n) in shared memory (commutative op).
+// Block-wide inclusive scan of a[0..n) in shared memory (associative,
+// commutative op): per-thread contiguous segment, warp shuffle scan of the
+// segment totals, one warp over the warp totals. Three barriers.
 template <typename T, typename Op>
-__device__ void block_scan(T* a, int n, T ident, Op op, T* tmp) {
-    const int tid = threadIdx.x, B = blockDim.x;
-    const int per = (n + B - 1) / B;
+__device__ void block_scan(T* a, int n, T ident, Op op, double* wtot_raw) {
+    T* wtot = reinterpret_cast<T*>(wtot_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
     const int b = min(n, tid * per), e = min(n, b + per);
     T run = ident;
-    for (int i = b; i < e; ++i) {
-        run = op(run, a[i]);
-        a[i] = run;
+    for (int i = b; i < e; ++i) run = op(run, a[i]);
+    T incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = op(v, incl);
     }
-    tmp[tid] = run;
+    if (lane == 31) wtot[warp] = incl;
     __syncthreads();
-    for (int o = 1; o < B; o <<= 1) {
-        T v = tid >= o ? tmp[tid - o] : ident;
-        __syncthreads();
-        tmp[tid] = op(tmp[tid], v);
-        __syncthreads();
+    if (warp == 0) {
+        T w = lane < kWarps ? wtot[lane] : ident;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w = op(v, w);
+        }
+        if (lane < kWarps) wtot[lane] = w;
     }
-    const T pre = tid > 0 ? tmp[tid - 1] : ident;
-    for (int i = b; i < e; ++i) a[i] = op(pre, a[i]);
+    __syncthreads();
+    const T excl_in_warp = __shfl_up_sync(0xffffffffu, incl, 1);
+    T pre = warp > 0 ? wtot[warp - 1] : ident;
+    if (lane > 0) pre = op(pre, excl_in_warp);
+    for (int i = b; i < e; ++i) {
+        pre = op(pre, a[i]);
+        a[i] = pre;
+    }
     __syncthreads();
 }
 
@@ -116,7 +129,6 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
     const uint64_t total = k > 0 ? pre[k - 1] : 0;
     const uint64_t nc = static_cast<uint64_t>(g.n_chunks);
-    // raw chunk index (i1) and chunk-start marks (i2, scanned to compacted ids)
     for (int r = tid; r < k; r += B) {
         const uint64_t bytes = g.counts[ord[r]] * static_cast<uint64_t>(g.bpe);
         const uint64_t cum = pre[r] - bytes;
@@ -131,7 +143,7 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     __syncthreads();
     for (int r = tid; r < k; r += B) s.i2[r] = (r == 0 || s.i1[r] != s.i1[r - 1]) ? 1 : 0;
     __syncthreads();
-    block_scan<int>(s.i2, k, 0, [](int a, int b) { return a + b; }, reinterpret_cast<int*>(s.tmp));
+    block_scan<int>(s.i2, k, 0, [](int a, int b) { return a + b; }, s.wtot);
     const int n_used = k > 0 ? s.i2[k - 1] : 0;
     for (int r = tid; r < k; r += B) {
         const int l = ord[r];
@@ -142,12 +154,9 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         if (r == 0 || s.i2[r] != s.i2[r - 1]) g.chunk_begin[c] = r;
     }
     __syncthreads();
-    for (int r = tid; r < k; r += B) {
-        const int l = ord[r];
-        s.i1[r] = g.tile_base[l + 1] - g.tile_base[l];  // tiles of the layer
-    }
+    for (int r = tid; r < k; r += B) s.i1[r] = g.tile_base[ord[r] + 1] - g.tile_base[ord[r]];
     __syncthreads();
-    block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, reinterpret_cast<int*>(s.tmp));
+    block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, s.wtot);
     for (int r = tid; r <= k; r += B) g.ics_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
     if (tid == 0) {
         g.chunk_begin[n_used] = k;
@@ -156,15 +165,11 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         g.meta64[META64_DEFERRED] = total;
         g.meta64[META64_TAG] = tag;
         if (g.hist) g.hist[tag % kHist] = total;
-        g.gib_bytes[0] = tag & 0xff;
-        g.gib_bytes[1] = (tag >> 8) & 0xff;
-        g.gib_bytes[2] = (tag >> 16) & 0xff;
-        g.gib_bytes[3] = (tag >> 24) & 0xff;
         const uint32_t ul = static_cast<uint32_t>(L);
-        g.gib_bytes[4] = ul & 0xff;
-        g.gib_bytes[5] = (ul >> 8) & 0xff;
-        g.gib_bytes[6] = (ul >> 16) & 0xff;
-        g.gib_bytes[7] = (ul >> 24) & 0xff;
+        for (int i = 0; i < 4; ++i) {
+            g.gib_bytes[i] = (tag >> (8 * i)) & 0xff;
+            g.gib_bytes[4 + i] = (ul >> (8 * i)) & 0xff;
+        }
     }
     __syncthreads();
     for (int byte = tid; byte < (L + 7) / 8; byte += B) {
@@ -177,106 +182,11 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     }
 }
 
-__global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, int pass) {
-    extern __shared__ __align__(16) char smem_raw[];
-    const int L = g.L;
-    const Smem s = carve(smem_raw, L);
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
-    if (pass == 2 && g.meta[META_NEED_FB] == 0) return;
-
-    if (pass == 1) {
-        // per-layer tree sum of the tile partials: lanes stride, fixed shuffle tree
-        for (int l = warp; l < L; l += nwarp) {
-            const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
-            double acc = 0.0;
-            for (int t = t0 + lane; t < t1; t += 32) acc = __dadd_rn(acc, g.partials[t]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
-            if (lane == 0) {
-                const int nt = t1 - t0;
-                const double D = tile_depth(g.T) + (nt + 31) / 32 + 5 + 2;
-                const double n = static_cast<double>(g.counts[l]);
-                s.key[l] = acc;
-                s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
-                g.scores[l] = acc;
-            }
-        }
-    } else {
-        for (int l = tid; l < L; l += blockDim.x) {
-            if (g.marked[l]) {
-                s.key[l] = g.exact[l];
-                s.rad[l] = 0.0;
-            } else {
-                s.key[l] = g.scores[l];
-                s.rad[l] = 1.0;  // unused
-            }
-        }
-    }
-    __syncthreads();
-    rank_layers_block(s, L);
-
-    if (pass == 1) {
-        // certificate: interval overlap between any two layers -> mark both
-        for (int r = tid; r < L; r += blockDim.x) {
-            const int l = s.sorted[r];
-            s.a1[r] = s.key[l] + s.rad[l];                  // hi, prefix max
-            s.a2[L - 1 - r] = s.key[l] - s.rad[l];          // lo, reversed for suffix min
-        }
-        if (tid == 0) s.flag[0] = 0;
-        __syncthreads();
-        block_scan<double>(s.a1, L, -1.0, [](double a, double b) { return a > b ? a : b; }, s.tmp);
-        block_scan<double>(s.a2, L, 1e308, [](double a, double b) { return a < b ? a : b; }, s.tmp);
-        for (int r = tid; r < L; r += blockDim.x) {
-            const int l = s.sorted[r];
-            const double k = s.key[l], rd = s.rad[l];
-            const double hi = k + rd, lo = k - rd;
-            const double premax = r > 0 ? s.a1[r - 1] : -1.0;
-            const double sufmin = r < L - 1 ? s.a2[L - 2 - r] : 1e308;
-            const bool exact_zero = (k == 0.0);
-            const bool m = !exact_zero && (hi >= sufmin || lo <= premax);
-            g.marked[l] = m ? 1 : 0;
-            if (m) atomicAdd(&s.flag[0], 1);
-        }
-        __syncthreads();
-        if (s.flag[0] > 0) {
-            if (tid == 0) {
-                g.meta[META_NEED_FB] = 1;
-                g.meta64[META64_FB_LAYERS] += static_cast<uint64_t>(s.flag[0]);
-                g.meta64[META64_FB_RESOLVES] += 1;
-            }
-            return;
-        }
-        if (tid == 0) g.meta[META_NEED_FB] = 0;
-    }
-
-    // prefix rule: inclusive byte scan in rank order, k = #prefix <= budget
-    uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
-    for (int r = tid; r < L; r += blockDim.x)
-        pre[r] = g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
-    __syncthreads();
-    block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; },
-                         reinterpret_cast<uint64_t*>(s.tmp));
-    const uint64_t budget = g.meta64[META64_BUDGET];
-    if (tid == 0) s.flag[1] = 0;
-    __syncthreads();
-    int cnt = 0;
-    for (int r = tid; r < L; r += blockDim.x) cnt += pre[r] <= budget ? 1 : 0;
-    if (cnt) atomicAdd(&s.flag[1], cnt);
-    __syncthreads();
-    const int k = s.flag[1];
-    const uint32_t tag = static_cast<uint32_t>(g.meta64[META64_RESOLVED] + 1);
-    __syncthreads();
-    if (tid == 0) g.meta64[META64_RESOLVED] += 1;
-    finalize_lists(g, s, s.sorted, k, tag);
-}
-
-// Exact sequential PGP for marked layers (importance.cpp:20-25 order), with the
-// aggregated delta recomputed from the worker deltas exactly as the stages did.
-__global__ void k_fallback(GroupView g, AggParams ap, const float* __restrict__ X, uint64_t ldX) {
-    if (g.meta[META_NEED_FB] == 0) return;
-    const int l = blockIdx.x;
-    if (!g.marked[l]) return;
-    const int lane = threadIdx.x;
+// Exact sequential PGP of one layer (importance.cpp:20-25 order) by one warp,
+// with the aggregated delta recomputed from the worker deltas exactly as the
+// stage kernels computed it, against the post-update global vector.
+__device__ double exact_layer_pgp(const GroupView& g, const AggParams& ap, const float* X,
+                                  uint64_t ldX, int l, int lane) {
     const uint64_t off = g.offsets[l], end = off + g.counts[l];
     double sum = 0.0;
     for (uint64_t b = off; b < end; b += 32) {
@@ -294,7 +204,101 @@ __global__ void k_fallback(GroupView g, AggParams ap, const float* __restrict__ 
         const int valid = static_cast<int>((end - b) < 32 ? (end - b) : 32);
         for (int i = 0; i < valid; ++i) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, t, i));
     }
-    if (lane == 0) g.exact[l] = sum;
+    return sum;
+}
+
+__global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggParams ap,
+                                                             const float* __restrict__ X,
+                                                             uint64_t ldX) {
+    extern __shared__ __align__(16) char smem_raw[];
+    const int L = g.L;
+    const Smem s = carve(smem_raw, L);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    // 1. per-layer tree sum of the tile partials (lanes stride, fixed shuffle tree)
+    for (int l = warp; l < L; l += kWarps) {
+        const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
+        double acc = 0.0;
+        for (int t = t0 + lane; t < t1; t += 32) acc = __dadd_rn(acc, g.partials[t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (lane == 0) {
+            const int nt = t1 - t0;
+            const double D = tile_depth(g.T) + (nt + 31) / 32 + 5 + 2;
+            const double n = static_cast<double>(g.counts[l]);
+            s.key[l] = acc;
+            s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
+            g.scores[l] = acc;
+        }
+    }
+    if (tid == 0) {
+        s.flag[0] = 0;
+        s.flag[1] = 0;
+    }
+    __syncthreads();
+    rank_layers_block(s, L);
+
+    // 2. certificate: any interval overlap between two layers marks both
+    for (int r = tid; r < L; r += blockDim.x) {
+        const int l = s.sorted[r];
+        s.a1[r] = s.key[l] + s.rad[l];          // hi, prefix max
+        s.a2[L - 1 - r] = s.key[l] - s.rad[l];  // lo, reversed for the suffix min
+    }
+    __syncthreads();
+    block_scan<double>(s.a1, L, -1.0, [](double a, double b) { return a > b ? a : b; }, s.wtot);
+    block_scan<double>(s.a2, L, 1e308, [](double a, double b) { return a < b ? a : b; }, s.wtot);
+    int my_marks = 0;
+    for (int r = tid; r < L; r += blockDim.x) {
+        const int l = s.sorted[r];
+        const double k = s.key[l], rd = s.rad[l];
+        const double premax = r > 0 ? s.a1[r - 1] : -1.0;
+        const double sufmin = r < L - 1 ? s.a2[L - 2 - r] : 1e308;
+        const bool m = (k != 0.0) && (k + rd >= sufmin || k - rd <= premax);
+        g.marked[l] = m ? 1 : 0;
+        s.i1[r] = m ? 1 : 0;
+        my_marks += m ? 1 : 0;
+    }
+    if (my_marks) atomicAdd(&s.flag[0], my_marks);
+    __syncthreads();
+    const int n_marked = s.flag[0];
+    if (n_marked > 0) {
+        // 3. exact sequential scores for the marked layers, one warp each, then re-rank
+        block_scan<int>(s.i1, L, 0, [](int a, int b) { return a + b; }, s.wtot);
+        for (int r = tid; r < L; r += blockDim.x)
+            if (g.marked[s.sorted[r]]) s.i2[s.i1[r] - 1] = s.sorted[r];
+        __syncthreads();
+        for (int m = warp; m < n_marked; m += kWarps) {
+            const int l = s.i2[m];
+            const double ex = exact_layer_pgp(g, ap, X, ldX, l, lane);
+            if (lane == 0) {
+                g.exact[l] = ex;
+                s.key[l] = ex;
+            }
+        }
+        if (tid == 0) {
+            g.meta64[META64_FB_LAYERS] += static_cast<uint64_t>(n_marked);
+            g.meta64[META64_FB_RESOLVES] += 1;
+        }
+        __syncthreads();
+        rank_layers_block(s, L);
+    }
+
+    // 4. prefix rule: inclusive byte scan in rank order, k = #prefix <= budget
+    uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
+    for (int r = tid; r < L; r += blockDim.x)
+        pre[r] = g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
+    __syncthreads();
+    block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; }, s.wtot);
+    const uint64_t budget = g.meta64[META64_BUDGET];
+    int cnt = 0;
+    for (int r = tid; r < L; r += blockDim.x) cnt += pre[r] <= budget ? 1 : 0;
+    if (cnt) atomicAdd(&s.flag[1], cnt);
+    __syncthreads();
+    const int k = s.flag[1];
+    const uint32_t tag = static_cast<uint32_t>(g.meta64[META64_RESOLVED] + 1);
+    __syncthreads();
+    if (tid == 0) g.meta64[META64_RESOLVED] += 1;
+    finalize_lists(g, s, s.sorted, k, tag);
 }
 
 // Install a host-provided GIB: g.flags already written; order (device) is the
@@ -324,8 +328,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const 
             run += g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
             pre[r] = run;
         }
-        g.meta64[META64_RESOLVED] = tag;
-        g.meta[META_NEED_FB] = 0;
+        if (g.meta64) g.meta64[META64_RESOLVED] = tag;
     }
     __syncthreads();
     finalize_lists(g, s, s.sorted, s.flag[1], tag);
@@ -362,8 +365,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_rank_gib(const double* scor
     uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
     for (int r = threadIdx.x; r < L; r += blockDim.x) pre[r] = counts[s.sorted[r]] * uint64_t(bpe);
     __syncthreads();
-    block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; },
-                         reinterpret_cast<uint64_t*>(s.tmp));
+    block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; }, s.wtot);
     for (int r = threadIdx.x; r < L; r += blockDim.x) {
         order[r] = s.sorted[r];
         flags[s.sorted[r]] = pre[r] <= budget ? 1 : 0;
@@ -382,11 +384,7 @@ cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float*
     const size_t sm = smem_bytes(g.L);
     cudaError_t e = set_smem(reinterpret_cast<const void*>(k_resolve), sm);
     if (e != cudaSuccess) return e;
-    k_resolve<<<1, kResolveThreads, sm, st>>>(g, 1);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_fallback<<<g.L, 32, 0, st>>>(g, ap, X, ldX);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    k_resolve<<<1, kResolveThreads, sm, st>>>(g, 2);
+    k_resolve<<<1, kResolveThreads, sm, st>>>(g, ap, X, ldX);
     return cudaGetLastError();
 }
 

@@ -7,8 +7,8 @@
 //                      G' = G + agg;  P_w = G'  for every worker  (p + 1.0f*agg, p == G)
 //                      PGP partial += |(double)agg * (double)G'|
 //   ICS layer element: P_w = G + x_w                              (base + local estimate)
-// stage 2 (one ICS chunk; on_push_ics_chunk -> finish_layer, protocol.cpp:326-353,
-//   and lgp_correct, protocol.cpp:99-116):
+// stage 2 (ICS chunks [c0, c1); on_push_ics_chunk -> finish_layer,
+//   protocol.cpp:326-353, and lgp_correct, protocol.cpp:99-116):
 //   element of a chunk layer: agg as above; G' = G + agg; P_w = G' (base + global,
 //   base == G by gradient conservation); PGP partial.
 //
@@ -17,22 +17,20 @@
 // conservation check, checks.cpp:126-184), so `p` in lgp_partial is G and the
 // per-worker `base` copies of the reference are never materialised.
 //
-// Work decomposition: the flat vector is cut into tiles of T elements that
-// never straddle a layer (tile -> layer table built once per partition). A
-// persistent grid walks tiles; each tile is a 128-bit vectorised streaming pass
-// (two quads in flight per thread, nc/no_allocate loads of the deltas,
-// evict-first stores of the worker rows) with scalar head/tail for layers whose
-// offset is not 16-byte aligned. The PGP partial of a tile is reduced in a fixed
-// order and written to partials[tile], so the per-layer sum is deterministic.
+// Work decomposition. The flat vector is cut into tiles of T elements that never
+// straddle a layer. A tile is owned by ONE WARP: lanes stream it with 128-bit
+// loads (two quads per lane in flight per iteration, nc/no_allocate loads of the
+// deltas, evict-first stores of the worker rows; scalar head/tail when a layer
+// offset is not 16-byte aligned) and reduce the tile's PGP partial with a fixed
+// shuffle tree — no block barrier anywhere in the streaming loop. Warps take
+// tiles from a device work counter (one atomic per tile, prefetched one tile
+// ahead), so the tail is a fraction of one tile however ragged the layer table
+// is; the last warp out resets the counter for the next launch.
 
 #include "common.cuh"
 
 namespace osp {
 namespace {
-
-// ---------------------------------------------------------------------------
-// per-element bodies
-// ---------------------------------------------------------------------------
 
 __device__ __forceinline__ float ldx1(const AggParams& ap, const float* X, uint64_t ldX, int w,
                                       uint64_t f) {
@@ -50,12 +48,18 @@ __device__ __forceinline__ float4 cvt4(const AggParams& ap, float4 v) {
     return v;
 }
 
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                       __fadd_rn(a.w, b.w));
+}
+
 template <int NS>
 __device__ __forceinline__ int nworkers(const AggParams& ap) {
     return NS > 0 ? NS : ap.n;
 }
 
-// Aggregate + apply one scalar element.
+// ---- aggregate + apply ------------------------------------------------------
+
 template <int NS>
 __device__ __forceinline__ void agg_scalar(const GroupView& g, const AggParams& ap,
                                            const float* X, uint64_t ldX, uint64_t f,
@@ -70,20 +74,27 @@ __device__ __forceinline__ void agg_scalar(const GroupView& g, const AggParams& 
     acc = __dadd_rn(acc, pgp_term(a, gn));
 }
 
-template <int NS>
-__device__ __forceinline__ void local_scalar(const GroupView& g, const AggParams& ap,
-                                             const float* X, uint64_t ldX, uint64_t f) {
-    const int n = nworkers<NS>(ap);
-    const float go = g.G[f];
-    for (int w = 0; w < n; ++w)
-        g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, ldx1(ap, X, ldX, w, f));
+__device__ __forceinline__ void agg_finish4(const GroupView& g, const AggParams& ap, double s0,
+                                            double s1, double s2, double s3, float4 go,
+                                            uint64_t f, int n, double& acc) {
+    float4 a, gn;
+    a.x = agg_finish(ap, s0);
+    a.y = agg_finish(ap, s1);
+    a.z = agg_finish(ap, s2);
+    a.w = agg_finish(ap, s3);
+    gn = add4(go, a);
+    *reinterpret_cast<float4*>(g.G + f) = gn;
+    for (int w = 0; w < n; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+    acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
+    acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
+    acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
+    acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
 }
 
-// Finish one quad whose deltas are already in registers.
 template <int NS>
-__device__ __forceinline__ void agg_quad_finish(const GroupView& g, const AggParams& ap,
-                                                const float4* x, float4 go, uint64_t f,
-                                                double& acc) {
+__device__ __forceinline__ void agg_quad_regs(const GroupView& g, const AggParams& ap,
+                                              const float4* x, float4 go, uint64_t f,
+                                              double& acc) {
     double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
     for (int w = 0; w < NS; ++w) {
@@ -94,25 +105,9 @@ __device__ __forceinline__ void agg_quad_finish(const GroupView& g, const AggPar
         s2 = agg_acc(s2, wt, v.z);
         s3 = agg_acc(s3, wt, v.w);
     }
-    float4 a, gn;
-    a.x = agg_finish(ap, s0);
-    a.y = agg_finish(ap, s1);
-    a.z = agg_finish(ap, s2);
-    a.w = agg_finish(ap, s3);
-    gn.x = __fadd_rn(go.x, a.x);
-    gn.y = __fadd_rn(go.y, a.y);
-    gn.z = __fadd_rn(go.z, a.z);
-    gn.w = __fadd_rn(go.w, a.w);
-    *reinterpret_cast<float4*>(g.G + f) = gn;
-#pragma unroll
-    for (int w = 0; w < NS; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
-    acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
-    acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
-    acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
-    acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
+    agg_finish4(g, ap, s0, s1, s2, s3, go, f, NS, acc);
 }
 
-// Dynamic worker count: accumulate while loading (no register arrays).
 __device__ __forceinline__ void agg_quad_dyn(const GroupView& g, const AggParams& ap,
                                              const float* X, uint64_t ldX, uint64_t f,
                                              double& acc) {
@@ -126,51 +121,23 @@ __device__ __forceinline__ void agg_quad_dyn(const GroupView& g, const AggParams
         s2 = agg_acc(s2, wt, v.z);
         s3 = agg_acc(s3, wt, v.w);
     }
-    float4 a, gn;
-    a.x = agg_finish(ap, s0);
-    a.y = agg_finish(ap, s1);
-    a.z = agg_finish(ap, s2);
-    a.w = agg_finish(ap, s3);
-    gn.x = __fadd_rn(go.x, a.x);
-    gn.y = __fadd_rn(go.y, a.y);
-    gn.z = __fadd_rn(go.z, a.z);
-    gn.w = __fadd_rn(go.w, a.w);
-    *reinterpret_cast<float4*>(g.G + f) = gn;
-    for (int w = 0; w < ap.n; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
-    acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
-    acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
-    acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
-    acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
+    agg_finish4(g, ap, s0, s1, s2, s3, go, f, ap.n, acc);
 }
 
-__device__ __forceinline__ float4 add4(float4 a, float4 b) {
-    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
-                       __fadd_rn(a.w, b.w));
-}
-
-// ---------------------------------------------------------------------------
-// tile bodies
-// ---------------------------------------------------------------------------
-
-// RS (stage 1) / ICS chunk (stage 2): aggregate + apply + broadcast to workers.
+// One warp aggregates [s, e) of one layer.
 template <int NS>
-__device__ void tile_agg(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                         uint64_t s, uint64_t e, bool vec, double& acc) {
-    const int tid = threadIdx.x;
-    const int B = blockDim.x;
-    uint64_t hs = s, he = s, be = s;
+__device__ void warp_tile_agg(const GroupView& g, const AggParams& ap, const float* X,
+                              uint64_t ldX, uint64_t s, uint64_t e, bool vec, int lane,
+                              double& acc) {
+    uint64_t he = e, be = e;
     if (vec) {
         he = min(e, (s + 3) & ~uint64_t(3));
         be = he + ((e - he) & ~uint64_t(3));
-    } else {
-        he = e;
-        be = e;
     }
-    for (uint64_t f = hs + tid; f < he; f += B) agg_scalar<NS>(g, ap, X, ldX, f, acc);
+    for (uint64_t f = s + lane; f < he; f += 32) agg_scalar<NS>(g, ap, X, ldX, f, acc);
     if constexpr (NS > 0) {
-        const uint64_t step = 4ull * B;
-        for (uint64_t f0 = he + 4ull * tid; f0 < be; f0 += 2 * step) {
-            const uint64_t f1 = f0 + step;
+        for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 256) {
+            const uint64_t f1 = f0 + 128;
             const bool has1 = f1 < be;
             float4 xa[NS], xb[NS];
 #pragma unroll
@@ -181,32 +148,38 @@ __device__ void tile_agg(const GroupView& g, const AggParams& ap, const float* X
             const float4 ga = *reinterpret_cast<const float4*>(g.G + f0);
             float4 gb = make_float4(0.f, 0.f, 0.f, 0.f);
             if (has1) gb = *reinterpret_cast<const float4*>(g.G + f1);
-            agg_quad_finish<NS>(g, ap, xa, ga, f0, acc);
-            if (has1) agg_quad_finish<NS>(g, ap, xb, gb, f1, acc);
+            agg_quad_regs<NS>(g, ap, xa, ga, f0, acc);
+            if (has1) agg_quad_regs<NS>(g, ap, xb, gb, f1, acc);
         }
     } else {
-        for (uint64_t f0 = he + 4ull * tid; f0 < be; f0 += 4ull * B)
-            agg_quad_dyn(g, ap, X, ldX, f0, acc);
+        for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 128) agg_quad_dyn(g, ap, X, ldX, f0, acc);
     }
-    for (uint64_t f = be + tid; f < e; f += B) agg_scalar<NS>(g, ap, X, ldX, f, acc);
+    for (uint64_t f = be + lane; f < e; f += 32) agg_scalar<NS>(g, ap, X, ldX, f, acc);
 }
 
-// ICS layer at the barrier: each worker takes its own delta on top of G.
+// ---- local estimate (ICS layers at the barrier) -------------------------------
+
 template <int NS>
-__device__ void tile_local(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                           uint64_t s, uint64_t e, bool vec) {
-    const int tid = threadIdx.x;
-    const int B = blockDim.x;
+__device__ __forceinline__ void local_scalar(const GroupView& g, const AggParams& ap,
+                                             const float* X, uint64_t ldX, uint64_t f) {
+    const int n = nworkers<NS>(ap);
+    const float go = g.G[f];
+    for (int w = 0; w < n; ++w)
+        g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, ldx1(ap, X, ldX, w, f));
+}
+
+template <int NS>
+__device__ void warp_tile_local(const GroupView& g, const AggParams& ap, const float* X,
+                                uint64_t ldX, uint64_t s, uint64_t e, bool vec, int lane) {
     uint64_t he = e, be = e;
     if (vec) {
         he = min(e, (s + 3) & ~uint64_t(3));
         be = he + ((e - he) & ~uint64_t(3));
     }
-    for (uint64_t f = s + tid; f < he; f += B) local_scalar<NS>(g, ap, X, ldX, f);
+    for (uint64_t f = s + lane; f < he; f += 32) local_scalar<NS>(g, ap, X, ldX, f);
     if constexpr (NS > 0) {
-        const uint64_t step = 4ull * B;
-        for (uint64_t f0 = he + 4ull * tid; f0 < be; f0 += 2 * step) {
-            const uint64_t f1 = f0 + step;
+        for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 256) {
+            const uint64_t f1 = f0 + 128;
             const bool has1 = f1 < be;
             float4 xa[NS], xb[NS];
 #pragma unroll
@@ -228,7 +201,7 @@ __device__ void tile_local(const GroupView& g, const AggParams& ap, const float*
             }
         }
     } else {
-        for (uint64_t f0 = he + 4ull * tid; f0 < be; f0 += 4ull * B) {
+        for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 128) {
             const float4 go = *reinterpret_cast<const float4*>(g.G + f0);
             for (int w = 0; w < ap.n; ++w) {
                 const float4 v = cvt4(ap, ld_stream4(X + static_cast<uint64_t>(w) * ldX + f0));
@@ -236,44 +209,81 @@ __device__ void tile_local(const GroupView& g, const AggParams& ap, const float*
             }
         }
     }
-    for (uint64_t f = be + tid; f < e; f += B) local_scalar<NS>(g, ap, X, ldX, f);
+    for (uint64_t f = be + lane; f < e; f += 32) local_scalar<NS>(g, ap, X, ldX, f);
 }
 
-// ---------------------------------------------------------------------------
-// kernels
-// ---------------------------------------------------------------------------
+// ---- dynamic tile scheduler ------------------------------------------------------
+
+__device__ __forceinline__ int grab(int* next, int lane) {
+    int t = 0;
+    if (lane == 0) t = atomicAdd(next, 1);
+    return __shfl_sync(0xffffffffu, t, 0);
+}
+
+__device__ __forceinline__ void retire(int* next, int* done, int lane) {
+    if (lane == 0) {
+        const int total = static_cast<int>(gridDim.x * (blockDim.x >> 5));
+        if (atomicAdd(done, 1) == total - 1) {  // every warp has made its last grab
+            atomicExch(next, 0);
+            atomicExch(done, 0);
+        }
+    }
+}
+
+__device__ __forceinline__ double warp_sum_fixed(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_down_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// ---- kernels -------------------------------------------------------------------
 
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_stage1(GroupView g, AggParams ap,
                                                           const float* __restrict__ X,
                                                           uint64_t ldX, int vec) {
-    __shared__ double red[kStageThreads / 32];
-    for (int t = blockIdx.x; t < g.NT; t += gridDim.x) {
+    const int lane = threadIdx.x & 31;
+    int* next = g.sched + SCHED_S1_NEXT;
+    int t = grab(next, lane);
+    while (t < g.NT) {
+        const int tn = grab(next, lane);  // prefetch the next tile id
         const int l = g.tile_layer[t];
         const uint64_t lo = g.offsets[l];
         const uint64_t s = lo + static_cast<uint64_t>(t - g.tile_base[l]) * g.T;
         const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
         if (g.flags[l]) {
-            tile_local<NS>(g, ap, X, ldX, s, e, vec != 0);
+            warp_tile_local<NS>(g, ap, X, ldX, s, e, vec != 0, lane);
         } else {
             double acc = 0.0;
-            tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, acc);
-            const double tot = block_sum_fixed<kStageThreads>(acc, red);
-            if (threadIdx.x == 0) g.partials[t] = tot;
+            warp_tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, lane, acc);
+            acc = warp_sum_fixed(acc);
+            if (lane == 0) g.partials[t] = acc;
         }
+        t = tn;
     }
+    retire(next, g.sched + SCHED_S1_DONE, lane);
 }
 
+// Chunks [c0, c1) of the current ICS list (clamped to the non-empty chunks).
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams ap,
                                                           const float* __restrict__ X,
-                                                          uint64_t ldX, int chunk, int vec) {
-    __shared__ double red[kStageThreads / 32];
-    if (chunk >= g.meta[META_N_USED]) return;
-    const int jb = g.chunk_begin[chunk], je = g.chunk_begin[chunk + 1];
-    const int u0 = g.ics_tile_prefix[jb], u1 = g.ics_tile_prefix[je];
-    for (int u = u0 + blockIdx.x; u < u1; u += gridDim.x) {
-        // layer j of the chunk with ics_tile_prefix[j] <= u < ics_tile_prefix[j+1]
+                                                          uint64_t ldX, int c0, int c1, int vec) {
+    const int lane = threadIdx.x & 31;
+    int* next = g.sched + SCHED_S2_NEXT;
+    const int used = g.meta[META_N_USED];
+    if (c1 > used) c1 = used;
+    int u0 = 0, u1 = 0, jb = 0, je = 0;
+    if (c0 < c1) {
+        jb = g.chunk_begin[c0];
+        je = g.chunk_begin[c1];
+        u0 = g.ics_tile_prefix[jb];
+        u1 = g.ics_tile_prefix[je];
+    }
+    int u = u0 + grab(next, lane);
+    while (u < u1) {
+        const int un = u0 + grab(next, lane);
+        // ICS list position a with ics_tile_prefix[a] <= u < ics_tile_prefix[a+1]
         int a = jb, b = je - 1;
         while (a < b) {
             const int m = (a + b + 1) >> 1;
@@ -286,10 +296,12 @@ __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams
         const uint64_t s = lo + static_cast<uint64_t>(k) * g.T;
         const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
         double acc = 0.0;
-        tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, acc);
-        const double tot = block_sum_fixed<kStageThreads>(acc, red);
-        if (threadIdx.x == 0) g.partials[g.tile_base[l] + k] = tot;
+        warp_tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, lane, acc);
+        acc = warp_sum_fixed(acc);
+        if (lane == 0) g.partials[g.tile_base[l] + k] = acc;
+        u = un;
     }
+    retire(next, g.sched + SCHED_S2_DONE, lane);
 }
 
 bool vec_ok(const GroupView& g, const float* X, uint64_t ldX) {
@@ -326,7 +338,6 @@ int stage_blocks_per_sm(int n_workers) {
 cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int grid, cudaStream_t s) {
     const int vec = vec_ok(g, X, ldX) ? 1 : 0;
-    grid = grid < g.NT ? grid : g.NT;
     if (grid < 1) return cudaSuccess;
     return dispatch_n(ap.n, [&](auto nc) -> cudaError_t {
         constexpr int NS = decltype(nc)::value;
@@ -336,13 +347,12 @@ cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* 
 }
 
 cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                          int chunk, int grid, cudaStream_t s) {
+                          int c0, int c1, int grid, cudaStream_t s) {
     const int vec = vec_ok(g, X, ldX) ? 1 : 0;
-    grid = grid < g.NT ? grid : g.NT;
     if (grid < 1) return cudaSuccess;
     return dispatch_n(ap.n, [&](auto nc) -> cudaError_t {
         constexpr int NS = decltype(nc)::value;
-        k_stage2<NS><<<grid, kStageThreads, 0, s>>>(g, ap, X, ldX, chunk, vec);
+        k_stage2<NS><<<grid, kStageThreads, 0, s>>>(g, ap, X, ldX, c0, c1, vec);
         return cudaGetLastError();
     });
 }

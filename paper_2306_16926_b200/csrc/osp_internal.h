@@ -70,8 +70,10 @@ struct GroupView {
     int* chunk_of;               // [L] compacted chunk or -1
     uint8_t* gib_bytes;          // [8 + ceil(L/8)] encoded current GIB
     uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
+    int* sched;                  // [8] dynamic tile scheduler counters (SchedIdx)
 };
 
+enum SchedIdx { SCHED_S1_NEXT = 0, SCHED_S1_DONE = 1, SCHED_S2_NEXT = 2, SCHED_S2_DONE = 3 };
 enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2 };
 enum Meta64Idx {
     META64_BUDGET = 0,
@@ -85,13 +87,15 @@ enum Meta64Idx {
 constexpr int kHist = 1024;
 constexpr int kMaxLayers = 4096;  // single-CTA resolve (resolve.cu)
 constexpr int kStageThreads = 256;
+constexpr uint32_t kDefaultTile = 1024;  // elements per warp tile
 constexpr int kResolveThreads = 1024;
 
 // ---- launchers (kernels/*.cu) ----------------------------------------------
 cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int grid, cudaStream_t s);
+// Chunks [c0, c1) of the current ICS list in one launch.
 cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                          int chunk, int grid, cudaStream_t s);
+                          int c0, int c1, int grid, cudaStream_t s);
 cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                            cudaStream_t s);
 cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t s);

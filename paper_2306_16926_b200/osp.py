@@ -419,6 +419,10 @@ class OspGroup:
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_stage2_chunk(self._h, chunk, p, ld, _stream(stream)))
 
+    def stage2_all(self, deltas: torch.Tensor, stream=None):
+        p, ld = self._deltas(deltas)
+        _check(lib().osp_group_stage2_all(self._h, p, ld, _stream(stream)))
+
     def resolve(self, deltas: torch.Tensor, stream=None):
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_resolve(self._h, p, ld, _stream(stream)))
