@@ -191,7 +191,7 @@ typedef struct osp_group_config {
     int n_workers;            /* N, 1..OSP_MAX_WORKERS */
     const double* weights;    /* HOST, N subset weights (OspServer weights) */
     int n_chunks;             /* ICS chunk slots per iteration (>= 1) */
-    uint32_t tile_elems;      /* elements per warp tile; 0 = default 1024 (power of two, 256..65536) */
+    uint32_t tile_elems;      /* elements per warp tile; 0 = default 512 (power of two, 256..65536) */
     double sgd_lr;            /* 0 = inputs are deltas; > 0 fuse sgd_delta */
 } osp_group_config;
 

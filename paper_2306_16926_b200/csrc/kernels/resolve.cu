@@ -215,21 +215,16 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     const Smem s = carve(smem_raw, L);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    // 1. per-layer tree sum of the tile partials (lanes stride, fixed shuffle tree)
-    for (int l = warp; l < L; l += kWarps) {
-        const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
-        double acc = 0.0;
-        for (int t = t0 + lane; t < t1; t += 32) acc = __dadd_rn(acc, g.partials[t]);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
-        if (lane == 0) {
-            const int nt = t1 - t0;
-            const double D = tile_depth(g.T) + (nt + 31) / 32 + 5 + 2;
-            const double n = static_cast<double>(g.counts[l]);
-            s.key[l] = acc;
-            s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
-            g.scores[l] = acc;
-        }
+    // 1. per-layer tree sums, reduced by the stage kernels (stage.cu finish_tile:
+    //    4 lane-strided accumulators over the tile partials, pairwise, shuffle tree)
+    for (int l = tid; l < L; l += blockDim.x) {
+        const double acc = g.lscore[l];
+        const int nt = g.tile_base[l + 1] - g.tile_base[l];
+        const double D = tile_depth(g.T) + (nt + 127) / 128 + 2 + 5 + 2;
+        const double n = static_cast<double>(g.counts[l]);
+        s.key[l] = acc;
+        s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
+        g.scores[l] = acc;
     }
     if (tid == 0) {
         s.flag[0] = 0;

@@ -71,6 +71,8 @@ struct GroupView {
     uint8_t* gib_bytes;          // [8 + ceil(L/8)] encoded current GIB
     uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
     int* sched;                  // [8] dynamic tile scheduler counters (SchedIdx)
+    int* layer_cnt;              // [L] tiles of the layer finished in the current stage
+    double* lscore;              // [L] per-layer tree sum of the tile partials
 };
 
 enum SchedIdx { SCHED_S1_NEXT = 0, SCHED_S1_DONE = 1, SCHED_S2_NEXT = 2, SCHED_S2_DONE = 3 };
@@ -87,7 +89,7 @@ enum Meta64Idx {
 constexpr int kHist = 1024;
 constexpr int kMaxLayers = 4096;  // single-CTA resolve (resolve.cu)
 constexpr int kStageThreads = 256;
-constexpr uint32_t kDefaultTile = 1024;  // elements per warp tile
+constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profiles/)
 constexpr int kResolveThreads = 1024;
 
 // ---- launchers (kernels/*.cu) ----------------------------------------------
