@@ -664,7 +664,6 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &g->d_order_tmp, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.hist, kHist)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.sched, 8)) != OSP_OK) return cleanup(st);
-    if ((st = dalloc(g, &v.layer_cnt, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.lscore, L)) != OSP_OK) return cleanup(st);
 
     cudaStream_t s = as_stream(stream);
@@ -692,8 +691,6 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = cu(cudaMemsetAsync(v.flags, 0, L, s), "flags")) != OSP_OK) return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.marked, 0, L, s), "marked")) != OSP_OK) return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.sched, 0, 8 * sizeof(int), s), "sched")) != OSP_OK)
-        return cleanup(st);
-    if ((st = cu(cudaMemsetAsync(v.layer_cnt, 0, L * sizeof(int), s), "layer_cnt")) != OSP_OK)
         return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.lscore, 0, L * sizeof(double), s), "lscore")) != OSP_OK)
         return cleanup(st);

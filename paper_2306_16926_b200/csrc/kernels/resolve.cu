@@ -215,12 +215,39 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     const Smem s = carve(smem_raw, L);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    // 1. per-layer tree sums, reduced by the stage kernels (stage.cu finish_tile:
-    //    4 lane-strided accumulators over the tile partials, pairwise, shuffle tree)
+    // 0. every block: per-layer tree sums of the tile partials (fixed order:
+    //    thread-strided sequential, shuffle tree, warps in order)
+    for (int l = blockIdx.x; l < L; l += gridDim.x) {
+        const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
+        double acc = 0.0;
+        for (int t = t0 + tid; t < t1; t += blockDim.x) acc = __dadd_rn(acc, g.partials[t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (lane == 0) s.wtot[warp] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < kWarps; ++w) tot = __dadd_rn(tot, s.wtot[w]);
+            g.lscore[l] = tot;
+        }
+        __syncthreads();
+    }
+    // the last block to finish does the single-CTA part
+    if (tid == 0) {
+        __threadfence();
+        s.flag[2] = atomicAdd(g.sched + SCHED_RESOLVE_DONE, 1) == static_cast<int>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!s.flag[2]) return;
+    __threadfence();
+    if (tid == 0) g.sched[SCHED_RESOLVE_DONE] = 0;
+
+    // 1. per-layer scores and certificate radii
     for (int l = tid; l < L; l += blockDim.x) {
-        const double acc = g.lscore[l];
+        const double acc = __ldcg(g.lscore + l);
         const int nt = g.tile_base[l + 1] - g.tile_base[l];
-        const double D = tile_depth(g.T) + (nt + 127) / 128 + 2 + 5 + 2;
+        const double D = tile_depth(g.T) + (nt + kResolveThreads - 1) / kResolveThreads + 5 +
+                         kWarps + 2;
         const double n = static_cast<double>(g.counts[l]);
         s.key[l] = acc;
         s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
@@ -379,7 +406,8 @@ cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float*
     const size_t sm = smem_bytes(g.L);
     cudaError_t e = set_smem(reinterpret_cast<const void*>(k_resolve), sm);
     if (e != cudaSuccess) return e;
-    k_resolve<<<1, kResolveThreads, sm, st>>>(g, ap, X, ldX);
+    const int blocks = g.L < sm_count() ? g.L : sm_count();
+    k_resolve<<<blocks, kResolveThreads, sm, st>>>(g, ap, X, ldX);
     return cudaGetLastError();
 }
 

@@ -236,34 +236,11 @@ __device__ __forceinline__ double warp_sum_fixed(double v) {
     return v;
 }
 
-// Publish a tile's PGP partial; the warp that completes the layer's last tile
-// reduces the layer (fixed order: 4 lane-strided accumulators per lane,
-// combined pairwise, then the shuffle tree — depth ceil(nt/128) + 2 + 5, see
-// resolve.cu) into lscore[l], so the single-CTA resolve reads L numbers.
-__device__ __forceinline__ void finish_tile(const GroupView& g, int t, int l, double acc,
-                                            int lane) {
+// Publish a tile's PGP partial (fixed shuffle tree); resolve.cu reduces the
+// layer's partials in a fixed order.
+__device__ __forceinline__ void finish_tile(const GroupView& g, int t, double acc, int lane) {
     acc = warp_sum_fixed(acc);
-    int last = 0;
-    const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
-    if (lane == 0) {
-        g.partials[t] = acc;
-        __threadfence();
-        last = atomicAdd(&g.layer_cnt[l], 1) == (t1 - t0) - 1;
-    }
-    if (!__shfl_sync(0xffffffffu, last, 0)) return;
-    __threadfence();
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int k = t0 + lane; k < t1; k += 128) {
-        a0 = __dadd_rn(a0, __ldcg(g.partials + k));
-        if (k + 32 < t1) a1 = __dadd_rn(a1, __ldcg(g.partials + k + 32));
-        if (k + 64 < t1) a2 = __dadd_rn(a2, __ldcg(g.partials + k + 64));
-        if (k + 96 < t1) a3 = __dadd_rn(a3, __ldcg(g.partials + k + 96));
-    }
-    const double s = warp_sum_fixed(__dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3)));
-    if (lane == 0) {
-        g.lscore[l] = s;
-        g.layer_cnt[l] = 0;
-    }
+    if (lane == 0) g.partials[t] = acc;
 }
 
 // ---- kernels -------------------------------------------------------------------
@@ -286,7 +263,7 @@ __global__ void __launch_bounds__(kStageThreads) k_stage1(GroupView g, AggParams
         } else {
             double acc = 0.0;
             warp_tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, lane, acc);
-            finish_tile(g, t, l, acc, lane);
+            finish_tile(g, t, acc, lane);
         }
         t = tn;
     }
@@ -326,7 +303,7 @@ __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams
         const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
         double acc = 0.0;
         warp_tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, lane, acc);
-        finish_tile(g, g.tile_base[l] + k, l, acc, lane);
+        finish_tile(g, g.tile_base[l] + k, acc, lane);
         u = un;
     }
     retire(next, g.sched + SCHED_S2_DONE, lane);

@@ -71,11 +71,16 @@ struct GroupView {
     uint8_t* gib_bytes;          // [8 + ceil(L/8)] encoded current GIB
     uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
     int* sched;                  // [8] dynamic tile scheduler counters (SchedIdx)
-    int* layer_cnt;              // [L] tiles of the layer finished in the current stage
     double* lscore;              // [L] per-layer tree sum of the tile partials
 };
 
-enum SchedIdx { SCHED_S1_NEXT = 0, SCHED_S1_DONE = 1, SCHED_S2_NEXT = 2, SCHED_S2_DONE = 3 };
+enum SchedIdx {
+    SCHED_S1_NEXT = 0,
+    SCHED_S1_DONE = 1,
+    SCHED_S2_NEXT = 2,
+    SCHED_S2_DONE = 3,
+    SCHED_RESOLVE_DONE = 4
+};
 enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2 };
 enum Meta64Idx {
     META64_BUDGET = 0,
