@@ -248,6 +248,56 @@ osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, u
 osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,
                               int* grid_blocks, int* block_threads);
 
+/* ------------------------------------------------------------------------
+ * Shard: the multi-GPU path, one process per GPU (PS sharded one shard per
+ * GPU). Rank r hosts workers [r*N/P, (r+1)*N/P) and a full
+ * replica of the global vector. Per stage, the owner of each slice of the
+ * stage's tile sequence reads every worker's delta rows from the peers' HBM
+ * over NVLink (CUDA IPC), aggregates them in the reference's fixed worker
+ * order in fp64 (push = reduce-scatter, bit-exact) and stores the fp32
+ * aggregate into every rank's buffer (pull = all-gather), all in one kernel;
+ * each rank then applies locally and resolves the identical next GIB.
+ *
+ * Setup: create on every rank, export a handle, exchange the handles (e.g.
+ * torch.distributed all_gather), connect with all of them (rank order).
+ * The caller writes its workers' deltas into osp_shard_deltas(buf) and steps
+ * with that buffer index (two buffers, so the next iteration's compute can
+ * fill one while stage 2 still reads the other).
+ * ---------------------------------------------------------------------- */
+#define OSP_SHARD_HANDLE_BYTES 512
+typedef struct osp_shard osp_shard;
+typedef struct osp_shard_config {
+    int world;              /* ranks (GPUs), <= 8 */
+    int rank;
+    int n_workers;          /* N total logical workers, N % world == 0 */
+    const double* weights;  /* HOST, N weights (all workers) */
+    int n_chunks;
+    uint32_t tile_elems;    /* 0 = default */
+    double sgd_lr;          /* 0 = deltas; > 0 fused sgd_delta */
+} osp_shard_config;
+
+osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* cfg,
+                            const float* init_params, void* stream, osp_shard** out);
+void osp_shard_destroy(osp_shard* s);
+uint64_t osp_shard_handle_size(void);
+osp_status osp_shard_export(osp_shard* s, uint8_t* handle);
+/* handles: world consecutive OSP_SHARD_HANDLE_BYTES blocks in rank order. */
+osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles);
+/* Local workers' delta rows of buffer buf (0/1): [N/P][ld] device floats. */
+float* osp_shard_deltas(osp_shard* s, int buf, uint64_t* ld);
+/* The rank-local state (global replica, worker rows, GIB, stats): use the
+ * osp_group_* getters on it. Do not step it directly. */
+osp_group* osp_shard_group(osp_shard* s);
+osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream);
+osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream);
+osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream);
+osp_status osp_shard_step(osp_shard* s, int buf, void* stream);
+/* ProtocolError if a cross-GPU barrier timed out (synchronises `stream`). */
+osp_status osp_shard_check(osp_shard* s, void* stream);
+/* Synthetic deltas of workers [worker0, worker0+n_workers) into [n_workers][ld]. */
+osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
+                                  uint64_t n, float* out, uint64_t ld, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

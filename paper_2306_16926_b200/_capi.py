@@ -25,6 +25,14 @@ class osp_group_config(ctypes.Structure):
                 ("tile_elems", c_u32), ("sgd_lr", c_dbl)]
 
 
+class osp_shard_config(ctypes.Structure):
+    _fields_ = [("world", c_int), ("rank", c_int), ("n_workers", c_int), ("weights", P(c_dbl)),
+                ("n_chunks", c_int), ("tile_elems", c_u32), ("sgd_lr", c_dbl)]
+
+
+SHARD_HANDLE_BYTES = 512
+
+
 class osp_sgu_schedule(ctypes.Structure):
     _fields_ = [("u_max", c_u64), ("has_initial_loss", c_int), ("initial_loss", c_dbl),
                 ("current_budget", c_u64), ("epoch", c_u64)]
@@ -94,6 +102,21 @@ _SIGS = {
     "osp_group_stats": (c_int, [c_void_p, P(c_u64), P(c_u64), P(c_u64), c_void_p]),
     "osp_group_deferred_history": (c_int, [c_void_p, c_u32, c_int, P(c_u64), c_void_p]),
     "osp_group_geometry": (c_int, [c_void_p, P(c_u32), P(c_u64), P(c_int), P(c_int)]),
+    "osp_shard_create": (c_int, [c_void_p, P(osp_shard_config), c_void_p, c_void_p,
+                                 P(c_void_p)]),
+    "osp_shard_destroy": (None, [c_void_p]),
+    "osp_shard_handle_size": (c_u64, []),
+    "osp_shard_export": (c_int, [c_void_p, P(ctypes.c_uint8)]),
+    "osp_shard_connect": (c_int, [c_void_p, P(ctypes.c_uint8)]),
+    "osp_shard_deltas": (c_void_p, [c_void_p, c_int, P(c_u64)]),
+    "osp_shard_group": (c_void_p, [c_void_p]),
+    "osp_shard_stage1": (c_int, [c_void_p, c_int, c_void_p]),
+    "osp_shard_stage2": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p]),
+    "osp_shard_resolve": (c_int, [c_void_p, c_int, c_void_p]),
+    "osp_shard_step": (c_int, [c_void_p, c_int, c_void_p]),
+    "osp_shard_check": (c_int, [c_void_p, c_void_p]),
+    "osp_synth_deltas_range": (c_int, [c_u64, c_int, c_int, c_u64, c_u64, c_void_p, c_u64,
+                                       c_void_p]),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -1,0 +1,39 @@
+// Handle layouts shared by the C-ABI translation units (not part of the ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "../osp_internal.h"
+
+struct osp_partition {
+    std::vector<uint64_t> counts;
+    std::vector<uint64_t> offsets;
+    uint64_t total = 0;
+    uint32_t bpe = 4;
+    uint64_t* d_offsets = nullptr;
+    uint64_t* d_counts = nullptr;
+};
+
+struct osp_group {
+    const osp_partition* part = nullptr;
+    int N = 0;
+    int n_chunks = 1;
+    double sgd_lr = 0.0;
+    std::vector<double> weights;
+    osp::AggParams ap{};
+    osp::GroupView v{};
+    int grid = 1;
+    int blocks_per_sm = 1;
+    // owned device buffers
+    std::vector<void*> owned;
+    int* d_order_tmp = nullptr;
+    float* d_staging = nullptr;
+};
+
+#define OSP_TRY(expr)                \
+    do {                             \
+        osp_status s_ = (expr);      \
+        if (s_ != OSP_OK) return s_; \
+    } while (0)

@@ -12,7 +12,7 @@
 #include <string>
 #include <vector>
 
-#include "../osp_internal.h"
+#include "handles.h"
 
 namespace osp {
 
@@ -67,31 +67,6 @@ using namespace osp;
 // handles
 // ---------------------------------------------------------------------------
 
-struct osp_partition {
-    std::vector<uint64_t> counts;
-    std::vector<uint64_t> offsets;
-    uint64_t total = 0;
-    uint32_t bpe = 4;
-    uint64_t* d_offsets = nullptr;
-    uint64_t* d_counts = nullptr;
-};
-
-struct osp_group {
-    const osp_partition* part = nullptr;
-    int N = 0;
-    int n_chunks = 1;
-    double sgd_lr = 0.0;
-    std::vector<double> weights;
-    AggParams ap{};
-    GroupView v{};
-    int grid = 1;
-    int blocks_per_sm = 1;
-    // owned device buffers
-    std::vector<void*> owned;
-    int* d_order_tmp = nullptr;
-    float* d_staging = nullptr;
-};
-
 namespace {
 
 template <typename T>
@@ -103,12 +78,6 @@ osp_status dalloc(osp_group* g, T** out, size_t count) {
     *out = static_cast<T*>(p);
     return OSP_OK;
 }
-
-#define OSP_TRY(expr)                      \
-    do {                                   \
-        osp_status s_ = (expr);            \
-        if (s_ != OSP_OK) return s_;       \
-    } while (0)
 
 osp_status check_weights(int n, const double* weights) {
     if (n < 1) return fail(OSP_ERR_PROTOCOL, "aggregation needs one contribution per worker");
@@ -665,6 +634,8 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &v.hist, kHist)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.sched, 8)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.lscore, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.rs_layers, L)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.rs_tile_prefix, L + 1)) != OSP_OK) return cleanup(st);
 
     cudaStream_t s = as_stream(stream);
     auto cu = [&](cudaError_t e, const char* what) -> osp_status {

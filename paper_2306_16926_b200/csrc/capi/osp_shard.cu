@@ -1,0 +1,267 @@
+// C-ABI of the sharded multi-GPU path (include/osp_c.h, "Shard" section).
+//
+// One process per GPU. Rank r hosts workers [r*N/P, (r+1)*N/P), a full replica
+// of the global vector, and the PS shard of every stage's tile sequence. The
+// push (reduce-scatter) and the pull (all-gather) are fused into k_shard_agg
+// over CUDA-IPC peer mappings of the other ranks' delta rows and agg buffers;
+// cross-GPU ordering uses k_barrier on peer-mapped flag slots. The local state
+// (G replica, worker rows, PGP partials, GIB lists) is an osp_group with the
+// rank's workers, so resolve and every read-back reuse the group code.
+
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "handles.h"
+
+using namespace osp;
+
+namespace {
+
+constexpr uint32_t kMagic = 0x0500b200u;
+
+struct ShardHandle {
+    uint32_t magic;
+    int32_t rank, world, n_loc;
+    uint64_t M, L, ldX, buf_stride;
+    cudaIpcMemHandle_t hx, hagg, hflags;
+};
+static_assert(sizeof(ShardHandle) <= OSP_SHARD_HANDLE_BYTES, "handle too large");
+
+}  // namespace
+
+struct osp_shard {
+    osp_group* grp = nullptr;  // local state: rank's workers
+    const osp_partition* part = nullptr;
+    int world = 1, rank = 0, n_loc = 1, N = 1, n_chunks = 1;
+    AggParams ap_all{};        // every worker, global weights (aggregation)
+    AggParams ap_loc{};        // local workers (sgd conversion on the local estimate)
+    float* X = nullptr;        // [2][n_loc][ldX] local delta rows, IPC-exported
+    uint64_t ldX = 0, buf_stride = 0;
+    float* agg = nullptr;      // [ldX] agg_full, IPC-exported
+    unsigned* flags = nullptr; // [kBarKinds][kMaxRanks], IPC-exported
+    unsigned* epoch = nullptr; // [kBarKinds] local
+    unsigned* error = nullptr; // [1] local
+    PeerTable pt[2]{};         // per delta buffer
+    std::vector<void*> opened; // peer mappings to close
+    bool connected = false;
+};
+
+extern "C" {
+
+osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* cfg,
+                            const float* init_params, void* stream, osp_shard** out) {
+    if (!out || !part || !cfg || !cfg->weights) return fail(OSP_ERR_INVALID, "null argument");
+    *out = nullptr;
+    if (cfg->world < 1 || cfg->world > kMaxRanks)
+        return fail(OSP_ERR_INVALID, "world size must be in [1, " + std::to_string(kMaxRanks) + "]");
+    if (cfg->rank < 0 || cfg->rank >= cfg->world) return fail(OSP_ERR_INVALID, "rank out of range");
+    if (cfg->n_workers < 1 || cfg->n_workers > OSP_MAX_WORKERS)
+        return fail(OSP_ERR_CONFIG, "worker count out of range");
+    if (cfg->n_workers % cfg->world != 0)
+        return fail(OSP_ERR_CONFIG, "workers must split evenly across ranks");
+    for (int w = 0; w < cfg->n_workers; ++w)
+        if (cfg->weights[w] <= 0) return fail(OSP_ERR_CONFIG, "subset weight must be positive");
+    double tw = 0.0;
+    for (int w = 0; w < cfg->n_workers; ++w) tw += cfg->weights[w];
+    if (!(tw > 0.0)) return fail(OSP_ERR_PROTOCOL, "aggregation weights must sum > 0");
+
+    auto* s = new osp_shard();
+    s->part = part;
+    s->world = cfg->world;
+    s->rank = cfg->rank;
+    s->N = cfg->n_workers;
+    s->n_loc = cfg->n_workers / cfg->world;
+    s->n_chunks = cfg->n_chunks;
+    s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
+    s->ap_loc = make_agg_params(s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->sgd_lr);
+    osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks,
+                        cfg->tile_elems, cfg->sgd_lr};
+    osp_status st = osp_group_create(part, &gc, init_params, stream, &s->grp);
+    if (st != OSP_OK) {
+        delete s;
+        return st;
+    }
+    const uint64_t M = part->total;
+    s->ldX = (M + 3) & ~uint64_t(3);
+    s->buf_stride = s->ldX * s->n_loc;
+    cudaError_t e = cudaMalloc(&s->X, 2 * s->buf_stride * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&s->agg, s->ldX * sizeof(float));
+    if (e == cudaSuccess) e = cudaMalloc(&s->flags, kBarKinds * kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->epoch, kBarKinds * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->error, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->X, 0, 2 * s->buf_stride * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemset(s->agg, 0, s->ldX * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemset(s->flags, 0, kBarKinds * kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->epoch, 0, kBarKinds * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) {
+        osp_shard_destroy(s);
+        return cuda_fail(e, "shard buffers");
+    }
+    s->grp->v.agg_full = s->agg;
+    *out = s;
+    return OSP_OK;
+}
+
+void osp_shard_destroy(osp_shard* s) {
+    if (!s) return;
+    cudaDeviceSynchronize();
+    for (void* p : s->opened) cudaIpcCloseMemHandle(p);
+    if (s->X) cudaFree(s->X);
+    if (s->agg) cudaFree(s->agg);
+    if (s->flags) cudaFree(s->flags);
+    if (s->epoch) cudaFree(s->epoch);
+    if (s->error) cudaFree(s->error);
+    if (s->grp) osp_group_destroy(s->grp);
+    delete s;
+}
+
+uint64_t osp_shard_handle_size(void) { return OSP_SHARD_HANDLE_BYTES; }
+
+osp_status osp_shard_export(osp_shard* s, uint8_t* handle) {
+    if (!s || !handle) return fail(OSP_ERR_INVALID, "null argument");
+    ShardHandle h{};
+    h.magic = kMagic;
+    h.rank = s->rank;
+    h.world = s->world;
+    h.n_loc = s->n_loc;
+    h.M = s->part->total;
+    h.L = s->part->counts.size();
+    h.ldX = s->ldX;
+    h.buf_stride = s->buf_stride;
+    OSP_CUDA(cudaIpcGetMemHandle(&h.hx, s->X));
+    OSP_CUDA(cudaIpcGetMemHandle(&h.hagg, s->agg));
+    OSP_CUDA(cudaIpcGetMemHandle(&h.hflags, s->flags));
+    std::memset(handle, 0, OSP_SHARD_HANDLE_BYTES);
+    std::memcpy(handle, &h, sizeof h);
+    return OSP_OK;
+}
+
+osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
+    if (!s || !handles) return fail(OSP_ERR_INVALID, "null argument");
+    if (s->connected) return fail(OSP_ERR_PROTOCOL, "shard already connected");
+    std::vector<const float*> xbase(s->world);
+    std::vector<float*> aggs(s->world);
+    std::vector<unsigned*> flags(s->world);
+    for (int q = 0; q < s->world; ++q) {
+        ShardHandle h;
+        std::memcpy(&h, handles + static_cast<size_t>(q) * OSP_SHARD_HANDLE_BYTES, sizeof h);
+        if (h.magic != kMagic || h.rank != q || h.world != s->world || h.n_loc != s->n_loc ||
+            h.M != s->part->total || h.L != s->part->counts.size() || h.ldX != s->ldX ||
+            h.buf_stride != s->buf_stride)
+            return fail(OSP_ERR_CONFIG, "rank " + std::to_string(q) +
+                                            " exported an incompatible shard (partition, worker "
+                                            "split or world size differ)");
+        if (q == s->rank) {
+            xbase[q] = s->X;
+            aggs[q] = s->agg;
+            flags[q] = s->flags;
+            continue;
+        }
+        void *px = nullptr, *pa = nullptr, *pf = nullptr;
+        OSP_CUDA(cudaIpcOpenMemHandle(&px, h.hx, cudaIpcMemLazyEnablePeerAccess));
+        s->opened.push_back(px);
+        OSP_CUDA(cudaIpcOpenMemHandle(&pa, h.hagg, cudaIpcMemLazyEnablePeerAccess));
+        s->opened.push_back(pa);
+        OSP_CUDA(cudaIpcOpenMemHandle(&pf, h.hflags, cudaIpcMemLazyEnablePeerAccess));
+        s->opened.push_back(pf);
+        xbase[q] = static_cast<const float*>(px);
+        aggs[q] = static_cast<float*>(pa);
+        flags[q] = static_cast<unsigned*>(pf);
+    }
+    for (int b = 0; b < 2; ++b) {
+        PeerTable& pt = s->pt[b];
+        pt = PeerTable{};
+        pt.world = s->world;
+        pt.rank = s->rank;
+        pt.n_loc = s->n_loc;
+        for (int w = 0; w < s->N; ++w) {
+            const int q = w / s->n_loc, i = w % s->n_loc;
+            pt.xrow[w] = xbase[q] + b * s->buf_stride + static_cast<uint64_t>(i) * s->ldX;
+        }
+        for (int q = 0; q < s->world; ++q) {
+            pt.agg[q] = aggs[q];
+            pt.flags[q] = flags[q];
+        }
+        pt.epoch = s->epoch;
+        pt.error = s->error;
+    }
+    s->connected = true;
+    return OSP_OK;
+}
+
+float* osp_shard_deltas(osp_shard* s, int buf, uint64_t* ld) {
+    if (!s || buf < 0 || buf > 1) return nullptr;
+    if (ld) *ld = s->ldX;
+    return s->X + buf * s->buf_stride;
+}
+
+osp_group* osp_shard_group(osp_shard* s) { return s ? s->grp : nullptr; }
+
+static osp_status check_ready(osp_shard* s, int buf) {
+    if (!s) return fail(OSP_ERR_INVALID, "null shard");
+    if (!s->connected) return fail(OSP_ERR_PROTOCOL, "shard not connected to its peers");
+    if (buf < 0 || buf > 1) return fail(OSP_ERR_INVALID, "delta buffer index must be 0 or 1");
+    return OSP_OK;
+}
+
+osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
+    OSP_TRY(check_ready(s, buf));
+    cudaStream_t st = as_stream(stream);
+    osp_group* g = s->grp;
+    OSP_CUDA(launch_barrier(s->pt[buf], 0, st));  // deltas ready; previous agg reads done
+    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st));
+    OSP_CUDA(launch_barrier(s->pt[buf], 1, st));  // every shard's aggregate landed here
+    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->X + buf * s->buf_stride, s->ldX, 1, 0, 0,
+                                g->grid, st));
+    return OSP_OK;
+}
+
+osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream) {
+    OSP_TRY(check_ready(s, buf));
+    if (c0 < 0 || c1 > s->n_chunks || c0 > c1) return fail(OSP_ERR_INVALID, "chunk range");
+    cudaStream_t st = as_stream(stream);
+    osp_group* g = s->grp;
+    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, c0, c1, g->grid, st));
+    OSP_CUDA(launch_barrier(s->pt[buf], 2, st));
+    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->X + buf * s->buf_stride, s->ldX, 2, c0, c1,
+                                g->grid, st));
+    return OSP_OK;
+}
+
+osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
+    OSP_TRY(check_ready(s, buf));
+    return osp_group_resolve(s->grp, s->X + buf * s->buf_stride, s->ldX, stream);
+}
+
+osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
+    OSP_TRY(osp_shard_stage1(s, buf, stream));
+    OSP_TRY(osp_shard_stage2(s, 0, s->n_chunks, buf, stream));
+    return osp_shard_resolve(s, buf, stream);
+}
+
+osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
+                                  uint64_t n, float* out, uint64_t ld, void* stream) {
+    if (worker0 < 0 || n_workers < 0 || n_workers > 65535)
+        return fail(OSP_ERR_INVALID, "bad worker range");
+    if (ld < n) return fail(OSP_ERR_SHAPE, "ld smaller than the vector length");
+    OSP_CUDA(launch_synth(seed, n_workers, iteration, 0, n, out, ld,
+                          static_cast<uint64_t>(worker0), as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_shard_check(osp_shard* s, void* stream) {
+    if (!s) return fail(OSP_ERR_INVALID, "null shard");
+    unsigned err = 0;
+    cudaStream_t st = as_stream(stream);
+    OSP_CUDA(cudaMemcpyAsync(&err, s->error, sizeof err, cudaMemcpyDeviceToHost, st));
+    OSP_CUDA(cudaStreamSynchronize(st));
+    if (err) return fail(OSP_ERR_PROTOCOL, "cross-GPU barrier timed out (a peer did not arrive)");
+    return OSP_OK;
+}
+
+}  // extern "C"

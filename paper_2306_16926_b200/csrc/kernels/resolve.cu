@@ -158,10 +158,28 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     __syncthreads();
     block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, s.wtot);
     for (int r = tid; r <= k; r += B) g.ics_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
+    // RS list: non-deferred layers in ascending id, with their tile prefix
+    int n_rs = L - k;
+    if (g.rs_layers) {
+        for (int l = tid; l < L; l += B) s.i2[l] = g.flags[l] ? 0 : 1;
+        __syncthreads();
+        block_scan<int>(s.i2, L, 0, [](int a, int b) { return a + b; }, s.wtot);
+        for (int l = tid; l < L; l += B) {
+            const int excl = l == 0 ? 0 : s.i2[l - 1];
+            if (!g.flags[l]) {
+                g.rs_layers[excl] = l;
+                s.i1[excl] = g.tile_base[l + 1] - g.tile_base[l];
+            }
+        }
+        __syncthreads();
+        block_scan<int>(s.i1, n_rs, 0, [](int a, int b) { return a + b; }, s.wtot);
+        for (int r = tid; r <= n_rs; r += B) g.rs_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
+    }
     if (tid == 0) {
         g.chunk_begin[n_used] = k;
         g.meta[META_N_ICS] = k;
         g.meta[META_N_USED] = n_used;
+        g.meta[META_N_RS] = n_rs;
         g.meta64[META64_DEFERRED] = total;
         g.meta64[META64_TAG] = tag;
         if (g.hist) g.hist[tag % kHist] = total;
@@ -193,13 +211,19 @@ __device__ double exact_layer_pgp(const GroupView& g, const AggParams& ap, const
         const uint64_t f = b + lane;
         double t = 0.0;
         if (f < end) {
-            double a = 0.0;
-            for (int w = 0; w < ap.n; ++w) {
-                float x = X[static_cast<uint64_t>(w) * ldX + f];
-                if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
-                a = agg_acc(a, ap.w[w], x);
+            float agg;
+            if (g.agg_full) {  // sharded path: the applied aggregate is resident
+                agg = g.agg_full[f];
+            } else {
+                double a = 0.0;
+                for (int w = 0; w < ap.n; ++w) {
+                    float x = X[static_cast<uint64_t>(w) * ldX + f];
+                    if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                    a = agg_acc(a, ap.w[w], x);
+                }
+                agg = agg_finish(ap, a);
             }
-            t = pgp_term(agg_finish(ap, a), g.G[f]);
+            t = pgp_term(agg, g.G[f]);
         }
         const int valid = static_cast<int>((end - b) < 32 ? (end - b) : 32);
         for (int i = 0; i < valid; ++i) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, t, i));

@@ -309,6 +309,263 @@ __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams
     retire(next, g.sched + SCHED_S2_DONE, lane);
 }
 
+// ===========================================================================
+// Sharded path (one process per GPU, PS sharded one shard per GPU).
+//
+// push = reduce-scatter fused into k_shard_agg: the owner of a tile range reads
+//   every worker's delta rows straight out of the peers' HBM over NVLink
+//   (CUDA IPC mappings, 128-bit loads), aggregates in the reference's fixed
+//   ascending worker order in fp64 (bit-exact, unlike an fp32 NCCL
+//   reduce-scatter), and
+// pull = all-gather fused into the same kernel: the fp32 aggregate is stored
+//   into every rank's agg_full buffer (NVLink stores).
+// Then each rank applies locally (k_shard_apply): G' = G + agg, its workers'
+// rows, PGP partials — so every rank holds an identical G replica and computes
+// the identical next GIB with no further exchange.
+// A stage's tile sequence (RS list for stage 1, ICS chunks [c0,c1) for stage 2)
+// is split into P equal tile-count ranges, one per rank.
+// ===========================================================================
+
+// Sequence of (layer list, tile prefix) for a stage.
+struct StageSeq {
+    const int* layers;
+    const int* tprefix;
+    int jb, je;  // positions in the layer list
+};
+
+__device__ __forceinline__ StageSeq stage_seq(const GroupView& g, int stage, int c0, int c1) {
+    StageSeq q;
+    if (stage == 1) {
+        q.layers = g.rs_layers;
+        q.tprefix = g.rs_tile_prefix;
+        q.jb = 0;
+        q.je = g.meta[META_N_RS];
+    } else {
+        q.layers = g.ics_layers;
+        q.tprefix = g.ics_tile_prefix;
+        const int used = g.meta[META_N_USED];
+        if (c1 > used) c1 = used;
+        if (c0 >= c1) {
+            q.jb = q.je = 0;
+        } else {
+            q.jb = g.chunk_begin[c0];
+            q.je = g.chunk_begin[c1];
+        }
+    }
+    return q;
+}
+
+// tile u of the sequence -> (layer, tile-in-layer)
+__device__ __forceinline__ void seq_tile(const StageSeq& q, int u, int& l, int& k) {
+    int a = q.jb, b = q.je - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (q.tprefix[m] <= u) a = m;
+        else b = m - 1;
+    }
+    l = q.layers[a];
+    k = u - q.tprefix[a];
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggParams ap,
+                                                             PeerTable pt, int stage, int c0,
+                                                             int c1, int vec) {
+    const int lane = threadIdx.x & 31;
+    int* next = g.sched + SCHED_AGG_NEXT;
+    const StageSeq q = stage_seq(g, stage, c0, c1);
+    const int U0 = q.jb < q.je ? q.tprefix[q.jb] : 0;
+    const int U = q.jb < q.je ? q.tprefix[q.je] - U0 : 0;
+    const int lo = U0 + static_cast<int>((static_cast<int64_t>(U) * pt.rank) / pt.world);
+    const int hi = U0 + static_cast<int>((static_cast<int64_t>(U) * (pt.rank + 1)) / pt.world);
+    const int n = nworkers<NS>(ap);
+    int u = lo + grab(next, lane);
+    while (u < hi) {
+        const int un = lo + grab(next, lane);
+        int l, k;
+        seq_tile(q, u, l, k);
+        const uint64_t base = g.offsets[l];
+        const uint64_t s = base + static_cast<uint64_t>(k) * g.T;
+        const uint64_t e = min(s + static_cast<uint64_t>(g.T), base + g.counts[l]);
+        uint64_t he = e, be = e;
+        if (vec) {
+            he = min(e, (s + 3) & ~uint64_t(3));
+            be = he + ((e - he) & ~uint64_t(3));
+        }
+        for (uint64_t f = s + lane; f < he; f += 32) {
+            double acc = 0.0;
+            for (int w = 0; w < n; ++w) {
+                float x = ld_stream1(pt.xrow[w] + f);
+                if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                acc = agg_acc(acc, ap.w[w], x);
+            }
+            const float a = agg_finish(ap, acc);
+            for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
+        }
+        for (uint64_t f = he + 4ull * lane; f < be; f += 128) {
+            float4 xs[NS > 0 ? NS : 1];
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            if constexpr (NS > 0) {
+#pragma unroll
+                for (int w = 0; w < NS; ++w) xs[w] = ld_stream4(pt.xrow[w] + f);
+#pragma unroll
+                for (int w = 0; w < NS; ++w) {
+                    const float4 v = cvt4(ap, xs[w]);
+                    s0 = agg_acc(s0, ap.w[w], v.x);
+                    s1 = agg_acc(s1, ap.w[w], v.y);
+                    s2 = agg_acc(s2, ap.w[w], v.z);
+                    s3 = agg_acc(s3, ap.w[w], v.w);
+                }
+            } else {
+                for (int w = 0; w < n; ++w) {
+                    const float4 v = cvt4(ap, ld_stream4(pt.xrow[w] + f));
+                    s0 = agg_acc(s0, ap.w[w], v.x);
+                    s1 = agg_acc(s1, ap.w[w], v.y);
+                    s2 = agg_acc(s2, ap.w[w], v.z);
+                    s3 = agg_acc(s3, ap.w[w], v.w);
+                }
+            }
+            const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
+                                         agg_finish(ap, s2), agg_finish(ap, s3));
+            for (int r = 0; r < pt.world; ++r) *reinterpret_cast<float4*>(pt.agg[r] + f) = a;
+        }
+        for (uint64_t f = be + lane; f < e; f += 32) {
+            double acc = 0.0;
+            for (int w = 0; w < n; ++w) {
+                float x = ld_stream1(pt.xrow[w] + f);
+                if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                acc = agg_acc(acc, ap.w[w], x);
+            }
+            const float a = agg_finish(ap, acc);
+            for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
+        }
+        u = un;
+    }
+    __threadfence_system();  // peer stores visible before the barrier kernel signals
+    retire(next, g.sched + SCHED_AGG_DONE, lane);
+}
+
+// Apply one element range from agg_full: G' = G + a; local worker rows = G'; PGP.
+__device__ void warp_tile_apply(const GroupView& g, int n_loc, uint64_t s, uint64_t e, bool vec,
+                                int lane, double& acc) {
+    uint64_t he = e, be = e;
+    if (vec) {
+        he = min(e, (s + 3) & ~uint64_t(3));
+        be = he + ((e - he) & ~uint64_t(3));
+    }
+    for (uint64_t f = s + lane; f < he; f += 32) {
+        const float a = g.agg_full[f];
+        const float gn = __fadd_rn(g.G[f], a);
+        g.G[f] = gn;
+        for (int w = 0; w < n_loc; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+        acc = __dadd_rn(acc, pgp_term(a, gn));
+    }
+    for (uint64_t f = he + 4ull * lane; f < be; f += 128) {
+        const float4 a = *reinterpret_cast<const float4*>(g.agg_full + f);
+        const float4 go = *reinterpret_cast<const float4*>(g.G + f);
+        const float4 gn = add4(go, a);
+        *reinterpret_cast<float4*>(g.G + f) = gn;
+        for (int w = 0; w < n_loc; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+        acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
+        acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
+        acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
+        acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
+    }
+    for (uint64_t f = be + lane; f < e; f += 32) {
+        const float a = g.agg_full[f];
+        const float gn = __fadd_rn(g.G[f], a);
+        g.G[f] = gn;
+        for (int w = 0; w < n_loc; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+        acc = __dadd_rn(acc, pgp_term(a, gn));
+    }
+}
+
+// stage 1 apply: RS tiles from agg_full, ICS tiles = local estimate of the
+// local workers (same body as k_stage1's ICS path).
+__global__ void __launch_bounds__(kStageThreads) k_shard_apply1(GroupView g, AggParams ap_loc,
+                                                                const float* __restrict__ X,
+                                                                uint64_t ldX, int vec) {
+    const int lane = threadIdx.x & 31;
+    int* next = g.sched + SCHED_S1_NEXT;
+    int t = grab(next, lane);
+    while (t < g.NT) {
+        const int tn = grab(next, lane);
+        const int l = g.tile_layer[t];
+        const uint64_t lo = g.offsets[l];
+        const uint64_t s = lo + static_cast<uint64_t>(t - g.tile_base[l]) * g.T;
+        const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
+        if (g.flags[l]) {
+            warp_tile_local<0>(g, ap_loc, X, ldX, s, e, vec != 0, lane);
+        } else {
+            double acc = 0.0;
+            warp_tile_apply(g, ap_loc.n, s, e, vec != 0, lane, acc);
+            finish_tile(g, t, acc, lane);
+        }
+        t = tn;
+    }
+    retire(next, g.sched + SCHED_S1_DONE, lane);
+}
+
+__global__ void __launch_bounds__(kStageThreads) k_shard_apply2(GroupView g, int n_loc, int c0,
+                                                                int c1, int vec) {
+    const int lane = threadIdx.x & 31;
+    int* next = g.sched + SCHED_S2_NEXT;
+    const StageSeq q = stage_seq(g, 2, c0, c1);
+    const int U0 = q.jb < q.je ? q.tprefix[q.jb] : 0;
+    const int U1 = q.jb < q.je ? q.tprefix[q.je] : 0;
+    int u = U0 + grab(next, lane);
+    while (u < U1) {
+        const int un = U0 + grab(next, lane);
+        int l, k;
+        seq_tile(q, u, l, k);
+        const uint64_t base = g.offsets[l];
+        const uint64_t s = base + static_cast<uint64_t>(k) * g.T;
+        const uint64_t e = min(s + static_cast<uint64_t>(g.T), base + g.counts[l]);
+        double acc = 0.0;
+        warp_tile_apply(g, n_loc, s, e, vec != 0, lane, acc);
+        finish_tile(g, g.tile_base[l] + k, acc, lane);
+        u = un;
+    }
+    retire(next, g.sched + SCHED_S2_DONE, lane);
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Cross-GPU barrier on peer-mapped flag slots. Every rank runs the same
+// barrier sequence, so the local epoch counters advance in lockstep. A
+// bounded spin (20 s) records an error instead of hanging the device.
+__global__ void k_barrier(PeerTable pt, int kind) {
+    __shared__ unsigned ep;
+    if (threadIdx.x == 0) {
+        ep = pt.epoch[kind] + 1;
+        pt.epoch[kind] = ep;
+    }
+    __syncthreads();
+    const int q = threadIdx.x;
+    __threadfence_system();
+    if (q < pt.world) {
+        volatile unsigned* slot = pt.flags[q] + kind * kMaxRanks + pt.rank;
+        *slot = ep;
+    }
+    __threadfence_system();
+    if (q < pt.world) {
+        volatile unsigned* mine = pt.flags[pt.rank] + kind * kMaxRanks + q;
+        const uint64_t t0 = global_ns();
+        while (static_cast<int>(*mine - ep) < 0) {
+            __nanosleep(256);
+            if (global_ns() - t0 > 20000000000ull) {
+                atomicExch(pt.error, 1u);
+                break;
+            }
+        }
+    }
+    __threadfence_system();
+}
+
 bool vec_ok(const GroupView& g, const float* X, uint64_t ldX) {
     return (ldX % 4 == 0) && (g.ldP % 4 == 0) &&
            (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
@@ -360,6 +617,35 @@ cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* 
         k_stage2<NS><<<grid, kStageThreads, 0, s>>>(g, ap, X, ldX, c0, c1, vec);
         return cudaGetLastError();
     });
+}
+
+cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
+                             int stage, int c0, int c1, int grid, cudaStream_t s) {
+    bool vec = (g.ldP % 4 == 0);
+    for (int w = 0; w < ap.n; ++w) vec = vec && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
+    for (int r = 0; r < pt.world; ++r) vec = vec && (reinterpret_cast<uintptr_t>(pt.agg[r]) % 16 == 0);
+    if (grid < 1) return cudaSuccess;
+    return dispatch_n(ap.n, [&](auto nc) -> cudaError_t {
+        constexpr int NS = decltype(nc)::value;
+        k_shard_agg<NS><<<grid, kStageThreads, 0, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0);
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const float* Xloc,
+                               uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s) {
+    const bool vec = vec_ok(g, Xloc, ldX) && (reinterpret_cast<uintptr_t>(g.agg_full) % 16 == 0);
+    if (grid < 1) return cudaSuccess;
+    if (stage == 1)
+        k_shard_apply1<<<grid, kStageThreads, 0, s>>>(g, ap_loc, Xloc, ldX, vec ? 1 : 0);
+    else
+        k_shard_apply2<<<grid, kStageThreads, 0, s>>>(g, ap_loc.n, c0, c1, vec ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s) {
+    k_barrier<<<1, 32, 0, s>>>(pt, kind);
+    return cudaGetLastError();
 }
 
 }  // namespace osp

@@ -72,6 +72,9 @@ struct GroupView {
     uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
     int* sched;                  // [8] dynamic tile scheduler counters (SchedIdx)
     double* lscore;              // [L] per-layer tree sum of the tile partials
+    int* rs_layers;              // [L] RS (barrier) layers, ascending id (valid prefix n_rs)
+    int* rs_tile_prefix;         // [L+1] exclusive tile prefix along rs_layers
+    const float* agg_full;       // [M] aggregated deltas (sharded path), or null
 };
 
 enum SchedIdx {
@@ -79,9 +82,11 @@ enum SchedIdx {
     SCHED_S1_DONE = 1,
     SCHED_S2_NEXT = 2,
     SCHED_S2_DONE = 3,
-    SCHED_RESOLVE_DONE = 4
+    SCHED_RESOLVE_DONE = 4,
+    SCHED_AGG_NEXT = 5,
+    SCHED_AGG_DONE = 6
 };
-enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2 };
+enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2, META_N_RS = 3 };
 enum Meta64Idx {
     META64_BUDGET = 0,
     META64_TAG = 1,
@@ -96,6 +101,27 @@ constexpr int kMaxLayers = 4096;  // single-CTA resolve (resolve.cu)
 constexpr int kStageThreads = 256;
 constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profiles/)
 constexpr int kResolveThreads = 1024;
+
+// ---- sharded (multi-GPU) path: peer tables ---------------------------------
+constexpr int kMaxRanks = 8;      // one NVLink/NVSwitch node
+constexpr int kBarKinds = 4;      // independent barrier sequences (stage1-in, stage1-out, stage2, spare)
+
+struct PeerTable {
+    int world;
+    int rank;
+    int n_loc;                                   // workers hosted per rank
+    const float* xrow[OSP_MAX_WORKERS];          // delta row of every worker (peer or local)
+    float* agg[kMaxRanks];                       // every rank's agg_full buffer
+    unsigned* flags[kMaxRanks];                  // every rank's barrier slots [kBarKinds][kMaxRanks]
+    unsigned* epoch;                             // local barrier counters [kBarKinds]
+    unsigned* error;                             // local: set on barrier timeout
+};
+
+cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
+                             int stage, int c0, int c1, int grid, cudaStream_t s);
+cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const float* Xloc,
+                               uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s);
+cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s);
 
 // ---- launchers (kernels/*.cu) ----------------------------------------------
 cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,

@@ -1,0 +1,127 @@
+"""Multi-GPU OSP: one process per GPU, PS sharded one shard per GPU (osp_shard_*).
+
+torch.distributed is plumbing only: it exchanges the 512-byte CUDA-IPC handles
+once at setup and provides the host barrier / max-over-ranks timing. The
+exchange itself (push = reduce-scatter, pull = all-gather) happens inside the
+library's kernels over NVLink peer memory.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _capi
+from ._capi import P, c_dbl, c_u64, c_void_p
+from .osp import (ConfigError, OspGroup, Partition, _check, _dev_f32, _ptr, _stream, _view,
+                  lib)
+
+
+class ShardGroup:
+    """This rank's slice of an N-worker OSP job spread over `world` GPUs."""
+
+    def __init__(self, part: Partition, n_workers: int, weights: Optional[Sequence[float]] = None,
+                 n_chunks: int = 4, init_params: Optional[torch.Tensor] = None,
+                 tile_elems: int = 0, sgd_lr: float = 0.0, rank: Optional[int] = None,
+                 world: Optional[int] = None, group=None, stream=None):
+        self.rank = dist.get_rank(group) if rank is None else rank
+        self.world = dist.get_world_size(group) if world is None else world
+        if n_workers % self.world:
+            raise ConfigError("workers must split evenly across ranks")
+        self.part = part
+        self.N = n_workers
+        self.n_loc = n_workers // self.world
+        self.M = part.total_count()
+        self.n_chunks = n_chunks
+        w = list(weights) if weights is not None else [1.0 / n_workers] * n_workers
+        self._w = (c_dbl * n_workers)(*w)
+        cfg = _capi.osp_shard_config(self.world, self.rank, n_workers, ctypes.cast(self._w, P(c_dbl)),
+                                     n_chunks, tile_elems, sgd_lr)
+        init = None
+        if init_params is not None:
+            _dev_f32(init_params, "init_params")
+            init = _ptr(init_params)
+        h = c_void_p()
+        _check(lib().osp_shard_create(part.handle, ctypes.byref(cfg), init, _stream(stream),
+                                      ctypes.byref(h)))
+        self._h = h
+        self.local = OspGroup._borrow(lib().osp_shard_group(h), part, self.n_loc, n_chunks, self)
+        ld = c_u64()
+        self._x = []
+        for b in range(2):
+            ptr = lib().osp_shard_deltas(h, b, ctypes.byref(ld))
+            self._x.append(_view(ptr, (self.n_loc, self.M), "<f4", strides=(int(ld.value) * 4, 4),
+                                 owner=self))
+        self.ldX = int(ld.value)
+
+    def export_handle(self) -> bytes:
+        buf = np.zeros(_capi.SHARD_HANDLE_BYTES, dtype=np.uint8)
+        _check(lib().osp_shard_export(self._h, buf.ctypes.data_as(P(ctypes.c_uint8))))
+        return buf.tobytes()
+
+    def connect(self, handles: Sequence[bytes]):
+        if len(handles) != self.world:
+            raise ConfigError("need one handle per rank")
+        blob = np.frombuffer(b"".join(handles), dtype=np.uint8).copy()
+        _check(lib().osp_shard_connect(self._h, blob.ctypes.data_as(P(ctypes.c_uint8))))
+
+    def connect_via(self, group=None):
+        """Exchange handles with torch.distributed (all_gather_object) and connect."""
+        mine = self.export_handle()
+        allh = [None] * self.world
+        dist.all_gather_object(allh, mine, group=group)
+        self.connect(allh)
+
+    # ---- data -------------------------------------------------------------
+    def deltas(self, buf: int) -> torch.Tensor:
+        """This rank's workers' delta rows [N/P, M] of buffer 0/1 (write into it)."""
+        return self._x[buf]
+
+    def fill_synth(self, seed: int, iteration: int, buf: int, stream=None):
+        """Reference synthetic deltas (runner.cpp:312-321) of this rank's workers."""
+        _check(lib().osp_synth_deltas_range(seed, self.rank * self.n_loc, self.n_loc, iteration,
+                                            self.M, _ptr(self._x[buf]), self.ldX, _stream(stream)))
+
+    # ---- the step ------------------------------------------------------------
+    def set_budget(self, budget: int, stream=None):
+        self.local.set_budget(budget, stream)
+
+    def stage1(self, buf: int, stream=None):
+        _check(lib().osp_shard_stage1(self._h, buf, _stream(stream)))
+
+    def stage2(self, buf: int, c0: int = 0, c1: Optional[int] = None, stream=None):
+        c1 = self.n_chunks if c1 is None else c1
+        _check(lib().osp_shard_stage2(self._h, c0, c1, buf, _stream(stream)))
+
+    def resolve(self, buf: int, stream=None):
+        _check(lib().osp_shard_resolve(self._h, buf, _stream(stream)))
+
+    def step(self, buf: int, stream=None):
+        _check(lib().osp_shard_step(self._h, buf, _stream(stream)))
+
+    def check(self, stream=None):
+        _check(lib().osp_shard_check(self._h, _stream(stream)))
+
+    @property
+    def global_params(self) -> torch.Tensor:
+        return self.local.global_params
+
+    @property
+    def worker_params(self) -> torch.Tensor:
+        return self.local.worker_params
+
+    def read_gib(self):
+        return self.local.read_gib()
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h and _capi._lib is not None:
+            self.local._h = None
+            _capi._lib.osp_shard_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        self.close()

@@ -1,0 +1,156 @@
+"""bench.py --gpus N (N > 1, launched by torchrun): the sharded OSP step.
+
+N_w = 8 logical workers spread N_w/N per GPU (strong scaling: the job is one
+OSP iteration over the whole model per step, whatever N). Timing: W warm-up
+steps, barrier + synchronize, K steps bracketed by CUDA events on the launching
+stream, max over ranks.
+"""
+from __future__ import annotations
+
+import json
+import os
+import statistics
+import time
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def run(args, metric: str, unit: str):
+    from . import layouts, osp
+    from .dist import ShardGroup
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    counts = layouts.get(args.layout)
+    N, M, L = args.workers, sum(counts), len(counts)
+    model_bytes = 4 * M
+    budget = int(args.budget_frac * model_bytes)
+    part = osp.Partition(counts)
+    sh = ShardGroup(part, N, None, n_chunks=args.chunks, tile_elems=args.tile)
+    sh.connect_via()
+    for b in range(2):
+        sh.fill_synth(args.seed, b, b)
+    sh.set_budget(budget)
+    stream = torch.cuda.current_stream()
+
+    def step(k, evs=None):
+        buf = k % 2
+        if evs is not None:
+            evs[0].record(stream)
+        sh.stage1(buf)
+        if evs is not None:
+            evs[1].record(stream)
+        if args.per_chunk:
+            for c in range(args.chunks):
+                sh.stage2(buf, c, c + 1)
+        else:
+            sh.stage2(buf)
+        if evs is not None:
+            evs[2].record(stream)
+        sh.resolve(buf)
+
+    for k in range(args.warmup):
+        step(k)
+    sh.check()
+    torch.cuda.synchronize()
+    tag0 = sh.read_gib()["tag"]
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    clocks = None
+    if rank == 0:
+        from bench import ClockSampler
+        clocks = ClockSampler(local)
+        clocks.start()
+        time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    start.record(stream)
+    for k in range(K):
+        step(args.warmup + k, evs[k])
+    end.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop() if clocks else None
+    sh.check()
+    local_ms = start.elapsed_time(end)
+    s1 = sum(evs[k][0].elapsed_time(evs[k][1]) for k in range(K)) / K
+    s2 = sum(evs[k][1].elapsed_time(evs[k][2]) for k in range(K)) / K
+    t = torch.tensor([local_ms, s1, s2], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, s1_max, s2_max = (float(x) for x in t.tolist())
+    ms_step = total_ms / K
+    u = sh.local.deferred_history(tag0, K).astype(np.float64) / model_bytes
+    n_loc = N // world
+    u_mean = float(u.mean())
+    # per-GPU algorithmic HBM bytes per step: own rows served to the shard owners,
+    # agg written + read, G read + written, worker rows (+ local estimate on ICS layers)
+    hbm_bytes = 4.0 * M * (4 + n_loc * (2 + 2 * u_mean))
+    # per-GPU NVLink bytes per step (each direction): remote delta rows read by this
+    # rank's shard + its aggregate stored to the other ranks
+    nvl_bytes = 4.0 * M * ((N - n_loc) / world + (world - 1) / world)
+
+    # ---- e2e: pinned host deltas -> device (this rank's rows), step, GIB read-back
+    host = [sh.deltas(b).cpu().pin_memory() for b in range(2)]
+    gib = torch.empty(8 + (L + 7) // 8, dtype=torch.uint8).pin_memory()
+    e2e = []
+    for k in range(args.e2e_steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sh.deltas(k % 2).copy_(host[k % 2], non_blocking=True)
+        step(k)
+        st = sh.read_gib()  # synchronising D2H of the next GIB
+        t1 = time.perf_counter()
+        if k > 0:
+            e2e.append((t1 - t0) * 1e3)
+    e2e_t = torch.tensor([statistics.median(e2e)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(e2e_t.item())
+    peaks = {}
+    try:
+        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                               "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    nvl_peak = 770.0
+    if rank == 0:
+        hbm_gbs = hbm_bytes / (ms_step * 1e-3) / 1e9
+        nvl_gbs = nvl_bytes / (ms_step * 1e-3) / 1e9
+        line = {
+            "metric": metric, "value": M / (ms_step * 1e-3), "unit": unit, "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
+            "config": {"workload": f"{args.layout}-size OSP sync+LGP step, PS sharded over "
+                                   f"{world} GPUs (NVLink peer memory)",
+                       "params": M, "layers": L, "workers": N, "workers_per_gpu": n_loc,
+                       "budget_frac": args.budget_frac, "chunks": args.chunks,
+                       "deltas": "reference synth generator, 2 sets alternating (> L2)",
+                       "parallelism": f"ps-shard{world}"},
+            "roofline": {"bound": "nvlink" if nvl_bytes / nvl_peak > hbm_bytes / hbm_peak else "hbm",
+                         "achieved": nvl_gbs, "peak": nvl_peak, "unit": "GB/s",
+                         "frac": nvl_gbs / nvl_peak, "traffic": None,
+                         "note": "per-GPU NVLink bytes each direction / step time; peak = measured "
+                                 "peer copy 770 GB/s (B200_PROFILING.md)",
+                         "hbm_gbs_per_gpu": hbm_gbs, "hbm_frac": hbm_gbs / hbm_peak},
+            "breakdown_ms": {"stage1": s1_max, "stage2": s2_max,
+                             "resolve": ms_step - s1_max - s2_max},
+            "u_mean": u_mean,
+            "e2e": {"value": M / (e2e_ms * 1e-3), "unit": unit, "ms_per_step": e2e_ms,
+                    "h2d_bytes_per_step": n_loc * M * 4 * world,
+                    "d2h_bytes_per_step": (8 + (L + 7) // 8) * world,
+                    "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read"},
+            "gpu_launches": K * (3 + 3 + (3 * args.chunks if args.per_chunk else 3) + 1),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    sh.close()
+    dist.destroy_process_group()

@@ -375,6 +375,21 @@ class OspGroup:
         h = c_void_p()
         _check(lib().osp_group_create(part.handle, ctypes.byref(cfg), init or None,
                                       _stream(stream), ctypes.byref(h)))
+        self._owned = True
+        self._attach(h)
+
+    @classmethod
+    def _borrow(cls, handle, part: Partition, n_workers: int, n_chunks: int, owner):
+        """View of a group owned by another handle (the local state of a shard)."""
+        self = cls.__new__(cls)
+        self.part, self.N, self.n_chunks = part, n_workers, n_chunks
+        self.M, self.L = part.total_count(), part.layer_count()
+        self._owned = False
+        self._parent = owner
+        self._attach(c_void_p(handle))
+        return self
+
+    def _attach(self, h):
         self._h = h
         ld = c_u64()
         pp = lib().osp_group_worker_params(h, ctypes.byref(ld))
@@ -482,7 +497,7 @@ class OspGroup:
 
     def close(self):
         h = getattr(self, "_h", None)
-        if h and _capi._lib is not None:
+        if h and getattr(self, "_owned", True) and _capi._lib is not None:
             _capi._lib.osp_group_destroy(h)
         self._h = None
 

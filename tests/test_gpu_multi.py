@@ -1,0 +1,117 @@
+"""Multi-GPU parity (>= 2 GPUs): the sharded path (osp_shard_*, NVLink peer
+memory) must be bit-identical to the oracle — global replica on every rank,
+every rank's worker rows, and the next GIB — for several iterations."""
+import os
+import socket
+import sys
+import traceback
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, q):
+    try:
+        sys.path.insert(0, REPO)
+        import torch.distributed as dist
+
+        from oracle import oracle
+        from paper_2306_16926_b200 import dist as odist
+        from paper_2306_16926_b200 import osp
+
+        torch.cuda.set_device(rank)
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        counts = np.asarray(cfg["counts"], dtype=np.uint64)
+        N, M, nc = cfg["N"], int(counts.sum()), cfg["chunks"]
+        w = cfg["weights"]
+        budget = int(cfg["budget_frac"] * M * 4)
+        rng = np.random.default_rng(cfg["p0_seed"])
+        p0 = rng.uniform(-1, 1, M).astype(np.float32) if cfg["p0_seed"] else np.zeros(M, np.float32)
+        part = osp.Partition(counts)
+        sh = odist.ShardGroup(part, N, w, n_chunks=nc, init_params=torch.as_tensor(p0, device="cuda"),
+                              tile_elems=cfg.get("tile", 0))
+        sh.connect_via()
+        G = p0.copy()
+        P = np.tile(p0, (N, 1))
+        flags = np.zeros(len(counts), np.uint8)
+        order = np.zeros(0, np.int32)
+        for it in range(cfg["iters"]):
+            buf = it % 2
+            sh.fill_synth(cfg["seed"], it, buf)
+            deltas = np.stack([oracle.synth_delta(cfg["seed"], k, it, M) for k in range(N)])
+            r = oracle.step(counts, 4, w, deltas, G, P, flags, order, nc, budget)
+            sh.set_budget(budget)
+            if cfg.get("per_chunk"):
+                sh.stage1(buf)
+                for c in range(nc):
+                    sh.stage2(buf, c, c + 1)
+                sh.resolve(buf)
+            else:
+                sh.step(buf)
+            sh.check()
+            g_dev = sh.global_params.cpu().numpy()
+            assert np.array_equal(g_dev.view(np.uint32), G.view(np.uint32)), f"G rank {rank} it {it}"
+            p_dev = sh.worker_params.cpu().numpy()
+            mine = P[rank * sh.n_loc:(rank + 1) * sh.n_loc]
+            assert np.array_equal(p_dev.view(np.uint32), mine.view(np.uint32)), f"P rank {rank}"
+            nxt = sh.read_gib()
+            assert np.array_equal(nxt["flags"], r["flags_out"]), f"flags rank {rank} it {it}"
+            assert np.array_equal(nxt["order"], r["order_out"]), f"order rank {rank} it {it}"
+            flags, order = r["flags_out"], r["order_out"]
+        dist.barrier()
+        sh.close()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        q.put((rank, traceback.format_exc()))
+
+
+def run_world(cfg, world=2):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, cfg, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    bad = {r: m for r, m in results.items() if m != "ok"}
+    assert not bad, bad
+
+
+def test_shard_two_gpus_resnet_like():
+    from paper_2306_16926_b200 import layouts
+    run_world(dict(counts=layouts.resnet50()[:60], N=8, weights=[0.125] * 8, chunks=4,
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0))
+
+
+def test_shard_two_gpus_ragged_unequal_weights():
+    rng = np.random.default_rng(3)
+    counts = [int(c) for c in rng.integers(1, 7000, 37)]
+    w = [float(x) for x in 0.1 + rng.random(4)]
+    run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=0.7, iters=4, seed=5,
+                   p0_seed=9, tile=256, per_chunk=True))
+
+
+def test_shard_four_gpus():
+    from paper_2306_16926_b200 import layouts
+    run_world(dict(counts=layouts.resnet50()[:80], N=8, weights=[0.125] * 8, chunks=4,
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0), world=4)
