@@ -19,11 +19,33 @@ CU_SRCS := $(CSRC)/kernels/stage.cu $(CSRC)/kernels/resolve.cu $(CSRC)/kernels/e
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HDRS := include/osp_c.h $(CSRC)/osp_internal.h $(CSRC)/kernels/common.cuh $(CSRC)/capi/handles.h
 
-.PHONY: all lib oracle ref clean
+# C++ façade of the reference pslab API (include/pslab/*.hpp) over the C-ABI
+CXX ?= g++
+FACADE := $(PKG)/libpslab_b200.so
+FACADE_SRCS := $(wildcard $(CSRC)/pslab/*.cpp)
+FACADE_OBJS := $(patsubst $(CSRC)/%.cpp,build/%.o,$(FACADE_SRCS))
+FACADE_HDRS := $(wildcard include/pslab/*.hpp) $(CSRC)/pslab/device.hpp include/osp_c.h
+CXXFLAGS_FACADE := -std=c++20 -O2 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude -I$(CSRC)/pslab
 
-all: lib oracle
+.PHONY: all lib facade oracle ref dropin clean
+
+all: lib facade oracle
 
 lib: $(LIB)
+
+facade: $(FACADE)
+
+build/pslab/%.o: $(CSRC)/pslab/%.cpp $(FACADE_HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS_FACADE) -c $< -o $@
+
+$(FACADE): $(FACADE_OBJS) $(LIB)
+	$(CXX) -shared -o $@ $(FACADE_OBJS) -L$(PKG) -losp_b200 -Wl,-rpath,'$$ORIGIN' \
+	    -Wl,-soname,libpslab_b200.so
+
+# drop-in proof: the reference harness/tests linked against the façade (needs /root/reference)
+dropin: $(FACADE)
+	$(MAKE) -C oracle -f Makefile.dropin
 
 build/%.o: $(CSRC)/%.cu $(HDRS)
 	@mkdir -p $(dir $@)

@@ -116,8 +116,8 @@ osp_status osp_synth_deltas(uint64_t seed, int n_workers, uint64_t iteration, ui
 
 /* lgp_partial (protocol.cpp:69-97) on flat vectors. ics_flags (HOST, one byte per
  * layer): 0 = the layer takes the global delta (p += 1.0f*global_delta),
- * 1 = local estimate (base = p; p += local_delta). base is written on flagged
- * layers only. */
+ * 1 = local estimate (base = p; p += local_delta), 2 = in neither payload
+ * (untouched). base is written on local layers only. */
 osp_status osp_lgp_partial(const osp_partition* part, float* params, const float* global_delta,
                            const float* local_delta, const uint8_t* ics_flags, float* base,
                            void* stream);

@@ -334,19 +334,21 @@ osp_status osp_lgp_partial(const osp_partition* part, float* params, const float
                            void* stream) {
     if (!part || !ics_flags) return fail(OSP_ERR_INVALID, "null argument");
     const size_t L = part->counts.size();
-    std::vector<uint64_t> off(L), cnt(L);
-    std::vector<uint8_t> loc(L);
+    std::vector<uint64_t> off, cnt;
+    std::vector<uint8_t> loc;
     for (size_t l = 0; l < L; ++l) {
-        off[l] = part->offsets[l];
-        cnt[l] = part->counts[l];
-        loc[l] = ics_flags[l] ? 1 : 0;
+        if (ics_flags[l] > 1) continue;  // 2: in neither payload, left untouched
+        off.push_back(part->offsets[l]);
+        cnt.push_back(part->counts[l]);
+        loc.push_back(ics_flags[l]);
     }
-    if (L > 65535) return fail(OSP_ERR_INVALID, "too many layers in one call");
+    if (off.empty()) return OSP_OK;
+    if (off.size() > 65535) return fail(OSP_ERR_INVALID, "too many layers in one call");
     cudaStream_t s = as_stream(stream);
     SegTable t;
     OSP_TRY(upload_segments(t, off, cnt, &loc, s));
     OSP_CUDA(launch_lgp_partial_segments(params, global_delta, local_delta, base, t.off, t.cnt, t.flag,
-                                         static_cast<int>(L), s));
+                                         static_cast<int>(off.size()), s));
     return OSP_OK;
 }
 
