@@ -675,7 +675,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     // bootstrap GIB: nothing deferred, tag 0 (first_iteration_bootstrap, protocol.cpp:58-63)
     if ((st = cu(launch_install_gib(v, g->d_order_tmp, 0, 0, s), "install bootstrap gib")) != OSP_OK)
         return cleanup(st);
-    g->blocks_per_sm = stage_blocks_per_sm(N);
+    g->blocks_per_sm = stage_blocks_per_sm(N, static_cast<int>(L));
     g->grid = sm_count() * g->blocks_per_sm;
     if ((st = cu(cudaStreamSynchronize(s), "group create")) != OSP_OK) return cleanup(st);
     *out = g;

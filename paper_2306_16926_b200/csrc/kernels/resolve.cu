@@ -136,9 +136,12 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         if (idx > nc - 1) idx = nc - 1;
         s.i1[r] = static_cast<int>(idx);
     }
+    // flags and chunk map are built in shared memory (pos / a2 are free here)
+    int* fl = s.pos;
+    int* cof = reinterpret_cast<int*>(s.a2);
     for (int l = tid; l < L; l += B) {
-        g.flags[l] = 0;
-        g.chunk_of[l] = -1;
+        fl[l] = 0;
+        cof[l] = -1;
     }
     __syncthreads();
     for (int r = tid; r < k; r += B) s.i2[r] = (r == 0 || s.i1[r] != s.i1[r - 1]) ? 1 : 0;
@@ -148,8 +151,8 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     for (int r = tid; r < k; r += B) {
         const int l = ord[r];
         const int c = s.i2[r] - 1;
-        g.flags[l] = 1;
-        g.chunk_of[l] = c;
+        fl[l] = 1;
+        cof[l] = c;
         g.ics_layers[r] = l;
         if (r == 0 || s.i2[r] != s.i2[r - 1]) g.chunk_begin[c] = r;
     }
@@ -158,15 +161,19 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     __syncthreads();
     block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, s.wtot);
     for (int r = tid; r <= k; r += B) g.ics_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
+    for (int l = tid; l < L; l += B) {
+        g.flags[l] = static_cast<uint8_t>(fl[l]);
+        g.chunk_of[l] = cof[l];
+    }
     // RS list: non-deferred layers in ascending id, with their tile prefix
     int n_rs = L - k;
     if (g.rs_layers) {
-        for (int l = tid; l < L; l += B) s.i2[l] = g.flags[l] ? 0 : 1;
+        for (int l = tid; l < L; l += B) s.i2[l] = fl[l] ? 0 : 1;
         __syncthreads();
         block_scan<int>(s.i2, L, 0, [](int a, int b) { return a + b; }, s.wtot);
         for (int l = tid; l < L; l += B) {
             const int excl = l == 0 ? 0 : s.i2[l - 1];
-            if (!g.flags[l]) {
+            if (!fl[l]) {
                 g.rs_layers[excl] = l;
                 s.i1[excl] = g.tile_base[l + 1] - g.tile_base[l];
             }
@@ -194,7 +201,7 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         uint8_t v = 0;
         for (int b = 0; b < 8; ++b) {
             const int l = byte * 8 + b;
-            if (l < L && g.flags[l]) v |= static_cast<uint8_t>(1u << b);
+            if (l < L && fl[l]) v |= static_cast<uint8_t>(1u << b);
         }
         g.gib_bytes[8 + byte] = v;
     }

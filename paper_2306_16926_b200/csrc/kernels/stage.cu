@@ -27,6 +27,9 @@
 // ahead), so the tail is a fraction of one tile however ragged the layer table
 // is; the last warp out resets the counter for the next launch.
 
+#include <mutex>
+#include <set>
+
 #include "common.cuh"
 
 namespace osp {
@@ -243,22 +246,120 @@ __device__ __forceinline__ void finish_tile(const GroupView& g, int t, double ac
     if (lane == 0) g.partials[t] = acc;
 }
 
+// ---- per-block layer tables ----------------------------------------------------
+// Each tile needs its layer's offset, size, first tile and flag, and (stage 2)
+// its position in the ICS list. Loading those from global memory is a chain of
+// dependent L2 round trips per tile (~1-2 us against ~13 us of streaming per
+// tile), so every block first copies the tables into shared memory (layouts up
+// to kSmemLayers layers) and resolves tiles there; larger layouts read global.
+
+constexpr int kSmemLayers = 2048;
+
+struct Tab {
+    const uint64_t* off;  // [L]
+    const uint64_t* cnt;  // [L]
+    const int* tb;        // [L+1] first tile of each layer
+    const uint8_t* flag;  // [L]
+    const int* sl;        // sequence layers [n]
+    const int* sp;        // sequence tile prefix [n+1]
+    int n;                // sequence length
+    int L;
+};
+
+size_t tab_smem_bytes(int L) {
+    return L <= kSmemLayers ? static_cast<size_t>(L) * 29 + 64 : 0;
+}
+
+// seq: layer list + tile prefix for positions [jb, je) (stage 2 / shard), or null.
+__device__ Tab load_tab(const GroupView& g, unsigned char* sm, const int* seq_layers,
+                        const int* seq_pref, int jb, int je) {
+    Tab t;
+    t.L = g.L;
+    t.n = je - jb;
+    if (g.L > kSmemLayers) {
+        t.off = g.offsets;
+        t.cnt = g.counts;
+        t.tb = g.tile_base;
+        t.flag = g.flags;
+        t.sl = seq_layers ? seq_layers + jb : nullptr;
+        t.sp = seq_pref ? seq_pref + jb : nullptr;
+        return t;
+    }
+    const int L = g.L;
+    uint64_t* off = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* cnt = off + L;
+    int* tb = reinterpret_cast<int*>(cnt + L);
+    int* sl = tb + L + 1;
+    int* sp = sl + L;
+    uint8_t* flag = reinterpret_cast<uint8_t*>(sp + L + 1);
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        off[i] = g.offsets[i];
+        cnt[i] = g.counts[i];
+        tb[i] = g.tile_base[i];
+        flag[i] = g.flags[i];
+    }
+    if (threadIdx.x == 0) tb[L] = g.tile_base[L];
+    if (seq_layers)
+        for (int i = threadIdx.x; i < t.n; i += blockDim.x) sl[i] = seq_layers[jb + i];
+    if (seq_pref)
+        for (int i = threadIdx.x; i <= t.n; i += blockDim.x) sp[i] = seq_pref[jb + i];
+    __syncthreads();
+    t.off = off;
+    t.cnt = cnt;
+    t.tb = tb;
+    t.flag = flag;
+    t.sl = sl;
+    t.sp = sp;
+    return t;
+}
+
+// global tile index -> layer (largest l with tb[l] <= t)
+__device__ __forceinline__ int tab_layer_of_tile(const Tab& tab, int t) {
+    int a = 0, b = tab.L - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (tab.tb[m] <= t) a = m;
+        else b = m - 1;
+    }
+    return a;
+}
+
+// sequence tile u (absolute prefix value) -> (layer, tile within layer)
+__device__ __forceinline__ void tab_seq_tile(const Tab& tab, int u, int& l, int& k) {
+    int a = 0, b = tab.n - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (tab.sp[m] <= u) a = m;
+        else b = m - 1;
+    }
+    l = tab.sl[a];
+    k = u - tab.sp[a];
+}
+
+__device__ __forceinline__ void tab_range(const Tab& tab, const GroupView& g, int l, int k,
+                                          uint64_t& s, uint64_t& e) {
+    const uint64_t lo = tab.off[l];
+    s = lo + static_cast<uint64_t>(k) * g.T;
+    e = min(s + static_cast<uint64_t>(g.T), lo + tab.cnt[l]);
+}
+
 // ---- kernels -------------------------------------------------------------------
 
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_stage1(GroupView g, AggParams ap,
                                                           const float* __restrict__ X,
                                                           uint64_t ldX, int vec) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
     const int lane = threadIdx.x & 31;
+    const Tab tab = load_tab(g, smem_tab, nullptr, nullptr, 0, 0);
     int* next = g.sched + SCHED_S1_NEXT;
     int t = grab(next, lane);
     while (t < g.NT) {
         const int tn = grab(next, lane);  // prefetch the next tile id
-        const int l = g.tile_layer[t];
-        const uint64_t lo = g.offsets[l];
-        const uint64_t s = lo + static_cast<uint64_t>(t - g.tile_base[l]) * g.T;
-        const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
-        if (g.flags[l]) {
+        const int l = tab_layer_of_tile(tab, t);
+        uint64_t s, e;
+        tab_range(tab, g, l, t - tab.tb[l], s, e);
+        if (tab.flag[l]) {
             warp_tile_local<NS>(g, ap, X, ldX, s, e, vec != 0, lane);
         } else {
             double acc = 0.0;
@@ -275,35 +376,28 @@ template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams ap,
                                                           const float* __restrict__ X,
                                                           uint64_t ldX, int c0, int c1, int vec) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_S2_NEXT;
     const int used = g.meta[META_N_USED];
     if (c1 > used) c1 = used;
-    int u0 = 0, u1 = 0, jb = 0, je = 0;
+    int jb = 0, je = 0;
     if (c0 < c1) {
         jb = g.chunk_begin[c0];
         je = g.chunk_begin[c1];
-        u0 = g.ics_tile_prefix[jb];
-        u1 = g.ics_tile_prefix[je];
     }
+    const Tab tab = load_tab(g, smem_tab, g.ics_layers, g.ics_tile_prefix, jb, je);
+    const int u0 = tab.n > 0 ? tab.sp[0] : 0, u1 = tab.n > 0 ? tab.sp[tab.n] : 0;
     int u = u0 + grab(next, lane);
     while (u < u1) {
         const int un = u0 + grab(next, lane);
-        // ICS list position a with ics_tile_prefix[a] <= u < ics_tile_prefix[a+1]
-        int a = jb, b = je - 1;
-        while (a < b) {
-            const int m = (a + b + 1) >> 1;
-            if (g.ics_tile_prefix[m] <= u) a = m;
-            else b = m - 1;
-        }
-        const int l = g.ics_layers[a];
-        const int k = u - g.ics_tile_prefix[a];
-        const uint64_t lo = g.offsets[l];
-        const uint64_t s = lo + static_cast<uint64_t>(k) * g.T;
-        const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
+        int l, k;
+        tab_seq_tile(tab, u, l, k);
+        uint64_t s, e;
+        tab_range(tab, g, l, k, s, e);
         double acc = 0.0;
         warp_tile_agg<NS>(g, ap, X, ldX, s, e, vec != 0, lane, acc);
-        finish_tile(g, g.tile_base[l] + k, acc, lane);
+        finish_tile(g, tab.tb[l] + k, acc, lane);
         u = un;
     }
     retire(next, g.sched + SCHED_S2_DONE, lane);
@@ -326,56 +420,31 @@ __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams
 // is split into P equal tile-count ranges, one per rank.
 // ===========================================================================
 
-// Sequence of (layer list, tile prefix) for a stage.
-struct StageSeq {
-    const int* layers;
-    const int* tprefix;
-    int jb, je;  // positions in the layer list
-};
-
-__device__ __forceinline__ StageSeq stage_seq(const GroupView& g, int stage, int c0, int c1) {
-    StageSeq q;
-    if (stage == 1) {
-        q.layers = g.rs_layers;
-        q.tprefix = g.rs_tile_prefix;
-        q.jb = 0;
-        q.je = g.meta[META_N_RS];
-    } else {
-        q.layers = g.ics_layers;
-        q.tprefix = g.ics_tile_prefix;
-        const int used = g.meta[META_N_USED];
-        if (c1 > used) c1 = used;
-        if (c0 >= c1) {
-            q.jb = q.je = 0;
-        } else {
-            q.jb = g.chunk_begin[c0];
-            q.je = g.chunk_begin[c1];
-        }
+// The stage's (layer list, tile prefix, positions [jb, je)): RS layers
+// ascending for stage 1, ICS chunks [c0, c1) in rank order for stage 2.
+__device__ __forceinline__ Tab stage_tab(const GroupView& g, unsigned char* sm, int stage, int c0,
+                                         int c1) {
+    if (stage == 1) return load_tab(g, sm, g.rs_layers, g.rs_tile_prefix, 0, g.meta[META_N_RS]);
+    const int used = g.meta[META_N_USED];
+    if (c1 > used) c1 = used;
+    int jb = 0, je = 0;
+    if (c0 < c1) {
+        jb = g.chunk_begin[c0];
+        je = g.chunk_begin[c1];
     }
-    return q;
-}
-
-// tile u of the sequence -> (layer, tile-in-layer)
-__device__ __forceinline__ void seq_tile(const StageSeq& q, int u, int& l, int& k) {
-    int a = q.jb, b = q.je - 1;
-    while (a < b) {
-        const int m = (a + b + 1) >> 1;
-        if (q.tprefix[m] <= u) a = m;
-        else b = m - 1;
-    }
-    l = q.layers[a];
-    k = u - q.tprefix[a];
+    return load_tab(g, sm, g.ics_layers, g.ics_tile_prefix, jb, je);
 }
 
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggParams ap,
                                                              PeerTable pt, int stage, int c0,
                                                              int c1, int vec) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_AGG_NEXT;
-    const StageSeq q = stage_seq(g, stage, c0, c1);
-    const int U0 = q.jb < q.je ? q.tprefix[q.jb] : 0;
-    const int U = q.jb < q.je ? q.tprefix[q.je] - U0 : 0;
+    const Tab tab = stage_tab(g, smem_tab, stage, c0, c1);
+    const int U0 = tab.n > 0 ? tab.sp[0] : 0;
+    const int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
     const int lo = U0 + static_cast<int>((static_cast<int64_t>(U) * pt.rank) / pt.world);
     const int hi = U0 + static_cast<int>((static_cast<int64_t>(U) * (pt.rank + 1)) / pt.world);
     const int n = nworkers<NS>(ap);
@@ -383,10 +452,9 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggPar
     while (u < hi) {
         const int un = lo + grab(next, lane);
         int l, k;
-        seq_tile(q, u, l, k);
-        const uint64_t base = g.offsets[l];
-        const uint64_t s = base + static_cast<uint64_t>(k) * g.T;
-        const uint64_t e = min(s + static_cast<uint64_t>(g.T), base + g.counts[l]);
+        tab_seq_tile(tab, u, l, k);
+        uint64_t s, e;
+        tab_range(tab, g, l, k, s, e);
         uint64_t he = e, be = e;
         if (vec) {
             he = min(e, (s + 3) & ~uint64_t(3));
@@ -485,16 +553,17 @@ __device__ void warp_tile_apply(const GroupView& g, int n_loc, uint64_t s, uint6
 __global__ void __launch_bounds__(kStageThreads) k_shard_apply1(GroupView g, AggParams ap_loc,
                                                                 const float* __restrict__ X,
                                                                 uint64_t ldX, int vec) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_S1_NEXT;
+    const Tab tab = load_tab(g, smem_tab, nullptr, nullptr, 0, 0);
     int t = grab(next, lane);
     while (t < g.NT) {
         const int tn = grab(next, lane);
-        const int l = g.tile_layer[t];
-        const uint64_t lo = g.offsets[l];
-        const uint64_t s = lo + static_cast<uint64_t>(t - g.tile_base[l]) * g.T;
-        const uint64_t e = min(s + static_cast<uint64_t>(g.T), lo + g.counts[l]);
-        if (g.flags[l]) {
+        const int l = tab_layer_of_tile(tab, t);
+        uint64_t s, e;
+        tab_range(tab, g, l, t - tab.tb[l], s, e);
+        if (tab.flag[l]) {
             warp_tile_local<0>(g, ap_loc, X, ldX, s, e, vec != 0, lane);
         } else {
             double acc = 0.0;
@@ -508,22 +577,22 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_apply1(GroupView g, Agg
 
 __global__ void __launch_bounds__(kStageThreads) k_shard_apply2(GroupView g, int n_loc, int c0,
                                                                 int c1, int vec) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_S2_NEXT;
-    const StageSeq q = stage_seq(g, 2, c0, c1);
-    const int U0 = q.jb < q.je ? q.tprefix[q.jb] : 0;
-    const int U1 = q.jb < q.je ? q.tprefix[q.je] : 0;
+    const Tab tab = stage_tab(g, smem_tab, 2, c0, c1);
+    const int U0 = tab.n > 0 ? tab.sp[0] : 0;
+    const int U1 = tab.n > 0 ? tab.sp[tab.n] : 0;
     int u = U0 + grab(next, lane);
     while (u < U1) {
         const int un = U0 + grab(next, lane);
         int l, k;
-        seq_tile(q, u, l, k);
-        const uint64_t base = g.offsets[l];
-        const uint64_t s = base + static_cast<uint64_t>(k) * g.T;
-        const uint64_t e = min(s + static_cast<uint64_t>(g.T), base + g.counts[l]);
+        tab_seq_tile(tab, u, l, k);
+        uint64_t s, e;
+        tab_range(tab, g, l, k, s, e);
         double acc = 0.0;
         warp_tile_apply(g, n_loc, s, e, vec != 0, lane, acc);
-        finish_tile(g, g.tile_base[l] + k, acc, lane);
+        finish_tile(g, tab.tb[l] + k, acc, lane);
         u = un;
     }
     retire(next, g.sched + SCHED_S2_DONE, lane);
@@ -586,12 +655,26 @@ cudaError_t dispatch_n(int n, K1&& k) {
 
 }  // namespace
 
-int stage_blocks_per_sm(int n_workers) {
+// Opt a kernel into the largest table size once (dynamic smem above 48 KB).
+cudaError_t allow_tab_smem(const void* fn) {
+    static std::mutex mu;
+    static std::set<const void*> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count(fn)) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(tab_smem_bytes(kSmemLayers)));
+    if (e == cudaSuccess) done.insert(fn);
+    return e;
+}
+
+int stage_blocks_per_sm(int n_workers, int n_layers) {
     int blocks = 0;
     cudaError_t e = dispatch_n(n_workers, [&](auto nc) -> cudaError_t {
         constexpr int NS = decltype(nc)::value;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_stage1<NS>,
-                                                             kStageThreads, 0);
+        cudaError_t r = allow_tab_smem(reinterpret_cast<const void*>(k_stage1<NS>));
+        if (r != cudaSuccess) return r;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k_stage1<NS>, kStageThreads,
+                                                             tab_smem_bytes(n_layers));
     });
     if (e != cudaSuccess || blocks < 1) blocks = 1;
     return blocks;
@@ -601,9 +684,12 @@ cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* 
                           int grid, cudaStream_t s) {
     const int vec = vec_ok(g, X, ldX) ? 1 : 0;
     if (grid < 1) return cudaSuccess;
+    const size_t sm = tab_smem_bytes(g.L);
     return dispatch_n(ap.n, [&](auto nc) -> cudaError_t {
         constexpr int NS = decltype(nc)::value;
-        k_stage1<NS><<<grid, kStageThreads, 0, s>>>(g, ap, X, ldX, vec);
+        cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_stage1<NS>));
+        if (e != cudaSuccess) return e;
+        k_stage1<NS><<<grid, kStageThreads, sm, s>>>(g, ap, X, ldX, vec);
         return cudaGetLastError();
     });
 }
@@ -612,9 +698,12 @@ cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* 
                           int c0, int c1, int grid, cudaStream_t s) {
     const int vec = vec_ok(g, X, ldX) ? 1 : 0;
     if (grid < 1) return cudaSuccess;
+    const size_t sm = tab_smem_bytes(g.L);
     return dispatch_n(ap.n, [&](auto nc) -> cudaError_t {
         constexpr int NS = decltype(nc)::value;
-        k_stage2<NS><<<grid, kStageThreads, 0, s>>>(g, ap, X, ldX, c0, c1, vec);
+        cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_stage2<NS>));
+        if (e != cudaSuccess) return e;
+        k_stage2<NS><<<grid, kStageThreads, sm, s>>>(g, ap, X, ldX, c0, c1, vec);
         return cudaGetLastError();
     });
 }
@@ -625,9 +714,12 @@ cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const Peer
     for (int w = 0; w < ap.n; ++w) vec = vec && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
     for (int r = 0; r < pt.world; ++r) vec = vec && (reinterpret_cast<uintptr_t>(pt.agg[r]) % 16 == 0);
     if (grid < 1) return cudaSuccess;
+    const size_t sm = tab_smem_bytes(g.L);
     return dispatch_n(ap.n, [&](auto nc) -> cudaError_t {
         constexpr int NS = decltype(nc)::value;
-        k_shard_agg<NS><<<grid, kStageThreads, 0, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0);
+        cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_agg<NS>));
+        if (e != cudaSuccess) return e;
+        k_shard_agg<NS><<<grid, kStageThreads, sm, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0);
         return cudaGetLastError();
     });
 }
@@ -636,10 +728,15 @@ cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, cons
                                uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s) {
     const bool vec = vec_ok(g, Xloc, ldX) && (reinterpret_cast<uintptr_t>(g.agg_full) % 16 == 0);
     if (grid < 1) return cudaSuccess;
-    if (stage == 1)
-        k_shard_apply1<<<grid, kStageThreads, 0, s>>>(g, ap_loc, Xloc, ldX, vec ? 1 : 0);
-    else
-        k_shard_apply2<<<grid, kStageThreads, 0, s>>>(g, ap_loc.n, c0, c1, vec ? 1 : 0);
+    const size_t sm = tab_smem_bytes(g.L);
+    cudaError_t e;
+    if (stage == 1) {
+        if ((e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_apply1))) != cudaSuccess) return e;
+        k_shard_apply1<<<grid, kStageThreads, sm, s>>>(g, ap_loc, Xloc, ldX, vec ? 1 : 0);
+    } else {
+        if ((e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_apply2))) != cudaSuccess) return e;
+        k_shard_apply2<<<grid, kStageThreads, sm, s>>>(g, ap_loc.n, c0, c1, vec ? 1 : 0);
+    }
     return cudaGetLastError();
 }
 

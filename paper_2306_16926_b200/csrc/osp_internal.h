@@ -135,7 +135,7 @@ cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t 
 // Rebuild device lists from g.flags + the given rank-ordered ICS ids (device).
 cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,
                                cudaStream_t s);
-int stage_blocks_per_sm(int n_workers);
+int stage_blocks_per_sm(int n_workers, int n_layers);
 
 cudaError_t launch_aggregate_layer(const float* const* contribs, const AggParams& ap, uint64_t n,
                                    float* out, cudaStream_t s);

@@ -1,0 +1,150 @@
+"""CPU (gloo, world_size 2) test of the multi-GPU decomposition's host logic.
+
+Mirrors what osp_shard_* does on the device, with torch.distributed over gloo as
+the transport: per stage, the tile sequence (RS layers ascending for stage 1,
+ICS chunks in rank order for stage 2; tiles of T elements that never straddle a
+layer) is split into P equal tile-count ranges (k_shard_agg); the owner
+aggregates its range over ALL workers in the fixed ascending worker order
+(fp64, oracle.aggregate_layer); the aggregates are all-gathered; every rank
+applies G += agg and its own workers' rows. Asserts bit-equality with the
+single-process oracle step (global vector, every rank's worker rows, next GIB)
+and that the owner ranges cover every element of every stage exactly once.
+"""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def stage_sequences(counts, flags, order, n_chunks, bpe, T):
+    """[(stage, [(layer, start, end), ...tiles in sequence order]), ...]"""
+    from oracle import oracle
+    offsets = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
+
+    def tiles_of(layers):
+        out = []
+        for l in layers:
+            for s in range(0, int(counts[l]), T):
+                out.append((l, int(offsets[l]) + s, int(offsets[l]) + min(s + T, int(counts[l]))))
+        return out
+
+    rs = [l for l in range(len(counts)) if not flags[l]]
+    seqs = [(1, tiles_of(rs))]
+    _, chunk_of, used = oracle.split(counts, bpe, flags, order, n_chunks)
+    ics_order = [l for l in order if flags[l]] + [l for l in range(len(counts))
+                                                  if flags[l] and l not in set(order)]
+    for c in range(used):
+        seqs.append((2, tiles_of([l for l in ics_order if chunk_of[l] == c])))
+    return seqs
+
+
+def _rank_main(rank, world, port, cfg, q):
+    try:
+        sys.path.insert(0, REPO)
+        from oracle import oracle
+        dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                                world_size=world)
+        counts = np.asarray(cfg["counts"], dtype=np.uint64)
+        N, M, nc, T = cfg["N"], int(counts.sum()), cfg["chunks"], cfg["T"]
+        n_loc = N // world
+        w = cfg["weights"]
+        budget = int(cfg["budget_frac"] * M * 4)
+        G = np.zeros(M, np.float32)
+        P_all = np.zeros((N, M), np.float32)  # oracle reference state (all workers)
+        G_mine = G.copy()
+        P_mine = np.zeros((n_loc, M), np.float32)
+        flags = np.zeros(len(counts), np.uint8)
+        order = np.zeros(0, np.int32)
+        for it in range(cfg["iters"]):
+            mine = np.stack([oracle.synth_delta(cfg["seed"], rank * n_loc + i, it, M)
+                             for i in range(n_loc)])
+            # transport: every rank sees every worker's rows (peer loads on the GPU)
+            gathered = [torch.zeros((n_loc, M), dtype=torch.float32) for _ in range(world)]
+            dist.all_gather(gathered, torch.from_numpy(mine))
+            X = np.concatenate([g.numpy() for g in gathered])
+            agg = np.zeros(M, np.float32)
+            covered = np.zeros(M, np.int32)
+            for stage, tiles in stage_sequences(counts, flags, order, nc, 4, T):
+                U = len(tiles)
+                lo, hi = (U * rank) // world, (U * (rank + 1)) // world
+                part = np.zeros(M, np.float32)
+                for (l, s, e) in tiles[lo:hi]:
+                    part[s:e] = oracle.aggregate_layer([X[k][s:e] for k in range(N)], w)
+                    covered[s:e] += 1
+                got = [torch.zeros(M, dtype=torch.float32) for _ in range(world)]
+                dist.all_gather(got, torch.from_numpy(part))
+                cov = [torch.zeros(M, dtype=torch.int32) for _ in range(world)]
+                dist.all_gather(cov, torch.from_numpy(covered))
+                for r, t in enumerate(got):
+                    lo_r, hi_r = (U * r) // world, (U * (r + 1)) // world
+                    for (l, s, e) in tiles[lo_r:hi_r]:
+                        agg[s:e] = t.numpy()[s:e]
+                if stage == 1:
+                    # barrier: RS elements G' = G + agg; ICS elements local estimate
+                    rs_mask = np.zeros(M, bool)
+                    for (l, s, e) in tiles:
+                        rs_mask[s:e] = True
+                    G_new = G_mine.copy()
+                    G_new[rs_mask] = (G_mine[rs_mask] + agg[rs_mask]).astype(np.float32)
+                    for i in range(n_loc):
+                        P_mine[i] = np.where(rs_mask, G_new, (G_mine + X[rank * n_loc + i]).astype(np.float32))
+                    G_mine = G_new
+                else:
+                    sel = np.zeros(M, bool)
+                    for (l, s, e) in tiles:
+                        sel[s:e] = True
+                    G_mine[sel] = (G_mine[sel] + agg[sel]).astype(np.float32)
+                    for i in range(n_loc):
+                        P_mine[i][sel] = G_mine[sel]
+            total_cov = sum(c.numpy() for c in cov)
+            assert np.all(total_cov == 1), "owner ranges must cover every element exactly once"
+            r = oracle.step(counts, 4, w, X, G, P_all, flags, order, nc, budget)
+            assert np.array_equal(G_mine.view(np.uint32), G.view(np.uint32)), f"G it {it}"
+            mine_ref = P_all[rank * n_loc:(rank + 1) * n_loc]
+            assert np.array_equal(P_mine.view(np.uint32), mine_ref.view(np.uint32)), f"P it {it}"
+            # every rank resolves the identical GIB from its replica (no exchange)
+            scores = oracle.pgp(counts, G_mine, agg)
+            flags_mine = oracle.build_gib(scores, counts, 4, budget)
+            assert np.array_equal(flags_mine, r["flags_out"])
+            flags, order = r["flags_out"], r["order_out"]
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, "ok"))
+    except Exception:
+        import traceback
+        q.put((rank, traceback.format_exc()))
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(counts=[700, 64, 1000, 3, 2048, 129, 512, 77], N=4, weights=[0.25] * 4, chunks=3,
+         budget_frac=0.5, iters=3, seed=11, T=256),
+    dict(counts=[100, 7, 300, 33, 64, 5, 17, 999], N=2, weights=[0.3, 0.9], chunks=4,
+         budget_frac=0.8, iters=3, seed=5, T=64),
+])
+def test_sharded_decomposition_gloo(cfg):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, cfg, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    bad = {r: m for r, m in res.items() if m != "ok"}
+    assert not bad, bad
