@@ -244,6 +244,45 @@ osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
     return osp_shard_resolve(s, buf, stream);
 }
 
+osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream) {
+    OSP_TRY(check_ready(s, buf));
+    if (!ms) return fail(OSP_ERR_INVALID, "null output");
+    cudaStream_t st = as_stream(stream);
+    osp_group* g = s->grp;
+    cudaEvent_t ev[9];
+    for (auto& e : ev) OSP_CUDA(cudaEventCreate(&e));
+    osp_status rc = OSP_OK;
+    auto step = [&]() -> cudaError_t {
+        cudaError_t e;
+        float* Xb = s->X + buf * s->buf_stride;
+        if ((e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
+        if ((e = launch_barrier(s->pt[buf], 0, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+        if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
+        if ((e = launch_barrier(s->pt[buf], 1, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
+        if ((e = launch_shard_apply(g->v, s->ap_loc, Xb, s->ldX, 1, 0, 0, g->grid, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
+        if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, 0, s->n_chunks, g->grid, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[5], st)) != cudaSuccess) return e;
+        if ((e = launch_barrier(s->pt[buf], 2, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[6], st)) != cudaSuccess) return e;
+        if ((e = launch_shard_apply(g->v, s->ap_loc, Xb, s->ldX, 2, 0, s->n_chunks, g->grid, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[7], st)) != cudaSuccess) return e;
+        if ((e = launch_resolve(g->v, g->ap, Xb, s->ldX, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[8], st)) != cudaSuccess) return e;
+        if ((e = cudaEventSynchronize(ev[8])) != cudaSuccess) return e;
+        for (int i = 0; i < 8; ++i)
+            if ((e = cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1])) != cudaSuccess) return e;
+        return cudaSuccess;
+    };
+    cudaError_t e = step();
+    if (e != cudaSuccess) rc = cuda_fail(e, "shard profile");
+    for (auto& x : ev) cudaEventDestroy(x);
+    return rc;
+}
+
 osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
                                   uint64_t n, float* out, uint64_t ld, void* stream) {
     if (worker0 < 0 || n_workers < 0 || n_workers > 65535)

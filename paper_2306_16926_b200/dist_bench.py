@@ -95,6 +95,15 @@ def run(args, metric: str, unit: str):
     # rank's shard + its aggregate stored to the other ranks
     nvl_bytes = 4.0 * M * ((N - n_loc) / world + (world - 1) / world)
 
+    # ---- per-phase breakdown (events between kernels, 5 profiled steps, max over ranks)
+    phases = None
+    prof = [sh.profile(k % 2) for k in range(5)]
+    keys = list(prof[0])
+    pt = torch.tensor([sum(p[k] for p in prof) / len(prof) for k in keys], dtype=torch.float64,
+                      device="cuda")
+    dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+    phases = {k: float(v) for k, v in zip(keys, pt.tolist())}
+
     # ---- e2e: pinned host deltas -> device (this rank's rows), step, GIB read-back
     host = [sh.deltas(b).cpu().pin_memory() for b in range(2)]
     gib = torch.empty(8 + (L + 7) // 8, dtype=torch.uint8).pin_memory()
@@ -142,6 +151,7 @@ def run(args, metric: str, unit: str):
                          "hbm_gbs_per_gpu": hbm_gbs, "hbm_frac": hbm_gbs / hbm_peak},
             "breakdown_ms": {"stage1": s1_max, "stage2": s2_max,
                              "resolve": ms_step - s1_max - s2_max},
+            "phase_ms": phases,
             "u_mean": u_mean,
             "e2e": {"value": M / (e2e_ms * 1e-3), "unit": unit, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": n_loc * M * 4 * world,
