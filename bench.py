@@ -45,6 +45,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-chunk", action="store_true", help="one stage-2 launch per ICS chunk")
     ap.add_argument("--cpu-iters", type=int, default=3)
+    ap.add_argument("--overlap-ms", type=float, default=2.0,
+                    help="synthetic compute t_c for the stage-2 overlap report (0 = skip)")
     return ap.parse_args()
 
 
@@ -257,6 +259,19 @@ def b200_single(args):
     stats = grp.stats()
     launches_per_step = 1 + (args.chunks if args.per_chunk else 1) + 1  # stage1, stage2, resolve
 
+    # ---- stage 2 overlapped with the next iteration's (synthetic) compute
+    ovl = None
+    if args.overlap_ms > 0:
+        from paper_2306_16926_b200 import overlap
+        comp = overlap.SyntheticCompute(args.overlap_ms)
+
+        def s2r(i):
+            grp.stage2_all(X[i % 2])
+            grp.resolve(X[i % 2])
+
+        ovl = overlap.run(lambda i: grp.stage1(X[i % 2]), s2r, comp, K=min(K, 50), W=3)
+        ovl["t_c_ms"] = comp.ms
+
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + step + D2H of the GIB
     # one pinned host set for small layouts two; the 1B layout's 40 GB set is pinned once
     n_sets = 2 if N * M * 4 <= (8 << 30) else 1
@@ -296,6 +311,7 @@ def b200_single(args):
         "gpu_launches": launches_per_step * K,
         "certificate": stats,
         "clocks": clk,
+        "overlap": ovl,
     }
     if not args.no_cpu_baseline:
         try:

@@ -470,21 +470,41 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggPar
             const float a = agg_finish(ap, acc);
             for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
         }
-        for (uint64_t f = he + 4ull * lane; f < be; f += 128) {
-            float4 xs[NS > 0 ? NS : 1];
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            if constexpr (NS > 0) {
-#pragma unroll
-                for (int w = 0; w < NS; ++w) xs[w] = ld_stream4(pt.xrow[w] + f);
+        if constexpr (NS > 0) {
+            // two quads per lane in flight: NVLink peer loads have ~2 us latency
+            for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 256) {
+                const uint64_t f1 = f0 + 128;
+                const bool has1 = f1 < be;
+                float4 xa[NS], xb[NS];
 #pragma unroll
                 for (int w = 0; w < NS; ++w) {
-                    const float4 v = cvt4(ap, xs[w]);
-                    s0 = agg_acc(s0, ap.w[w], v.x);
-                    s1 = agg_acc(s1, ap.w[w], v.y);
-                    s2 = agg_acc(s2, ap.w[w], v.z);
-                    s3 = agg_acc(s3, ap.w[w], v.w);
+                    xa[w] = ld_stream4(pt.xrow[w] + f0);
+                    if (has1) xb[w] = ld_stream4(pt.xrow[w] + f1);
                 }
-            } else {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (q == 1 && !has1) break;
+                    const float4* xs = q == 0 ? xa : xb;
+                    const uint64_t f = q == 0 ? f0 : f1;
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+                    for (int w = 0; w < NS; ++w) {
+                        const float4 v = cvt4(ap, xs[w]);
+                        s0 = agg_acc(s0, ap.w[w], v.x);
+                        s1 = agg_acc(s1, ap.w[w], v.y);
+                        s2 = agg_acc(s2, ap.w[w], v.z);
+                        s3 = agg_acc(s3, ap.w[w], v.w);
+                    }
+                    const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
+                                                 agg_finish(ap, s2), agg_finish(ap, s3));
+                    for (int r = 0; r < pt.world; ++r)
+                        *reinterpret_cast<float4*>(pt.agg[r] + f) = a;
+                }
+            }
+        }
+        for (uint64_t f = he + 4ull * lane; NS == 0 && f < be; f += 128) {
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            {
                 for (int w = 0; w < n; ++w) {
                     const float4 v = cvt4(ap, ld_stream4(pt.xrow[w] + f));
                     s0 = agg_acc(s0, ap.w[w], v.x);

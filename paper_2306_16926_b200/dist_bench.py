@@ -104,6 +104,24 @@ def run(args, metric: str, unit: str):
     dist.all_reduce(pt, op=dist.ReduceOp.MAX)
     phases = {k: float(v) for k, v in zip(keys, pt.tolist())}
 
+    # ---- stage 2 overlapped with the next iteration's (synthetic) compute
+    ovl = None
+    if args.overlap_ms > 0:
+        from . import overlap
+        comp = overlap.SyntheticCompute(args.overlap_ms)
+
+        def s2r(i):
+            sh.stage2(i % 2)
+            sh.resolve(i % 2)
+
+        res = overlap.run(lambda i: sh.stage1(i % 2), s2r, comp, K=min(K, 50), W=3)
+        sh.check()
+        keys = ["iter_ms_overlapped", "iter_ms_serial", "exposed_stage2_ms_mean",
+                "exposed_stage2_ms_max", "stage2_plus_resolve_ms_mean"]
+        ot = torch.tensor([res[k] for k in keys] + [comp.ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(ot, op=dist.ReduceOp.MAX)
+        ovl = {k: float(v) for k, v in zip(keys + ["t_c_ms"], ot.tolist())}
+
     # ---- e2e: pinned host deltas -> device (this rank's rows), step, GIB read-back
     host = [sh.deltas(b).cpu().pin_memory() for b in range(2)]
     gib = torch.empty(8 + (L + 7) // 8, dtype=torch.uint8).pin_memory()
@@ -152,6 +170,7 @@ def run(args, metric: str, unit: str):
             "breakdown_ms": {"stage1": s1_max, "stage2": s2_max,
                              "resolve": ms_step - s1_max - s2_max},
             "phase_ms": phases,
+            "overlap": ovl,
             "u_mean": u_mean,
             "e2e": {"value": M / (e2e_ms * 1e-3), "unit": unit, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": n_loc * M * 4 * world,
