@@ -25,6 +25,24 @@ __device__ __forceinline__ float ld_stream1(const float* p) {
     return r;
 }
 
+// Loads from peer GPUs' HBM over NVLink (CUDA IPC mappings): mode 0 = nc /
+// no_allocate (as local streaming), 1 = .cg (L2 only), 2 = default caching.
+__device__ __forceinline__ float4 ld_peer4(const float* p, int mode) {
+    float4 r;
+    if (mode == 1) {
+        asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p));
+    } else if (mode == 2) {
+        asm volatile("ld.global.v4.f32 {%0,%1,%2,%3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                     : "l"(p));
+    } else {
+        r = ld_stream4(p);
+    }
+    return r;
+}
+
 __device__ __forceinline__ void st_stream4(float* p, float4 v) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
                  "f"(v.z), "f"(v.w)

@@ -478,8 +478,8 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggPar
                 float4 xa[NS], xb[NS];
 #pragma unroll
                 for (int w = 0; w < NS; ++w) {
-                    xa[w] = ld_stream4(pt.xrow[w] + f0);
-                    if (has1) xb[w] = ld_stream4(pt.xrow[w] + f1);
+                    xa[w] = ld_peer4(pt.xrow[w] + f0, pt.ldmode);
+                    if (has1) xb[w] = ld_peer4(pt.xrow[w] + f1, pt.ldmode);
                 }
 #pragma unroll
                 for (int q = 0; q < 2; ++q) {

@@ -110,6 +110,7 @@ struct PeerTable {
     int world;
     int rank;
     int n_loc;                                   // workers hosted per rank
+    int ldmode;                                  // peer load flavour (common.cuh ld_peer4)
     const float* xrow[OSP_MAX_WORKERS];          // delta row of every worker (peer or local)
     float* agg[kMaxRanks];                       // every rank's agg_full buffer
     unsigned* flags[kMaxRanks];                  // every rank's barrier slots [kBarKinds][kMaxRanks]
