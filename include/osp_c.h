@@ -292,9 +292,10 @@ osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream);
 osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream);
 osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream);
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream);
-/* One step with CUDA events between the kernels; ms[0..7] = barrier-in,
- * stage-1 aggregate, barrier, stage-1 apply, stage-2 aggregate (all chunks),
- * barrier, stage-2 apply, resolve (synchronises `stream`). */
+/* One osp_shard_step with CUDA events between the kernels; ms[0..7] =
+ * barrier-in, stage-1 aggregate, barrier, stage-1 apply fused with the stage-2
+ * aggregate (all chunks), 0 (unused), barrier, stage-2 apply, resolve
+ * (synchronises `stream`). */
 osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream);
 /* ProtocolError if a cross-GPU barrier timed out (synchronises `stream`). */
 osp_status osp_shard_check(osp_shard* s, void* stream);

@@ -241,9 +241,21 @@ osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
     return osp_group_resolve(s->grp, s->X + buf * s->buf_stride, s->ldX, stream);
 }
 
+// Whole iteration with stage 2's push/pull running inside the stage-1 apply
+// launch (k_shard_fused): barrier, agg1, barrier, apply1 || agg2, barrier,
+// apply2, resolve. Same results as stage1 + stage2 + resolve.
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
-    OSP_TRY(osp_shard_stage1(s, buf, stream));
-    OSP_TRY(osp_shard_stage2(s, 0, s->n_chunks, buf, stream));
+    OSP_TRY(check_ready(s, buf));
+    cudaStream_t st = as_stream(stream);
+    osp_group* g = s->grp;
+    float* Xb = s->X + buf * s->buf_stride;
+    OSP_CUDA(launch_barrier(s->pt[buf], 0, st));
+    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st));
+    OSP_CUDA(launch_barrier(s->pt[buf], 1, st));
+    OSP_CUDA(launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0, s->n_chunks,
+                                g->grid, st));
+    OSP_CUDA(launch_barrier(s->pt[buf], 2, st));
+    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, Xb, s->ldX, 2, 0, s->n_chunks, g->grid, st));
     return osp_shard_resolve(s, buf, stream);
 }
 
@@ -265,9 +277,9 @@ osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream) {
         if ((e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
         if ((e = launch_barrier(s->pt[buf], 1, st)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_apply(g->v, s->ap_loc, Xb, s->ldX, 1, 0, 0, g->grid, st)) != cudaSuccess) return e;
+        if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0,
+                                    s->n_chunks, g->grid, st)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, 0, s->n_chunks, g->grid, st)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ev[5], st)) != cudaSuccess) return e;
         if ((e = launch_barrier(s->pt[buf], 2, st)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ev[6], st)) != cudaSuccess) return e;

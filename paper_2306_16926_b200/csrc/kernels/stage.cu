@@ -435,6 +435,87 @@ __device__ __forceinline__ Tab stage_tab(const GroupView& g, unsigned char* sm, 
     return load_tab(g, sm, g.ics_layers, g.ics_tile_prefix, jb, je);
 }
 
+// The owner's part of the push/pull for elements [s, e): read every worker's
+// row (local or peer HBM over NVLink), aggregate in the fixed worker order,
+// store the fp32 aggregate into every rank's agg buffer.
+template <int NS>
+__device__ void peer_agg_range(const AggParams& ap, const PeerTable& pt, uint64_t s, uint64_t e,
+                               bool vec, int lane) {
+    const int n = nworkers<NS>(ap);
+    uint64_t he = e, be = e;
+    if (vec) {
+        he = min(e, (s + 3) & ~uint64_t(3));
+        be = he + ((e - he) & ~uint64_t(3));
+    }
+    for (uint64_t f = s + lane; f < he; f += 32) {
+        double acc = 0.0;
+        for (int w = 0; w < n; ++w) {
+            float x = ld_stream1(pt.xrow[w] + f);
+            if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+            acc = agg_acc(acc, ap.w[w], x);
+        }
+        const float a = agg_finish(ap, acc);
+        for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
+    }
+    if constexpr (NS > 0) {
+        // two quads per lane in flight: NVLink peer loads have ~2 us latency
+        for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 256) {
+            const uint64_t f1 = f0 + 128;
+            const bool has1 = f1 < be;
+            float4 xa[NS], xb[NS];
+#pragma unroll
+            for (int w = 0; w < NS; ++w) {
+                xa[w] = ld_peer4(pt.xrow[w] + f0, pt.ldmode);
+                if (has1) xb[w] = ld_peer4(pt.xrow[w] + f1, pt.ldmode);
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                if (q == 1 && !has1) break;
+                const float4* xs = q == 0 ? xa : xb;
+                const uint64_t f = q == 0 ? f0 : f1;
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+                for (int w = 0; w < NS; ++w) {
+                    const float4 v = cvt4(ap, xs[w]);
+                    s0 = agg_acc(s0, ap.w[w], v.x);
+                    s1 = agg_acc(s1, ap.w[w], v.y);
+                    s2 = agg_acc(s2, ap.w[w], v.z);
+                    s3 = agg_acc(s3, ap.w[w], v.w);
+                }
+                const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
+                                             agg_finish(ap, s2), agg_finish(ap, s3));
+                for (int r = 0; r < pt.world; ++r)
+                    *reinterpret_cast<float4*>(pt.agg[r] + f) = a;
+            }
+        }
+    }
+    for (uint64_t f = he + 4ull * lane; NS == 0 && f < be; f += 128) {
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        {
+            for (int w = 0; w < n; ++w) {
+                const float4 v = cvt4(ap, ld_stream4(pt.xrow[w] + f));
+                s0 = agg_acc(s0, ap.w[w], v.x);
+                s1 = agg_acc(s1, ap.w[w], v.y);
+                s2 = agg_acc(s2, ap.w[w], v.z);
+                s3 = agg_acc(s3, ap.w[w], v.w);
+            }
+        }
+        const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
+                                     agg_finish(ap, s2), agg_finish(ap, s3));
+        for (int r = 0; r < pt.world; ++r) *reinterpret_cast<float4*>(pt.agg[r] + f) = a;
+    }
+    for (uint64_t f = be + lane; f < e; f += 32) {
+        double acc = 0.0;
+        for (int w = 0; w < n; ++w) {
+            float x = ld_stream1(pt.xrow[w] + f);
+            if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+            acc = agg_acc(acc, ap.w[w], x);
+        }
+        const float a = agg_finish(ap, acc);
+        for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
+    }
+}
+
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggParams ap,
                                                              PeerTable pt, int stage, int c0,
@@ -447,7 +528,6 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggPar
     const int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
     const int lo = U0 + static_cast<int>((static_cast<int64_t>(U) * pt.rank) / pt.world);
     const int hi = U0 + static_cast<int>((static_cast<int64_t>(U) * (pt.rank + 1)) / pt.world);
-    const int n = nworkers<NS>(ap);
     int u = lo + grab(next, lane);
     while (u < hi) {
         const int un = lo + grab(next, lane);
@@ -455,78 +535,7 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggPar
         tab_seq_tile(tab, u, l, k);
         uint64_t s, e;
         tab_range(tab, g, l, k, s, e);
-        uint64_t he = e, be = e;
-        if (vec) {
-            he = min(e, (s + 3) & ~uint64_t(3));
-            be = he + ((e - he) & ~uint64_t(3));
-        }
-        for (uint64_t f = s + lane; f < he; f += 32) {
-            double acc = 0.0;
-            for (int w = 0; w < n; ++w) {
-                float x = ld_stream1(pt.xrow[w] + f);
-                if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
-                acc = agg_acc(acc, ap.w[w], x);
-            }
-            const float a = agg_finish(ap, acc);
-            for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
-        }
-        if constexpr (NS > 0) {
-            // two quads per lane in flight: NVLink peer loads have ~2 us latency
-            for (uint64_t f0 = he + 4ull * lane; f0 < be; f0 += 256) {
-                const uint64_t f1 = f0 + 128;
-                const bool has1 = f1 < be;
-                float4 xa[NS], xb[NS];
-#pragma unroll
-                for (int w = 0; w < NS; ++w) {
-                    xa[w] = ld_peer4(pt.xrow[w] + f0, pt.ldmode);
-                    if (has1) xb[w] = ld_peer4(pt.xrow[w] + f1, pt.ldmode);
-                }
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                    if (q == 1 && !has1) break;
-                    const float4* xs = q == 0 ? xa : xb;
-                    const uint64_t f = q == 0 ? f0 : f1;
-                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-                    for (int w = 0; w < NS; ++w) {
-                        const float4 v = cvt4(ap, xs[w]);
-                        s0 = agg_acc(s0, ap.w[w], v.x);
-                        s1 = agg_acc(s1, ap.w[w], v.y);
-                        s2 = agg_acc(s2, ap.w[w], v.z);
-                        s3 = agg_acc(s3, ap.w[w], v.w);
-                    }
-                    const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
-                                                 agg_finish(ap, s2), agg_finish(ap, s3));
-                    for (int r = 0; r < pt.world; ++r)
-                        *reinterpret_cast<float4*>(pt.agg[r] + f) = a;
-                }
-            }
-        }
-        for (uint64_t f = he + 4ull * lane; NS == 0 && f < be; f += 128) {
-            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-            {
-                for (int w = 0; w < n; ++w) {
-                    const float4 v = cvt4(ap, ld_stream4(pt.xrow[w] + f));
-                    s0 = agg_acc(s0, ap.w[w], v.x);
-                    s1 = agg_acc(s1, ap.w[w], v.y);
-                    s2 = agg_acc(s2, ap.w[w], v.z);
-                    s3 = agg_acc(s3, ap.w[w], v.w);
-                }
-            }
-            const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
-                                         agg_finish(ap, s2), agg_finish(ap, s3));
-            for (int r = 0; r < pt.world; ++r) *reinterpret_cast<float4*>(pt.agg[r] + f) = a;
-        }
-        for (uint64_t f = be + lane; f < e; f += 32) {
-            double acc = 0.0;
-            for (int w = 0; w < n; ++w) {
-                float x = ld_stream1(pt.xrow[w] + f);
-                if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
-                acc = agg_acc(acc, ap.w[w], x);
-            }
-            const float a = agg_finish(ap, acc);
-            for (int r = 0; r < pt.world; ++r) pt.agg[r][f] = a;
-        }
+        peer_agg_range<NS>(ap, pt, s, e, vec != 0, lane);
         u = un;
     }
     __threadfence_system();  // peer stores visible before the barrier kernel signals
@@ -616,6 +625,79 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_apply2(GroupView g, int
         u = un;
     }
     retire(next, g.sched + SCHED_S2_DONE, lane);
+}
+
+// Stage-1 apply fused with the stage-2 push/pull. The two are independent
+// (disjoint elements of agg_full and G; both only read the deltas), and one is
+// HBM-bound (apply) while the other is NVLink-bound (peer aggregate), so one
+// launch runs both: even warps start on the apply tiles, odd warps on this
+// rank's stage-2 aggregate tiles, and a warp whose list runs dry switches to
+// the other. The last warp out resets both work counters.
+template <int NS>
+__global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggParams ap_all,
+                                                               AggParams ap_loc, PeerTable pt,
+                                                               const float* __restrict__ X,
+                                                               uint64_t ldX, int c0, int c1,
+                                                               int vec_apply, int vec_agg) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
+    const int lane = threadIdx.x & 31;
+    const Tab tab = stage_tab(g, smem_tab, 2, c0, c1);
+    const int U0 = tab.n > 0 ? tab.sp[0] : 0;
+    const int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
+    const int lo = U0 + static_cast<int>((static_cast<int64_t>(U) * pt.rank) / pt.world);
+    const int hi = U0 + static_cast<int>((static_cast<int64_t>(U) * (pt.rank + 1)) / pt.world);
+    int* next_apply = g.sched + SCHED_S1_NEXT;
+    int* next_agg = g.sched + SCHED_AGG_NEXT;
+    auto fetch = [&](int list) -> int {
+        if (list == 0) {
+            const int t = grab(next_apply, lane);
+            return t < g.NT ? t : -1;
+        }
+        const int u = lo + grab(next_agg, lane);
+        return u < hi ? u : -1;
+    };
+    int list = ((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) & 1;
+    int dry = 0;
+    int cur = fetch(list);
+    while (true) {
+        if (cur < 0) {
+            dry |= 1 << list;
+            if (dry == 3) break;
+            list ^= 1;
+            cur = fetch(list);
+            continue;
+        }
+        const int nxt = fetch(list);
+        if (list == 0) {
+            const int t = cur;
+            const int l = tab_layer_of_tile(tab, t);
+            uint64_t s, e;
+            tab_range(tab, g, l, t - tab.tb[l], s, e);
+            if (tab.flag[l]) {
+                warp_tile_local<0>(g, ap_loc, X, ldX, s, e, vec_apply != 0, lane);
+            } else {
+                double acc = 0.0;
+                warp_tile_apply(g, ap_loc.n, s, e, vec_apply != 0, lane, acc);
+                finish_tile(g, t, acc, lane);
+            }
+        } else {
+            int l, k;
+            tab_seq_tile(tab, cur, l, k);
+            uint64_t s, e;
+            tab_range(tab, g, l, k, s, e);
+            peer_agg_range<NS>(ap_all, pt, s, e, vec_agg != 0, lane);
+        }
+        cur = nxt;
+    }
+    __threadfence_system();
+    if (lane == 0) {
+        const int total = static_cast<int>(gridDim.x * (blockDim.x >> 5));
+        if (atomicAdd(g.sched + SCHED_S1_DONE, 1) == total - 1) {
+            atomicExch(next_apply, 0);
+            atomicExch(next_agg, 0);
+            atomicExch(g.sched + SCHED_S1_DONE, 0);
+        }
+    }
 }
 
 __device__ __forceinline__ uint64_t global_ns() {
@@ -758,6 +840,28 @@ cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, cons
         k_shard_apply2<<<grid, kStageThreads, sm, s>>>(g, ap_loc.n, c0, c1, vec ? 1 : 0);
     }
     return cudaGetLastError();
+}
+
+cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
+                               const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
+                               int grid, cudaStream_t s) {
+    const bool vec_apply =
+        vec_ok(g, Xloc, ldX) && (reinterpret_cast<uintptr_t>(g.agg_full) % 16 == 0);
+    bool vec_agg = true;
+    for (int w = 0; w < ap_all.n; ++w)
+        vec_agg = vec_agg && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
+    for (int r = 0; r < pt.world; ++r)
+        vec_agg = vec_agg && (reinterpret_cast<uintptr_t>(pt.agg[r]) % 16 == 0);
+    if (grid < 1) return cudaSuccess;
+    const size_t sm = tab_smem_bytes(g.L);
+    return dispatch_n(ap_all.n, [&](auto nc) -> cudaError_t {
+        constexpr int NS = decltype(nc)::value;
+        cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_fused<NS>));
+        if (e != cudaSuccess) return e;
+        k_shard_fused<NS><<<grid, kStageThreads, sm, s>>>(g, ap_all, ap_loc, pt, Xloc, ldX, c0, c1,
+                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0);
+        return cudaGetLastError();
+    });
 }
 
 cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s) {

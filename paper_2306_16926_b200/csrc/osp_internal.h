@@ -123,6 +123,10 @@ cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const Peer
 cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const float* Xloc,
                                uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s);
 cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s);
+// stage-1 apply + stage-2 aggregate of chunks [c0, c1) in one launch
+cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
+                               const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
+                               int grid, cudaStream_t s);
 
 // ---- launchers (kernels/*.cu) ----------------------------------------------
 cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
