@@ -181,7 +181,7 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
         pt.rank = s->rank;
         pt.n_loc = s->n_loc;
         const char* lm = std::getenv("OSP_PEER_LOAD");
-        pt.ldmode = lm ? std::atoi(lm) : 0;
+        pt.ldmode = lm ? std::atoi(lm) : 2;  // default-cached peer loads measured fastest
         for (int w = 0; w < s->N; ++w) {
             const int q = w / s->n_loc, i = w % s->n_loc;
             pt.xrow[w] = xbase[q] + b * s->buf_stride + static_cast<uint64_t>(i) * s->ldX;

@@ -242,6 +242,8 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
                                                              const float* __restrict__ X,
                                                              uint64_t ldX) {
     extern __shared__ __align__(16) char smem_raw[];
+    pdl_wait();
+    pdl_trigger();
     const int L = g.L;
     const Smem s = carve(smem_raw, L);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -438,8 +440,7 @@ cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float*
     cudaError_t e = set_smem(reinterpret_cast<const void*>(k_resolve), sm);
     if (e != cudaSuccess) return e;
     const int blocks = g.L < sm_count() ? g.L : sm_count();
-    k_resolve<<<blocks, kResolveThreads, sm, st>>>(g, ap, X, ldX);
-    return cudaGetLastError();
+    return launch_pdl(k_resolve, dim3(blocks), dim3(kResolveThreads), sm, st, g, ap, X, ldX);
 }
 
 cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,

@@ -350,6 +350,8 @@ __global__ void __launch_bounds__(kStageThreads) k_stage1(GroupView g, AggParams
                                                           const float* __restrict__ X,
                                                           uint64_t ldX, int vec) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     const Tab tab = load_tab(g, smem_tab, nullptr, nullptr, 0, 0);
     int* next = g.sched + SCHED_S1_NEXT;
@@ -377,6 +379,8 @@ __global__ void __launch_bounds__(kStageThreads) k_stage2(GroupView g, AggParams
                                                           const float* __restrict__ X,
                                                           uint64_t ldX, int c0, int c1, int vec) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
+    pdl_wait();
+    pdl_trigger();
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_S2_NEXT;
     const int used = g.meta[META_N_USED];
@@ -791,8 +795,7 @@ cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* 
         constexpr int NS = decltype(nc)::value;
         cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_stage1<NS>));
         if (e != cudaSuccess) return e;
-        k_stage1<NS><<<grid, kStageThreads, sm, s>>>(g, ap, X, ldX, vec);
-        return cudaGetLastError();
+        return launch_pdl(k_stage1<NS>, dim3(grid), dim3(kStageThreads), sm, s, g, ap, X, ldX, vec);
     });
 }
 
@@ -805,8 +808,8 @@ cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* 
         constexpr int NS = decltype(nc)::value;
         cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_stage2<NS>));
         if (e != cudaSuccess) return e;
-        k_stage2<NS><<<grid, kStageThreads, sm, s>>>(g, ap, X, ldX, c0, c1, vec);
-        return cudaGetLastError();
+        return launch_pdl(k_stage2<NS>, dim3(grid), dim3(kStageThreads), sm, s, g, ap, X, ldX, c0,
+                          c1, vec);
     });
 }
 

@@ -42,17 +42,22 @@ def run(args, metric: str, unit: str):
         buf = k % 2
         if evs is not None:
             evs[0].record(stream)
-        sh.stage1(buf)
-        if evs is not None:
-            evs[1].record(stream)
         if args.per_chunk:
+            # message-by-message shape: barrier stage, then one launch set per chunk
+            sh.stage1(buf)
+            if evs is not None:
+                evs[1].record(stream)
             for c in range(args.chunks):
                 sh.stage2(buf, c, c + 1)
+            if evs is not None:
+                evs[2].record(stream)
+            sh.resolve(buf)
         else:
-            sh.stage2(buf)
-        if evs is not None:
-            evs[2].record(stream)
-        sh.resolve(buf)
+            # fused step: stage-2 push/pull inside the stage-1 apply launch
+            sh.step(buf)
+            if evs is not None:
+                evs[1].record(stream)
+                evs[2].record(stream)
 
     for k in range(args.warmup):
         step(k)
@@ -167,8 +172,9 @@ def run(args, metric: str, unit: str):
                          "note": "per-GPU NVLink bytes each direction / step time; peak = measured "
                                  "peer copy 770 GB/s (B200_PROFILING.md)",
                          "hbm_gbs_per_gpu": hbm_gbs, "hbm_frac": hbm_gbs / hbm_peak},
-            "breakdown_ms": {"stage1": s1_max, "stage2": s2_max,
-                             "resolve": ms_step - s1_max - s2_max},
+            "breakdown_ms": ({"stage1": s1_max, "stage2": s2_max,
+                              "resolve": ms_step - s1_max - s2_max} if args.per_chunk
+                             else {"step": s1_max}),
             "phase_ms": phases,
             "overlap": ovl,
             "u_mean": u_mean,
@@ -176,7 +182,8 @@ def run(args, metric: str, unit: str):
                     "h2d_bytes_per_step": n_loc * M * 4 * world,
                     "d2h_bytes_per_step": (8 + (L + 7) // 8) * world,
                     "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read"},
-            "gpu_launches": K * (3 + 3 + (3 * args.chunks if args.per_chunk else 3) + 1),
+            # fused step: barrier, agg1, barrier, apply1+agg2, barrier, apply2, resolve
+            "gpu_launches": K * ((4 + 3 * args.chunks + 1) if args.per_chunk else 7),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
