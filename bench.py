@@ -50,6 +50,16 @@ def parse():
     return ap.parse_args()
 
 
+def ncu_traffic(key: str, kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture, or None."""
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_traffic.json")) as f:
+            d = json.load(f)[key][kernel]
+        return d["dram_read_bytes"] + d["dram_write_bytes"]
+    except Exception:
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -308,7 +318,9 @@ def b200_single(args):
         "hbm_gbs_step": ach_step,
         "roofline": {"bound": "hbm", "kernel": "k_stage1 (barrier: RS agg/apply + LGP)",
                      "achieved": ach_s1, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": ach_s1 / peak, "traffic": None,
+                     "frac": ach_s1 / peak,
+                     "traffic": ncu_traffic(f"{args.layout}/N{N}/b{args.budget_frac}", "k_stage1"),
+                     "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)",
                      "alg_bytes_per_launch": sum(b_s1) / K, "avg_launch_ms": s1_avg,
                      "step_frac": ach_step / peak},
         "breakdown_ms": {"stage1": s1_avg, "stage2_chunks": sum(s2) / KB,
