@@ -159,6 +159,28 @@ osp_status osp_gib_encode(uint32_t tag, uint64_t n_layers, const uint8_t* ics_fl
 osp_status osp_gib_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint32_t* n_layers,
                           uint8_t* ics_flags, uint64_t flags_cap);
 
+/* Payload wire codec on the device: encode_payload_message /
+ * decode_payload_message (message.cpp:53-99) for payloads resident in HBM, so a
+ * byte transport can send straight from the device. Layout: kind u8 |
+ * iteration u32 LE | entries u16 LE | per layer: id u32 LE, count u32 LE,
+ * count fp32 LE.
+ * encode: the listed layers (HOST ids, strictly ascending = std::map order) of
+ *   the flat DEVICE vector `values` into DEVICE `out`; FormatError above 65535
+ *   layers. osp_payload_encoded_size gives the byte count (0 on a bad id).
+ * decode: DEVICE buffer -> values scattered into the flat DEVICE vector at the
+ *   layers' offsets; ids (HOST, first occurrence kept like std::map::emplace),
+ *   kind and iteration returned; FormatError on truncation or trailing bytes,
+ *   LayerError / ShapeError if an entry does not fit the partition. */
+uint64_t osp_payload_encoded_size(const osp_partition* part, const int32_t* layer_ids,
+                                  int64_t n_ids);
+osp_status osp_encode_payload(const osp_partition* part, const float* values,
+                              const int32_t* layer_ids, int64_t n_ids, uint8_t kind,
+                              uint32_t iteration, uint8_t* out, uint64_t out_cap,
+                              uint64_t* out_len, void* stream);
+osp_status osp_decode_payload(const osp_partition* part, const uint8_t* buf, uint64_t len,
+                              float* values, uint8_t* kind, uint32_t* iteration, int32_t* layer_ids,
+                              int64_t ids_cap, int64_t* n_ids, void* stream);
+
 /* compute_umax / tune_sgu (tuning.cpp:8-48), host scalar logic. */
 osp_status osp_compute_umax(double bandwidth_bps, double latency_s, double loss_rate,
                             double t_c_seconds, int n_workers, uint64_t model_bytes,

@@ -65,6 +65,9 @@ def lib():
         L.oo_tune_sgu.restype = ctypes.c_int64
         L.oo_tune_sgu.argtypes = [_f64p, ctypes.POINTER(ctypes.c_int), ctypes.c_uint64,
                                   ctypes.c_uint64, ctypes.c_double]
+        L.oo_encode_payload.restype = ctypes.c_uint64
+        L.oo_encode_payload.argtypes = [ctypes.c_uint8, ctypes.c_uint32, ctypes.c_int64, _u64p,
+                                        _f32p, _i32p, ctypes.c_int64, _u8p]
         L.oo_step.restype = ctypes.c_int
         L.oo_step.argtypes = [ctypes.c_int64, _u64p, ctypes.c_uint32, ctypes.c_int, _f64p,
                               _f32p, _f32p, _f32p, _u8p, _i32p, ctypes.c_int64, ctypes.c_int,
@@ -211,6 +214,19 @@ class SguSchedule:
         if rc < 0:
             raise ValueError({-1: "ConfigError", -2: "NumericError", -3: "ProtocolError"}[int(rc)])
         return int(rc)
+
+
+def encode_payload(kind: int, iteration: int, counts, values, ids) -> bytes:
+    """message.cpp:53-78 (payload wire encoding of the listed layers of a flat vector)"""
+    c = _c(counts, np.uint64)
+    v = _c(values, np.float32)
+    i = _c(ids if len(ids) else [0], np.int32)
+    n = 7 + sum(8 + 4 * int(c[k]) for k in ids)
+    out = np.zeros(n, dtype=np.uint8)
+    got = lib().oo_encode_payload(kind, iteration, c.size, _p(c, _u64p), _p(v, _f32p),
+                                  _p(i, _i32p), len(ids), _p(out, _u8p))
+    assert got == n
+    return out.tobytes()
 
 
 def step(counts, bpe, weights, deltas, G, P, flags_in, order_in, n_chunks, budget):

@@ -340,3 +340,33 @@ int oo_step(int64_t n_layers, const uint64_t* counts, uint32_t bpe, int n_worker
     free(chunks);
     return used;
 }
+
+/* ---- message.cpp:53-78 (payload wire encoding) -------------------------- */
+
+uint64_t oo_encode_payload(uint8_t kind, uint32_t iteration, int64_t n_layers,
+                           const uint64_t* counts, const float* values, const int32_t* ids,
+                           int64_t n_ids, uint8_t* out) {
+    uint64_t* offsets = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(n_layers + 1));
+    offsets[0] = 0;
+    for (int64_t l = 0; l < n_layers; ++l) offsets[l + 1] = offsets[l] + counts[l];
+    uint64_t at = 0;
+    out[at++] = kind;
+    put_u32le(out + at, iteration);
+    at += 4;
+    out[at++] = (uint8_t)(n_ids & 0xff);
+    out[at++] = (uint8_t)((n_ids >> 8) & 0xff);
+    for (int64_t i = 0; i < n_ids; ++i) {
+        const int32_t id = ids[i];
+        put_u32le(out + at, (uint32_t)id);
+        put_u32le(out + at + 4, (uint32_t)counts[id]);
+        at += 8;
+        for (uint64_t e = 0; e < counts[id]; ++e) {
+            uint32_t bits;
+            memcpy(&bits, &values[offsets[id] + e], 4);
+            put_u32le(out + at, bits);
+            at += 4;
+        }
+    }
+    free(offsets);
+    return at;
+}

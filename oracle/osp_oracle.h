@@ -72,6 +72,12 @@ uint64_t oo_compute_umax(double bandwidth_bps, double loss_rate, double t_c_seco
 int64_t oo_tune_sgu(double* initial_loss, int* has_initial, uint64_t u_max,
                     uint64_t epoch_index, double epoch_loss);
 
+/* message.cpp:53-78: kind u8 | iteration u32 | entries u16 | per layer id u32,
+ * count u32, fp32 values; ids ascending. Returns bytes written. */
+uint64_t oo_encode_payload(uint8_t kind, uint32_t iteration, int64_t n_layers,
+                           const uint64_t* counts, const float* values, const int32_t* ids,
+                           int64_t n_ids, uint8_t* out);
+
 /* One synchronous OSP iteration for N co-resident workers, restated from the
  * OspWorker/OspServer message flow (protocol.cpp:172-447) in the order of
  * oracle/ref_driver.cpp. Worker parameters are read (not assumed equal to the

@@ -80,6 +80,11 @@ _SIGS = {
     "osp_gib_encode": (c_int, [c_u32, c_u64, P(ctypes.c_uint8), P(ctypes.c_uint8), c_u64]),
     "osp_gib_decode": (c_int, [P(ctypes.c_uint8), c_u64, P(c_u32), P(c_u32), P(ctypes.c_uint8),
                                c_u64]),
+    "osp_payload_encoded_size": (c_u64, [c_void_p, P(ctypes.c_int32), c_i64]),
+    "osp_encode_payload": (c_int, [c_void_p, c_void_p, P(ctypes.c_int32), c_i64, ctypes.c_uint8,
+                                   c_u32, c_void_p, c_u64, P(c_u64), c_void_p]),
+    "osp_decode_payload": (c_int, [c_void_p, c_void_p, c_u64, c_void_p, P(ctypes.c_uint8),
+                                   P(c_u32), P(ctypes.c_int32), c_i64, P(c_i64), c_void_p]),
     "osp_compute_umax": (c_int, [c_dbl, c_dbl, c_dbl, c_dbl, c_int, c_u64, c_int, P(c_u64)]),
     "osp_tune_sgu": (c_int, [P(osp_sgu_schedule), c_u64, c_dbl, P(c_u64)]),
     "osp_group_create": (c_int, [c_void_p, P(osp_group_config), c_void_p, c_void_p,

@@ -128,6 +128,20 @@ cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, cons
                                const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
                                int grid, cudaStream_t s);
 
+// ---- payload wire codec (kernels/codec.cu) -----------------------------------
+struct CodecSeg {
+    uint64_t hdr;    // encode: byte offset of the layer's (id, count) header; decode: value offset
+    uint64_t src;    // element offset in the flat vector
+    uint32_t id;
+    uint32_t count;
+};
+cudaError_t launch_encode(const float* values, const CodecSeg* segs_dev, int n_seg,
+                          uint64_t max_count, uint8_t* out, cudaStream_t s);
+cudaError_t launch_decode_index(const uint8_t* buf, uint64_t len, uint64_t* idx, int* status,
+                                uint32_t* hdr, cudaStream_t s);
+cudaError_t launch_decode_scatter(const uint8_t* buf, const CodecSeg* segs_dev, int n_seg,
+                                  uint64_t max_count, float* values, cudaStream_t s);
+
 // ---- launchers (kernels/*.cu) ----------------------------------------------
 cudaError_t launch_stage1(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int grid, cudaStream_t s);

@@ -306,6 +306,38 @@ def gib_decode(buf: bytes):
     return int(tag.value), flags[: L.value].copy()
 
 
+def encode_payload(part: Partition, values: torch.Tensor, layer_ids, kind: int, iteration: int,
+                   stream=None) -> torch.Tensor:
+    """encode_payload_message (message.cpp:53-78) of device-resident layers -> device bytes."""
+    _dev_f32(values, "values")
+    ids, ip = _i32(layer_ids)
+    n = len(layer_ids)
+    size = int(lib().osp_payload_encoded_size(part.handle, ip, n))
+    if size == 0:
+        raise LayerError("layer id out of range")
+    out = torch.empty(size, dtype=torch.uint8, device=values.device)
+    got = c_u64()
+    _check(lib().osp_encode_payload(part.handle, _ptr(values), ip, n, kind, iteration, _ptr(out),
+                                    size, ctypes.byref(got), _stream(stream)))
+    return out[: got.value]
+
+
+def decode_payload(part: Partition, buf: torch.Tensor, values: torch.Tensor, stream=None):
+    """decode_payload_message (message.cpp:80-99) from device bytes into a flat device
+    vector -> (kind, iteration, layer ids)."""
+    _dev_f32(values, "values")
+    if not (buf.is_cuda and buf.dtype == torch.uint8 and buf.is_contiguous()):
+        raise InvalidArgument("buf must be a contiguous uint8 CUDA tensor")
+    L = part.layer_count()
+    ids = np.empty(max(min(L, 65535), 1), dtype=np.int32)
+    kind, it, n = ctypes.c_uint8(), c_u32(), c_i64()
+    _check(lib().osp_decode_payload(part.handle, _ptr(buf), buf.numel(), _ptr(values),
+                                    ctypes.byref(kind), ctypes.byref(it),
+                                    ids.ctypes.data_as(P(ctypes.c_int32)), ids.size,
+                                    ctypes.byref(n), _stream(stream)))
+    return int(kind.value), int(it.value), ids[: n.value].copy()
+
+
 def compute_umax(bandwidth_bps, t_c, n_workers, model_bytes, latency_s=0.0, loss_rate=0.0,
                  eq5_literal=False) -> int:
     """compute_umax (tuning.cpp:8-21)."""

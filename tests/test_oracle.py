@@ -196,3 +196,15 @@ def test_oracle_step_matches_reference_engine(golden: Golden):
         assert oracle.gib_encode(it + 1, r["flags_out"]) == bytes(g.get(it, "gib_out"))
         assert np.array_equal(r["order_out"], g.get(it, "order_out"))
         flags, order = r["flags_out"], r["order_out"]
+
+
+def test_payload_encoding_hand_vector():
+    # test_message.cpp:10-35: PushImportant, iteration 0x01020304, layer 7 = {1.0f}
+    counts = [1] * 8
+    vals = np.zeros(8, np.float32)
+    vals[7] = 1.0
+    b = oracle.encode_payload(0, 0x01020304, counts, vals, [7])
+    assert len(b) == 7 + 8 + 4
+    assert b[0] == 0 and list(b[1:5]) == [4, 3, 2, 1] and list(b[5:7]) == [1, 0]
+    assert b[7] == 7 and b[11] == 1
+    assert b[15] == 0x00 and b[17] == 0x80 and b[18] == 0x3f
