@@ -126,6 +126,12 @@ def run(args, metric: str, unit: str):
         ot = torch.tensor([res[k] for k in keys] + [comp.ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(ot, op=dist.ReduceOp.MAX)
         ovl = {k: float(v) for k, v in zip(keys + ["t_c_ms"], ot.tolist())}
+        # Eq. 5 budget from the measured compute time and the measured per-GPU
+        # NVLink rate of this run (runner.cpp:364-376 umax_measured, on hardware)
+        nvl_bps = nvl_bytes / (total_ms / K * 1e-3)
+        ovl["umax_measured_bytes"] = osp.compute_umax(nvl_bps, ovl["t_c_ms"] * 1e-3, N,
+                                                      model_bytes)
+        ovl["umax_frac_of_model"] = ovl["umax_measured_bytes"] / model_bytes
 
     # ---- e2e: pinned host deltas -> device (this rank's rows), step, GIB read-back
     host = [sh.deltas(b).cpu().pin_memory() for b in range(2)]
