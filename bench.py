@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--chunks", type=int, default=4)
     ap.add_argument("--seed", type=int, default=11)
     ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--stage-kernels", default="auto", choices=["auto", "tma", "register"],
+                    help="stage-kernel family (OSP_GROUP_TMA / OSP_GROUP_REGISTER)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-chunk", action="store_true", help="one stage-2 launch per ICS chunk")
@@ -213,7 +215,8 @@ def b200_single(args):
     model_bytes = M * 4
     budget = int(args.budget_frac * model_bytes)
     part = osp.Partition(counts)
-    grp = osp.OspGroup(part, N, [1.0 / N] * N, n_chunks=args.chunks, tile_elems=args.tile)
+    grp = osp.OspGroup(part, N, [1.0 / N] * N, n_chunks=args.chunks, tile_elems=args.tile,
+                       tma={"auto": None, "tma": True, "register": False}[args.stage_kernels])
     X = [osp.synth_deltas(args.seed, N, i, M) for i in range(2)]
     grp.set_budget(budget)
     stream = torch.cuda.current_stream()
@@ -314,12 +317,16 @@ def b200_single(args):
                    "params": M, "layers": L, "workers": N, "budget_frac": args.budget_frac,
                    "chunks": args.chunks, "deltas": "reference synth generator, seed "
                    f"{args.seed}, 2 sets alternating (1.6 GB > L2, no flush)",
-                   "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU"},
+                   "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU",
+                   "stage_kernels": grp.stage_kernels},
         "hbm_gbs_step": ach_step,
-        "roofline": {"bound": "hbm", "kernel": "k_stage1 (barrier: RS agg/apply + LGP)",
+        "roofline": {"bound": "hbm", "kernel": ("k_stage_tma<1>" if grp.stage_kernels == "tma-staged" else "k_stage1")
+                     + " (barrier: RS agg/apply + LGP)",
                      "achieved": ach_s1, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach_s1 / peak,
-                     "traffic": ncu_traffic(f"{args.layout}/N{N}/b{args.budget_frac}", "k_stage1"),
+                     "traffic": ncu_traffic(f"{args.layout}/N{N}/b{args.budget_frac}",
+                                            "k_stage_tma<1>" if grp.stage_kernels == "tma-staged"
+                                            else "k_stage1"),
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)",
                      "alg_bytes_per_launch": sum(b_s1) / K, "avg_launch_ms": s1_avg,
                      "step_frac": ach_step / peak},

@@ -215,7 +215,17 @@ typedef struct osp_group_config {
     int n_chunks;             /* ICS chunk slots per iteration (>= 1) */
     uint32_t tile_elems;      /* elements per warp tile; 0 = default 512 (power of two, 256..65536) */
     double sgd_lr;            /* 0 = inputs are deltas; > 0 fuse sgd_delta */
+    uint32_t flags;           /* OSP_GROUP_* bits */
 } osp_group_config;
+
+/* Stage-kernel family. Default (flags 0): the TMA-staged kernels (tiles moved
+ * global->shared by cp.async.bulk into an mbarrier ring, tile_elems default 1024)
+ * when the shape allows them (N in {1,2,4,8}, tile_elems in [512, 4096]), else
+ * the register-staged kernels (tile_elems default 512). OSP_GROUP_TMA requires
+ * the TMA family (OSP_ERR_INVALID if unsupported); OSP_GROUP_REGISTER forces the
+ * register-staged one. Both produce identical results. */
+#define OSP_GROUP_TMA 1u
+#define OSP_GROUP_REGISTER 2u
 
 /* init_params: DEVICE pointer to M floats (P0), or NULL for zeros. Every worker
  * and the server start from it (runner.cpp:214-231). */
@@ -267,6 +277,8 @@ osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fallback_
 osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, uint64_t* out,
                                       void* stream);
 /* Tile geometry (for roofline accounting and tests). */
+/* Effective flags of a group (OSP_GROUP_TMA or OSP_GROUP_REGISTER). */
+uint32_t osp_group_flags(const osp_group* g);
 osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,
                               int* grid_blocks, int* block_threads);
 

@@ -22,7 +22,11 @@ P = ctypes.POINTER
 
 class osp_group_config(ctypes.Structure):
     _fields_ = [("n_workers", c_int), ("weights", P(c_dbl)), ("n_chunks", c_int),
-                ("tile_elems", c_u32), ("sgd_lr", c_dbl)]
+                ("tile_elems", c_u32), ("sgd_lr", c_dbl), ("flags", c_u32)]
+
+
+GROUP_TMA = 1
+GROUP_REGISTER = 2
 
 
 class osp_shard_config(ctypes.Structure):
@@ -107,6 +111,7 @@ _SIGS = {
     "osp_group_stats": (c_int, [c_void_p, P(c_u64), P(c_u64), P(c_u64), c_void_p]),
     "osp_group_deferred_history": (c_int, [c_void_p, c_u32, c_int, P(c_u64), c_void_p]),
     "osp_group_geometry": (c_int, [c_void_p, P(c_u32), P(c_u64), P(c_int), P(c_int)]),
+    "osp_group_flags": (c_u32, [c_void_p]),
     "osp_shard_create": (c_int, [c_void_p, P(osp_shard_config), c_void_p, c_void_p,
                                  P(c_void_p)]),
     "osp_shard_destroy": (None, [c_void_p]),

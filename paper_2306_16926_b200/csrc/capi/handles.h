@@ -26,6 +26,7 @@ struct osp_group {
     osp::GroupView v{};
     int grid = 1;
     int blocks_per_sm = 1;
+    bool tma = false;  // OSP_GROUP_TMA
     // owned device buffers
     std::vector<void*> owned;
     int* d_order_tmp = nullptr;

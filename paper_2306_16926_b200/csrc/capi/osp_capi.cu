@@ -573,7 +573,22 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     const uint64_t L = part->counts.size();
     if (L > static_cast<uint64_t>(kMaxLayers))
         return fail(OSP_ERR_INVALID, "more than " + std::to_string(kMaxLayers) + " layers");
-    uint32_t T = cfg->tile_elems ? cfg->tile_elems : kDefaultTile;
+    // Stage kernels: TMA-staged unless OSP_GROUP_REGISTER (or unsupported shape
+    // without an explicit OSP_GROUP_TMA request); default tiles 1024 / 512.
+    const bool want_tma = (cfg->flags & OSP_GROUP_TMA) != 0;
+    const bool force_reg = (cfg->flags & OSP_GROUP_REGISTER) != 0;
+    if (want_tma && force_reg)
+        return fail(OSP_ERR_INVALID, "OSP_GROUP_TMA and OSP_GROUP_REGISTER are exclusive");
+    bool use_tma = false;
+    if (!force_reg) {
+        const uint32_t Tt = cfg->tile_elems ? cfg->tile_elems : kDefaultTmaTile;
+        use_tma = tma_supported(N, static_cast<int>(Tt), static_cast<int>(L));
+        if (want_tma && !use_tma)
+            return fail(OSP_ERR_INVALID, "OSP_GROUP_TMA needs N in {1,2,4,8}, tile_elems in "
+                                         "[512, 4096] and the ring + layer tables within "
+                                         "shared memory");
+    }
+    uint32_t T = cfg->tile_elems ? cfg->tile_elems : (use_tma ? kDefaultTmaTile : kDefaultTile);
     if (T < 256 || T > 65536 || (T & (T - 1)))
         return fail(OSP_ERR_INVALID, "tile_elems must be a power of two in [256, 65536]");
 
@@ -676,6 +691,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = cu(launch_install_gib(v, g->d_order_tmp, 0, 0, s), "install bootstrap gib")) != OSP_OK)
         return cleanup(st);
     g->blocks_per_sm = stage_blocks_per_sm(N, static_cast<int>(L));
+    g->tma = use_tma;
     g->grid = sm_count() * g->blocks_per_sm;
     if ((st = cu(cudaStreamSynchronize(s), "group create")) != OSP_OK) return cleanup(st);
     *out = g;
@@ -716,7 +732,8 @@ osp_status osp_group_set_gib(osp_group* g, const uint8_t* flags, const int32_t* 
 osp_status osp_group_stage1(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
-    OSP_CUDA(launch_stage1(g->v, g->ap, deltas, ld, g->grid, as_stream(stream)));
+    if (g->tma) OSP_CUDA(launch_stage1_tma(g->v, g->ap, deltas, ld, as_stream(stream)));
+    else OSP_CUDA(launch_stage1(g->v, g->ap, deltas, ld, g->grid, as_stream(stream)));
     return OSP_OK;
 }
 
@@ -725,14 +742,16 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (chunk < 0 || chunk >= g->n_chunks) return fail(OSP_ERR_INVALID, "chunk out of range");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
-    OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, chunk + 1, g->grid, as_stream(stream)));
+    if (g->tma) OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, chunk, chunk + 1, as_stream(stream)));
+    else OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, chunk + 1, g->grid, as_stream(stream)));
     return OSP_OK;
 }
 
 osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
-    OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, 0, g->n_chunks, g->grid, as_stream(stream)));
+    if (g->tma) OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, 0, g->n_chunks, as_stream(stream)));
+    else OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, 0, g->n_chunks, g->grid, as_stream(stream)));
     return OSP_OK;
 }
 
@@ -821,6 +840,11 @@ osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, u
     OSP_CUDA(cudaStreamSynchronize(s));
     for (int i = 0; i < n; ++i) out[i] = h[(first_tag + i) % kHist];
     return OSP_OK;
+}
+
+uint32_t osp_group_flags(const osp_group* g) {
+    if (!g) return 0;
+    return g->tma ? OSP_GROUP_TMA : OSP_GROUP_REGISTER;
 }
 
 osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,

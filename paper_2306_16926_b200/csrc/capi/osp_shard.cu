@@ -79,7 +79,7 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
     s->ap_loc = make_agg_params(s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->sgd_lr);
     osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks,
-                        cfg->tile_elems, cfg->sgd_lr};
+                        cfg->tile_elems, cfg->sgd_lr, OSP_GROUP_REGISTER};
     osp_status st = osp_group_create(part, &gc, init_params, stream, &s->grp);
     if (st != OSP_OK) {
         delete s;

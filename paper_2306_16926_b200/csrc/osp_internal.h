@@ -100,6 +100,7 @@ constexpr int kHist = 1024;
 constexpr int kMaxLayers = 4096;  // single-CTA resolve (resolve.cu)
 constexpr int kStageThreads = 256;
 constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profiles/)
+constexpr uint32_t kDefaultTmaTile = 1024;  // TMA-staged kernels (tools/tma_sweep.sh)
 constexpr int kResolveThreads = 1024;
 
 // ---- sharded (multi-GPU) path: peer tables ---------------------------------
@@ -155,6 +156,12 @@ cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t 
 cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,
                                cudaStream_t s);
 int stage_blocks_per_sm(int n_workers, int n_layers);
+// TMA-staged stage kernels (stage_tma.cu)
+bool tma_supported(int n_workers, int T, int L);
+cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
+                              cudaStream_t s);
+cudaError_t launch_stage2_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
+                              int c0, int c1, cudaStream_t s);
 
 cudaError_t launch_aggregate_layer(const float* const* contribs, const AggParams& ap, uint64_t n,
                                    float* out, cudaStream_t s);

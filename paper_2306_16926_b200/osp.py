@@ -386,7 +386,10 @@ class OspGroup:
 
     def __init__(self, part: Partition, n_workers: int, weights: Optional[Sequence[float]] = None,
                  n_chunks: int = 4, init_params: Optional[torch.Tensor] = None,
-                 tile_elems: int = 0, sgd_lr: float = 0.0, stream=None):
+                 tile_elems: int = 0, sgd_lr: float = 0.0, tma: Optional[bool] = None,
+                 stream=None):
+        """tma: None = TMA-staged stage kernels when the shape allows them, True =
+        require them, False = register-staged kernels (identical results)."""
         self.part = part
         self.N = n_workers
         self.M = part.total_count()
@@ -397,7 +400,9 @@ class OspGroup:
             raise ConfigError("one weight per worker")
         self._w = (c_dbl * max(n_workers, 1))(*w)
         cfg = _capi.osp_group_config(n_workers, ctypes.cast(self._w, P(c_dbl)), n_chunks,
-                                     tile_elems, sgd_lr)
+                                     tile_elems, sgd_lr,
+                                     {None: 0, True: _capi.GROUP_TMA,
+                                      False: _capi.GROUP_REGISTER}[tma])
         init = 0
         if init_params is not None:
             _dev_f32(init_params, "init_params")
@@ -525,7 +530,13 @@ class OspGroup:
         _check(lib().osp_group_geometry(self._h, ctypes.byref(t), ctypes.byref(nt),
                                         ctypes.byref(gb), ctypes.byref(bt)))
         return dict(tile_elems=int(t.value), n_tiles=int(nt.value), grid_blocks=int(gb.value),
-                    block_threads=int(bt.value))
+                    block_threads=int(bt.value), stage_kernels=self.stage_kernels)
+
+    @property
+    def stage_kernels(self) -> str:
+        """"tma-staged" or "register-staged"."""
+        f = lib().osp_group_flags(self._h)
+        return "tma-staged" if f & _capi.GROUP_TMA else "register-staged"
 
     def close(self):
         h = getattr(self, "_h", None)

@@ -188,10 +188,10 @@ def test_split_vs_oracle(osp):
 
 # ---- the group step against the reference-engine goldens ----------------------
 
-def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0):
+def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0, tma=None):
     part = osp.Partition(g.counts, g.bpe)
     grp = osp.OspGroup(part, g.N, list(g.weights), n_chunks=g.n_chunks,
-                       init_params=cuda(g.p0), tile_elems=tile_elems)
+                       init_params=cuda(g.p0), tile_elems=tile_elems, tma=tma)
     for it in range(g.iters):
         d = g.deltas(it)
         X = torch.zeros((g.N, g.M + pad_ld), dtype=torch.float32, device="cuda")
@@ -234,19 +234,20 @@ def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0):
     return grp
 
 
-def test_group_matches_reference_engine(osp, golden):
-    run_group_against_golden(osp, golden)
+@pytest.mark.parametrize("tma", [None, False])
+def test_group_matches_reference_engine(osp, golden, tma):
+    run_group_against_golden(osp, golden, tma=tma)
 
 
 def test_group_small_tiles_and_unaligned_rows(osp, golden):
     # multi-tile layers, and rows whose stride breaks 16-byte alignment (scalar path)
-    run_group_against_golden(osp, golden, tile_elems=1024, pad_ld=1)
+    run_group_against_golden(osp, golden, tile_elems=1024, pad_ld=1, tma=False)
 
 
 # ---- the group step against the oracle at larger sizes ---------------------------
 
 def oracle_vs_group(osp, counts, N, weights, budget_frac, n_chunks, iters, seed, p0=None,
-                    sgd_lr=0.0, tile_elems=0):
+                    sgd_lr=0.0, tile_elems=0, tma=None):
     counts = np.asarray(counts, dtype=np.uint64)
     M = int(counts.sum())
     bpe = 4
@@ -255,7 +256,7 @@ def oracle_vs_group(osp, counts, N, weights, budget_frac, n_chunks, iters, seed,
     P = np.tile(G, (N, 1))
     part = osp.Partition(counts)
     grp = osp.OspGroup(part, N, weights, n_chunks=n_chunks, init_params=cuda(G),
-                       sgd_lr=sgd_lr, tile_elems=tile_elems)
+                       sgd_lr=sgd_lr, tile_elems=tile_elems, tma=tma)
     flags = np.zeros(len(counts), np.uint8)
     order = np.zeros(0, np.int32)
     X = torch.empty((N, M), dtype=torch.float32, device="cuda")
@@ -283,8 +284,9 @@ def oracle_vs_group(osp, counts, N, weights, budget_frac, n_chunks, iters, seed,
 
 def test_group_resnet50_layout_vs_oracle(osp):
     from paper_2306_16926_b200 import layouts
-    grp = oracle_vs_group(osp, layouts.resnet50(), 8, [0.125] * 8, 0.5, 4, 3, seed=11)
+    grp = oracle_vs_group(osp, layouts.resnet50(), 8, [0.125] * 8, 0.5, 4, 3, seed=11, tma=False)
     assert grp.stats()["resolved"] == 3
+    assert grp.stage_kernels == "register-staged"
 
 
 def test_group_odd_workers_unequal_weights(osp):
@@ -292,20 +294,21 @@ def test_group_odd_workers_unequal_weights(osp):
     counts = rng.integers(1, 20000, 57)
     w = list(0.1 + rng.random(5))
     p0 = rng.uniform(-1, 1, int(counts.sum())).astype(np.float32)
-    oracle_vs_group(osp, counts, 5, w, 0.6, 3, 4, seed=3, p0=p0, tile_elems=2048)
+    grp = oracle_vs_group(osp, counts, 5, w, 0.6, 3, 4, seed=3, p0=p0, tile_elems=2048)
+    assert grp.stage_kernels == "register-staged"  # N=5: no TMA family
 
 
 def test_group_fused_sgd(osp):
     rng = np.random.default_rng(8)
     counts = rng.integers(1, 9000, 40)
-    oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 4, 3, seed=19, sgd_lr=0.05)
+    oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 4, 3, seed=19, sgd_lr=0.05, tma=False)
 
 
 def test_group_budget_edges(osp):
     counts = [4096, 12, 70000, 1, 333, 8192, 5]
     for frac in (0.0, 1.0, 0.33):
-        oracle_vs_group(osp, counts, 2, [0.5, 0.5], frac, 4, 3, seed=23)
-    oracle_vs_group(osp, counts, 1, [1.0], 0.7, 1, 3, seed=29)
+        oracle_vs_group(osp, counts, 2, [0.5, 0.5], frac, 4, 3, seed=23, tma=False)
+    oracle_vs_group(osp, counts, 1, [1.0], 0.7, 1, 3, seed=29, tma=False)
     oracle_vs_group(osp, counts, 3, [0.2, 0.3, 0.5], 0.9, 9, 3, seed=31)
 
 
@@ -356,6 +359,67 @@ def test_step_host_matches_device_step(osp):
         assert np.array_equal(bits(a.global_params), bits(b.global_params))
         ra = a.read_gib()
         assert gib == oracle.gib_encode(ra["tag"], ra["flags"])
+
+
+# ---- TMA-staged stage kernels (OSP_GROUP_TMA): same results --------------------
+
+@pytest.mark.parametrize("pad_ld", [0, 1])
+def test_tma_group_matches_reference_engine(osp, golden, pad_ld):
+    if golden.N not in (1, 2, 4, 8):
+        with pytest.raises(osp.InvalidArgument):
+            osp.OspGroup(osp.Partition(golden.counts, golden.bpe), golden.N,
+                         list(golden.weights), tma=True)
+        return
+    # pad_ld=1: unaligned rows, every tile takes the unstaged path
+    run_group_against_golden(osp, golden, pad_ld=pad_ld, tma=True)
+
+
+@pytest.mark.parametrize("tile", [512, 1024, 2048])
+def test_tma_group_resnet50_layout_vs_oracle(osp, tile):
+    from paper_2306_16926_b200 import layouts
+    grp = oracle_vs_group(osp, layouts.resnet50(), 8, [0.125] * 8, 0.5, 4, 3, seed=11,
+                          tile_elems=tile, tma=True)
+    assert grp.stage_kernels == "tma-staged"
+
+
+def test_default_group_is_tma_staged(osp):
+    part = osp.Partition([1000, 5000])
+    assert osp.OspGroup(part, 8).geometry()["tile_elems"] == 1024
+    assert osp.OspGroup(part, 8).stage_kernels == "tma-staged"
+    assert osp.OspGroup(part, 3).stage_kernels == "register-staged"
+    assert osp.OspGroup(part, 3).geometry()["tile_elems"] == 512
+    with pytest.raises(osp.InvalidArgument):
+        osp.OspGroup(part, 8, tile_elems=256, tma=True)
+
+
+def test_tma_group_ragged_sgd_and_budget_edges(osp):
+    rng = np.random.default_rng(8)
+    counts = rng.integers(1, 9000, 40)
+    oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 4, 3, seed=19, sgd_lr=0.05, tma=True)
+    counts = [4096, 12, 70000, 1, 333, 8192, 5]
+    for frac in (0.0, 1.0, 0.33):
+        oracle_vs_group(osp, counts, 2, [0.5, 0.5], frac, 4, 3, seed=23, tma=True)
+    oracle_vs_group(osp, counts, 1, [1.0], 0.7, 1, 3, seed=29, tma=True)
+
+
+def test_tma_matches_default_kernels(osp):
+    """Both kernel families on the same inputs: identical G, rows, scores bits."""
+    from paper_2306_16926_b200 import layouts
+    counts = layouts.resnet50()
+    M = sum(counts)
+    N = 8
+    part = osp.Partition(counts)
+    a = osp.OspGroup(part, N, [0.125] * N, n_chunks=4, tma=False)
+    b = osp.OspGroup(part, N, [0.125] * N, n_chunks=4, tma=True)
+    for it in range(4):
+        X = osp.synth_deltas(5, N, it, M)
+        a.set_budget(M * 2)
+        b.set_budget(M * 2)
+        a.step(X)
+        b.step(X)
+        assert np.array_equal(bits(a.global_params), bits(b.global_params))
+        assert np.array_equal(bits(a.worker_params), bits(b.worker_params))
+        assert np.array_equal(a.read_gib()["order"], b.read_gib()["order"])
 
 
 def test_group_errors(osp):
