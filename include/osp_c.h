@@ -285,12 +285,21 @@ osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_ti
 /* ------------------------------------------------------------------------
  * Shard: the multi-GPU path, one process per GPU (PS sharded one shard per
  * GPU). Rank r hosts workers [r*N/P, (r+1)*N/P) and a full
- * replica of the global vector. Per stage, the owner of each slice of the
+ * replica of the global vector. Per stage, the owner of each tile of the
  * stage's tile sequence reads every worker's delta rows from the peers' HBM
  * over NVLink (CUDA IPC), aggregates them in the reference's fixed worker
- * order in fp64 (push = reduce-scatter, bit-exact) and stores the fp32
- * aggregate into every rank's buffer (pull = all-gather), all in one kernel;
- * each rank then applies locally and resolves the identical next GIB.
+ * order in fp64 (push = reduce-scatter, bit-exact) and stores the result
+ * into every rank's buffer (pull = all-gather); each rank applies locally and
+ * resolves the identical next GIB.
+ *
+ * Default (barrier) mode: per stage an aggregate kernel (the owners' push +
+ * pull), a cross-GPU barrier kernel and an apply kernel; stage 1's apply runs
+ * in the same launch as stage 2's aggregate. Streaming mode (opt-in with
+ * OSP_SHARD_STREAM=1 in the environment at create; N in {1,2,4,8}, tile_elems
+ * 1024/2048, default 2048): one kernel per stage, tiles dealt round-robin to
+ * owners, each owner publishes a tile with a per-tile ready flag and the other
+ * ranks apply it as the flag lands — no grid-wide barrier. Both are
+ * bit-identical; barrier mode is faster on the measured configurations.
  *
  * Setup: create on every rank, export a handle, exchange the handles (e.g.
  * torch.distributed all_gather), connect with all of them (rank order).
@@ -326,12 +335,15 @@ osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream);
 osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream);
 osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream);
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream);
-/* One osp_shard_step with CUDA events between the kernels; ms[0..7] =
- * barrier-in, stage-1 aggregate, barrier, stage-1 apply fused with the stage-2
- * aggregate (all chunks), 0 (unused), barrier, stage-2 apply, resolve
- * (synchronises `stream`). */
+/* One osp_shard_step with CUDA events between the kernels (synchronises
+ * `stream`). Streaming mode: ms[0..2] = stage 1, stage 2 (all chunks),
+ * resolve; ms[3..7] = 0. Barrier mode: ms[0..7] = barrier-in, stage-1
+ * aggregate, barrier, stage-1 apply fused with the stage-2 aggregate, 0,
+ * barrier, stage-2 apply, resolve. */
 osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream);
-/* ProtocolError if a cross-GPU barrier timed out (synchronises `stream`). */
+/* 1 if the shard runs the streaming kernels, 0 for barrier mode. */
+int osp_shard_streaming(const osp_shard* s);
+/* ProtocolError if a cross-GPU wait timed out (synchronises `stream`). */
 osp_status osp_shard_check(osp_shard* s, void* stream);
 /* Synthetic deltas of workers [worker0, worker0+n_workers) into [n_workers][ld]. */
 osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,

@@ -649,7 +649,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &v.gib_bytes, osp_gib_encoded_size(L))) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &g->d_order_tmp, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.hist, kHist)) != OSP_OK) return cleanup(st);
-    if ((st = dalloc(g, &v.sched, 8)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.sched, 16)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.lscore, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.rs_layers, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.rs_tile_prefix, L + 1)) != OSP_OK) return cleanup(st);
@@ -678,7 +678,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.flags, 0, L, s), "flags")) != OSP_OK) return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.marked, 0, L, s), "marked")) != OSP_OK) return cleanup(st);
-    if ((st = cu(cudaMemsetAsync(v.sched, 0, 8 * sizeof(int), s), "sched")) != OSP_OK)
+    if ((st = cu(cudaMemsetAsync(v.sched, 0, 16 * sizeof(int), s), "sched")) != OSP_OK)
         return cleanup(st);
     if ((st = cu(cudaMemsetAsync(v.lscore, 0, L * sizeof(double), s), "lscore")) != OSP_OK)
         return cleanup(st);

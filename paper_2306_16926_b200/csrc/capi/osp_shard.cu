@@ -28,6 +28,9 @@ struct ShardHandle {
     int32_t rank, world, n_loc;
     uint64_t M, L, ldX, buf_stride;
     cudaIpcMemHandle_t hx, hagg, hflags;
+    int32_t stream;      // streaming kernel in use
+    uint64_t NT;         // tiles (streaming mode)
+    cudaIpcMemHandle_t htf, hpart;
 };
 static_assert(sizeof(ShardHandle) <= OSP_SHARD_HANDLE_BYTES, "handle too large");
 
@@ -48,6 +51,15 @@ struct osp_shard {
     PeerTable pt[2]{};         // per delta buffer
     std::vector<void*> opened; // peer mappings to close
     bool connected = false;
+    // streaming mode (kernels/shard_stream.cu)
+    bool stream = false;
+    uint64_t NT = 0;
+    unsigned* tflag = nullptr; // [NT] per-tile ready flags, IPC-exported
+    double* pbuf = nullptr;    // [NT] per-tile PGP partials (the group's), IPC-exported
+    StreamArgs sa{};           // peer tables of tflag/pbuf
+    int vec[2]{};              // per delta buffer: 16-byte aligned rows
+    unsigned iter = 0;         // iterations started (stage-1 launches)
+    unsigned long long* dbg = nullptr;  // [2 stages][3 roles][16] diagnostics counters (OSP_SS_DEBUG=1)
 };
 
 extern "C" {
@@ -78,8 +90,15 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     s->n_chunks = cfg->n_chunks;
     s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
     s->ap_loc = make_agg_params(s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->sgd_lr);
+    // streaming kernel (opt-in: OSP_SHARD_STREAM=1) when the shape supports it;
+    // barrier mode is the default (faster on the measured configurations, see
+    // DESIGN.md "Multi-GPU")
+    const char* se = std::getenv("OSP_SHARD_STREAM");
+    const uint32_t Ts = cfg->tile_elems ? cfg->tile_elems : 2048u;
+    s->stream = (se && se[0] == '1') &&
+                shard_stream_supported(s->N, static_cast<int>(Ts), static_cast<int>(part->counts.size()));
     osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks,
-                        cfg->tile_elems, cfg->sgd_lr, OSP_GROUP_REGISTER};
+                        s->stream ? Ts : cfg->tile_elems, cfg->sgd_lr, OSP_GROUP_REGISTER};
     osp_status st = osp_group_create(part, &gc, init_params, stream, &s->grp);
     if (st != OSP_OK) {
         delete s;
@@ -98,12 +117,26 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     if (e == cudaSuccess) e = cudaMemset(s->flags, 0, kBarKinds * kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->epoch, 0, kBarKinds * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
+    if (s->stream) {
+        const char* de = std::getenv("OSP_SS_DEBUG");
+        if (de && de[0] == '1') {
+            if (e == cudaSuccess) e = cudaMalloc(&s->dbg, 96 * sizeof(unsigned long long));
+            if (e == cudaSuccess) e = cudaMemset(s->dbg, 0, 96 * sizeof(unsigned long long));
+        }
+        s->NT = static_cast<uint64_t>(s->grp->v.NT);
+        const uint64_t nt = s->NT ? s->NT : 1;
+        if (e == cudaSuccess) e = cudaMalloc(&s->tflag, nt * sizeof(unsigned));
+        if (e == cudaSuccess) e = cudaMalloc(&s->pbuf, nt * sizeof(double));
+        if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, nt * sizeof(unsigned));
+        if (e == cudaSuccess) e = cudaMemset(s->pbuf, 0, nt * sizeof(double));
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         osp_shard_destroy(s);
         return cuda_fail(e, "shard buffers");
     }
     s->grp->v.agg_full = s->agg;
+    if (s->stream) s->grp->v.partials = s->pbuf;  // resolve reads the exchanged partials
     *out = s;
     return OSP_OK;
 }
@@ -117,6 +150,9 @@ void osp_shard_destroy(osp_shard* s) {
     if (s->flags) cudaFree(s->flags);
     if (s->epoch) cudaFree(s->epoch);
     if (s->error) cudaFree(s->error);
+    if (s->tflag) cudaFree(s->tflag);
+    if (s->dbg) cudaFree(s->dbg);
+    if (s->pbuf) cudaFree(s->pbuf);
     if (s->grp) osp_group_destroy(s->grp);
     delete s;
 }
@@ -137,6 +173,12 @@ osp_status osp_shard_export(osp_shard* s, uint8_t* handle) {
     OSP_CUDA(cudaIpcGetMemHandle(&h.hx, s->X));
     OSP_CUDA(cudaIpcGetMemHandle(&h.hagg, s->agg));
     OSP_CUDA(cudaIpcGetMemHandle(&h.hflags, s->flags));
+    h.stream = s->stream ? 1 : 0;
+    h.NT = s->NT;
+    if (s->stream) {
+        OSP_CUDA(cudaIpcGetMemHandle(&h.htf, s->tflag));
+        OSP_CUDA(cudaIpcGetMemHandle(&h.hpart, s->pbuf));
+    }
     std::memset(handle, 0, OSP_SHARD_HANDLE_BYTES);
     std::memcpy(handle, &h, sizeof h);
     return OSP_OK;
@@ -153,7 +195,7 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
         std::memcpy(&h, handles + static_cast<size_t>(q) * OSP_SHARD_HANDLE_BYTES, sizeof h);
         if (h.magic != kMagic || h.rank != q || h.world != s->world || h.n_loc != s->n_loc ||
             h.M != s->part->total || h.L != s->part->counts.size() || h.ldX != s->ldX ||
-            h.buf_stride != s->buf_stride)
+            h.buf_stride != s->buf_stride || h.stream != (s->stream ? 1 : 0) || h.NT != s->NT)
             return fail(OSP_ERR_CONFIG, "rank " + std::to_string(q) +
                                             " exported an incompatible shard (partition, worker "
                                             "split or world size differ)");
@@ -161,7 +203,18 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
             xbase[q] = s->X;
             aggs[q] = s->agg;
             flags[q] = s->flags;
+            s->sa.tflag[q] = s->tflag;
+            s->sa.part[q] = s->pbuf;
             continue;
+        }
+        if (s->stream) {
+            void *pt = nullptr, *pp = nullptr;
+            OSP_CUDA(cudaIpcOpenMemHandle(&pt, h.htf, cudaIpcMemLazyEnablePeerAccess));
+            s->opened.push_back(pt);
+            OSP_CUDA(cudaIpcOpenMemHandle(&pp, h.hpart, cudaIpcMemLazyEnablePeerAccess));
+            s->opened.push_back(pp);
+            s->sa.tflag[q] = static_cast<unsigned*>(pt);
+            s->sa.part[q] = static_cast<double*>(pp);
         }
         void *px = nullptr, *pa = nullptr, *pf = nullptr;
         OSP_CUDA(cudaIpcOpenMemHandle(&px, h.hx, cudaIpcMemLazyEnablePeerAccess));
@@ -192,6 +245,12 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
         }
         pt.epoch = s->epoch;
         pt.error = s->error;
+        bool vec = (s->ldX % 4 == 0) && (s->grp->v.ldP % 4 == 0) &&
+                   (reinterpret_cast<uintptr_t>(s->grp->v.G) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(s->grp->v.P) % 16 == 0);
+        for (int w = 0; w < s->N; ++w) vec = vec && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
+        for (int q = 0; q < s->world; ++q) vec = vec && (reinterpret_cast<uintptr_t>(pt.agg[q]) % 16 == 0);
+        s->vec[b] = vec ? 1 : 0;
     }
     s->connected = true;
     return OSP_OK;
@@ -212,10 +271,27 @@ static osp_status check_ready(osp_shard* s, int buf) {
     return OSP_OK;
 }
 
+static cudaError_t stream_stage(osp_shard* s, int buf, int stage, int c0, int c1, cudaStream_t st) {
+    StreamArgs a = s->sa;
+    a.stage = stage;
+    a.c0 = c0;
+    a.c1 = c1;
+    a.tepoch = 2u * s->iter + static_cast<unsigned>(stage) - 2u;
+    a.xepoch = s->iter;
+    a.vec = s->vec[buf];
+    a.dbg = s->dbg ? s->dbg + (stage - 1) * 48 : nullptr;
+    return launch_shard_stream(s->grp->v, s->ap_all, s->pt[buf], a, st);
+}
+
 osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
     osp_group* g = s->grp;
+    if (s->stream) {
+        s->iter += 1;
+        OSP_CUDA(stream_stage(s, buf, 1, 0, 0, st));
+        return OSP_OK;
+    }
     OSP_CUDA(launch_barrier(s->pt[buf], 0, st));  // deltas ready; previous agg reads done
     OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st));
     OSP_CUDA(launch_barrier(s->pt[buf], 1, st));  // every shard's aggregate landed here
@@ -229,6 +305,11 @@ osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream)
     if (c0 < 0 || c1 > s->n_chunks || c0 > c1) return fail(OSP_ERR_INVALID, "chunk range");
     cudaStream_t st = as_stream(stream);
     osp_group* g = s->grp;
+    if (s->stream) {
+        if (s->iter == 0) return fail(OSP_ERR_PROTOCOL, "stage 2 before any stage 1");
+        OSP_CUDA(stream_stage(s, buf, 2, c0, c1, st));
+        return OSP_OK;
+    }
     OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, c0, c1, g->grid, st));
     OSP_CUDA(launch_barrier(s->pt[buf], 2, st));
     OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->X + buf * s->buf_stride, s->ldX, 2, c0, c1,
@@ -248,6 +329,12 @@ osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
     osp_group* g = s->grp;
+    if (s->stream) {
+        s->iter += 1;
+        OSP_CUDA(stream_stage(s, buf, 1, 0, 0, st));
+        OSP_CUDA(stream_stage(s, buf, 2, 0, s->n_chunks, st));
+        return osp_shard_resolve(s, buf, stream);
+    }
     float* Xb = s->X + buf * s->buf_stride;
     OSP_CUDA(launch_barrier(s->pt[buf], 0, st));
     OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st));
@@ -270,6 +357,21 @@ osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream) {
     auto step = [&]() -> cudaError_t {
         cudaError_t e;
         float* Xb = s->X + buf * s->buf_stride;
+        if (s->stream) {
+            s->iter += 1;
+            for (int i = 0; i < 8; ++i) ms[i] = 0.f;
+            if ((e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
+            if ((e = stream_stage(s, buf, 1, 0, 0, st)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+            if ((e = stream_stage(s, buf, 2, 0, s->n_chunks, st)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
+            if ((e = launch_resolve(g->v, g->ap, Xb, s->ldX, st)) != cudaSuccess) return e;
+            if ((e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
+            if ((e = cudaEventSynchronize(ev[3])) != cudaSuccess) return e;
+            for (int i = 0; i < 3; ++i)
+                if ((e = cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1])) != cudaSuccess) return e;
+            return cudaSuccess;
+        }
         if ((e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
         if ((e = launch_barrier(s->pt[buf], 0, st)) != cudaSuccess) return e;
         if ((e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
@@ -306,6 +408,20 @@ osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uin
     OSP_CUDA(launch_synth(seed, n_workers, iteration, 0, n, out, ld,
                           static_cast<uint64_t>(worker0), as_stream(stream)));
     return OSP_OK;
+}
+
+int osp_shard_streaming(const osp_shard* s) { return s && s->stream ? 1 : 0; }
+
+// Diagnostics of the streaming kernel (OSP_SS_DEBUG=1 at create): 96 counters
+// accumulated since create, [stage 1 | stage 2][48]: producer empty-wait
+// cycles, peer-flag wait cycles, 0, A/B/C items, producer cycles, 0, consumer
+// warp-0 full-wait cycles, consumer warp-0 processing cycles, 0, 0, producers,
+// max producer cycles (atomicMax, never reset), 0... Returns 0 when disabled.
+int osp_shard_debug_counters(osp_shard* s, unsigned long long* out96) {
+    if (!s || !s->dbg || !out96) return 0;
+    if (cudaMemcpy(out96, s->dbg, 96 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return 1;
 }
 
 osp_status osp_shard_check(osp_shard* s, void* stream) {

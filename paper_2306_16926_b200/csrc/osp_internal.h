@@ -70,7 +70,7 @@ struct GroupView {
     int* chunk_of;               // [L] compacted chunk or -1
     uint8_t* gib_bytes;          // [8 + ceil(L/8)] encoded current GIB
     uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
-    int* sched;                  // [8] dynamic tile scheduler counters (SchedIdx)
+    int* sched;                  // [16] dynamic tile scheduler counters (SchedIdx)
     double* lscore;              // [L] per-layer tree sum of the tile partials
     int* rs_layers;              // [L] RS (barrier) layers, ascending id (valid prefix n_rs)
     int* rs_tile_prefix;         // [L+1] exclusive tile prefix along rs_layers
@@ -84,7 +84,11 @@ enum SchedIdx {
     SCHED_S2_DONE = 3,
     SCHED_RESOLVE_DONE = 4,
     SCHED_AGG_NEXT = 5,
-    SCHED_AGG_DONE = 6
+    SCHED_AGG_DONE = 6,
+    SCHED_SS_A = 8,     // streaming shard kernel: own exchange tiles
+    SCHED_SS_B = 9,     //   peers' exchange tiles
+    SCHED_SS_C = 10,    //   local-estimate tiles (stage 1)
+    SCHED_SS_DONE = 11
 };
 enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2, META_N_RS = 3 };
 enum Meta64Idx {
@@ -124,6 +128,21 @@ cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const Peer
 cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const float* Xloc,
                                uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s);
 cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s);
+// Streaming shard kernel (kernels/shard_stream.cu): push, aggregate, pull and
+// apply of one stage in one launch, per-tile flags instead of grid barriers.
+struct StreamArgs {
+    unsigned* tflag[kMaxRanks];  // every rank's per-tile ready flags [NT]
+    double* part[kMaxRanks];     // every rank's per-tile PGP partials [NT]
+    unsigned tepoch;             // tile-flag value of this launch (2*iteration + stage - 2)
+    unsigned xepoch;             // deltas-ready value of this iteration
+    int stage, c0, c1;
+    int vec;                     // rows, G, P and pull buffers 16-byte aligned
+    unsigned long long* dbg;     // optional counters (diagnostics), or null
+    size_t ring_bytes;           // shared-memory ring per CTA (set by the launcher)
+};
+bool shard_stream_supported(int n_workers, int T, int L);
+cudaError_t launch_shard_stream(const GroupView& g, const AggParams& ap, const PeerTable& pt,
+                                const StreamArgs& sa, cudaStream_t s);
 // stage-1 apply + stage-2 aggregate of chunks [c0, c1) in one launch
 cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
                                const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,

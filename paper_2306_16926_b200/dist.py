@@ -106,9 +106,17 @@ class ShardGroup:
         """One step with events between the kernels (ms per phase)."""
         out = (ctypes.c_float * 8)()
         _check(lib().osp_shard_profile(self._h, buf, out, _stream(stream)))
-        names = ["barrier_in", "agg1", "barrier1", "apply1+agg2", None, "barrier2", "apply2",
-                 "resolve"]
+        if self.streaming:
+            names = ["stage1", "stage2", "resolve"]
+        else:
+            names = ["barrier_in", "agg1", "barrier1", "apply1+agg2", None, "barrier2", "apply2",
+                     "resolve"]
         return {n: float(v) for n, v in zip(names, out) if n}
+
+    @property
+    def streaming(self) -> bool:
+        """True: streaming kernels (per-tile flags); False: barrier mode."""
+        return bool(lib().osp_shard_streaming(self._h))
 
     def check(self, stream=None):
         _check(lib().osp_shard_check(self._h, _stream(stream)))

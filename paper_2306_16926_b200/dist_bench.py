@@ -93,9 +93,18 @@ def run(args, metric: str, unit: str):
     u = sh.local.deferred_history(tag0, K).astype(np.float64) / model_bytes
     n_loc = N // world
     u_mean = float(u.mean())
-    # per-GPU algorithmic HBM bytes per step: own rows served to the shard owners,
-    # agg written + read, G read + written, worker rows (+ local estimate on ICS layers)
-    hbm_bytes = 4.0 * M * (4 + n_loc * (2 + 2 * u_mean))
+    # per-GPU algorithmic HBM bytes per step
+    if sh.streaming:
+        # local rows read once (by this rank or an owner), G read + written, agg
+        # written into the pull buffer (own tiles locally, the rest by the peers)
+        # and read back on the peers' tiles, worker rows, local estimate on ICS
+        # layers
+        hbm_bytes = 4.0 * M * (2 * n_loc + 2 + 1 + (world - 1.0) / world
+                               + u_mean * (2 * n_loc + 1))
+    else:
+        # own rows served to the shard owners, agg written + read, G read + written,
+        # worker rows (+ local estimate on ICS layers)
+        hbm_bytes = 4.0 * M * (4 + n_loc * (2 + 2 * u_mean))
     # per-GPU NVLink bytes per step (each direction): remote delta rows read by this
     # rank's shard + its aggregate stored to the other ranks
     nvl_bytes = 4.0 * M * ((N - n_loc) / world + (world - 1) / world)
@@ -171,7 +180,10 @@ def run(args, metric: str, unit: str):
                        "params": M, "layers": L, "workers": N, "workers_per_gpu": n_loc,
                        "budget_frac": args.budget_frac, "chunks": args.chunks,
                        "deltas": "reference synth generator, 2 sets alternating (> L2)",
-                       "parallelism": f"ps-shard{world}"},
+                       "parallelism": f"ps-shard{world}",
+                       "shard_kernels": "streaming (per-tile flags)" if sh.streaming
+                       else "barrier (agg / barrier / apply)",
+                       "tile_elems": sh.local.geometry()["tile_elems"]},
             "roofline": {"bound": "nvlink" if nvl_bytes / nvl_peak > hbm_bytes / hbm_peak else "hbm",
                          "achieved": nvl_gbs, "peak": nvl_peak, "unit": "GB/s",
                          "frac": nvl_gbs / nvl_peak, "traffic": None,
@@ -188,8 +200,11 @@ def run(args, metric: str, unit: str):
                     "h2d_bytes_per_step": n_loc * M * 4 * world,
                     "d2h_bytes_per_step": (8 + (L + 7) // 8) * world,
                     "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read"},
-            # fused step: barrier, agg1, barrier, apply1+agg2, barrier, apply2, resolve
-            "gpu_launches": K * ((4 + 3 * args.chunks + 1) if args.per_chunk else 7),
+            # streaming: stage1, stage2, resolve per step (per chunk: one stage-2 launch
+            # each); barrier mode: barrier, agg1, barrier, apply1+agg2, barrier, apply2,
+            # resolve
+            "gpu_launches": K * (((2 + args.chunks) if args.per_chunk else 3) if sh.streaming
+                                 else ((4 + 3 * args.chunks + 1) if args.per_chunk else 7)),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

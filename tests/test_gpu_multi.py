@@ -32,6 +32,8 @@ def _worker(rank, world, port, cfg, q):
         from paper_2306_16926_b200 import dist as odist
         from paper_2306_16926_b200 import osp
 
+        if "stream" in cfg:
+            os.environ["OSP_SHARD_STREAM"] = "1" if cfg["stream"] else "0"
         torch.cuda.set_device(rank)
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
@@ -45,6 +47,8 @@ def _worker(rank, world, port, cfg, q):
         sh = odist.ShardGroup(part, N, w, n_chunks=nc, init_params=torch.as_tensor(p0, device="cuda"),
                               tile_elems=cfg.get("tile", 0))
         sh.connect_via()
+        if "stream" in cfg:
+            assert sh.streaming == bool(cfg["stream"]), "shard kernel family"
         G = p0.copy()
         P = np.tile(p0, (N, 1))
         flags = np.zeros(len(counts), np.uint8)
@@ -97,21 +101,49 @@ def run_world(cfg, world=2):
     assert not bad, bad
 
 
-def test_shard_two_gpus_resnet_like():
+@pytest.mark.parametrize("stream", [True, False])
+def test_shard_two_gpus_resnet_like(stream):
     from paper_2306_16926_b200 import layouts
     run_world(dict(counts=layouts.resnet50()[:60], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=0.5, iters=3, seed=11, p0_seed=0))
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, stream=stream))
 
 
 def test_shard_two_gpus_ragged_unequal_weights():
+    # tile 256: no streaming kernel for this shape, barrier mode
     rng = np.random.default_rng(3)
     counts = [int(c) for c in rng.integers(1, 7000, 37)]
     w = [float(x) for x in 0.1 + rng.random(4)]
     run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=0.7, iters=4, seed=5,
-                   p0_seed=9, tile=256, per_chunk=True))
+                   p0_seed=9, tile=256, per_chunk=True, stream=False))
 
 
-def test_shard_four_gpus():
+def test_shard_stream_ragged_per_chunk():
+    # odd layer sizes: unstaged (scalar) tiles next to staged ones; per-chunk stage 2
+    rng = np.random.default_rng(4)
+    counts = [int(c) for c in rng.integers(1, 9000, 41)]
+    w = [float(x) for x in 0.1 + rng.random(4)]
+    run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=0.6, iters=4, seed=6,
+                   p0_seed=2, per_chunk=True, stream=True))
+
+
+@pytest.mark.parametrize("frac", [0.0, 1.0])
+def test_shard_stream_budget_edges(frac):
+    # 0.0: every layer in stage 1's exchange; 1.0: stage 1 only local estimates
+    from paper_2306_16926_b200 import layouts
+    run_world(dict(counts=layouts.resnet50()[:50], N=8, weights=[0.125] * 8, chunks=4,
+                   budget_frac=frac, iters=3, seed=13, p0_seed=7, stream=True))
+
+
+@pytest.mark.parametrize("stream", [True, False])
+def test_shard_four_gpus(stream):
     from paper_2306_16926_b200 import layouts
     run_world(dict(counts=layouts.resnet50()[:80], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=0.5, iters=3, seed=11, p0_seed=0), world=4)
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, stream=stream), world=4)
+
+
+def test_shard_four_gpus_stream_ragged():
+    rng = np.random.default_rng(12)
+    counts = [int(c) for c in rng.integers(1, 20000, 30)]
+    w = [float(x) for x in 0.1 + rng.random(8)]
+    run_world(dict(counts=counts, N=8, weights=w, chunks=4, budget_frac=0.5, iters=3, seed=3,
+                   p0_seed=5, stream=True), world=4)
