@@ -320,8 +320,9 @@ def b200_single(args):
                    "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU",
                    "stage_kernels": grp.stage_kernels},
         "hbm_gbs_step": ach_step,
-        "roofline": {"bound": "hbm", "kernel": ("k_stage_tma<1>" if grp.stage_kernels == "tma-staged" else "k_stage1")
-                     + " (barrier: RS agg/apply + LGP)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_stage_tma<1>" if grp.stage_kernels == "tma-staged" else "k_stage1")
+                               + " (barrier: RS agg/apply + LGP)",
                      "achieved": ach_s1, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach_s1 / peak,
                      "traffic": ncu_traffic(f"{args.layout}/N{N}/b{args.budget_frac}",

@@ -250,7 +250,10 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
  * transfers (multi-GPU) and for the reference's message-by-message flow. */
 osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream);
-/* stage1 + stage2_all + resolve. */
+/* stage1 + stage2_all (two launches; a single-launch variant with per-tile
+ * dependency flags measured slower, profiles/r1_ncu_summary.md). */
+osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void* stream);
+/* osp_group_stages + resolve. */
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 /* End-to-end step from HOST (pinned or pageable) deltas: H2D copy of the N rows
  * into the group's staging buffer, the step, and a D2H read of the encoded next

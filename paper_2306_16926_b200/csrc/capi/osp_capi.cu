@@ -761,9 +761,13 @@ osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, voi
     return OSP_OK;
 }
 
-osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     OSP_TRY(osp_group_stage1(g, deltas, ld, stream));
-    OSP_TRY(osp_group_stage2_all(g, deltas, ld, stream));
+    return osp_group_stage2_all(g, deltas, ld, stream);
+}
+
+osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_TRY(osp_group_stages(g, deltas, ld, stream));
     return osp_group_resolve(g, deltas, ld, stream);
 }
 

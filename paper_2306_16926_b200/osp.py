@@ -475,6 +475,11 @@ class OspGroup:
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_stage2_all(self._h, p, ld, _stream(stream)))
 
+    def stages(self, deltas: torch.Tensor, stream=None):
+        """stage1 + stage2_all."""
+        p, ld = self._deltas(deltas)
+        _check(lib().osp_group_stages(self._h, p, ld, _stream(stream)))
+
     def resolve(self, deltas: torch.Tensor, stream=None):
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_resolve(self._h, p, ld, _stream(stream)))
