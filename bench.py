@@ -190,9 +190,12 @@ def reference_arm(args, rank: int):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
-            "config": {"workload": f"{args.layout}-size OSP step", "params": M,
+            "config": {"workload": f"{args.layout}-size OSP sync+LGP step (BASELINE configs[1])",
+                       "params": M, "layers": len(layouts.get(args.layout)),
                        "workers": args.workers, "budget_frac": args.budget_frac,
-                       "chunks": args.chunks},
+                       "chunks": args.chunks, "deltas": "reference synth generator, seed "
+                       f"{args.seed} (generated outside the timed region)",
+                       "parallelism": "host threads (reference CPU engine)"},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
