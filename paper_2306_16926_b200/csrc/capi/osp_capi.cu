@@ -653,6 +653,25 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &v.lscore, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.rs_layers, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.rs_tile_prefix, L + 1)) != OSP_OK) return cleanup(st);
+    // resolve sum items: each layer's tiles in chunks of <= kSumChunk
+    std::vector<int> items, layer_items(L + 1);
+    for (uint64_t l = 0; l < L; ++l) {
+        layer_items[l] = static_cast<int>(items.size() / 3);
+        for (int t = tile_base[l]; t < tile_base[l + 1]; t += kSumChunk) {
+            items.push_back(static_cast<int>(l));
+            items.push_back(t);
+            items.push_back(std::min(t + kSumChunk, tile_base[l + 1]));
+        }
+    }
+    layer_items[L] = static_cast<int>(items.size() / 3);
+    int *d_items = nullptr, *d_litems = nullptr;
+    if ((st = dalloc(g, &d_items, std::max<size_t>(items.size(), 3))) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &d_litems, L + 1)) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.item_sums, std::max<size_t>(items.size() / 3, 1))) != OSP_OK)
+        return cleanup(st);
+    v.sum_items = d_items;
+    v.layer_items = d_litems;
+    v.n_sum_items = static_cast<int>(items.size() / 3);
 
     cudaStream_t s = as_stream(stream);
     auto cu = [&](cudaError_t e, const char* what) -> osp_status {
@@ -663,6 +682,13 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         return cleanup(st);
     if ((st = cu(cudaMemcpyAsync(d_tl, tile_layer.data(), nt_total * sizeof(int),
                                  cudaMemcpyHostToDevice, s), "tile_layer")) != OSP_OK)
+        return cleanup(st);
+    if (!items.empty() &&
+        (st = cu(cudaMemcpyAsync(d_items, items.data(), items.size() * sizeof(int),
+                                 cudaMemcpyHostToDevice, s), "sum items")) != OSP_OK)
+        return cleanup(st);
+    if ((st = cu(cudaMemcpyAsync(d_litems, layer_items.data(), (L + 1) * sizeof(int),
+                                 cudaMemcpyHostToDevice, s), "layer items")) != OSP_OK)
         return cleanup(st);
     if (init_params) {
         st = cu(cudaMemcpyAsync(v.G, init_params, M * 4, cudaMemcpyDeviceToDevice, s), "init G");

@@ -42,6 +42,8 @@ struct Smem {
     int* i1;
     int* i2;
     double* wtot;  // [kWarps] scan scratch (8-byte slots)
+    uint64_t* cnt; // [L] layer element counts (staged from global)
+    int* tb;       // [L+1] tile_base (staged from global)
     int* flag;     // [8]
 };
 
@@ -52,17 +54,30 @@ __device__ Smem carve(char* base, int L) {
     s.a1 = s.rad + L;
     s.a2 = s.a1 + L;
     s.wtot = s.a2 + L;
-    s.sorted = reinterpret_cast<int*>(s.wtot + kWarps);
+    s.cnt = reinterpret_cast<uint64_t*>(s.wtot + kWarps);
+    s.sorted = reinterpret_cast<int*>(s.cnt + L);
     s.pos = s.sorted + L;
     s.i1 = s.pos + L;
     s.i2 = s.i1 + L;
-    s.flag = s.i2 + L;
+    s.tb = s.i2 + L;
+    s.flag = s.tb + L + 1;
     return s;
 }
 
 size_t smem_bytes(int L) {
-    return static_cast<size_t>(L) * (4 * sizeof(double) + 4 * sizeof(int)) +
+    return static_cast<size_t>(L) * (5 * sizeof(double) + 5 * sizeof(int)) + sizeof(int) +
            kWarps * sizeof(double) + 8 * sizeof(int);
+}
+
+// One coalesced load of the layer geometry into shared memory; everything the
+// single-CTA phases need per layer is then a shared-memory read.
+__device__ void stage_geometry(const GroupView& g, const Smem& s) {
+    for (int l = threadIdx.x; l < g.L; l += blockDim.x) {
+        s.cnt[l] = g.counts[l];
+        s.tb[l] = g.tile_base[l];
+    }
+    if (threadIdx.x == 0) s.tb[g.L] = g.tile_base[g.L];
+    __syncthreads();
 }
 
 // Block-wide inclusive scan of a[0..n) in shared memory (associative,
@@ -105,16 +120,29 @@ __device__ void block_scan(T* a, int n, T ident, Op op, double* wtot_raw) {
 }
 
 // Rank by (key, id): the reference's stable_sort by score with id tie-break.
+// rank(l) = #{j : (key_j, j) < (key_l, l)}; with L small against the block,
+// G = 2^k lanes of a warp share one layer's count (strided over j, xor-shuffle
+// sum inside the group).
 __device__ void rank_layers_block(const Smem& s, int L) {
-    for (int l = threadIdx.x; l < L; l += blockDim.x) {
-        const double kl = s.key[l];
+    int G = 1;
+    while (G < 32 && 2 * G * L <= static_cast<int>(blockDim.x)) G *= 2;
+    const int sub = threadIdx.x % G;
+    const int lanes = blockDim.x / G;
+    for (int base = 0; base < L; base += lanes) {
+        const int l = base + static_cast<int>(threadIdx.x) / G;
         int r = 0;
-        for (int j = 0; j < L; ++j) {
-            const double kj = s.key[j];
-            r += (kj < kl) || (kj == kl && j < l);
+        if (l < L) {
+            const double kl = s.key[l];
+            for (int j = sub; j < L; j += G) {
+                const double kj = s.key[j];
+                r += (kj < kl) || (kj == kl && j < l);
+            }
         }
-        s.pos[l] = r;
-        s.sorted[r] = l;
+        for (int o = 1; o < G; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+        if (l < L && sub == 0) {
+            s.pos[l] = r;
+            s.sorted[r] = l;
+        }
     }
     __syncthreads();
 }
@@ -130,7 +158,7 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     const uint64_t total = k > 0 ? pre[k - 1] : 0;
     const uint64_t nc = static_cast<uint64_t>(g.n_chunks);
     for (int r = tid; r < k; r += B) {
-        const uint64_t bytes = g.counts[ord[r]] * static_cast<uint64_t>(g.bpe);
+        const uint64_t bytes = s.cnt[ord[r]] * static_cast<uint64_t>(g.bpe);
         const uint64_t cum = pre[r] - bytes;
         uint64_t idx = total == 0 ? 0 : (cum * nc) / total;
         if (idx > nc - 1) idx = nc - 1;
@@ -157,7 +185,7 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         if (r == 0 || s.i2[r] != s.i2[r - 1]) g.chunk_begin[c] = r;
     }
     __syncthreads();
-    for (int r = tid; r < k; r += B) s.i1[r] = g.tile_base[ord[r] + 1] - g.tile_base[ord[r]];
+    for (int r = tid; r < k; r += B) s.i1[r] = s.tb[ord[r] + 1] - s.tb[ord[r]];
     __syncthreads();
     block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, s.wtot);
     for (int r = tid; r <= k; r += B) g.ics_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
@@ -175,7 +203,7 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
             const int excl = l == 0 ? 0 : s.i2[l - 1];
             if (!fl[l]) {
                 g.rs_layers[excl] = l;
-                s.i1[excl] = g.tile_base[l + 1] - g.tile_base[l];
+                s.i1[excl] = s.tb[l + 1] - s.tb[l];
             }
         }
         __syncthreads();
@@ -248,10 +276,11 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     const Smem s = carve(smem_raw, L);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-    // 0. every block: per-layer tree sums of the tile partials (fixed order:
-    //    thread-strided sequential, shuffle tree, warps in order)
-    for (int l = blockIdx.x; l < L; l += gridDim.x) {
-        const int t0 = g.tile_base[l], t1 = g.tile_base[l + 1];
+    // 0. every block: tree sums of the tile partials per sum item (<= kSumChunk
+    //    tiles of one layer; fixed order: thread-strided sequential, shuffle
+    //    tree, warps in order)
+    for (int it = blockIdx.x; it < g.n_sum_items; it += gridDim.x) {
+        const int t0 = g.sum_items[3 * it + 1], t1 = g.sum_items[3 * it + 2];
         double acc = 0.0;
         for (int t = t0 + tid; t < t1; t += blockDim.x) acc = __dadd_rn(acc, g.partials[t]);
 #pragma unroll
@@ -261,7 +290,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
         if (tid == 0) {
             double tot = 0.0;
             for (int w = 0; w < kWarps; ++w) tot = __dadd_rn(tot, s.wtot[w]);
-            g.lscore[l] = tot;
+            g.item_sums[it] = tot;
         }
         __syncthreads();
     }
@@ -275,13 +304,20 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     __threadfence();
     if (tid == 0) g.sched[SCHED_RESOLVE_DONE] = 0;
 
-    // 1. per-layer scores and certificate radii
+    stage_geometry(g, s);
+    // 1. per-layer scores (items summed in order) and certificate radii. Depth
+    //    of any term: tile tree + item tree (<= ceil(kSumChunk/threads) strided
+    //    terms, 5 shuffles, kWarps warps) + the sequential item sum + slack
     for (int l = tid; l < L; l += blockDim.x) {
-        const double acc = __ldcg(g.lscore + l);
-        const int nt = g.tile_base[l + 1] - g.tile_base[l];
-        const double D = tile_depth(g.T) + (nt + kResolveThreads - 1) / kResolveThreads + 5 +
-                         kWarps + 2;
-        const double n = static_cast<double>(g.counts[l]);
+        const int i0 = g.layer_items[l], i1 = g.layer_items[l + 1];
+        double acc = 0.0;
+        for (int it = i0; it < i1; ++it) acc = __dadd_rn(acc, __ldcg(g.item_sums + it));
+        g.lscore[l] = acc;
+        const int nt = s.tb[l + 1] - s.tb[l];
+        const int per_item = nt < kSumChunk ? nt : kSumChunk;
+        const double D = tile_depth(g.T) + (per_item + kResolveThreads - 1) / kResolveThreads + 5 +
+                         kWarps + (i1 - i0) + 2;
+        const double n = static_cast<double>(s.cnt[l]);
         s.key[l] = acc;
         s.rad[l] = acc * (kU * (1.01 * (n - 1.0 + D) + 8.0));
         g.scores[l] = acc;
@@ -341,7 +377,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     // 4. prefix rule: inclusive byte scan in rank order, k = #prefix <= budget
     uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
     for (int r = tid; r < L; r += blockDim.x)
-        pre[r] = g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
+        pre[r] = s.cnt[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
     __syncthreads();
     block_scan<uint64_t>(pre, L, 0ull, [](uint64_t a, uint64_t b) { return a + b; }, s.wtot);
     const uint64_t budget = g.meta64[META64_BUDGET];
@@ -364,6 +400,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const 
     extern __shared__ __align__(16) char smem_raw[];
     const int L = g.L;
     const Smem s = carve(smem_raw, L);
+    stage_geometry(g, s);
     if (threadIdx.x == 0) {
         int k = 0;
         for (int l = 0; l < L; ++l) s.pos[l] = 0;  // seen
@@ -380,7 +417,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const 
         uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
         uint64_t run = 0;
         for (int r = 0; r < k; ++r) {
-            run += g.counts[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
+            run += s.cnt[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
             pre[r] = run;
         }
         if (g.meta64) g.meta64[META64_RESOLVED] = tag;
@@ -439,7 +476,8 @@ cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float*
     const size_t sm = smem_bytes(g.L);
     cudaError_t e = set_smem(reinterpret_cast<const void*>(k_resolve), sm);
     if (e != cudaSuccess) return e;
-    const int blocks = g.L < sm_count() ? g.L : sm_count();
+    const int items = g.n_sum_items > 0 ? g.n_sum_items : 1;
+    const int blocks = items < sm_count() ? items : sm_count();
     return launch_pdl(k_resolve, dim3(blocks), dim3(kResolveThreads), sm, st, g, ap, X, ldX);
 }
 

@@ -75,7 +75,14 @@ struct GroupView {
     int* rs_layers;              // [L] RS (barrier) layers, ascending id (valid prefix n_rs)
     int* rs_tile_prefix;         // [L+1] exclusive tile prefix along rs_layers
     const float* agg_full;       // [M] aggregated deltas (sharded path), or null
+    // resolve's per-layer sums are split into items of <= kSumChunk tiles so a
+    // huge layer is summed by many blocks (fixed order: items ascending)
+    const int* sum_items;        // [n_sum_items][3] layer, first tile, end tile
+    int n_sum_items;
+    const int* layer_items;      // [L+1] first item of each layer
+    double* item_sums;           // [n_sum_items]
 };
+constexpr int kSumChunk = 4096;  // tiles per resolve sum item
 
 enum SchedIdx {
     SCHED_S1_NEXT = 0,
