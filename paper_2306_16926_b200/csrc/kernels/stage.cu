@@ -634,15 +634,17 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_apply2(GroupView g, int
 // Stage-1 apply fused with the stage-2 push/pull. The two are independent
 // (disjoint elements of agg_full and G; both only read the deltas), and one is
 // HBM-bound (apply) while the other is NVLink-bound (peer aggregate), so one
-// launch runs both: even warps start on the apply tiles, odd warps on this
-// rank's stage-2 aggregate tiles, and a warp whose list runs dry switches to
-// the other. The last warp out resets both work counters.
+// launch runs both: three warps in four start on the apply tiles, the fourth
+// on this rank's stage-2 aggregate tiles (measured split), and a warp whose
+// list runs dry switches to the other. The last warp out resets both work
+// counters.
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggParams ap_all,
                                                                AggParams ap_loc, PeerTable pt,
                                                                const float* __restrict__ X,
                                                                uint64_t ldX, int c0, int c1,
-                                                               int vec_apply, int vec_agg) {
+                                                               int vec_apply, int vec_agg,
+                                                               int apply_every) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
     const int lane = threadIdx.x & 31;
     const Tab tab = stage_tab(g, smem_tab, 2, c0, c1);
@@ -660,7 +662,12 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggP
         const int u = lo + grab(next_agg, lane);
         return u < hi ? u : -1;
     };
-    int list = ((blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5)) & 1;
+    // apply_every > 0: one warp in apply_every starts on the (HBM-bound) apply
+    // list, the rest on the (NVLink-bound) aggregate list; < 0: one warp in
+    // -apply_every starts on the aggregate list. A warp whose list runs dry
+    // switches to the other.
+    const int gw = (blockIdx.x * (blockDim.x >> 5)) + (threadIdx.x >> 5);
+    int list = apply_every > 0 ? (gw % apply_every == 0 ? 0 : 1) : (gw % -apply_every == 0 ? 1 : 0);
     int dry = 0;
     int cur = fetch(list);
     while (true) {
@@ -861,8 +868,15 @@ cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, cons
         constexpr int NS = decltype(nc)::value;
         cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_fused<NS>));
         if (e != cudaSuccess) return e;
+        // measured (tools/fused_split.sh, ResNet-50): one warp in 4 starting on
+        // the aggregate: 0.608 -> 0.575 ms (P=2), 0.577 -> 0.514 ms (P=4)
+        static const int every = [] {
+            const char* v = std::getenv("OSP_FUSED_APPLY_EVERY");
+            const int e = v && *v ? std::atoi(v) : -4;
+            return e != 0 ? e : -4;
+        }();
         k_shard_fused<NS><<<grid, kStageThreads, sm, s>>>(g, ap_all, ap_loc, pt, Xloc, ldX, c0, c1,
-                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0);
+                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0, every);
         return cudaGetLastError();
     });
 }
