@@ -181,9 +181,10 @@ def reference_arm(args, rank: int):
         return
     threads = os.cpu_count() or 1
     t0 = time.time()
+    k_run = max(1, args.steps if args.steps <= 5 else 5)  # bounded CPU sample
+    w_run = max(1, min(args.warmup, 2))
     cb = run_reference_cpu(args.layout, args.workers, args.budget_frac, args.chunks, args.seed,
-                           max(1, args.steps if args.steps <= 5 else 5), max(1, min(args.warmup, 2)),
-                           threads)
+                           k_run, w_run, threads)
     from paper_2306_16926_b200 import layouts
     M = sum(layouts.get(args.layout))
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
@@ -199,6 +200,7 @@ def reference_arm(args, rank: int):
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
+            "cpu_steps_timed": k_run, "cpu_warmup_run": w_run,
             "wall_s": round(time.time() - t0, 2)}
     print(json.dumps(line), flush=True)
 
