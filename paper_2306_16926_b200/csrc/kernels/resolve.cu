@@ -3,7 +3,8 @@
 // (importance.cpp:30-40) -> prefix-rule GIB (importance.cpp:42-59) -> the
 // rank-ordered ICS list, its byte-balanced chunk map (split_for_sync,
 // protocol.cpp:122-166) and the tile lists the next iteration's stage-2
-// kernels walk. One CTA of 1024 threads, one launch; L <= kMaxLayers.
+// kernels walk. One CTA of 1024 threads, one launch; L <= kMaxLayers (shared
+// memory: ~60 B per layer).
 //
 // Bit-exact ranking from a parallel sum (SURVEY.md §7 hard part 1). The
 // reference sums |g*p| sequentially in double; a parallel tree rounds
@@ -41,7 +42,7 @@ struct Smem {
     int* pos;
     int* i1;
     int* i2;
-    double* wtot;  // [kWarps] scan scratch (8-byte slots)
+    double* wtot;  // [4 * kWarps] scan scratch (8-byte slots)
     uint64_t* cnt; // [L] layer element counts (staged from global)
     int* tb;       // [L+1] tile_base (staged from global)
     int* flag;     // [8]
@@ -54,7 +55,7 @@ __device__ Smem carve(char* base, int L) {
     s.a1 = s.rad + L;
     s.a2 = s.a1 + L;
     s.wtot = s.a2 + L;
-    s.cnt = reinterpret_cast<uint64_t*>(s.wtot + kWarps);
+    s.cnt = reinterpret_cast<uint64_t*>(s.wtot + 4 * kWarps);
     s.sorted = reinterpret_cast<int*>(s.cnt + L);
     s.pos = s.sorted + L;
     s.i1 = s.pos + L;
@@ -66,7 +67,7 @@ __device__ Smem carve(char* base, int L) {
 
 size_t smem_bytes(int L) {
     return static_cast<size_t>(L) * (5 * sizeof(double) + 5 * sizeof(int)) + sizeof(int) +
-           kWarps * sizeof(double) + 8 * sizeof(int);
+           4 * kWarps * sizeof(double) + 8 * sizeof(int);
 }
 
 // One coalesced load of the layer geometry into shared memory; everything the
@@ -119,44 +120,129 @@ __device__ void block_scan(T* a, int n, T ident, Op op, double* wtot_raw) {
     __syncthreads();
 }
 
-// Rank by (key, id): the reference's stable_sort by score with id tie-break.
-// rank(l) = #{j : (key_j, j) < (key_l, l)}; with L small against the block,
-// G = 2^k lanes of a warp share one layer's count (strided over j, xor-shuffle
-// sum inside the group).
-__device__ void rank_layers_block(const Smem& s, int L) {
-    int G = 1;
-    while (G < 32 && 2 * G * L <= static_cast<int>(blockDim.x)) G *= 2;
-    const int sub = threadIdx.x % G;
-    const int lanes = blockDim.x / G;
-    for (int base = 0; base < L; base += lanes) {
-        const int l = base + static_cast<int>(threadIdx.x) / G;
-        int r = 0;
-        if (l < L) {
-            const double kl = s.key[l];
-            for (int j = sub; j < L; j += G) {
-                const double kj = s.key[j];
-                r += (kj < kl) || (kj == kl && j < l);
-            }
+// K independent inclusive scans of a[j][0..n), j < K, with one op, sharing the
+// three barriers of block_scan (wtot_raw needs K * kWarps 8-byte slots).
+template <int K, typename T, typename Op>
+__device__ void block_scan_multi(T* const* a, int n, T ident, Op op, double* wtot_raw) {
+    T* wtot = reinterpret_cast<T*>(wtot_raw);  // [K][kWarps]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (n + blockDim.x - 1) / blockDim.x;
+    const int b = min(n, tid * per), e = min(n, b + per);
+    T incl[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        T run = ident;
+        for (int i = b; i < e; ++i) run = op(run, a[j][i]);
+        incl[j] = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T v = __shfl_up_sync(0xffffffffu, incl[j], o);
+            if (lane >= o) incl[j] = op(v, incl[j]);
         }
-        for (int o = 1; o < G; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-        if (l < L && sub == 0) {
-            s.pos[l] = r;
-            s.sorted[r] = l;
+        if (lane == 31) wtot[j * kWarps + warp] = incl[j];
+    }
+    __syncthreads();
+    if (warp < K) {
+        T w = lane < kWarps ? wtot[warp * kWarps + lane] : ident;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const T v = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w = op(v, w);
+        }
+        if (lane < kWarps) wtot[warp * kWarps + lane] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const T excl_in_warp = __shfl_up_sync(0xffffffffu, incl[j], 1);
+        T pre = warp > 0 ? wtot[j * kWarps + warp - 1] : ident;
+        if (lane > 0) pre = op(pre, excl_in_warp);
+        for (int i = b; i < e; ++i) {
+            pre = op(pre, a[j][i]);
+            a[j][i] = pre;
         }
     }
     __syncthreads();
 }
 
+// Rank by (key, id): the reference's stable_sort by score with id tie-break
+// (importance.cpp:30-40). Small L: counting rank. Larger L: bitonic sort of
+// (key, id) pairs padded to a power of two with (+inf, INT_MAX); a1..a2 (2L
+// doubles) and i1..i2 (2L ints) are free at every call site and hold the
+// pairs. Scores are non-negative sums, so the comparison is a plain total
+// order. (Measured crossover: counting 13.7 us vs bitonic 18.4 us resolve at
+// L = 161; 24.0 vs 22.5 us at L = 467.)
+constexpr int kCountRankMax = 320;
+__device__ void rank_layers_block(const Smem& s, int L) {
+    if (L <= kCountRankMax) {
+        // small L: rank(l) = #{j : (key_j, j) < (key_l, l)}, G = 2^k lanes of a
+        // warp share one layer's count (xor-shuffle sum inside the group)
+        int G = 1;
+        while (G < 32 && 2 * G * L <= static_cast<int>(blockDim.x)) G *= 2;
+        const int sub = threadIdx.x % G;
+        const int lanes = blockDim.x / G;
+        for (int base = 0; base < L; base += lanes) {
+            const int l = base + static_cast<int>(threadIdx.x) / G;
+            int r = 0;
+            if (l < L) {
+                const double kl = s.key[l];
+#pragma unroll 4
+                for (int j = sub; j < L; j += G) {
+                    const double kj = s.key[j];
+                    r += (kj < kl) || (kj == kl && j < l);
+                }
+            }
+            for (int o = 1; o < G; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+            if (l < L && sub == 0) s.sorted[r] = l;
+        }
+        __syncthreads();
+        return;
+    }
+    int P2 = 1;
+    while (P2 < L) P2 <<= 1;
+    double* sk = s.a1;  // [2L] (a1 then a2)
+    int* si = s.i1;     // [2L] (i1 then i2)
+    for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+        sk[i] = i < L ? s.key[i] : __longlong_as_double(0x7ff0000000000000ll);
+        si[i] = i < L ? i : 0x7fffffff;
+    }
+    __syncthreads();
+    for (int k = 2; k <= P2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < P2; i += blockDim.x) {
+                const int p = i ^ j;
+                if (p > i) {
+                    const double a = sk[i], b = sk[p];
+                    const int ia = si[i], ib = si[p];
+                    const bool gt = a > b || (a == b && ia > ib);
+                    if (gt == ((i & k) == 0)) {
+                        sk[i] = b;
+                        sk[p] = a;
+                        si[i] = ib;
+                        si[p] = ia;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int r = threadIdx.x; r < L; r += blockDim.x) s.sorted[r] = si[r];
+    __syncthreads();
+}
+
 // Given the ICS list ord[0..k) (rank order) and the inclusive byte prefix over
 // it in a1 (uint64 bit patterns), write flags, ICS list, compacted chunk map,
-// tile prefix, meta and the encoded GIB. Mirrors split_for_sync's chunking
-// (protocol.cpp:145-164): idx = min(n-1, cum*n/total) in u64, empty chunks dropped.
+// tile prefixes, RS list, meta and the encoded GIB. Mirrors split_for_sync's
+// chunking (protocol.cpp:145-164): idx = min(n-1, cum*n/total) in u64, empty
+// chunks dropped. key / rad are free here and hold the four scanned arrays.
 __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord, int k,
                                uint32_t tag) {
     const int tid = threadIdx.x, B = blockDim.x, L = g.L;
     uint64_t* pre = reinterpret_cast<uint64_t*>(s.a1);
     const uint64_t total = k > 0 ? pre[k - 1] : 0;
     const uint64_t nc = static_cast<uint64_t>(g.n_chunks);
+    int* fl = s.pos;
+    for (int l = tid; l < L; l += B) fl[l] = 0;
     for (int r = tid; r < k; r += B) {
         const uint64_t bytes = s.cnt[ord[r]] * static_cast<uint64_t>(g.bpe);
         const uint64_t cum = pre[r] - bytes;
@@ -164,53 +250,49 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         if (idx > nc - 1) idx = nc - 1;
         s.i1[r] = static_cast<int>(idx);
     }
-    // flags and chunk map are built in shared memory (pos / a2 are free here)
-    int* fl = s.pos;
-    int* cof = reinterpret_cast<int*>(s.a2);
-    for (int l = tid; l < L; l += B) {
-        fl[l] = 0;
-        cof[l] = -1;
+    __syncthreads();
+    for (int r = tid; r < k; r += B) fl[ord[r]] = 1;
+    __syncthreads();
+    // scans: new-chunk flags and ICS tile counts in rank order, RS flags and RS
+    // tile counts in id order
+    int* sc_new = reinterpret_cast<int*>(s.key);
+    int* sc_icst = sc_new + L;
+    int* sc_rsf = reinterpret_cast<int*>(s.rad);
+    int* sc_rst = sc_rsf + L;
+    for (int i = tid; i < L; i += B) {
+        const bool ics = i < k;
+        sc_new[i] = ics && (i == 0 || s.i1[i] != s.i1[i - 1]) ? 1 : 0;
+        sc_icst[i] = ics ? s.tb[ord[i] + 1] - s.tb[ord[i]] : 0;
+        sc_rsf[i] = fl[i] ? 0 : 1;
+        sc_rst[i] = fl[i] ? 0 : s.tb[i + 1] - s.tb[i];
     }
     __syncthreads();
-    for (int r = tid; r < k; r += B) s.i2[r] = (r == 0 || s.i1[r] != s.i1[r - 1]) ? 1 : 0;
-    __syncthreads();
-    block_scan<int>(s.i2, k, 0, [](int a, int b) { return a + b; }, s.wtot);
-    const int n_used = k > 0 ? s.i2[k - 1] : 0;
+    int* arrs[4] = {sc_new, sc_icst, sc_rsf, sc_rst};
+    block_scan_multi<4, int>(arrs, L, 0, [](int a, int b) { return a + b; }, s.wtot);
+    const int n_used = k > 0 ? sc_new[k - 1] : 0;
     for (int r = tid; r < k; r += B) {
         const int l = ord[r];
-        const int c = s.i2[r] - 1;
-        fl[l] = 1;
-        cof[l] = c;
+        const int c = sc_new[r] - 1;
+        g.chunk_of[l] = c;
         g.ics_layers[r] = l;
-        if (r == 0 || s.i2[r] != s.i2[r - 1]) g.chunk_begin[c] = r;
+        if (r == 0 || sc_new[r] != sc_new[r - 1]) g.chunk_begin[c] = r;
+        g.ics_tile_prefix[r + 1] = sc_icst[r];
     }
-    __syncthreads();
-    for (int r = tid; r < k; r += B) s.i1[r] = s.tb[ord[r] + 1] - s.tb[ord[r]];
-    __syncthreads();
-    block_scan<int>(s.i1, k, 0, [](int a, int b) { return a + b; }, s.wtot);
-    for (int r = tid; r <= k; r += B) g.ics_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
+    const int n_rs = L - k;
     for (int l = tid; l < L; l += B) {
         g.flags[l] = static_cast<uint8_t>(fl[l]);
-        g.chunk_of[l] = cof[l];
-    }
-    // RS list: non-deferred layers in ascending id, with their tile prefix
-    int n_rs = L - k;
-    if (g.rs_layers) {
-        for (int l = tid; l < L; l += B) s.i2[l] = fl[l] ? 0 : 1;
-        __syncthreads();
-        block_scan<int>(s.i2, L, 0, [](int a, int b) { return a + b; }, s.wtot);
-        for (int l = tid; l < L; l += B) {
-            const int excl = l == 0 ? 0 : s.i2[l - 1];
-            if (!fl[l]) {
-                g.rs_layers[excl] = l;
-                s.i1[excl] = s.tb[l + 1] - s.tb[l];
+        if (!fl[l]) {
+            g.chunk_of[l] = -1;
+            if (g.rs_layers) {
+                const int p = sc_rsf[l] - 1;
+                g.rs_layers[p] = l;
+                g.rs_tile_prefix[p + 1] = sc_rst[l];
             }
         }
-        __syncthreads();
-        block_scan<int>(s.i1, n_rs, 0, [](int a, int b) { return a + b; }, s.wtot);
-        for (int r = tid; r <= n_rs; r += B) g.rs_tile_prefix[r] = r == 0 ? 0 : s.i1[r - 1];
     }
     if (tid == 0) {
+        g.ics_tile_prefix[0] = 0;
+        if (g.rs_layers) g.rs_tile_prefix[0] = 0;
         g.chunk_begin[n_used] = k;
         g.meta[META_N_ICS] = k;
         g.meta[META_N_USED] = n_used;
@@ -224,7 +306,6 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
             g.gib_bytes[4 + i] = (ul >> (8 * i)) & 0xff;
         }
     }
-    __syncthreads();
     for (int byte = tid; byte < (L + 7) / 8; byte += B) {
         uint8_t v = 0;
         for (int b = 0; b < 8; ++b) {
@@ -332,18 +413,21 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     // 2. certificate: any interval overlap between two layers marks both
     for (int r = tid; r < L; r += blockDim.x) {
         const int l = s.sorted[r];
-        s.a1[r] = s.key[l] + s.rad[l];          // hi, prefix max
-        s.a2[L - 1 - r] = s.key[l] - s.rad[l];  // lo, reversed for the suffix min
+        s.a1[r] = s.key[l] + s.rad[l];             // hi, prefix max
+        s.a2[L - 1 - r] = -(s.key[l] - s.rad[l]);  // -lo, reversed: suffix min of lo
     }
     __syncthreads();
-    block_scan<double>(s.a1, L, -1.0, [](double a, double b) { return a > b ? a : b; }, s.wtot);
-    block_scan<double>(s.a2, L, 1e308, [](double a, double b) { return a < b ? a : b; }, s.wtot);
+    {
+        double* arrs[2] = {s.a1, s.a2};
+        block_scan_multi<2, double>(arrs, L, -1e308, [](double a, double b) { return a > b ? a : b; },
+                                    s.wtot);
+    }
     int my_marks = 0;
     for (int r = tid; r < L; r += blockDim.x) {
         const int l = s.sorted[r];
         const double k = s.key[l], rd = s.rad[l];
         const double premax = r > 0 ? s.a1[r - 1] : -1.0;
-        const double sufmin = r < L - 1 ? s.a2[L - 2 - r] : 1e308;
+        const double sufmin = r < L - 1 ? -s.a2[L - 2 - r] : 1e308;
         const bool m = (k != 0.0) && (k + rd >= sufmin || k - rd <= premax);
         g.marked[l] = m ? 1 : 0;
         s.i1[r] = m ? 1 : 0;

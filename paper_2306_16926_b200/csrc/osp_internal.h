@@ -108,7 +108,7 @@ enum Meta64Idx {
 };
 
 constexpr int kHist = 1024;
-constexpr int kMaxLayers = 4096;  // single-CTA resolve (resolve.cu)
+constexpr int kMaxLayers = 3072;  // single-CTA resolve (resolve.cu: ~60 B shared memory per layer)
 constexpr int kStageThreads = 256;
 constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profiles/)
 constexpr uint32_t kDefaultTmaTile = 1024;  // TMA-staged kernels (tools/tma_sweep.sh)

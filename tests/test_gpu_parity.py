@@ -304,6 +304,20 @@ def test_group_fused_sgd(osp):
     oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 4, 3, seed=19, sgd_lr=0.05, tma=False)
 
 
+@pytest.mark.parametrize("L", [1, 2, 33, 2500, 3072])
+def test_group_many_layers(osp, L):
+    """Layer counts from 1 to the kMaxLayers cap: bitonic rank padding, stage
+    kernels with global layer tables (L > 2048), resolve shared memory at the cap."""
+    rng = np.random.default_rng(L)
+    counts = rng.integers(1, 400, L)
+    oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 3, 2, seed=L)
+
+
+def test_group_too_many_layers(osp):
+    with pytest.raises(osp.InvalidArgument):
+        osp.OspGroup(osp.Partition([1] * 3073), 2)
+
+
 def test_group_budget_edges(osp):
     counts = [4096, 12, 70000, 1, 333, 8192, 5]
     for frac in (0.0, 1.0, 0.33):
