@@ -321,7 +321,10 @@ def b200_single(args):
         "config": {"workload": f"{args.layout}-size OSP sync+LGP step (BASELINE configs[1])",
                    "params": M, "layers": L, "workers": N, "budget_frac": args.budget_frac,
                    "chunks": args.chunks, "deltas": "reference synth generator, seed "
-                   f"{args.seed}, 2 sets alternating (1.6 GB > L2, no flush)",
+                   f"{args.seed}, 2 sets alternating ("
+                   + (f"{2 * N * M * 4 / 1e9:.2f} GB > the 126 MB L2, no flush)"
+                      if 2 * N * M * 4 > 126e6 else
+                      f"{2 * N * M * 4 / 1e6:.3f} MB, L2-resident: launch-bound case)"),
                    "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU",
                    "stage_kernels": grp.stage_kernels},
         "hbm_gbs_step": ach_step,
