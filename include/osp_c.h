@@ -296,8 +296,9 @@ osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_ti
  * resolves the identical next GIB.
  *
  * Default (barrier) mode: per stage an aggregate kernel (the owners' push +
- * pull), a cross-GPU barrier kernel and an apply kernel; stage 1's apply runs
- * in the same launch as stage 2's aggregate. Streaming mode (opt-in with
+ * pull) and an apply kernel, ordered across GPUs by epoch flags the kernels
+ * signal and wait on themselves (no barrier launches); stage 1's apply runs in
+ * the same launch as stage 2's aggregate. Streaming mode (opt-in with
  * OSP_SHARD_STREAM=1 in the environment at create; N in {1,2,4,8}, tile_elems
  * 1024/2048, default 2048): one kernel per stage, tiles dealt round-robin to
  * owners, each owner publishes a tile with a per-tile ready flag and the other
@@ -340,9 +341,9 @@ osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream);
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream);
 /* One osp_shard_step with CUDA events between the kernels (synchronises
  * `stream`). Streaming mode: ms[0..2] = stage 1, stage 2 (all chunks),
- * resolve; ms[3..7] = 0. Barrier mode: ms[0..7] = barrier-in, stage-1
- * aggregate, barrier, stage-1 apply fused with the stage-2 aggregate, 0,
- * barrier, stage-2 apply, resolve. */
+ * resolve. Barrier mode: ms[0..3] = stage-1 aggregate (with the entry wait),
+ * stage-1 apply fused with the stage-2 aggregate, stage-2 apply, resolve (each
+ * including its in-kernel cross-GPU wait). Unused entries are 0. */
 osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream);
 /* 1 if the shard runs the streaming kernels, 0 for barrier mode. */
 int osp_shard_streaming(const osp_shard* s);

@@ -4,7 +4,8 @@
 // of the global vector, and the PS shard of every stage's tile sequence. The
 // push (reduce-scatter) and the pull (all-gather) are fused into k_shard_agg
 // over CUDA-IPC peer mappings of the other ranks' delta rows and agg buffers;
-// cross-GPU ordering uses k_barrier on peer-mapped flag slots. The local state
+// cross-GPU ordering uses epoch flags on peer-mapped slots that the kernels
+// signal and wait on themselves (XSync in stage.cu). The local state
 // (G replica, worker rows, PGP partials, GIB lists) is an osp_group with the
 // rank's workers, so resolve and every read-back reuse the group code.
 
@@ -59,6 +60,7 @@ struct osp_shard {
     StreamArgs sa{};           // peer tables of tflag/pbuf
     int vec[2]{};              // per delta buffer: 16-byte aligned rows
     unsigned iter = 0;         // iterations started (stage-1 launches)
+    unsigned xep[3] = {0, 0, 0};  // barrier mode: epochs of the in-kernel cross-GPU syncs
     unsigned long long* dbg = nullptr;  // [2 stages][3 roles][16] diagnostics counters (OSP_SS_DEBUG=1)
 };
 
@@ -283,6 +285,62 @@ static cudaError_t stream_stage(osp_shard* s, int buf, int stage, int c0, int c1
     return launch_shard_stream(s->grp->v, s->ap_all, s->pt[buf], a, st);
 }
 
+static XSync sync_wait(int kind, unsigned ep) {
+    XSync y;
+    y.wait = kind;
+    y.ep_wait = ep;
+    return y;
+}
+
+static XSync sync_signal_end(int kind, unsigned ep) {
+    XSync y;
+    y.signal_end = kind;
+    y.ep_end = ep;
+    return y;
+}
+
+// agg1: announce "deltas ready, previous iteration done" and wait for every
+// peer's announcement before touching peer memory; signal kind 1 at the end
+static XSync sync_agg1(const osp_shard* s) {
+    XSync y;
+    y.signal_start = 0;
+    y.ep_start = s->xep[0];
+    y.wait = 0;
+    y.ep_wait = s->xep[0];
+    y.signal_end = 1;
+    y.ep_end = s->xep[1];
+    return y;
+}
+
+// Barrier-mode kernels of one step (no resolve); ev (optional) gets 4 records:
+// before agg1, before the fused launch, before apply2, after apply2.
+static cudaError_t barrier_step_kernels(osp_shard* s, int buf, cudaStream_t st,
+                                        cudaEvent_t* ev = nullptr) {
+    osp_group* g = s->grp;
+    float* Xb = s->X + buf * s->buf_stride;
+    ++s->xep[0];
+    ++s->xep[1];
+    ++s->xep[2];
+    cudaError_t e;
+    if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
+    if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st)) !=
+        cudaSuccess)
+        return e;
+    if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+    XSync yf = sync_wait(1, s->xep[1]);
+    yf.signal_end = 2;
+    yf.ep_end = s->xep[2];
+    if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0, s->n_chunks,
+                                g->grid, yf, st)) != cudaSuccess)
+        return e;
+    if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
+    if ((e = launch_shard_apply(g->v, s->ap_loc, s->pt[buf], Xb, s->ldX, 2, 0, s->n_chunks, g->grid,
+                                sync_wait(2, s->xep[2]), st)) != cudaSuccess)
+        return e;
+    if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
+    return cudaSuccess;
+}
+
 osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
@@ -292,11 +350,13 @@ osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
         OSP_CUDA(stream_stage(s, buf, 1, 0, 0, st));
         return OSP_OK;
     }
-    OSP_CUDA(launch_barrier(s->pt[buf], 0, st));  // deltas ready; previous agg reads done
-    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st));
-    OSP_CUDA(launch_barrier(s->pt[buf], 1, st));  // every shard's aggregate landed here
-    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->X + buf * s->buf_stride, s->ldX, 1, 0, 0,
-                                g->grid, st));
+    // kind 0: deltas ready / previous iteration's reads done (agg1 entry);
+    // kind 1: every shard's stage-1 aggregate landed here (apply1 entry)
+    ++s->xep[0];
+    ++s->xep[1];
+    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st));
+    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->pt[buf], s->X + buf * s->buf_stride, s->ldX, 1,
+                                0, 0, g->grid, sync_wait(1, s->xep[1]), st));
     return OSP_OK;
 }
 
@@ -310,10 +370,11 @@ osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream)
         OSP_CUDA(stream_stage(s, buf, 2, c0, c1, st));
         return OSP_OK;
     }
-    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, c0, c1, g->grid, st));
-    OSP_CUDA(launch_barrier(s->pt[buf], 2, st));
-    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->X + buf * s->buf_stride, s->ldX, 2, c0, c1,
-                                g->grid, st));
+    ++s->xep[2];  // kind 2: every shard's aggregate of these chunks landed here
+    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, c0, c1, g->grid,
+                              sync_signal_end(2, s->xep[2]), st));
+    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->pt[buf], s->X + buf * s->buf_stride, s->ldX, 2,
+                                c0, c1, g->grid, sync_wait(2, s->xep[2]), st));
     return OSP_OK;
 }
 
@@ -323,8 +384,9 @@ osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
 }
 
 // Whole iteration with stage 2's push/pull running inside the stage-1 apply
-// launch (k_shard_fused): barrier, agg1, barrier, apply1 || agg2, barrier,
-// apply2, resolve. Same results as stage1 + stage2 + resolve.
+// launch (k_shard_fused): agg1, apply1 || agg2, apply2, resolve — four
+// launches, the cross-GPU ordering inside them (XSync). Same results as
+// stage1 + stage2 + resolve.
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
@@ -336,13 +398,7 @@ osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
         return osp_shard_resolve(s, buf, stream);
     }
     float* Xb = s->X + buf * s->buf_stride;
-    OSP_CUDA(launch_barrier(s->pt[buf], 0, st));
-    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st));
-    OSP_CUDA(launch_barrier(s->pt[buf], 1, st));
-    OSP_CUDA(launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0, s->n_chunks,
-                                g->grid, st));
-    OSP_CUDA(launch_barrier(s->pt[buf], 2, st));
-    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, Xb, s->ldX, 2, 0, s->n_chunks, g->grid, st));
+    OSP_CUDA(barrier_step_kernels(s, buf, st));
     return osp_shard_resolve(s, buf, stream);
 }
 
@@ -372,25 +428,12 @@ osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream) {
                 if ((e = cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1])) != cudaSuccess) return e;
             return cudaSuccess;
         }
-        if ((e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-        if ((e = launch_barrier(s->pt[buf], 0, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-        if ((e = launch_barrier(s->pt[buf], 1, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0,
-                                    s->n_chunks, g->grid, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[5], st)) != cudaSuccess) return e;
-        if ((e = launch_barrier(s->pt[buf], 2, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[6], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_apply(g->v, s->ap_loc, Xb, s->ldX, 2, 0, s->n_chunks, g->grid, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[7], st)) != cudaSuccess) return e;
+        for (int i = 0; i < 8; ++i) ms[i] = 0.f;
+        if ((e = barrier_step_kernels(s, buf, st, ev)) != cudaSuccess) return e;
         if ((e = launch_resolve(g->v, g->ap, Xb, s->ldX, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[8], st)) != cudaSuccess) return e;
-        if ((e = cudaEventSynchronize(ev[8])) != cudaSuccess) return e;
-        for (int i = 0; i < 8; ++i)
+        if ((e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
+        if ((e = cudaEventSynchronize(ev[4])) != cudaSuccess) return e;
+        for (int i = 0; i < 4; ++i)
             if ((e = cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1])) != cudaSuccess) return e;
         return cudaSuccess;
     };

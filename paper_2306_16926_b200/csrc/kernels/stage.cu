@@ -520,11 +520,69 @@ __device__ void peer_agg_range(const AggParams& ap, const PeerTable& pt, uint64_
     }
 }
 
+// ---- in-kernel cross-GPU ordering (replaces separate barrier launches) --------
+// Slot [kind][q] of rank r's flag array holds the last epoch rank q signalled
+// for that kind. A kernel may wait at its start for every peer's slot to reach
+// its epoch, signal at its start (every CTA; idempotent), and/or signal when
+// its last CTA finishes (after every CTA's system-scope fence). Waits are
+// bounded (20 s) and record pt.error instead of hanging.
+__device__ __forceinline__ void xsync_signal(const PeerTable& pt, int kind, unsigned ep) {
+    for (int q = 0; q < pt.world; ++q) {
+        volatile unsigned* slot = pt.flags[q] + kind * kMaxRanks + pt.rank;
+        *slot = ep;
+    }
+}
+
+__device__ void xsync_start(const PeerTable& pt, const XSync& sy) {
+    if (threadIdx.x == 0) {
+        if (sy.signal_start >= 0) {
+            __threadfence_system();
+            xsync_signal(pt, sy.signal_start, sy.ep_start);
+        }
+        if (sy.wait >= 0) {
+            const unsigned ep = sy.ep_wait;
+            for (int q = 0; q < pt.world; ++q) {
+                volatile unsigned* mine = pt.flags[pt.rank] + sy.wait * kMaxRanks + q;
+                if (static_cast<int>(*mine - ep) >= 0) continue;
+                uint64_t t0;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                while (static_cast<int>(*mine - ep) < 0) {
+                    __nanosleep(128);
+                    uint64_t t;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                    if (t - t0 > 20000000000ull) {
+                        atomicExch(pt.error, 1u);
+                        break;
+                    }
+                }
+            }
+            __threadfence_system();
+        }
+    }
+    __syncthreads();
+}
+
+// Call with every thread of the block after its last memory operation.
+__device__ void xsync_end(const GroupView& g, const PeerTable& pt, const XSync& sy) {
+    if (sy.signal_end < 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        int* ticket = g.sched + SCHED_XSYNC_TICKET;
+        if (atomicAdd(ticket, 1) == static_cast<int>(gridDim.x) - 1) {
+            atomicExch(ticket, 0);
+            __threadfence_system();
+            xsync_signal(pt, sy.signal_end, sy.ep_end);
+        }
+    }
+}
+
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggParams ap,
                                                              PeerTable pt, int stage, int c0,
-                                                             int c1, int vec) {
+                                                             int c1, int vec, XSync sy) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
+    xsync_start(pt, sy);
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_AGG_NEXT;
     const Tab tab = stage_tab(g, smem_tab, stage, c0, c1);
@@ -542,8 +600,9 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggPar
         peer_agg_range<NS>(ap, pt, s, e, vec != 0, lane);
         u = un;
     }
-    __threadfence_system();  // peer stores visible before the barrier kernel signals
+    __threadfence_system();  // peer stores visible before the signal
     retire(next, g.sched + SCHED_AGG_DONE, lane);
+    xsync_end(g, pt, sy);
 }
 
 // Apply one element range from agg_full: G' = G + a; local worker rows = G'; PGP.
@@ -584,9 +643,11 @@ __device__ void warp_tile_apply(const GroupView& g, int n_loc, uint64_t s, uint6
 // stage 1 apply: RS tiles from agg_full, ICS tiles = local estimate of the
 // local workers (same body as k_stage1's ICS path).
 __global__ void __launch_bounds__(kStageThreads) k_shard_apply1(GroupView g, AggParams ap_loc,
+                                                                PeerTable pt,
                                                                 const float* __restrict__ X,
-                                                                uint64_t ldX, int vec) {
+                                                                uint64_t ldX, int vec, XSync sy) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
+    xsync_start(pt, sy);
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_S1_NEXT;
     const Tab tab = load_tab(g, smem_tab, nullptr, nullptr, 0, 0);
@@ -608,9 +669,11 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_apply1(GroupView g, Agg
     retire(next, g.sched + SCHED_S1_DONE, lane);
 }
 
-__global__ void __launch_bounds__(kStageThreads) k_shard_apply2(GroupView g, int n_loc, int c0,
-                                                                int c1, int vec) {
+__global__ void __launch_bounds__(kStageThreads) k_shard_apply2(GroupView g, PeerTable pt,
+                                                                int n_loc, int c0, int c1,
+                                                                int vec, XSync sy) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
+    xsync_start(pt, sy);
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_S2_NEXT;
     const Tab tab = stage_tab(g, smem_tab, 2, c0, c1);
@@ -644,8 +707,9 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggP
                                                                const float* __restrict__ X,
                                                                uint64_t ldX, int c0, int c1,
                                                                int vec_apply, int vec_agg,
-                                                               int apply_every) {
+                                                               int apply_every, XSync sy) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
+    xsync_start(pt, sy);
     const int lane = threadIdx.x & 31;
     const Tab tab = stage_tab(g, smem_tab, 2, c0, c1);
     const int U0 = tab.n > 0 ? tab.sp[0] : 0;
@@ -709,43 +773,13 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggP
             atomicExch(g.sched + SCHED_S1_DONE, 0);
         }
     }
+    xsync_end(g, pt, sy);
 }
 
 __device__ __forceinline__ uint64_t global_ns() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
-}
-
-// Cross-GPU barrier on peer-mapped flag slots. Every rank runs the same
-// barrier sequence, so the local epoch counters advance in lockstep. A
-// bounded spin (20 s) records an error instead of hanging the device.
-__global__ void k_barrier(PeerTable pt, int kind) {
-    __shared__ unsigned ep;
-    if (threadIdx.x == 0) {
-        ep = pt.epoch[kind] + 1;
-        pt.epoch[kind] = ep;
-    }
-    __syncthreads();
-    const int q = threadIdx.x;
-    __threadfence_system();
-    if (q < pt.world) {
-        volatile unsigned* slot = pt.flags[q] + kind * kMaxRanks + pt.rank;
-        *slot = ep;
-    }
-    __threadfence_system();
-    if (q < pt.world) {
-        volatile unsigned* mine = pt.flags[pt.rank] + kind * kMaxRanks + q;
-        const uint64_t t0 = global_ns();
-        while (static_cast<int>(*mine - ep) < 0) {
-            __nanosleep(256);
-            if (global_ns() - t0 > 20000000000ull) {
-                atomicExch(pt.error, 1u);
-                break;
-            }
-        }
-    }
-    __threadfence_system();
 }
 
 bool vec_ok(const GroupView& g, const float* X, uint64_t ldX) {
@@ -821,7 +855,7 @@ cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* 
 }
 
 cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
-                             int stage, int c0, int c1, int grid, cudaStream_t s) {
+                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s) {
     bool vec = (g.ldP % 4 == 0);
     for (int w = 0; w < ap.n; ++w) vec = vec && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
     for (int r = 0; r < pt.world; ++r) vec = vec && (reinterpret_cast<uintptr_t>(pt.agg[r]) % 16 == 0);
@@ -831,30 +865,31 @@ cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const Peer
         constexpr int NS = decltype(nc)::value;
         cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_agg<NS>));
         if (e != cudaSuccess) return e;
-        k_shard_agg<NS><<<grid, kStageThreads, sm, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0);
+        k_shard_agg<NS><<<grid, kStageThreads, sm, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0, sy);
         return cudaGetLastError();
     });
 }
 
-cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const float* Xloc,
-                               uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s) {
+cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const PeerTable& pt,
+                               const float* Xloc, uint64_t ldX, int stage, int c0, int c1, int grid,
+                               const XSync& sy, cudaStream_t s) {
     const bool vec = vec_ok(g, Xloc, ldX) && (reinterpret_cast<uintptr_t>(g.agg_full) % 16 == 0);
     if (grid < 1) return cudaSuccess;
     const size_t sm = tab_smem_bytes(g.L);
     cudaError_t e;
     if (stage == 1) {
         if ((e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_apply1))) != cudaSuccess) return e;
-        k_shard_apply1<<<grid, kStageThreads, sm, s>>>(g, ap_loc, Xloc, ldX, vec ? 1 : 0);
+        k_shard_apply1<<<grid, kStageThreads, sm, s>>>(g, ap_loc, pt, Xloc, ldX, vec ? 1 : 0, sy);
     } else {
         if ((e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_apply2))) != cudaSuccess) return e;
-        k_shard_apply2<<<grid, kStageThreads, sm, s>>>(g, ap_loc.n, c0, c1, vec ? 1 : 0);
+        k_shard_apply2<<<grid, kStageThreads, sm, s>>>(g, pt, ap_loc.n, c0, c1, vec ? 1 : 0, sy);
     }
     return cudaGetLastError();
 }
 
 cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
                                const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
-                               int grid, cudaStream_t s) {
+                               int grid, const XSync& sy, cudaStream_t s) {
     const bool vec_apply =
         vec_ok(g, Xloc, ldX) && (reinterpret_cast<uintptr_t>(g.agg_full) % 16 == 0);
     bool vec_agg = true;
@@ -876,14 +911,10 @@ cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, cons
             return e != 0 ? e : -4;
         }();
         k_shard_fused<NS><<<grid, kStageThreads, sm, s>>>(g, ap_all, ap_loc, pt, Xloc, ldX, c0, c1,
-                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0, every);
+                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0, every, sy);
         return cudaGetLastError();
     });
 }
 
-cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s) {
-    k_barrier<<<1, 32, 0, s>>>(pt, kind);
-    return cudaGetLastError();
-}
 
 }  // namespace osp

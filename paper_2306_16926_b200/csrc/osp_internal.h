@@ -95,7 +95,8 @@ enum SchedIdx {
     SCHED_SS_A = 8,     // streaming shard kernel: own exchange tiles
     SCHED_SS_B = 9,     //   peers' exchange tiles
     SCHED_SS_C = 10,    //   local-estimate tiles (stage 1)
-    SCHED_SS_DONE = 11
+    SCHED_SS_DONE = 11,
+    SCHED_XSYNC_TICKET = 12  // last-CTA ticket of the in-kernel cross-GPU signal
 };
 enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2, META_N_RS = 3 };
 enum Meta64Idx {
@@ -130,11 +131,20 @@ struct PeerTable {
     unsigned* error;                             // local: set on barrier timeout
 };
 
+// In-kernel cross-GPU ordering of the barrier-mode shard kernels (stage.cu):
+// kinds index PeerTable flag slots; -1 = none. Epochs are host counters that
+// every rank advances identically.
+struct XSync {
+    int wait = -1;          // at start: wait for every peer's slot[wait] >= ep_wait
+    int signal_start = -1;  // at start: signal slot[signal_start] = ep_start
+    int signal_end = -1;    // when the last CTA finishes: signal slot[signal_end] = ep_end
+    unsigned ep_wait = 0, ep_start = 0, ep_end = 0;
+};
 cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
-                             int stage, int c0, int c1, int grid, cudaStream_t s);
-cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const float* Xloc,
-                               uint64_t ldX, int stage, int c0, int c1, int grid, cudaStream_t s);
-cudaError_t launch_barrier(const PeerTable& pt, int kind, cudaStream_t s);
+                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s);
+cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const PeerTable& pt,
+                               const float* Xloc, uint64_t ldX, int stage, int c0, int c1, int grid,
+                               const XSync& sy, cudaStream_t s);
 // Streaming shard kernel (kernels/shard_stream.cu): push, aggregate, pull and
 // apply of one stage in one launch, per-tile flags instead of grid barriers.
 struct StreamArgs {
@@ -153,7 +163,7 @@ cudaError_t launch_shard_stream(const GroupView& g, const AggParams& ap, const P
 // stage-1 apply + stage-2 aggregate of chunks [c0, c1) in one launch
 cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
                                const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
-                               int grid, cudaStream_t s);
+                               int grid, const XSync& sy, cudaStream_t s);
 
 // ---- payload wire codec (kernels/codec.cu) -----------------------------------
 struct CodecSeg {

@@ -109,8 +109,7 @@ class ShardGroup:
         if self.streaming:
             names = ["stage1", "stage2", "resolve"]
         else:
-            names = ["barrier_in", "agg1", "barrier1", "apply1+agg2", None, "barrier2", "apply2",
-                     "resolve"]
+            names = ["agg1", "apply1+agg2", "apply2", "resolve"]
         return {n: float(v) for n, v in zip(names, out) if n}
 
     @property

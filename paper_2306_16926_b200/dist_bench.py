@@ -201,10 +201,10 @@ def run(args, metric: str, unit: str):
                     "d2h_bytes_per_step": (8 + (L + 7) // 8) * world,
                     "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read"},
             # streaming: stage1, stage2, resolve per step (per chunk: one stage-2 launch
-            # each); barrier mode: barrier, agg1, barrier, apply1+agg2, barrier, apply2,
-            # resolve
+            # each); barrier mode: agg1, apply1+agg2, apply2, resolve (per chunk: agg1,
+            # apply1, agg2 + apply2 per chunk, resolve)
             "gpu_launches": K * (((2 + args.chunks) if args.per_chunk else 3) if sh.streaming
-                                 else ((4 + 3 * args.chunks + 1) if args.per_chunk else 7)),
+                                 else ((3 + 2 * args.chunks) if args.per_chunk else 4)),
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
