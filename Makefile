@@ -25,7 +25,7 @@ CXX ?= g++
 FACADE := $(PKG)/libpslab_b200.so
 FACADE_SRCS := $(wildcard $(CSRC)/pslab/*.cpp)
 FACADE_OBJS := $(patsubst $(CSRC)/%.cpp,build/%.o,$(FACADE_SRCS))
-FACADE_HDRS := $(wildcard include/pslab/*.hpp) $(CSRC)/pslab/device.hpp include/osp_c.h
+FACADE_HDRS := $(wildcard include/pslab/*.hpp) $(CSRC)/pslab/device.hpp include/osp_c.h include/osp_engine.h
 CXXFLAGS_FACADE := -std=c++20 -O2 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude -I$(CSRC)/pslab
 
 .PHONY: all lib facade oracle ref dropin clean

@@ -8,10 +8,11 @@ import pytest
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 HEADER = os.path.join(REPO, "include", "osp_c.h")
+ENGINE_HEADER = os.path.join(REPO, "include", "osp_engine.h")
 
 
-def declared_functions():
-    src = open(HEADER).read()
+def declared_functions(header=HEADER):
+    src = open(header).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     names = set(re.findall(r"\b(osp_[a-z0-9_]+)\s*\(", src))
     return sorted(names)
@@ -70,3 +71,32 @@ def test_python_front_errors_without_gpu():
                             eq5_literal=True) == 19_531_250
     with pytest.raises(osp.ConfigError):
         osp.compute_umax(-1.0, 0.1, 8, 100)
+
+
+def test_engine_library_exports_every_declared_symbol():
+    """include/osp_engine.h (message-level worker/server C-ABI) is exported by
+    the façade library and fully bound by paper_2306_16926_b200/engine.py."""
+    from paper_2306_16926_b200 import engine
+    names = declared_functions(ENGINE_HEADER)
+    assert "osp_worker_compute_done" in names and "osp_server_on_push_important" in names
+    lib = engine.lib()
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(names) == set(engine.EXPORTED)
+
+
+def test_engine_messages_without_gpu():
+    """Partition and message codec are host logic: payload wire round trip
+    (message.cpp:53-99 layout) and its error class."""
+    import struct
+    from paper_2306_16926_b200 import engine, osp
+    part = engine.Partition([3, 2])
+    assert part.total == 5
+    raw = (struct.pack("<BIH", 0, 7, 2) + struct.pack("<II", 0, 3) + struct.pack("<3f", 1, 2, 3)
+           + struct.pack("<II", 1, 2) + struct.pack("<2f", -1, 0.5))
+    m = engine.Message.decode(raw, from_worker=2)
+    assert (m.kind, m.iteration, m.from_worker, m.layer_count) == ("PushImportant", 7, 2, 2)
+    assert m.size_bytes(part) == 20
+    assert m.encode() == raw
+    with pytest.raises(osp.FormatError):
+        engine.Message.decode(raw[:-3])
