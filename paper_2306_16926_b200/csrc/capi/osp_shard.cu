@@ -47,7 +47,6 @@ struct osp_shard {
     uint64_t ldX = 0, buf_stride = 0;
     float* agg = nullptr;      // [ldX] agg_full, IPC-exported
     unsigned* flags = nullptr; // [kBarKinds][kMaxRanks], IPC-exported
-    unsigned* epoch = nullptr; // [kBarKinds] local
     unsigned* error = nullptr; // [1] local
     PeerTable pt[2]{};         // per delta buffer
     std::vector<void*> opened; // peer mappings to close
@@ -112,12 +111,10 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     cudaError_t e = cudaMalloc(&s->X, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&s->agg, s->ldX * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&s->flags, kBarKinds * kMaxRanks * sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMalloc(&s->epoch, kBarKinds * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&s->error, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->X, 0, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(s->agg, 0, s->ldX * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(s->flags, 0, kBarKinds * kMaxRanks * sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMemset(s->epoch, 0, kBarKinds * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
     if (s->stream) {
         const char* de = std::getenv("OSP_SS_DEBUG");
@@ -150,7 +147,6 @@ void osp_shard_destroy(osp_shard* s) {
     if (s->X) cudaFree(s->X);
     if (s->agg) cudaFree(s->agg);
     if (s->flags) cudaFree(s->flags);
-    if (s->epoch) cudaFree(s->epoch);
     if (s->error) cudaFree(s->error);
     if (s->tflag) cudaFree(s->tflag);
     if (s->dbg) cudaFree(s->dbg);
@@ -245,7 +241,6 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
             pt.agg[q] = aggs[q];
             pt.flags[q] = flags[q];
         }
-        pt.epoch = s->epoch;
         pt.error = s->error;
         bool vec = (s->ldX % 4 == 0) && (s->grp->v.ldP % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(s->grp->v.G) % 16 == 0) &&

@@ -117,7 +117,7 @@ constexpr int kResolveThreads = 1024;
 
 // ---- sharded (multi-GPU) path: peer tables ---------------------------------
 constexpr int kMaxRanks = 8;      // one NVLink/NVSwitch node
-constexpr int kBarKinds = 4;      // independent barrier sequences (stage1-in, stage1-out, stage2, spare)
+constexpr int kBarKinds = 4;      // flag-slot kinds: deltas ready, stage-1 aggregate done, stage-2 aggregate done, streaming deltas ready
 
 struct PeerTable {
     int world;
@@ -127,7 +127,6 @@ struct PeerTable {
     const float* xrow[OSP_MAX_WORKERS];          // delta row of every worker (peer or local)
     float* agg[kMaxRanks];                       // every rank's agg_full buffer
     unsigned* flags[kMaxRanks];                  // every rank's barrier slots [kBarKinds][kMaxRanks]
-    unsigned* epoch;                             // local barrier counters [kBarKinds]
     unsigned* error;                             // local: set on barrier timeout
 };
 
