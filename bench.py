@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--stage-kernels", default="auto", choices=["auto", "tma", "register"],
                     help="stage-kernel family (OSP_GROUP_TMA / OSP_GROUP_REGISTER)")
+    ap.add_argument("--no-carry", action="store_true",
+                    help="OSP_GROUP_NO_CARRY: stage 2 re-reads the deltas (A/B of the ICS carry)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-chunk", action="store_true", help="one stage-2 launch per ICS chunk")
@@ -221,7 +223,9 @@ def b200_single(args):
     budget = int(args.budget_frac * model_bytes)
     part = osp.Partition(counts)
     grp = osp.OspGroup(part, N, [1.0 / N] * N, n_chunks=args.chunks, tile_elems=args.tile,
-                       tma={"auto": None, "tma": True, "register": False}[args.stage_kernels])
+                       tma={"auto": None, "tma": True, "register": False}[args.stage_kernels],
+                       carry=not args.no_carry)
+    carry = not (osp.lib().osp_group_flags(grp._h) & 4)
     X = [osp.synth_deltas(args.seed, N, i, M) for i in range(2)]
     grp.set_budget(budget)
     stream = torch.cuda.current_stream()
@@ -276,13 +280,19 @@ def b200_single(args):
     # u of each timed step = deferred bytes of the GIB it split with (tags tag0..)
     deferred = grp.deferred_history(tag0, K).astype(np.float64)
     u = deferred / model_bytes
-    # algorithmic bytes: stage 1 = 4M[(2N+2) - u]; step adds 4M u (2N+2)
-    b_s1 = [4.0 * M * ((2 * N + 2) - uk) for uk in u]
-    b_step = [4.0 * M * ((2 * N + 2) + uk * (2 * N + 1)) for uk in u]
+    # algorithmic bytes. SURVEY §8(d): stage 1 = 4M[(2N+2) - u] (N delta rows + G read,
+    # N worker rows + G on RS written), stage 2 = 4M u (2N+1) (N rows + G re-read,
+    # G + N rows written). With the ICS carry stage 1 also writes C on ICS
+    # (4M(2N+2)) and stage 2 reads C once and writes G + N rows (4M u (N+2)).
+    b_s1 = [4.0 * M * ((2 * N + 2) - (0.0 if carry else uk)) for uk in u]
+    b_step = [4.0 * M * ((2 * N + 2) + uk * ((N + 2) if carry else (2 * N + 1))) for uk in u]
+    b_survey = [4.0 * M * ((2 * N + 2) + uk * (2 * N + 1)) for uk in u]
     s1_avg = sum(s1) / K
     ach_s1 = (sum(b_s1) / K) / (s1_avg * 1e-3) / 1e9
     ach_step = (sum(b_step) / K) / (ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
+    # the step time the SURVEY byte model allows at the measured peak
+    survey_ms = (sum(b_survey) / K) / (peak * 1e9) * 1e3
     stats = grp.stats()
     launches_per_step = 1 + (args.chunks if args.per_chunk else 1) + 1  # stage1, stage2, resolve
 
@@ -314,6 +324,7 @@ def b200_single(args):
     e2e_step = statistics.median(e2e_ms)
     gib_bytes = 8 + (L + 7) // 8
 
+    s1_kernel = "k_stage_tma<1>" if grp.stage_kernels == "tma-staged" else "k_stage1"
     line = {
         "metric": METRIC, "value": M / (ms_step * 1e-3), "unit": UNIT, "n_gpus": 1,
         "steps": K, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -326,19 +337,24 @@ def b200_single(args):
                       if 2 * N * M * 4 > 126e6 else
                       f"{2 * N * M * 4 / 1e6:.3f} MB, L2-resident: launch-bound case)"),
                    "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU",
-                   "stage_kernels": grp.stage_kernels},
+                   "stage_kernels": grp.stage_kernels, "ics_carry": carry},
         "hbm_gbs_step": ach_step,
         "roofline": {"bound": "hbm",
-                     "kernel": ("k_stage_tma<1>" if grp.stage_kernels == "tma-staged" else "k_stage1")
-                               + " (barrier: RS agg/apply + LGP)",
+                     "kernel": s1_kernel + (" (barrier: RS agg/apply + LGP + ICS carry)" if carry
+                                            else " (barrier: RS agg/apply + LGP)"),
                      "achieved": ach_s1, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": ach_s1 / peak,
                      "traffic": ncu_traffic(f"{args.layout}/N{N}/b{args.budget_frac}",
-                                            "k_stage_tma<1>" if grp.stage_kernels == "tma-staged"
-                                            else "k_stage1"),
+                                            s1_kernel + ("" if carry or s1_kernel == "k_stage1"
+                                                         else " no-carry")),
                      "traffic_source": "profiles/ncu_traffic.json (ncu --set full, one launch)",
                      "alg_bytes_per_launch": sum(b_s1) / K, "avg_launch_ms": s1_avg,
-                     "step_frac": ach_step / peak},
+                     "step_frac": ach_step / peak,
+                     "step_alg_bytes": sum(b_step) / K,
+                     "step_bytes_model": ("4M[(2N+2) + u(N+2)] (ICS carry)" if carry else
+                                          "4M[(2N+2) + u(2N+1)] (SURVEY §8(d))"),
+                     "survey_roofline_ms": survey_ms,
+                     "vs_survey_roofline": survey_ms / ms_step},
         "breakdown_ms": {"stage1": s1_avg, "stage2_chunks": sum(s2) / KB,
                          "resolve_and_gaps": sum(s3) / KB,
                          "note": "stage1 from the timed region; stage2/resolve from a separate "

@@ -226,6 +226,14 @@ typedef struct osp_group_config {
  * register-staged one. Both produce identical results. */
 #define OSP_GROUP_TMA 1u
 #define OSP_GROUP_REGISTER 2u
+/* ICS carry (TMA family, on by default): stage 1 also aggregates the ICS
+ * elements from the delta rows it already holds in shared memory and keeps
+ * G_old + agg in an extra [M] device buffer, so stage 2 only writes G and the
+ * worker rows from it (reads 1 row instead of N + 1). The ICS payload is the
+ * one split at stage-1 time, as in the reference (split_for_sync copies it,
+ * protocol.cpp:122-166): stage 2 ignores its `deltas` argument then.
+ * OSP_GROUP_NO_CARRY keeps the re-reading stage 2 (identical results). */
+#define OSP_GROUP_NO_CARRY 4u
 
 /* init_params: DEVICE pointer to M floats (P0), or NULL for zeros. Every worker
  * and the server start from it (runner.cpp:214-231). */
@@ -280,7 +288,8 @@ osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fallback_
 osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, uint64_t* out,
                                       void* stream);
 /* Tile geometry (for roofline accounting and tests). */
-/* Effective flags of a group (OSP_GROUP_TMA or OSP_GROUP_REGISTER). */
+/* Effective flags of a group (OSP_GROUP_TMA or OSP_GROUP_REGISTER, plus
+ * OSP_GROUP_NO_CARRY when stage 2 re-reads the deltas). */
 uint32_t osp_group_flags(const osp_group* g);
 osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,
                               int* grid_blocks, int* block_threads);

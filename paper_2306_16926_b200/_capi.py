@@ -27,6 +27,7 @@ class osp_group_config(ctypes.Structure):
 
 GROUP_TMA = 1
 GROUP_REGISTER = 2
+GROUP_NO_CARRY = 4
 
 
 class osp_shard_config(ctypes.Structure):

@@ -716,6 +716,9 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     // bootstrap GIB: nothing deferred, tag 0 (first_iteration_bootstrap, protocol.cpp:58-63)
     if ((st = cu(launch_install_gib(v, g->d_order_tmp, 0, 0, s), "install bootstrap gib")) != OSP_OK)
         return cleanup(st);
+    if (use_tma && !(cfg->flags & OSP_GROUP_NO_CARRY)) {
+        if ((st = dalloc(g, &v.C, M)) != OSP_OK) return cleanup(st);
+    }
     g->blocks_per_sm = stage_blocks_per_sm(N, static_cast<int>(L));
     g->tma = use_tma;
     g->grid = sm_count() * g->blocks_per_sm;
@@ -874,7 +877,7 @@ osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, u
 
 uint32_t osp_group_flags(const osp_group* g) {
     if (!g) return 0;
-    return g->tma ? OSP_GROUP_TMA : OSP_GROUP_REGISTER;
+    return (g->tma ? OSP_GROUP_TMA : OSP_GROUP_REGISTER) | (g->v.C ? 0u : OSP_GROUP_NO_CARRY);
 }
 
 osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,

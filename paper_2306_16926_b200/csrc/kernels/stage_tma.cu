@@ -124,17 +124,77 @@ __device__ __forceinline__ void consume_local_quad(const GroupView& g, const Agg
     }
 }
 
+// Stage-1 ICS quad with the carry: the local estimates (as consume_local_quad)
+// and, from the same shared-memory rows, the aggregate the stage-2 kernel will
+// apply: C = G_old + agg (G itself keeps G_old until stage 2), PGP term now.
+template <int NS>
+__device__ __forceinline__ void consume_split_quad(const GroupView& g, const AggParams& ap,
+                                                   const float4* xs, float4 go, uint64_t f,
+                                                   double& acc) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NS; ++w) {
+        float4 v = xs[w];
+        if (ap.sgd) {
+            v.x = sgd_conv(ap.neg_lr, v.x);
+            v.y = sgd_conv(ap.neg_lr, v.y);
+            v.z = sgd_conv(ap.neg_lr, v.z);
+            v.w = sgd_conv(ap.neg_lr, v.w);
+        }
+        st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f,
+                   make_float4(__fadd_rn(go.x, v.x), __fadd_rn(go.y, v.y), __fadd_rn(go.z, v.z),
+                               __fadd_rn(go.w, v.w)));
+        s0 = agg_acc(s0, ap.w[w], v.x);
+        s1 = agg_acc(s1, ap.w[w], v.y);
+        s2 = agg_acc(s2, ap.w[w], v.z);
+        s3 = agg_acc(s3, ap.w[w], v.w);
+    }
+    float4 a;
+    a.x = agg_finish(ap, s0);
+    a.y = agg_finish(ap, s1);
+    a.z = agg_finish(ap, s2);
+    a.w = agg_finish(ap, s3);
+    const float4 gn = make_float4(__fadd_rn(go.x, a.x), __fadd_rn(go.y, a.y), __fadd_rn(go.z, a.z),
+                                  __fadd_rn(go.w, a.w));
+    st_stream4(g.C + f, gn);
+    acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
+    acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
+    acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
+    acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
+}
+
+// Stage-2 quad with the carry: G' = C, every worker row = C (lgp_correct:
+// base + agg == G_old + agg, protocol.cpp:99-116 with base == G_old).
+template <int NS>
+__device__ __forceinline__ void consume_bcast_quad(const GroupView& g, float4 gn, uint64_t f) {
+    *reinterpret_cast<float4*>(g.G + f) = gn;
+#pragma unroll
+    for (int w = 0; w < NS; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+}
+
 // Unstaged tile (unaligned layer): per-element from global memory.
 template <int NS, int CW>
 __device__ void consume_direct(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                                const StageMeta& m, int ctid, double& acc) {
     for (uint64_t f = m.s + ctid; f < m.e; f += CW * 32) {
-        if (m.kind == 1) {
+        if (m.kind == 2) {
+            const float gn = g.C[f];
+            g.G[f] = gn;
+            for (int w = 0; w < NS; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+        } else if (m.kind == 1) {
             const float go = g.G[f];
+            double s = 0.0;
             for (int w = 0; w < NS; ++w) {
                 float x = X[static_cast<uint64_t>(w) * ldX + f];
                 if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
                 g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
+                s = agg_acc(s, ap.w[w], x);
+            }
+            if (g.C) {
+                const float a = agg_finish(ap, s);
+                const float gn = __fadd_rn(go, a);
+                g.C[f] = gn;
+                acc = __dadd_rn(acc, pgp_term(a, gn));
             }
         } else {
             double s = 0.0;
@@ -152,7 +212,9 @@ __device__ void consume_direct(const GroupView& g, const AggParams& ap, const fl
     }
 }
 
-// STAGE 1: all tiles (RS aggregate / ICS local); STAGE 2: ICS chunks [c0, c1).
+// STAGE 1: all tiles (RS aggregate / ICS local estimate, + the ICS carry when
+// g.C is set); STAGE 2: ICS chunks [c0, c1) from the deltas; STAGE 3: ICS
+// chunks [c0, c1) from the carry (one staged row per tile instead of N + 1).
 template <int NS, int STAGE, int CW, int kStages>
 __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggParams ap,
                                                            const float* __restrict__ X,
@@ -163,7 +225,8 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int T = g.T;
-    const size_t stage_floats = static_cast<size_t>(NS + 1) * T;
+    constexpr int kRows = STAGE == 3 ? 1 : NS + 1;
+    const size_t stage_floats = static_cast<size_t>(kRows) * T;
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * stage_floats);
     uint64_t* empty = full + kStages;
@@ -180,7 +243,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
     int* t_sl = reinterpret_cast<int*>(t_flag + ((L + 15) & ~15));
     int* t_sp = t_sl + L;
     int jb = 0, je = 0;
-    if (STAGE == 2) {
+    if (STAGE >= 2) {
         const int used = g.meta[META_N_USED];
         const int cc1 = c1 > used ? used : c1;
         if (c0 < cc1) {
@@ -195,7 +258,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
         t_flag[i] = g.flags[i];
     }
     if (tid == 0) t_tb[L] = g.tile_base[L];
-    if (STAGE == 2) {
+    if (STAGE >= 2) {
         for (int i = tid; i < je - jb; i += blockDim.x) t_sl[i] = g.ics_layers[jb + i];
         for (int i = tid; i <= je - jb; i += blockDim.x) t_sp[i] = g.ics_tile_prefix[jb + i];
     }
@@ -214,8 +277,11 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
         int* next = g.sched + (STAGE == 1 ? SCHED_S1_NEXT : SCHED_S2_NEXT);
         const int lim = STAGE == 1 ? g.NT : (tab.n > 0 ? tab.sp[tab.n] : 0);
         const int base = STAGE == 1 ? 0 : (tab.n > 0 ? tab.sp[0] : 0);
+        // tile partial published for RS tiles, and for ICS tiles when stage 1
+        // carries their aggregate; never by the stage-3 broadcast
+        const bool carry = STAGE == 1 && g.C != nullptr;
         int pending_t[kStages];
-        int pending_kind[kStages];
+        bool pending_pub[kStages];
         for (int s = 0; s < kStages; ++s) pending_t[s] = -1;
         if (lane == 0) {
             for (int i = 0;; ++i) {
@@ -223,7 +289,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                 const int use = i / kStages;
                 if (use > 0) {
                     mbar_wait(&empty[s], (use - 1) & 1);
-                    if (pending_t[s] >= 0 && pending_kind[s] == 0) {
+                    if (pending_t[s] >= 0 && pending_pub[s]) {
                         double tot = 0.0;
                         for (int w = 0; w < CW; ++w)
                             tot = __dadd_rn(tot, red[s * CW + w]);
@@ -244,7 +310,7 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                         const int use2 = i2 / kStages;
                         if (use2 > 0 && pending_t[s2] >= 0) {
                             mbar_wait(&empty[s2], (use2 - 1) & 1);
-                            if (pending_kind[s2] == 0) {
+                            if (pending_pub[s2]) {
                                 double tot = 0.0;
                                 for (int w = 0; w < CW; ++w)
                                     tot = __dadd_rn(tot, red[s2 * CW + w]);
@@ -263,26 +329,31 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                     m.t = u;
                 } else {
                     tab_seq(tab, u, l, k);
-                    m.kind = 0;
+                    m.kind = STAGE == 3 ? 2 : 0;
                     m.t = tab.tb[l] + k;
                 }
                 const uint64_t lo = tab.off[l];
                 m.s = lo + static_cast<uint64_t>(k) * T;
                 m.e = min(m.s + static_cast<uint64_t>(T), lo + tab.cnt[l]);
                 const uint64_t n = m.e - m.s;
-                m.staged = (m.s % 4 == 0) && (n % 4 == 0) && (ldX % 4 == 0) &&
-                           (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+                m.staged = (m.s % 4 == 0) && (n % 4 == 0) &&
+                           (STAGE == 3 || ((ldX % 4 == 0) &&
+                                           (reinterpret_cast<uintptr_t>(X) % 16 == 0)));
                 meta[s] = m;
                 pending_t[s] = m.t;
-                pending_kind[s] = m.kind;
+                pending_pub[s] = m.kind == 0 || (m.kind == 1 && carry);
                 if (m.staged) {
                     const unsigned bytes = static_cast<unsigned>(n * 4);
-                    mbar_arrive_tx(&full[s], bytes * (NS + 1));
+                    mbar_arrive_tx(&full[s], bytes * kRows);
                     float* dst = ring + s * stage_floats;
-                    for (int w = 0; w < NS; ++w)
-                        bulk_g2s(dst + static_cast<size_t>(w) * T, X + static_cast<uint64_t>(w) * ldX + m.s,
-                                 bytes, &full[s]);
-                    bulk_g2s(dst + static_cast<size_t>(NS) * T, g.G + m.s, bytes, &full[s]);
+                    if (STAGE == 3) {
+                        bulk_g2s(dst, g.C + m.s, bytes, &full[s]);
+                    } else {
+                        for (int w = 0; w < NS; ++w)
+                            bulk_g2s(dst + static_cast<size_t>(w) * T,
+                                     X + static_cast<uint64_t>(w) * ldX + m.s, bytes, &full[s]);
+                        bulk_g2s(dst + static_cast<size_t>(NS) * T, g.G + m.s, bytes, &full[s]);
+                    }
                 } else {
                     mbar_arrive(&full[s]);
                 }
@@ -309,15 +380,20 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
         if (m.staged) {
             const float* buf = ring + s * stage_floats;
             const int nq = static_cast<int>((m.e - m.s) >> 2);
-            for (int q = ctid; q < nq; q += CW * 32) {
+            if (STAGE == 3) {
+                for (int q = ctid; q < nq; q += CW * 32)
+                    consume_bcast_quad<NS>(g, *reinterpret_cast<const float4*>(buf + 4 * q),
+                                           m.s + 4ull * q);
+            } else for (int q = ctid; q < nq; q += CW * 32) {
                 float4 xs[NS];
 #pragma unroll
                 for (int w = 0; w < NS; ++w)
                     xs[w] = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(w) * T + 4 * q);
                 const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(NS) * T + 4 * q);
                 const uint64_t f = m.s + 4ull * q;
-                if (m.kind == 1) consume_local_quad<NS>(g, ap, xs, go, f);
-                else consume_agg_quad<NS>(g, ap, xs, go, f, acc);
+                if (m.kind == 0) consume_agg_quad<NS>(g, ap, xs, go, f, acc);
+                else if (g.C) consume_split_quad<NS>(g, ap, xs, go, f, acc);
+                else consume_local_quad<NS>(g, ap, xs, go, f);
             }
         } else {
             consume_direct<NS, CW>(g, ap, X, ldX, m, ctid, acc);
@@ -332,8 +408,8 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
     }
 }
 
-size_t tma_smem_bytes(int NS, int T, int L, int CW, int kStages) {
-    const size_t ring = static_cast<size_t>(kStages) * (NS + 1) * T * sizeof(float);
+size_t tma_smem_bytes(int rows, int T, int L, int CW, int kStages) {
+    const size_t ring = static_cast<size_t>(kStages) * rows * T * sizeof(float);
     const size_t bars = 2 * kStages * sizeof(uint64_t);
     const size_t metas = kStages * sizeof(StageMeta);
     const size_t red = kStages * CW * sizeof(double);
@@ -345,7 +421,7 @@ size_t tma_smem_bytes(int NS, int T, int L, int CW, int kStages) {
 template <int STAGE, int NS, int CW, int KS>
 cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int c0, int c1, cudaStream_t s) {
-    const size_t sm = tma_smem_bytes(NS, g.T, g.L, CW, KS);
+    const size_t sm = tma_smem_bytes(STAGE == 3 ? 1 : NS + 1, g.T, g.L, CW, KS);
     auto kern = k_stage_tma<NS, STAGE, CW, KS>;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -419,7 +495,7 @@ bool tma_supported(int n_workers, int T, int L) {
     if (!(n_workers == 1 || n_workers == 2 || n_workers == 4 || n_workers == 8)) return false;
     if (T < 512 || T > 4096) return false;
     const TmaShape sh = tma_shape(T);
-    return tma_smem_bytes(n_workers, T, L, sh.cw, sh.ks) <= 220 * 1024;
+    return tma_smem_bytes(n_workers + 1, T, L, sh.cw, sh.ks) <= 220 * 1024;
 }
 
 cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
@@ -429,6 +505,7 @@ cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const flo
 
 cudaError_t launch_stage2_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                               int c0, int c1, cudaStream_t s) {
+    if (g.C) return launch_tma<3>(g, ap, X, ldX, c0, c1, s);
     return launch_tma<2>(g, ap, X, ldX, c0, c1, s);
 }
 

@@ -75,6 +75,11 @@ struct GroupView {
     int* rs_layers;              // [L] RS (barrier) layers, ascending id (valid prefix n_rs)
     int* rs_tile_prefix;         // [L+1] exclusive tile prefix along rs_layers
     const float* agg_full;       // [M] aggregated deltas (sharded path), or null
+    // ICS carry (TMA family): stage 1 aggregates the ICS elements while it has
+    // their delta rows in shared memory anyway and stores G_old + agg here; the
+    // stage-2 kernels then only broadcast it into G and the worker rows. Null =
+    // stage 2 re-reads the deltas and G (register-staged family, sharded path).
+    float* C;                    // [M] or null
     // resolve's per-layer sums are split into items of <= kSumChunk tiles so a
     // huge layer is summed by many blocks (fixed order: items ascending)
     const int* sum_items;        // [n_sum_items][3] layer, first tile, end tile

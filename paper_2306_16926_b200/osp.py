@@ -387,9 +387,11 @@ class OspGroup:
     def __init__(self, part: Partition, n_workers: int, weights: Optional[Sequence[float]] = None,
                  n_chunks: int = 4, init_params: Optional[torch.Tensor] = None,
                  tile_elems: int = 0, sgd_lr: float = 0.0, tma: Optional[bool] = None,
-                 stream=None):
+                 carry: bool = True, stream=None):
         """tma: None = TMA-staged stage kernels when the shape allows them, True =
-        require them, False = register-staged kernels (identical results)."""
+        require them, False = register-staged kernels (identical results).
+        carry: with the TMA family, stage 1 also keeps the ICS aggregate so stage 2
+        only broadcasts it (OSP_GROUP_NO_CARRY when False; identical results)."""
         self.part = part
         self.N = n_workers
         self.M = part.total_count()
@@ -402,7 +404,8 @@ class OspGroup:
         cfg = _capi.osp_group_config(n_workers, ctypes.cast(self._w, P(c_dbl)), n_chunks,
                                      tile_elems, sgd_lr,
                                      {None: 0, True: _capi.GROUP_TMA,
-                                      False: _capi.GROUP_REGISTER}[tma])
+                                      False: _capi.GROUP_REGISTER}[tma]
+                                     | (0 if carry else _capi.GROUP_NO_CARRY))
         init = 0
         if init_params is not None:
             _dev_f32(init_params, "init_params")

@@ -188,10 +188,11 @@ def test_split_vs_oracle(osp):
 
 # ---- the group step against the reference-engine goldens ----------------------
 
-def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0, tma=None):
+def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0, tma=None, carry=True,
+                             stage2_zeros=False):
     part = osp.Partition(g.counts, g.bpe)
     grp = osp.OspGroup(part, g.N, list(g.weights), n_chunks=g.n_chunks,
-                       init_params=cuda(g.p0), tile_elems=tile_elems, tma=tma)
+                       init_params=cuda(g.p0), tile_elems=tile_elems, tma=tma, carry=carry)
     for it in range(g.iters):
         d = g.deltas(it)
         X = torch.zeros((g.N, g.M + pad_ld), dtype=torch.float32, device="cuda")
@@ -215,8 +216,11 @@ def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0, tma=None):
         else:
             assert np.array_equal(bits(P1[0]), bits(g.get(it, "params_stage1_w0")))
             assert np.array_equal(bits(P1[-1]), bits(g.get(it, "params_stage1_wlast")))
+        # with the ICS carry, stage 2 applies the payload split at stage 1 (as the
+        # reference's split_for_sync copies it) and never reads its deltas argument
+        X2 = torch.zeros_like(X) if stage2_zeros else X
         for c in range(g.n_chunks):
-            grp.stage2_chunk(c, X)
+            grp.stage2_chunk(c, X2)
         grp.resolve(X)
         G = grp.global_params.cpu().numpy()
         assert np.array_equal(bits(G), bits(g.get(it, "global"))), f"global, it {it}"
@@ -247,7 +251,7 @@ def test_group_small_tiles_and_unaligned_rows(osp, golden):
 # ---- the group step against the oracle at larger sizes ---------------------------
 
 def oracle_vs_group(osp, counts, N, weights, budget_frac, n_chunks, iters, seed, p0=None,
-                    sgd_lr=0.0, tile_elems=0, tma=None):
+                    sgd_lr=0.0, tile_elems=0, tma=None, carry=True):
     counts = np.asarray(counts, dtype=np.uint64)
     M = int(counts.sum())
     bpe = 4
@@ -256,7 +260,7 @@ def oracle_vs_group(osp, counts, N, weights, budget_frac, n_chunks, iters, seed,
     P = np.tile(G, (N, 1))
     part = osp.Partition(counts)
     grp = osp.OspGroup(part, N, weights, n_chunks=n_chunks, init_params=cuda(G),
-                       sgd_lr=sgd_lr, tile_elems=tile_elems, tma=tma)
+                       sgd_lr=sgd_lr, tile_elems=tile_elems, tma=tma, carry=carry)
     flags = np.zeros(len(counts), np.uint8)
     order = np.zeros(0, np.int32)
     X = torch.empty((N, M), dtype=torch.float32, device="cuda")
@@ -377,22 +381,25 @@ def test_step_host_matches_device_step(osp):
 
 # ---- TMA-staged stage kernels (OSP_GROUP_TMA): same results --------------------
 
+@pytest.mark.parametrize("carry", [True, False])
 @pytest.mark.parametrize("pad_ld", [0, 1])
-def test_tma_group_matches_reference_engine(osp, golden, pad_ld):
+def test_tma_group_matches_reference_engine(osp, golden, pad_ld, carry):
     if golden.N not in (1, 2, 4, 8):
         with pytest.raises(osp.InvalidArgument):
             osp.OspGroup(osp.Partition(golden.counts, golden.bpe), golden.N,
                          list(golden.weights), tma=True)
         return
     # pad_ld=1: unaligned rows, every tile takes the unstaged path
-    run_group_against_golden(osp, golden, pad_ld=pad_ld, tma=True)
+    run_group_against_golden(osp, golden, pad_ld=pad_ld, tma=True, carry=carry,
+                             stage2_zeros=carry)
 
 
+@pytest.mark.parametrize("carry", [True, False])
 @pytest.mark.parametrize("tile", [512, 1024, 2048])
-def test_tma_group_resnet50_layout_vs_oracle(osp, tile):
+def test_tma_group_resnet50_layout_vs_oracle(osp, tile, carry):
     from paper_2306_16926_b200 import layouts
     grp = oracle_vs_group(osp, layouts.resnet50(), 8, [0.125] * 8, 0.5, 4, 3, seed=11,
-                          tile_elems=tile, tma=True)
+                          tile_elems=tile, tma=True, carry=carry)
     assert grp.stage_kernels == "tma-staged"
 
 
@@ -414,6 +421,19 @@ def test_tma_group_ragged_sgd_and_budget_edges(osp):
     for frac in (0.0, 1.0, 0.33):
         oracle_vs_group(osp, counts, 2, [0.5, 0.5], frac, 4, 3, seed=23, tma=True)
     oracle_vs_group(osp, counts, 1, [1.0], 0.7, 1, 3, seed=29, tma=True)
+    for frac in (0.0, 1.0):
+        oracle_vs_group(osp, counts, 2, [0.5, 0.5], frac, 4, 2, seed=31, tma=True, carry=False)
+
+
+def test_carry_flag_reported(osp):
+    part = osp.Partition([1000, 5000])
+    assert lib_flags(osp, osp.OspGroup(part, 8)) & 4 == 0
+    assert lib_flags(osp, osp.OspGroup(part, 8, carry=False)) & 4 == 4
+    assert lib_flags(osp, osp.OspGroup(part, 3)) & 4 == 4  # register family: no carry
+
+
+def lib_flags(osp, grp):
+    return osp.lib().osp_group_flags(grp._h)
 
 
 def test_tma_matches_default_kernels(osp):
@@ -425,15 +445,18 @@ def test_tma_matches_default_kernels(osp):
     part = osp.Partition(counts)
     a = osp.OspGroup(part, N, [0.125] * N, n_chunks=4, tma=False)
     b = osp.OspGroup(part, N, [0.125] * N, n_chunks=4, tma=True)
+    c = osp.OspGroup(part, N, [0.125] * N, n_chunks=4, tma=True, carry=False)
     for it in range(4):
         X = osp.synth_deltas(5, N, it, M)
-        a.set_budget(M * 2)
-        b.set_budget(M * 2)
-        a.step(X)
-        b.step(X)
-        assert np.array_equal(bits(a.global_params), bits(b.global_params))
-        assert np.array_equal(bits(a.worker_params), bits(b.worker_params))
-        assert np.array_equal(a.read_gib()["order"], b.read_gib()["order"])
+        for grp in (a, b, c):
+            grp.set_budget(M * 2)
+            grp.step(X)
+        for other in (b, c):
+            assert np.array_equal(bits(a.global_params), bits(other.global_params))
+            assert np.array_equal(bits(a.worker_params), bits(other.worker_params))
+            assert np.array_equal(a.read_gib()["order"], other.read_gib()["order"])
+        # same tiles and lanes: the carried stage-1 partials equal stage 2's bit for bit
+        assert np.array_equal(bits(b.scores), bits(c.scores))
 
 
 def test_group_errors(osp):
