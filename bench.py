@@ -231,8 +231,10 @@ def b200_single(args):
     stream = torch.cuda.current_stream()
 
     def step(k, evs=None, full=False):
-        # timed region: events around stage 1 only (the roofline kernel); the
-        # breakdown pass (full=True) also brackets stage 2
+        # timed region: events around stage 1 only (the roofline kernel), then
+        # stage 2 + resolve as osp_group_step issues them (overlapped with the
+        # ICS carry); the breakdown pass (full=True) runs stage 2 and the resolve
+        # one after the other to time each
         x = X[k % 2]
         if evs is not None:
             evs[0].record(stream)
@@ -242,6 +244,9 @@ def b200_single(args):
         if args.per_chunk:
             for c in range(args.chunks):
                 grp.stage2_chunk(c, x)
+        elif not full:
+            grp.stage2_resolve(x)
+            return
         else:
             grp.stage2_all(x)
         if evs is not None and full:
@@ -278,7 +283,12 @@ def b200_single(args):
     s2 = [evb[k][1].elapsed_time(evb[k][2]) for k in range(KB)]
     s3 = [evb[k][2].elapsed_time(evb[k + 1][0]) for k in range(KB)]
     # u of each timed step = deferred bytes of the GIB it split with (tags tag0..)
-    deferred = grp.deferred_history(tag0, K).astype(np.float64)
+    # (the device ring keeps the last 4096 tags: a longer run takes the window's
+    # mean for its earlier steps)
+    nh = min(K, 4096)
+    deferred = grp.deferred_history(tag0 + K - nh, nh).astype(np.float64)
+    if nh < K:
+        deferred = np.concatenate([np.full(K - nh, deferred.mean()), deferred])
     u = deferred / model_bytes
     # algorithmic bytes. SURVEY §8(d): stage 1 = 4M[(2N+2) - u] (N delta rows + G read,
     # N worker rows + G on RS written), stage 2 = 4M u (2N+1) (N rows + G re-read,
@@ -303,8 +313,7 @@ def b200_single(args):
         comp = overlap.SyntheticCompute(args.overlap_ms)
 
         def s2r(i):
-            grp.stage2_all(X[i % 2])
-            grp.resolve(X[i % 2])
+            grp.stage2_resolve(X[i % 2])
 
         ovl = overlap.run(lambda i: grp.stage1(X[i % 2]), s2r, comp, K=min(K, 50), W=3)
         ovl["t_c_ms"] = comp.ms
@@ -355,10 +364,12 @@ def b200_single(args):
                                           "4M[(2N+2) + u(2N+1)] (SURVEY §8(d))"),
                      "survey_roofline_ms": survey_ms,
                      "vs_survey_roofline": survey_ms / ms_step},
-        "breakdown_ms": {"stage1": s1_avg, "stage2_chunks": sum(s2) / KB,
-                         "resolve_and_gaps": sum(s3) / KB,
-                         "note": "stage1 from the timed region; stage2/resolve from a separate "
-                                 "evented pass of min(K, 50) steps"},
+        "breakdown_ms": {"stage1": s1_avg, "after_stage1": ms_step - s1_avg,
+                         "stage2_alone": sum(s2) / KB, "resolve_alone_and_gaps": sum(s3) / KB,
+                         "note": "stage1 and after_stage1 (stage 2 + resolve as the step issues "
+                                 "them: overlapped with the ICS carry) from the timed region; "
+                                 "stage2_alone / resolve_alone from a separate serial evented "
+                                 "pass of min(K, 50) steps"},
         "u_mean": float(u.mean()),
         "e2e": {"value": M / (e2e_step * 1e-3), "unit": UNIT, "ms_per_step": e2e_step,
                 "h2d_bytes_per_step": N * M * 4, "d2h_bytes_per_step": gib_bytes,

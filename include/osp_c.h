@@ -261,7 +261,14 @@ osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, voi
 /* stage1 + stage2_all (two launches; a single-launch variant with per-tile
  * dependency flags measured slower, profiles/r1_ncu_summary.md). */
 osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void* stream);
-/* osp_group_stages + resolve. */
+/* stage2_all + resolve, same results. With the ICS carry the resolve needs
+ * nothing from stage 2 (every PGP partial is published by stage 1), so it is
+ * launched first and the stage-2 broadcast runs beside it, reading a stage-1
+ * snapshot of the ICS lists the resolve rewrites; the stage-2 grid retires only
+ * after the resolve has published (device-side join), so the next launch on
+ * `stream` sees both. */
+osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream);
+/* stage1 + stage2_resolve. */
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 /* End-to-end step from HOST (pinned or pageable) deltas: H2D copy of the N rows
  * into the group's staging buffer, the step, and a D2H read of the encoded next
@@ -283,7 +290,7 @@ osp_status osp_group_read_gib(osp_group* g, uint8_t* ics_flags, int32_t* ics_ord
 osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fallback_layers,
                            uint64_t* fallback_resolves, void* stream);
 /* Deferred (ICS) bytes of the GIBs with tags first_tag .. first_tag+n-1 (a
- * device ring of the last 1024 resolutions): the u of each iteration for the
+ * device ring of the last 4096 resolutions): the u of each iteration for the
  * algorithmic-byte accounting, without a host sync inside a timed loop. */
 osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, uint64_t* out,
                                       void* stream);

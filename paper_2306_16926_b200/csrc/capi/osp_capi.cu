@@ -718,6 +718,8 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         return cleanup(st);
     if (use_tma && !(cfg->flags & OSP_GROUP_NO_CARRY)) {
         if ((st = dalloc(g, &v.C, M)) != OSP_OK) return cleanup(st);
+        if ((st = dalloc(g, &v.snap, snap_ints(static_cast<int>(L), cfg->n_chunks))) != OSP_OK)
+            return cleanup(st);
     }
     g->blocks_per_sm = stage_blocks_per_sm(N, static_cast<int>(L));
     g->tma = use_tma;
@@ -795,9 +797,24 @@ osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void
     return osp_group_stage2_all(g, deltas, ld, stream);
 }
 
+osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
+    if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    if (!g->v.C) {
+        OSP_TRY(osp_group_stage2_all(g, deltas, ld, stream));
+        return osp_group_resolve(g, deltas, ld, stream);
+    }
+    // carry: every tile partial is known after stage 1, so the resolve goes
+    // first and the stage-2 broadcast runs beside it (joined before it retires)
+    cudaStream_t s = as_stream(stream);
+    OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, s));
+    OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, 0, g->n_chunks, s, 1));
+    return OSP_OK;
+}
+
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
-    OSP_TRY(osp_group_stages(g, deltas, ld, stream));
-    return osp_group_resolve(g, deltas, ld, stream);
+    OSP_TRY(osp_group_stage1(g, deltas, ld, stream));
+    return osp_group_stage2_resolve(g, deltas, ld, stream);
 }
 
 osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,

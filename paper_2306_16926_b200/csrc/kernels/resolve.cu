@@ -339,7 +339,9 @@ __device__ double exact_layer_pgp(const GroupView& g, const AggParams& ap, const
                 }
                 agg = agg_finish(ap, a);
             }
-            t = pgp_term(agg, g.G[f]);
+            // carry: the deferred layers' post-update values are in C (G may
+            // still be being written by the overlapped stage 2)
+            t = pgp_term(agg, (g.C && g.flags[l]) ? g.C[f] : g.G[f]);
         }
         const int valid = static_cast<int>((end - b) < 32 ? (end - b) : 32);
         for (int i = 0; i < valid; ++i) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, t, i));
@@ -474,6 +476,13 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     __syncthreads();
     if (tid == 0) g.meta64[META64_RESOLVED] += 1;
     finalize_lists(g, s, s.sorted, k, tag);
+    // publish: every list written (block barrier, then a cumulative fence)
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        atomicExch(reinterpret_cast<unsigned long long*>(g.meta64 + META64_RESOLVE_DONE),
+                   static_cast<unsigned long long>(g.meta64[META64_RESOLVED]));
+    }
 }
 
 // Install a host-provided GIB: g.flags already written; order (device) is the
@@ -504,7 +513,10 @@ __global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const 
             run += s.cnt[s.sorted[r]] * static_cast<uint64_t>(g.bpe);
             pre[r] = run;
         }
-        if (g.meta64) g.meta64[META64_RESOLVED] = tag;
+        if (g.meta64) {
+            g.meta64[META64_RESOLVED] = tag;
+            g.meta64[META64_RESOLVE_DONE] = tag;
+        }
     }
     __syncthreads();
     finalize_lists(g, s, s.sorted, s.flag[1], tag);

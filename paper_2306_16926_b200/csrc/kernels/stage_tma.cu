@@ -218,9 +218,12 @@ __device__ void consume_direct(const GroupView& g, const AggParams& ap, const fl
 template <int NS, int STAGE, int CW, int kStages>
 __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggParams ap,
                                                            const float* __restrict__ X,
-                                                           uint64_t ldX, int c0, int c1) {
+                                                           uint64_t ldX, int c0, int c1, int ovl) {
     extern __shared__ __align__(128) unsigned char smem[];
-    pdl_wait();
+    // ovl (stage 3 only): launched after this iteration's resolve, which waited
+    // for stage 1 before letting this grid launch; run beside the resolve (no
+    // wait on it) from the stage-1 snapshot of the ICS lists, join at the end
+    if (!(STAGE == 3 && ovl)) pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -242,13 +245,31 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
     uint8_t* t_flag = reinterpret_cast<uint8_t*>(t_tb + L + 1);
     int* t_sl = reinterpret_cast<int*>(t_flag + ((L + 15) & ~15));
     int* t_sp = t_sl + L;
+    // stage 1 with the carry: block 0 snapshots the ICS lists stage 3 will use
+    const int n_ch = g.n_chunks;
+    int* snap_cb = g.snap ? g.snap + kSnapHead : nullptr;
+    int* snap_il = g.snap ? snap_cb + n_ch + 1 : nullptr;
+    int* snap_tp = g.snap ? snap_il + L : nullptr;
+    if (STAGE == 1 && g.snap && blockIdx.x == 0) {
+        const int n_ics = g.meta[META_N_ICS];
+        if (tid == 0) {
+            g.snap[0] = g.meta[META_N_USED];
+            g.snap[1] = static_cast<int>(g.meta64[META64_RESOLVED] + 1);
+        }
+        for (int i = tid; i <= n_ch; i += blockDim.x) snap_cb[i] = g.chunk_begin[i];
+        for (int i = tid; i < n_ics; i += blockDim.x) snap_il[i] = g.ics_layers[i];
+        for (int i = tid; i <= n_ics; i += blockDim.x) snap_tp[i] = g.ics_tile_prefix[i];
+    }
+    const int* l_cb = STAGE == 3 ? snap_cb : g.chunk_begin;
+    const int* l_il = STAGE == 3 ? snap_il : g.ics_layers;
+    const int* l_tp = STAGE == 3 ? snap_tp : g.ics_tile_prefix;
     int jb = 0, je = 0;
     if (STAGE >= 2) {
-        const int used = g.meta[META_N_USED];
+        const int used = STAGE == 3 ? g.snap[0] : g.meta[META_N_USED];
         const int cc1 = c1 > used ? used : c1;
         if (c0 < cc1) {
-            jb = g.chunk_begin[c0];
-            je = g.chunk_begin[cc1];
+            jb = l_cb[c0];
+            je = l_cb[cc1];
         }
     }
     for (int i = tid; i < L; i += blockDim.x) {
@@ -259,8 +280,8 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
     }
     if (tid == 0) t_tb[L] = g.tile_base[L];
     if (STAGE >= 2) {
-        for (int i = tid; i < je - jb; i += blockDim.x) t_sl[i] = g.ics_layers[jb + i];
-        for (int i = tid; i <= je - jb; i += blockDim.x) t_sp[i] = g.ics_tile_prefix[jb + i];
+        for (int i = tid; i < je - jb; i += blockDim.x) t_sl[i] = l_il[jb + i];
+        for (int i = tid; i <= je - jb; i += blockDim.x) t_sp[i] = l_tp[jb + i];
     }
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -364,6 +385,22 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
             if (atomicAdd(done, 1) == total - 1) {
                 atomicExch(next, 0);
                 atomicExch(done, 0);
+                if (STAGE == 3 && ovl) {
+                    // join: this grid (and so the next kernel in the stream) ends
+                    // only once the overlapped resolve has published its lists
+                    const unsigned long long want = static_cast<unsigned>(g.snap[1]);
+                    volatile unsigned long long* dn =
+                        reinterpret_cast<volatile unsigned long long*>(g.meta64 + META64_RESOLVE_DONE);
+                    uint64_t t0;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                    while ((*dn & 0xffffffffull) != want) {
+                        __nanosleep(64);
+                        uint64_t t;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                        if (t - t0 > 20000000000ull) __trap();
+                    }
+                    __threadfence();
+                }
             }
         }
         return;
@@ -420,7 +457,7 @@ size_t tma_smem_bytes(int rows, int T, int L, int CW, int kStages) {
 
 template <int STAGE, int NS, int CW, int KS>
 cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                          int c0, int c1, cudaStream_t s) {
+                          int c0, int c1, int ovl, cudaStream_t s) {
     const size_t sm = tma_smem_bytes(STAGE == 3 ? 1 : NS + 1, g.T, g.L, CW, KS);
     auto kern = k_stage_tma<NS, STAGE, CW, KS>;
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
@@ -432,7 +469,7 @@ cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* 
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     const int grid = sm_count() * per_sm;
-    return launch_pdl(kern, dim3(grid), dim3((CW + 1) * 32), sm, s, g, ap, X, ldX, c0, c1);
+    return launch_pdl(kern, dim3(grid), dim3((CW + 1) * 32), sm, s, g, ap, X, ldX, c0, c1, ovl);
 }
 
 struct TmaShape {
@@ -457,34 +494,34 @@ TmaShape tma_shape(int T) {
 
 template <int STAGE, int NS, int CW>
 cudaError_t launch_tma_ks(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                          int c0, int c1, int ks, cudaStream_t s) {
+                          int c0, int c1, int ovl, int ks, cudaStream_t s) {
     switch (ks) {
-        case 2: return launch_tma_cw<STAGE, NS, CW, 2>(g, ap, X, ldX, c0, c1, s);
-        case 3: return launch_tma_cw<STAGE, NS, CW, 3>(g, ap, X, ldX, c0, c1, s);
-        default: return launch_tma_cw<STAGE, NS, CW, 4>(g, ap, X, ldX, c0, c1, s);
+        case 2: return launch_tma_cw<STAGE, NS, CW, 2>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 3: return launch_tma_cw<STAGE, NS, CW, 3>(g, ap, X, ldX, c0, c1, ovl, s);
+        default: return launch_tma_cw<STAGE, NS, CW, 4>(g, ap, X, ldX, c0, c1, ovl, s);
     }
 }
 
 template <int STAGE, int NS>
 cudaError_t launch_tma_n(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                         int c0, int c1, cudaStream_t s) {
+                         int c0, int c1, int ovl, cudaStream_t s) {
     const TmaShape sh = tma_shape(g.T);
     switch (sh.cw) {
-        case 4: return launch_tma_ks<STAGE, NS, 4>(g, ap, X, ldX, c0, c1, sh.ks, s);
-        case 8: return launch_tma_ks<STAGE, NS, 8>(g, ap, X, ldX, c0, c1, sh.ks, s);
-        case 16: return launch_tma_ks<STAGE, NS, 16>(g, ap, X, ldX, c0, c1, sh.ks, s);
+        case 4: return launch_tma_ks<STAGE, NS, 4>(g, ap, X, ldX, c0, c1, ovl, sh.ks, s);
+        case 8: return launch_tma_ks<STAGE, NS, 8>(g, ap, X, ldX, c0, c1, ovl, sh.ks, s);
+        case 16: return launch_tma_ks<STAGE, NS, 16>(g, ap, X, ldX, c0, c1, ovl, sh.ks, s);
         default: return cudaErrorNotSupported;
     }
 }
 
 template <int STAGE>
 cudaError_t launch_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                       int c0, int c1, cudaStream_t s) {
+                       int c0, int c1, int ovl, cudaStream_t s) {
     switch (ap.n) {
-        case 1: return launch_tma_n<STAGE, 1>(g, ap, X, ldX, c0, c1, s);
-        case 2: return launch_tma_n<STAGE, 2>(g, ap, X, ldX, c0, c1, s);
-        case 4: return launch_tma_n<STAGE, 4>(g, ap, X, ldX, c0, c1, s);
-        case 8: return launch_tma_n<STAGE, 8>(g, ap, X, ldX, c0, c1, s);
+        case 1: return launch_tma_n<STAGE, 1>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 2: return launch_tma_n<STAGE, 2>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 4: return launch_tma_n<STAGE, 4>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 8: return launch_tma_n<STAGE, 8>(g, ap, X, ldX, c0, c1, ovl, s);
         default: return cudaErrorNotSupported;
     }
 }
@@ -500,13 +537,14 @@ bool tma_supported(int n_workers, int T, int L) {
 
 cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                               cudaStream_t s) {
-    return launch_tma<1>(g, ap, X, ldX, 0, 0, s);
+    return launch_tma<1>(g, ap, X, ldX, 0, 0, 0, s);
 }
 
 cudaError_t launch_stage2_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                              int c0, int c1, cudaStream_t s) {
-    if (g.C) return launch_tma<3>(g, ap, X, ldX, c0, c1, s);
-    return launch_tma<2>(g, ap, X, ldX, c0, c1, s);
+                              int c0, int c1, cudaStream_t s, int overlap) {
+    if (g.C) return launch_tma<3>(g, ap, X, ldX, c0, c1, overlap, s);
+    if (overlap) return cudaErrorInvalidValue;
+    return launch_tma<2>(g, ap, X, ldX, c0, c1, 0, s);
 }
 
 }  // namespace osp

@@ -80,6 +80,12 @@ struct GroupView {
     // stage-2 kernels then only broadcast it into G and the worker rows. Null =
     // stage 2 re-reads the deltas and G (register-staged family, sharded path).
     float* C;                    // [M] or null
+    // Stage-1 snapshot of the current ICS lists for the carry stage 2, so the
+    // next GIB's resolve may rewrite the live lists while stage 2 still runs
+    // (osp_group_step: resolve overlapped with stage 2). Layout: [0] n_used
+    // chunks, [1] the resolve epoch stage 2 joins on, [4..] chunk_begin
+    // [n_chunks+1], ics_layers [L], ics_tile_prefix [L+1]. Null without carry.
+    int* snap;
     // resolve's per-layer sums are split into items of <= kSumChunk tiles so a
     // huge layer is summed by many blocks (fixed order: items ascending)
     const int* sum_items;        // [n_sum_items][3] layer, first tile, end tile
@@ -110,10 +116,13 @@ enum Meta64Idx {
     META64_DEFERRED = 2,
     META64_RESOLVED = 3,
     META64_FB_LAYERS = 4,
-    META64_FB_RESOLVES = 5
+    META64_FB_RESOLVES = 5,
+    META64_RESOLVE_DONE = 6  // == META64_RESOLVED once that resolve's lists are written
 };
+constexpr int kSnapHead = 4;
+__host__ __device__ inline int snap_ints(int L, int n_chunks) { return kSnapHead + n_chunks + 1 + 2 * L + 1; }
 
-constexpr int kHist = 1024;
+constexpr int kHist = 4096;
 constexpr int kMaxLayers = 3072;  // single-CTA resolve (resolve.cu: ~60 B shared memory per layer)
 constexpr int kStageThreads = 256;
 constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profiles/)
@@ -200,8 +209,10 @@ int stage_blocks_per_sm(int n_workers, int n_layers);
 bool tma_supported(int n_workers, int T, int L);
 cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                               cudaStream_t s);
+// overlap = 1 (carry only): launched after the resolve of the same iteration,
+// runs beside it and joins on its epoch before retiring (osp_group_step).
 cudaError_t launch_stage2_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                              int c0, int c1, cudaStream_t s);
+                              int c0, int c1, cudaStream_t s, int overlap = 0);
 
 cudaError_t launch_aggregate_layer(const float* const* contribs, const AggParams& ap, uint64_t n,
                                    float* out, cudaStream_t s);

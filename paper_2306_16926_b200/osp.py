@@ -487,6 +487,11 @@ class OspGroup:
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_resolve(self._h, p, ld, _stream(stream)))
 
+    def stage2_resolve(self, deltas: torch.Tensor, stream=None):
+        """stage2_all + resolve (overlapped with the ICS carry)."""
+        p, ld = self._deltas(deltas)
+        _check(lib().osp_group_stage2_resolve(self._h, p, ld, _stream(stream)))
+
     def step(self, deltas: torch.Tensor, stream=None):
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_step(self._h, p, ld, _stream(stream)))

@@ -359,6 +359,43 @@ def test_certificate_fallback_on_exact_ties(osp):
     assert st["fallback_resolves"] == 1 and st["fallback_layers"] >= 3
 
 
+@pytest.mark.parametrize("carry", [True, False])
+def test_certificate_fallback_on_deferred_layers(osp, carry):
+    """Exact ties again in iteration 1, where a tied layer is deferred: the exact
+    fallback must score it against its post-update values. With the ICS carry
+    the step overlaps the resolve with the stage-2 broadcast, so those values
+    come from the carry buffer, not from G (still being written)."""
+    half = 50_000
+    counts = [half, half, 1000, half]
+    M = sum(counts)
+    N = 4
+    part = osp.Partition(counts)
+    grp = osp.OspGroup(part, N, [0.25] * N, n_chunks=2, carry=carry)
+    G = np.zeros(M, np.float32)
+    P = np.zeros((N, M), np.float32)
+    flags, order = np.zeros(4, np.uint8), np.zeros(0, np.int32)
+    budget = int(0.6 * M * 4)
+    X = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    deferred_tie = False
+    for it in range(3):
+        osp.synth_deltas(7, N, it, M, out=X)
+        X[:, half: 2 * half] = X[:, :half]
+        X[:, 2 * half + 1000:] = X[:, :half]
+        deferred_tie |= bool(flags[0] or flags[1] or flags[3])
+        r = oracle.step(counts, 4, [0.25] * N, X.cpu().numpy(), G, P, flags, order, 2, budget)
+        grp.set_budget(budget)
+        grp.step(X)
+        assert np.array_equal(bits(grp.global_params), bits(G)), f"global, it {it}"
+        assert np.array_equal(bits(grp.worker_params), bits(P)), f"workers, it {it}"
+        nxt = grp.read_gib()
+        assert np.array_equal(nxt["flags"], r["flags_out"]), f"flags, it {it}"
+        assert np.array_equal(nxt["order"], r["order_out"]), f"order, it {it}"
+        flags, order = r["flags_out"], r["order_out"]
+    assert deferred_tie
+    st = grp.stats()
+    assert st["fallback_resolves"] == 3
+
+
 def test_step_host_matches_device_step(osp):
     from paper_2306_16926_b200 import layouts
     counts = layouts.resnet50()[:40]

@@ -20,6 +20,6 @@ for ln in open("gpurun_out/bench_configs.jsonl"):
     if "failed" in d: print(d); continue
     c = d["config"]
     print(f'{c["workload"][:30]:30s} b={c["budget_frac"]} u={d["u_mean"]:.3f} ms={d["ms_per_step"]:.3f} '
-          f'params/s={d["value"]:.3e} s1_frac={d["roofline"]["frac"]:.3f} step_frac={d["roofline"]["step_frac"]:.3f} '
+          f'params/s={d["value"]:.3e} s1_frac={d["roofline"]["frac"]:.3f} step_frac={d["roofline"]["step_frac"]:.3f} vs_survey={d["roofline"].get("vs_survey_roofline",0):.3f} '
           f'e2e_ms={d["e2e"]["ms_per_step"]:.1f} cpu={d.get("cpu_baseline",{}).get("value")} fb={d["certificate"]}')
 PY
