@@ -159,6 +159,25 @@ osp_status osp_gib_encode(uint32_t tag, uint64_t n_layers, const uint8_t* ics_fl
 osp_status osp_gib_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint32_t* n_layers,
                           uint8_t* ics_flags, uint64_t flags_cap);
 
+/* GIB wire with the rank-order side channel (the gap named
+ * in the reference README.md:207-210 — the bitmap alone does not carry the
+ * chunk emission order). Layout: the gib_encode bytes above, then n u32 LE and
+ * n layer ids u32 LE, the deferred layers least important first
+ * (Message::ics_rank_order, message.hpp:33-36). The reference's gib_decode
+ * reads only the bitmap prefix (it accepts longer buffers, importance.cpp:99-
+ * 117), so a wire is still a valid reference GIB message.
+ * encode: every order id must be a distinct deferred layer (LayerError beyond
+ *   L, ProtocolError otherwise); *len = bytes (out may be NULL to query).
+ * decode: FormatError on truncation, a bad length or a bad id; *n_order = -1
+ *   for a bitmap-only buffer (no side channel). Any output may be NULL. */
+uint64_t osp_gib_wire_size(uint64_t n_layers, uint64_t n_order);
+osp_status osp_gib_wire_encode(uint32_t tag, uint64_t n_layers, const uint8_t* ics_flags,
+                               const int32_t* order, uint64_t n_order, uint8_t* out,
+                               uint64_t cap, uint64_t* len);
+osp_status osp_gib_wire_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint32_t* n_layers,
+                               uint8_t* ics_flags, uint64_t flags_cap, int32_t* order,
+                               uint64_t order_cap, int64_t* n_order);
+
 /* Payload wire codec on the device: encode_payload_message /
  * decode_payload_message (message.cpp:53-99) for payloads resident in HBM, so a
  * byte transport can send straight from the device. Layout: kind u8 |
@@ -285,6 +304,16 @@ double* osp_group_scores(osp_group* g);
 osp_status osp_group_read_gib(osp_group* g, uint8_t* ics_flags, int32_t* ics_order,
                               int64_t* n_order, int32_t* chunk_of, int* n_used_chunks,
                               uint32_t* tag, uint64_t* deferred_bytes, void* stream);
+/* The current GIB as a wire (bitmap + rank order), written on the device by
+ * every resolve and install: HOST copy (synchronises `stream`; *len = bytes,
+ * out may be NULL to query), the DEVICE buffer itself for a transport that
+ * sends from HBM (valid until destroy; its length is in the header: bitmap
+ * size, then n), and install from a wire (a bitmap-only wire installs the
+ * ascending deferred ids, the reference's convention for a missing order). */
+osp_status osp_group_gib_wire(osp_group* g, uint8_t* out, uint64_t cap, uint64_t* len,
+                              void* stream);
+const uint8_t* osp_group_gib_wire_device(const osp_group* g, uint64_t* max_len);
+osp_status osp_group_set_gib_wire(osp_group* g, const uint8_t* buf, uint64_t len, void* stream);
 /* Counters: iterations resolved, layers that needed the exact sequential PGP
  * fallback (certificate failures), and resolves that used it. */
 osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fallback_layers,

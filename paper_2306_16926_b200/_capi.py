@@ -85,6 +85,14 @@ _SIGS = {
     "osp_gib_encode": (c_int, [c_u32, c_u64, P(ctypes.c_uint8), P(ctypes.c_uint8), c_u64]),
     "osp_gib_decode": (c_int, [P(ctypes.c_uint8), c_u64, P(c_u32), P(c_u32), P(ctypes.c_uint8),
                                c_u64]),
+    "osp_gib_wire_size": (c_u64, [c_u64, c_u64]),
+    "osp_gib_wire_encode": (c_int, [c_u32, c_u64, P(ctypes.c_uint8), P(ctypes.c_int32), c_u64,
+                                    P(ctypes.c_uint8), c_u64, P(c_u64)]),
+    "osp_gib_wire_decode": (c_int, [P(ctypes.c_uint8), c_u64, P(c_u32), P(c_u32),
+                                    P(ctypes.c_uint8), c_u64, P(ctypes.c_int32), c_u64, P(c_i64)]),
+    "osp_group_gib_wire": (c_int, [c_void_p, P(ctypes.c_uint8), c_u64, P(c_u64), c_void_p]),
+    "osp_group_gib_wire_device": (c_void_p, [c_void_p, P(c_u64)]),
+    "osp_group_set_gib_wire": (c_int, [c_void_p, P(ctypes.c_uint8), c_u64, c_void_p]),
     "osp_payload_encoded_size": (c_u64, [c_void_p, P(ctypes.c_int32), c_i64]),
     "osp_encode_payload": (c_int, [c_void_p, c_void_p, P(ctypes.c_int32), c_i64, ctypes.c_uint8,
                                    c_u32, c_void_p, c_u64, P(c_u64), c_void_p]),

@@ -457,7 +457,7 @@ osp_status osp_split_for_sync(const osp_partition* part, const uint8_t* ics_flag
     if (e == cudaSuccess) e = al(&v.meta, 8 * sizeof(int));
     if (e == cudaSuccess) e = al(&v.meta64, 8 * sizeof(uint64_t));
     if (e == cudaSuccess) e = al(&v.chunk_of, L * sizeof(int));
-    if (e == cudaSuccess) e = al(&v.gib_bytes, osp_gib_encoded_size(L));
+    if (e == cudaSuccess) e = al(&v.gib_bytes, osp_gib_wire_size(L, L));
     v.tile_base = d_tb;
     if (e == cudaSuccess) e = cudaMemcpy(d_tb, tb.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(v.flags, f.data(), L, cudaMemcpyHostToDevice);
@@ -512,6 +512,79 @@ osp_status osp_gib_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint3
         if (L > flags_cap) return fail(OSP_ERR_INVALID, "flags buffer too small");
         for (uint64_t k = 0; k < L; ++k) ics_flags[k] = (buf[8 + k / 8] >> (k % 8)) & 1u;
     }
+    return OSP_OK;
+}
+
+uint64_t osp_gib_wire_size(uint64_t n_layers, uint64_t n_order) {
+    return osp_gib_encoded_size(n_layers) + 4 + 4 * n_order;
+}
+
+osp_status osp_gib_wire_encode(uint32_t tag, uint64_t n_layers, const uint8_t* ics_flags,
+                               const int32_t* order, uint64_t n_order, uint8_t* out,
+                               uint64_t cap, uint64_t* len) {
+    if (!ics_flags && n_layers > 0) return fail(OSP_ERR_INVALID, "null flags");
+    if (n_order > 0 && !order) return fail(OSP_ERR_INVALID, "null rank order");
+    if (n_layers > 0xffffffffull || n_order > n_layers)
+        return fail(OSP_ERR_INVALID, "rank order longer than the layer count");
+    std::vector<uint8_t> seen(n_layers, 0);
+    for (uint64_t r = 0; r < n_order; ++r) {
+        const int32_t id = order[r];
+        if (id < 0 || static_cast<uint64_t>(id) >= n_layers)
+            return fail(OSP_ERR_LAYER, "rank order names layer " + std::to_string(id) +
+                                           " beyond the partition");
+        if (!ics_flags[id])
+            return fail(OSP_ERR_PROTOCOL, "rank order names layer " + std::to_string(id) +
+                                              " that the bitmap does not defer");
+        if (seen[id]++) return fail(OSP_ERR_PROTOCOL, "rank order repeats layer " + std::to_string(id));
+    }
+    const uint64_t need = osp_gib_wire_size(n_layers, n_order);
+    if (len) *len = need;
+    if (!out) return OSP_OK;
+    if (cap < need) return fail(OSP_ERR_INVALID, "gib wire buffer too small");
+    OSP_TRY(osp_gib_encode(tag, n_layers, ics_flags, out, cap));
+    uint8_t* p = out + osp_gib_encoded_size(n_layers);
+    put_u32le(p, static_cast<uint32_t>(n_order));
+    for (uint64_t r = 0; r < n_order; ++r) put_u32le(p + 4 + 4 * r, static_cast<uint32_t>(order[r]));
+    return OSP_OK;
+}
+
+osp_status osp_gib_wire_decode(const uint8_t* buf, uint64_t len, uint32_t* tag, uint32_t* n_layers,
+                               uint8_t* ics_flags, uint64_t flags_cap, int32_t* order,
+                               uint64_t order_cap, int64_t* n_order) {
+    if (!buf && len > 0) return fail(OSP_ERR_INVALID, "null buffer");
+    uint32_t t = 0, L = 0;
+    OSP_TRY(osp_gib_decode(buf, len, &t, &L, nullptr, 0));
+    const uint64_t base = osp_gib_encoded_size(L);
+    int64_t n = -1;  // -1: bitmap only (no side channel)
+    if (len > base) {
+        if (len < base + 4)
+            return fail(OSP_ERR_FORMAT, "gib rank order truncated: " + std::to_string(len) + " bytes");
+        const uint32_t k = get_u32le(buf + base);
+        if (k > L) return fail(OSP_ERR_FORMAT, "gib rank order longer than the layer count");
+        if (len != osp_gib_wire_size(L, k))
+            return fail(OSP_ERR_FORMAT, "gib rank order of " + std::to_string(k) + " ids needs " +
+                                            std::to_string(osp_gib_wire_size(L, k)) + " bytes, have " +
+                                            std::to_string(len));
+        n = k;
+    }
+    std::vector<uint8_t> f(L);
+    for (uint64_t l = 0; l < L; ++l) f[l] = (buf[8 + l / 8] >> (l % 8)) & 1u;
+    std::vector<uint8_t> seen(L, 0);
+    for (int64_t r = 0; r < n; ++r) {
+        const uint32_t id = get_u32le(buf + base + 4 + 4 * r);
+        if (id >= L || !f[id] || seen[id]++)
+            return fail(OSP_ERR_FORMAT, "gib rank order entry " + std::to_string(r) +
+                                            " is not a distinct deferred layer");
+    }
+    if (ics_flags && L > flags_cap) return fail(OSP_ERR_INVALID, "flags buffer too small");
+    if (order && n > 0 && static_cast<uint64_t>(n) > order_cap)
+        return fail(OSP_ERR_INVALID, "rank order buffer too small");
+    if (tag) *tag = t;
+    if (n_layers) *n_layers = L;
+    if (n_order) *n_order = n;
+    if (ics_flags) std::copy(f.begin(), f.end(), ics_flags);
+    if (order)
+        for (int64_t r = 0; r < n; ++r) order[r] = static_cast<int32_t>(get_u32le(buf + base + 4 + 4 * r));
     return OSP_OK;
 }
 
@@ -646,7 +719,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &v.exact, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.marked, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.chunk_of, L)) != OSP_OK) return cleanup(st);
-    if ((st = dalloc(g, &v.gib_bytes, osp_gib_encoded_size(L))) != OSP_OK) return cleanup(st);
+    if ((st = dalloc(g, &v.gib_bytes, osp_gib_wire_size(L, L))) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &g->d_order_tmp, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.hist, kHist)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.sched, 16)) != OSP_OK) return cleanup(st);
@@ -865,6 +938,45 @@ osp_status osp_group_read_gib(osp_group* g, uint8_t* flags, int32_t* order, int6
     if (tag) *tag = static_cast<uint32_t>(meta64[META64_TAG]);
     if (deferred) *deferred = meta64[META64_DEFERRED];
     return OSP_OK;
+}
+
+osp_status osp_group_gib_wire(osp_group* g, uint8_t* out, uint64_t cap, uint64_t* len,
+                              void* stream) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    cudaStream_t s = as_stream(stream);
+    const uint64_t L = static_cast<uint64_t>(g->v.L);
+    std::vector<uint8_t> w(osp_gib_wire_size(L, L));
+    OSP_CUDA(cudaMemcpyAsync(w.data(), g->v.gib_bytes, w.size(), cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaStreamSynchronize(s));
+    const uint64_t k = get_u32le(w.data() + osp_gib_encoded_size(L));
+    const uint64_t need = osp_gib_wire_size(L, k);
+    if (len) *len = need;
+    if (!out) return OSP_OK;
+    if (cap < need) return fail(OSP_ERR_INVALID, "gib wire buffer too small");
+    std::memcpy(out, w.data(), need);
+    return OSP_OK;
+}
+
+const uint8_t* osp_group_gib_wire_device(const osp_group* g, uint64_t* max_len) {
+    if (!g) return nullptr;
+    if (max_len) *max_len = osp_gib_wire_size(g->v.L, g->v.L);
+    return g->v.gib_bytes;
+}
+
+osp_status osp_group_set_gib_wire(osp_group* g, const uint8_t* buf, uint64_t len, void* stream) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    uint32_t tag = 0, L = 0;
+    int64_t n = 0;
+    OSP_TRY(osp_gib_wire_decode(buf, len, &tag, &L, nullptr, 0, nullptr, 0, &n));
+    if (static_cast<int>(L) != g->v.L)
+        return fail(OSP_ERR_SHAPE, "gib covers " + std::to_string(L) + " layers, the group " +
+                                       std::to_string(g->v.L));
+    std::vector<uint8_t> f(L);
+    std::vector<int32_t> ord(L);
+    OSP_TRY(osp_gib_wire_decode(buf, len, nullptr, nullptr, f.data(), L, ord.data(), L, &n));
+    // bitmap-only wire: the reference's convention for a missing order (ascending
+    // ids, split_for_sync's "missing ids appended ascending", protocol.cpp:122-166)
+    return osp_group_set_gib(g, f.data(), ord.data(), n < 0 ? 0 : n, tag, stream);
 }
 
 osp_status osp_group_stats(osp_group* g, uint64_t* resolved, uint64_t* fb_layers,

@@ -314,6 +314,15 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
         }
         g.gib_bytes[8 + byte] = v;
     }
+    // rank-order side channel after the bitmap: n u32 LE, then the deferred ids
+    // least important first (osp_gib_wire_encode's layout)
+    uint8_t* tail = g.gib_bytes + 8 + (L + 7) / 8;
+    if (tid == 0)
+        for (int i = 0; i < 4; ++i) tail[i] = (static_cast<uint32_t>(k) >> (8 * i)) & 0xff;
+    for (int r = tid; r < k; r += B) {
+        const uint32_t id = static_cast<uint32_t>(ord[r]);
+        for (int i = 0; i < 4; ++i) tail[4 + 4 * r + i] = (id >> (8 * i)) & 0xff;
+    }
 }
 
 // Exact sequential PGP of one layer (importance.cpp:20-25 order) by one warp,

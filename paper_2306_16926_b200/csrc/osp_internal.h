@@ -68,7 +68,7 @@ struct GroupView {
     double* exact;               // [L] exact sequential scores (fallback layers)
     uint8_t* marked;             // [L] needs exact score
     int* chunk_of;               // [L] compacted chunk or -1
-    uint8_t* gib_bytes;          // [8 + ceil(L/8)] encoded current GIB
+    uint8_t* gib_bytes;          // [8 + ceil(L/8) + 4 + 4L] current GIB wire: bitmap || n || rank order
     uint64_t* hist;              // [kHist] deferred bytes of the GIB with tag t at t % kHist
     int* sched;                  // [16] dynamic tile scheduler counters (SchedIdx)
     double* lscore;              // [L] per-layer tree sum of the tile partials

@@ -288,6 +288,40 @@ def gib_encode(tag: int, ics_flags) -> bytes:
     return out.tobytes()
 
 
+def gib_wire_encode(tag: int, ics_flags, order) -> bytes:
+    """GIB wire with the rank-order side channel: gib_encode bytes, then n and the
+    deferred ids least important first (include/osp_c.h, osp_gib_wire_encode)."""
+    f, fp = _u8(ics_flags)
+    o = np.ascontiguousarray(np.asarray(order, dtype=np.int32).reshape(-1))
+    op = o.ctypes.data_as(P(ctypes.c_int32)) if o.size else None
+    n = c_u64()
+    _check(lib().osp_gib_wire_encode(tag, f.size, fp, op, o.size, None, 0, ctypes.byref(n)))
+    out = np.zeros(max(n.value, 1), dtype=np.uint8)
+    _check(lib().osp_gib_wire_encode(tag, f.size, fp, op, o.size,
+                                     out.ctypes.data_as(P(ctypes.c_uint8)), out.size,
+                                     ctypes.byref(n)))
+    return out[: n.value].tobytes()
+
+
+def gib_wire_decode(buf: bytes):
+    """-> (tag, flags, order); order is None for a bitmap-only buffer."""
+    b = np.frombuffer(bytes(buf), dtype=np.uint8).copy()
+    n = b.size
+    if b.size == 0:
+        b = np.zeros(1, dtype=np.uint8)
+    bp = b.ctypes.data_as(P(ctypes.c_uint8))
+    tag, L, k = c_u32(), c_u32(), c_i64()
+    _check(lib().osp_gib_wire_decode(bp, n, ctypes.byref(tag), ctypes.byref(L), None, 0, None, 0,
+                                     ctypes.byref(k)))
+    flags = np.zeros(max(L.value, 1), dtype=np.uint8)
+    order = np.zeros(max(k.value, 1), dtype=np.int32)
+    _check(lib().osp_gib_wire_decode(bp, n, None, None, flags.ctypes.data_as(P(ctypes.c_uint8)),
+                                     flags.size, order.ctypes.data_as(P(ctypes.c_int32)),
+                                     order.size, ctypes.byref(k)))
+    return (int(tag.value), flags[: L.value].copy(),
+            None if k.value < 0 else order[: k.value].copy())
+
+
 def gib_decode(buf: bytes):
     """gib_decode (importance.cpp:99-117) -> (tag, flags)."""
     b = np.frombuffer(bytes(buf), dtype=np.uint8).copy()
@@ -486,6 +520,20 @@ class OspGroup:
     def resolve(self, deltas: torch.Tensor, stream=None):
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_resolve(self._h, p, ld, _stream(stream)))
+
+    def gib_wire(self, stream=None) -> bytes:
+        """The current GIB as a wire (bitmap + rank order), from the device."""
+        n = c_u64()
+        _check(lib().osp_group_gib_wire(self._h, None, 0, ctypes.byref(n), _stream(stream)))
+        out = np.zeros(n.value, dtype=np.uint8)
+        _check(lib().osp_group_gib_wire(self._h, out.ctypes.data_as(P(ctypes.c_uint8)), out.size,
+                                        ctypes.byref(n), _stream(stream)))
+        return out.tobytes()
+
+    def set_gib_wire(self, buf: bytes, stream=None):
+        b = np.frombuffer(bytes(buf), dtype=np.uint8).copy()
+        _check(lib().osp_group_set_gib_wire(self._h, b.ctypes.data_as(P(ctypes.c_uint8)), b.size,
+                                            _stream(stream)))
 
     def stage2_resolve(self, deltas: torch.Tensor, stream=None):
         """stage2_all + resolve (overlapped with the ICS carry)."""

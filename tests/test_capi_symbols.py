@@ -49,6 +49,44 @@ def test_host_only_entry_points_without_gpu():
     assert out.value == 15_625_000
 
 
+def test_gib_wire_with_rank_order_without_gpu():
+    """GIB + rank-order side channel (README.md:207-210's gap): bitmap prefix is
+    the reference encoding (read by the reference decoder, here its restatement
+    in oracle/), the tail carries the emission order; malformed tails fail."""
+    import struct
+
+    import numpy as np
+
+    from oracle import oracle
+    from paper_2306_16926_b200 import osp
+    L = 1000
+    flags = np.zeros(L, np.uint8)
+    order = np.array([977, 3, 500, 4, 999], np.int32)
+    flags[order] = 1
+    w = osp.gib_wire_encode(12, flags, order)
+    assert len(w) == 133 + 4 + 4 * 5
+    assert w[:133] == osp.gib_encode(12, flags) == oracle.gib_encode(12, flags)
+    assert w[133:] == struct.pack("<I5I", 5, *order.tolist())
+    tag, f2 = oracle.gib_decode(w)  # the reference decoder reads the bitmap prefix
+    assert tag == 12 and np.array_equal(f2, flags)
+    tag, f3, o3 = osp.gib_wire_decode(w)
+    assert tag == 12 and np.array_equal(f3, flags) and np.array_equal(o3, order)
+    tag, f4, o4 = osp.gib_wire_decode(w[:133])
+    assert o4 is None and np.array_equal(f4, flags)
+    e = osp.gib_wire_encode(0, np.zeros(9, np.uint8), [])
+    assert osp.gib_wire_decode(e)[2].size == 0
+    for bad in (w[:135], w[:-1], w + b"\0", w[:137] + struct.pack("<I", 1000) + w[141:],
+                w[:137] + struct.pack("<I", 5) + w[141:], w[:133] + struct.pack("<I", 2000)):
+        with pytest.raises(osp.FormatError):
+            osp.gib_wire_decode(bad)
+    with pytest.raises(osp.LayerError):
+        osp.gib_wire_encode(1, flags, [1000])
+    with pytest.raises(osp.ProtocolError):
+        osp.gib_wire_encode(1, flags, [5])        # not deferred
+    with pytest.raises(osp.ProtocolError):
+        osp.gib_wire_encode(1, flags, [3, 3])     # repeated
+
+
 def test_python_front_errors_without_gpu():
     pytest.importorskip("torch")
     from paper_2306_16926_b200 import osp

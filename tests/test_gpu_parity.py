@@ -3,6 +3,8 @@ reference-engine goldens. Bit-exact for everything: masks, index lists, chunk
 maps, GIB bytes, aggregated/updated fp32 vectors. The only non-bit-exact
 quantity is the group's per-layer PGP score (a parallel tree sum, documented
 tolerance 1e-12 relative; the ranking built from it is certified exact)."""
+import struct
+
 import numpy as np
 import pytest
 import torch
@@ -235,6 +237,10 @@ def run_group_against_golden(osp, g: Golden, tile_elems=0, pad_ld=0, tma=None, c
         assert nxt["tag"] == tag_out == it + 1
         assert np.array_equal(nxt["flags"], flags_out), f"GIB flags, it {it}"
         assert np.array_equal(nxt["order"], g.get(it, "order_out")), f"ICS order, it {it}"
+        # the device-written wire: the reference's GIB bytes + the rank order
+        order_out = np.asarray(g.get(it, "order_out"), dtype="<u4")
+        assert grp.gib_wire() == (bytes(g.get(it, "gib_out")) + struct.pack("<I", order_out.size)
+                                  + order_out.tobytes()), f"GIB wire, it {it}"
     return grp
 
 
@@ -394,6 +400,33 @@ def test_certificate_fallback_on_deferred_layers(osp, carry):
     assert deferred_tie
     st = grp.stats()
     assert st["fallback_resolves"] == 3
+
+
+def test_gib_wire_installs_like_set_gib(osp):
+    """A wire read from one group and installed into another reproduces the
+    GIB, rank order and chunk map; a bitmap-only wire installs ascending ids."""
+    from paper_2306_16926_b200 import layouts
+    counts = layouts.resnet50()[:40]
+    M, N = sum(counts), 4
+    part = osp.Partition(counts)
+    a = osp.OspGroup(part, N, [0.25] * N, n_chunks=3)
+    b = osp.OspGroup(part, N, [0.25] * N, n_chunks=3)
+    for it in range(3):
+        a.set_budget(M * 2)
+        a.step(osp.synth_deltas(3, N, it, M))
+    w = a.gib_wire()
+    ra = a.read_gib()
+    assert w == osp.gib_wire_encode(ra["tag"], ra["flags"], ra["order"])
+    b.set_gib_wire(w)
+    rb = b.read_gib()
+    for k in ("tag", "flags", "order", "chunk_of", "n_used"):
+        assert np.array_equal(np.asarray(ra[k]), np.asarray(rb[k])), k
+    assert b.gib_wire() == w
+    b.set_gib_wire(w[: osp.lib().osp_gib_encoded_size(len(counts))])
+    rb = b.read_gib()
+    assert np.array_equal(rb["order"], np.flatnonzero(ra["flags"]))
+    with pytest.raises(osp.ShapeError):
+        osp.OspGroup(osp.Partition(counts[:5]), N).set_gib_wire(w)
 
 
 def test_step_host_matches_device_step(osp):
