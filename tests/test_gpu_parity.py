@@ -402,6 +402,41 @@ def test_certificate_fallback_on_deferred_layers(osp, carry):
     assert st["fallback_resolves"] == 3
 
 
+@pytest.mark.parametrize("carry", [True, False])
+def test_group_step_captured_in_cuda_graph(osp, carry):
+    """The step has no host sync and fixed arguments, so it can be captured in
+    a CUDA graph (programmatic-dependent launches become graph edges, incl. the
+    carry's resolve-beside-stage-2 join); replays equal direct steps bit for bit."""
+    from paper_2306_16926_b200 import layouts
+    counts = layouts.resnet50()[:60]
+    M, N = sum(counts), 8
+    part = osp.Partition(counts)
+    X = [osp.synth_deltas(11, N, i, M) for i in range(2)]
+    a = osp.OspGroup(part, N, n_chunks=4, carry=carry)
+    b = osp.OspGroup(part, N, n_chunks=4, carry=carry)
+    for grp in (a, b):
+        grp.set_budget(M * 2)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(graph, stream=cs, capture_error_mode="thread_local"):
+        b.step(X[0])
+        b.step(X[1])
+    torch.cuda.synchronize()
+    assert b.read_gib()["tag"] == 0  # capture launches nothing
+    for r in range(3):
+        a.step(X[0])
+        a.step(X[1])
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(a.global_params), bits(b.global_params)), f"replay {r}"
+        assert np.array_equal(bits(a.worker_params), bits(b.worker_params)), f"replay {r}"
+        ra, rb = a.read_gib(), b.read_gib()
+        assert ra["tag"] == rb["tag"] == 2 * (r + 1)
+        assert np.array_equal(ra["order"], rb["order"]) and np.array_equal(ra["flags"], rb["flags"])
+
+
 def test_gib_wire_installs_like_set_gib(osp):
     """A wire read from one group and installed into another reproduces the
     GIB, rank order and chunk map; a bitmap-only wire installs ascending ids."""

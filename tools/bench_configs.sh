@@ -6,7 +6,7 @@ mkdir -p gpurun_out
 out=gpurun_out/bench_configs.jsonl
 : > $out
 run() { timeout 900 python bench.py "$@" 2>gpurun_out/bench_err.log | tail -1 >> $out || echo "{\"failed\": \"$*\"}" >> $out; }
-run --layout mlp --budget-frac 0.5 --cpu-iters 20 --steps 2000 --e2e-steps 20
+run --layout mlp --budget-frac 0.5 --cpu-iters 20 --steps 2000 --e2e-steps 20 --graph
 run --layout resnet50 --budget-frac 0.5 --cpu-iters 3
 run --layout resnet152 --budget-frac 0.5 --cpu-iters 2
 run --layout vgg16 --budget-frac 0.5 --cpu-iters 1 --steps 100
