@@ -137,6 +137,20 @@ class ClockSampler:
 
 # ---- CPU baseline (reference engine on the host) ---------------------------------
 
+def host_cpu():
+    """CPU model and logical core count of this host (for the cpu_baseline line)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def run_reference_cpu(layout: str, workers: int, budget_frac: float, chunks: int, seed: int,
                       iters: int, warmup: int, threads: int):
     """Time the UNMODIFIED reference engine (oracle/_ref/ref_driver) on host cores."""
@@ -204,7 +218,8 @@ def reference_arm(args, rank: int):
                        "chunks": args.chunks, "deltas": "reference synth generator, seed "
                        f"{args.seed} (generated outside the timed region)",
                        "parallelism": "host threads (reference CPU engine)"},
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": dict({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                                 **host_cpu()),
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "cpu_steps_timed": k_run, "cpu_warmup_run": w_run,
@@ -303,6 +318,13 @@ def b200_single(args):
     for k in range(KB + 1):
         step(args.warmup + K + k, evb[k], full=True)
     torch.cuda.synchronize()
+    # per-step times in the timed region (stage-1 start to the next stage-1 start)
+    if graph is None and K > 1:
+        per = sorted(evs[k][0].elapsed_time(evs[k + 1][0]) for k in range(K - 1))
+        step_pct = {"p50_ms": per[len(per) // 2], "p90_ms": per[min(len(per) - 1, int(0.9 * len(per)))],
+                    "n": len(per)}
+    else:
+        step_pct = None
     # the same step replayed from a CUDA graph (separate pass, not the headline:
     # a replay carries no stage-1 events for the roofline)
     graph_pass = None
@@ -429,6 +451,7 @@ def b200_single(args):
         "gpu_launches": launches_per_step * K,
         "certificate": stats,
         "graph": graph_pass,
+        "step_ms_percentiles": step_pct,
         "clocks": clk,
         "overlap": ovl,
     }
@@ -437,6 +460,7 @@ def b200_single(args):
             cb = run_reference_cpu(args.layout, N, args.budget_frac, args.chunks, args.seed,
                                    args.cpu_iters, 1, 1)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"].update(host_cpu())
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"error": str(e)[:200]}
     print(json.dumps(line), flush=True)

@@ -24,8 +24,17 @@ def run(args, metric: str, unit: str):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    # OSP_BENCH_OVERSUB=1: more ranks than GPUs (ranks share devices, gloo for the
+    # host-side barrier / max-over-ranks): exercises the P-rank code path on a
+    # smaller box; its timings are meaningless and the line says so
+    oversub = os.environ.get("OSP_BENCH_OVERSUB") == "1"
+    if oversub:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     counts = layouts.get(args.layout)
     N, M, L = args.workers, sum(counts), len(counts)
     model_bytes = 4 * M
@@ -207,6 +216,9 @@ def run(args, metric: str, unit: str):
                                  else ((3 + 2 * args.chunks) if args.per_chunk else 4)),
             "clocks": clk,
         }
+        if oversub:
+            line["oversubscribed"] = (f"{world} ranks on {torch.cuda.device_count()} GPUs: "
+                                      "code-path check, timings not meaningful")
         print(json.dumps(line), flush=True)
     dist.barrier()
     sh.close()
