@@ -16,8 +16,8 @@ import torch.distributed as dist
 
 from . import _capi
 from ._capi import P, c_dbl, c_u64, c_void_p
-from .osp import (ConfigError, OspGroup, Partition, _check, _dev_f32, _ptr, _stream, _view,
-                  lib)
+from .osp import (ConfigError, OspGroup, Partition, _check, _dev_f32, _Handle, _ptr, _stream,
+                  _view, lib)
 
 
 class ShardGroup:
@@ -48,13 +48,15 @@ class ShardGroup:
         _check(lib().osp_shard_create(part.handle, ctypes.byref(cfg), init, _stream(stream),
                                       ctypes.byref(h)))
         self._h = h
-        self.local = OspGroup._borrow(lib().osp_shard_group(h), part, self.n_loc, n_chunks, self)
+        self._hnd = _Handle(h, "osp_shard_destroy")
+        self.local = OspGroup._borrow(lib().osp_shard_group(h), part, self.n_loc, n_chunks,
+                                      self._hnd)
         ld = c_u64()
         self._x = []
         for b in range(2):
             ptr = lib().osp_shard_deltas(h, b, ctypes.byref(ld))
             self._x.append(_view(ptr, (self.n_loc, self.M), "<f4", strides=(int(ld.value) * 4, 4),
-                                 owner=self))
+                                 owner=self._hnd))
         self.ldX = int(ld.value)
 
     def export_handle(self) -> bytes:
@@ -132,11 +134,11 @@ class ShardGroup:
         return self.local.read_gib()
 
     def close(self):
-        h = getattr(self, "_h", None)
-        if h and _capi._lib is not None:
-            self.local._h = None
-            _capi._lib.osp_shard_destroy(h)
+        """Destroy now (views must not be used afterwards); otherwise the handle
+        goes with the last of this object, its local group and their views."""
+        hnd = getattr(self, "_hnd", None)
+        if hnd is not None:
+            if getattr(self, "local", None) is not None:
+                self.local._h = None
+            hnd.close()
         self._h = None
-
-    def __del__(self):
-        self.close()

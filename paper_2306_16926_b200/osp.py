@@ -104,6 +104,26 @@ class _DevArray:
         self._owner = owner
 
 
+class _Handle:
+    """Owns one library handle. Zero-copy views reference this holder, not the
+    Python wrapper: a view's storage keeps its owner alive from C, where the
+    garbage collector cannot see it, so a wrapper <-> view cycle would never be
+    collected (and the device memory never freed)."""
+
+    __slots__ = ("h", "_destroy", "_parent")
+
+    def __init__(self, h, destroy: Optional[str] = None, parent=None):
+        self.h, self._destroy, self._parent = h, destroy, parent
+
+    def close(self):
+        h, self.h = self.h, None
+        if h and self._destroy is not None and _capi._lib is not None:
+            getattr(_capi._lib, self._destroy)(h)
+
+    def __del__(self):
+        self.close()
+
+
 def _view(ptr, shape, typestr, strides=None, owner=None) -> torch.Tensor:
     return torch.as_tensor(_DevArray(ptr, shape, typestr, strides, owner), device="cuda")
 
@@ -450,6 +470,7 @@ class OspGroup:
         _check(lib().osp_group_create(part.handle, ctypes.byref(cfg), init or None,
                                       _stream(stream), ctypes.byref(h)))
         self._owned = True
+        self._hnd = _Handle(h, "osp_group_destroy")
         self._attach(h)
 
     @classmethod
@@ -459,7 +480,7 @@ class OspGroup:
         self.part, self.N, self.n_chunks = part, n_workers, n_chunks
         self.M, self.L = part.total_count(), part.layer_count()
         self._owned = False
-        self._parent = owner
+        self._hnd = _Handle(c_void_p(handle), None, parent=owner)  # owner: the shard's _Handle
         self._attach(c_void_p(handle))
         return self
 
@@ -468,9 +489,10 @@ class OspGroup:
         ld = c_u64()
         pp = lib().osp_group_worker_params(h, ctypes.byref(ld))
         self.ldP = int(ld.value)
-        self._g = _view(lib().osp_group_global(h), (self.M,), "<f4", owner=self)
-        self._p = _view(pp, (self.N, self.M), "<f4", strides=(self.ldP * 4, 4), owner=self)
-        self._scores = _view(lib().osp_group_scores(h), (self.L,), "<f8", owner=self)
+        o = self._hnd
+        self._g = _view(lib().osp_group_global(h), (self.M,), "<f4", owner=o)
+        self._p = _view(pp, (self.N, self.M), "<f4", strides=(self.ldP * 4, 4), owner=o)
+        self._scores = _view(lib().osp_group_scores(h), (self.L,), "<f8", owner=o)
 
     # state views (device, zero-copy)
     @property
@@ -600,10 +622,9 @@ class OspGroup:
         return "tma-staged" if f & _capi.GROUP_TMA else "register-staged"
 
     def close(self):
-        h = getattr(self, "_h", None)
-        if h and getattr(self, "_owned", True) and _capi._lib is not None:
-            _capi._lib.osp_group_destroy(h)
+        """Destroy now (views taken from this group must not be used afterwards);
+        otherwise the handle goes when the group and its views are gone."""
+        hnd = getattr(self, "_hnd", None)
+        if hnd is not None and getattr(self, "_owned", True):
+            hnd.close()
         self._h = None
-
-    def __del__(self):
-        self.close()

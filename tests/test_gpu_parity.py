@@ -437,6 +437,34 @@ def test_group_step_captured_in_cuda_graph(osp, carry):
         assert np.array_equal(ra["order"], rb["order"]) and np.array_equal(ra["flags"], rb["flags"])
 
 
+def test_group_device_memory_released_without_gc(osp):
+    """Dropping a group (and its zero-copy views) frees its device memory at
+    once: the views keep a handle holder alive, not the group, so there is no
+    reference cycle for the garbage collector to find."""
+    import gc
+    gc.disable()
+    try:
+        part = osp.Partition([1 << 22] * 16)  # 67 M params: ~2.5 GB per group
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        for _ in range(4):
+            g = osp.OspGroup(part, 8)
+            v = g.worker_params
+            g.step(osp.synth_deltas(1, 8, 0, part.total_count()))
+            torch.cuda.synchronize()
+            del g, v
+        torch.cuda.empty_cache()
+        free1 = torch.cuda.mem_get_info()[0]
+        assert free0 - free1 < (256 << 20), (free0, free1)
+        g = osp.OspGroup(part, 8)
+        v = g.global_params
+        del g                     # the view alone keeps the group's memory valid
+        assert float(v.sum()) == 0.0
+        del v
+    finally:
+        gc.enable()
+
+
 def test_gib_wire_installs_like_set_gib(osp):
     """A wire read from one group and installed into another reproduces the
     GIB, rank order and chunk map; a bitmap-only wire installs ascending ids."""
