@@ -46,6 +46,10 @@ def parse():
     ap.add_argument("--graph", action="store_true",
                     help="capture two steps (both delta sets) in a CUDA graph and time replays "
                          "(launch-bound layouts such as the MLP of config #1)")
+    ap.add_argument("--sgd-lr", type=float, default=0.0,
+                    help="> 0: the inputs are gradients, sgd_delta fused into the stage kernels")
+    ap.add_argument("--momentum", type=float, default=0.0,
+                    help="heavy-ball momentum on the gradients (extension; needs --sgd-lr)")
     ap.add_argument("--no-graph-pass", action="store_true",
                     help="skip the extra CUDA-graph replay pass reported under 'graph'")
     ap.add_argument("--no-carry", action="store_true",
@@ -244,7 +248,9 @@ def b200_single(args):
     part = osp.Partition(counts)
     grp = osp.OspGroup(part, N, [1.0 / N] * N, n_chunks=args.chunks, tile_elems=args.tile,
                        tma={"auto": None, "tma": True, "register": False}[args.stage_kernels],
-                       carry=not args.no_carry)
+                       carry=not args.no_carry, sgd_lr=args.sgd_lr)
+    if args.momentum > 0:
+        grp.set_momentum(args.momentum)
     carry = not (osp.lib().osp_group_flags(grp._h) & 4)
     X = [osp.synth_deltas(args.seed, N, i, M) for i in range(2)]
     grp.set_budget(budget)
@@ -367,8 +373,11 @@ def b200_single(args):
     # N worker rows + G on RS written), stage 2 = 4M u (2N+1) (N rows + G re-read,
     # G + N rows written). With the ICS carry stage 1 also writes C on ICS
     # (4M(2N+2)) and stage 2 reads C once and writes G + N rows (4M u (N+2)).
-    b_s1 = [4.0 * M * ((2 * N + 2) - (0.0 if carry else uk)) for uk in u]
-    b_step = [4.0 * M * ((2 * N + 2) + uk * ((N + 2) if carry else (2 * N + 1))) for uk in u]
+    # momentum adds the velocity rows, read and written once in stage 1 (4M * 2N)
+    mom_b = 4.0 * M * 2 * N if args.momentum > 0 else 0.0
+    b_s1 = [4.0 * M * ((2 * N + 2) - (0.0 if carry else uk)) + mom_b for uk in u]
+    b_step = [4.0 * M * ((2 * N + 2) + uk * ((N + 2) if carry else (2 * N + 1))) + mom_b
+              for uk in u]
     b_survey = [4.0 * M * ((2 * N + 2) + uk * (2 * N + 1)) for uk in u]
     s1_avg = sum(s1) / len(s1)
     ach_s1 = (sum(b_s1) / K) / (s1_avg * 1e-3) / 1e9
@@ -420,6 +429,8 @@ def b200_single(args):
                       f"{2 * N * M * 4 / 1e6:.3f} MB, L2-resident: launch-bound case)"),
                    "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU",
                    "stage_kernels": grp.stage_kernels, "ics_carry": carry,
+                   "inputs": (f"gradients, sgd_delta lr {args.sgd_lr}" if args.sgd_lr > 0 else "deltas")
+                   + (f", momentum {args.momentum}" if args.momentum > 0 else ""),
                    "launch": "CUDA graph (2 steps per replay)" if graph is not None else "stream"},
         "hbm_gbs_step": ach_step,
         "roofline": {"bound": "hbm",

@@ -280,6 +280,14 @@ osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, voi
 /* stage1 + stage2_all (two launches; a single-launch variant with per-tile
  * dependency flags measured slower, profiles/r1_ncu_summary.md). */
 osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void* stream);
+/* Heavy-ball momentum on gradient inputs (extension beyond the reference, whose
+ * learner is plain SGD, learner.cpp:391-403; parity of mu > 0 is pinned to the
+ * oracle fed with deltas from the same rule, not to a reference run): per worker
+ * v <- fl(fl(mu*v) + g), delta = sgd_delta(v) = float(-lr*(double)v), fused into
+ * stage 1 (the velocity rows [N][M] are read and written once per step).
+ * mu = 0 returns to plain sgd_delta (bit-identical). Needs sgd_lr > 0
+ * (ConfigError) and the TMA family (OSP_ERR_INVALID); velocities start at 0. */
+osp_status osp_group_set_momentum(osp_group* g, double mu, void* stream);
 /* stage2_all + resolve, same results. With the ICS carry the resolve needs
  * nothing from stage 2 (every PGP partial is published by stage 1), so it is
  * launched first and the stage-2 broadcast runs beside it, reading a stage-1

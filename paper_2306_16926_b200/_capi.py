@@ -113,6 +113,7 @@ _SIGS = {
     "osp_group_step": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_stages": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_stage2_resolve": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
+    "osp_group_set_momentum": (c_int, [c_void_p, c_dbl, c_void_p]),
     "osp_group_step_host": (c_int, [c_void_p, c_void_p, c_u64, P(ctypes.c_uint8), c_void_p]),
     "osp_group_global": (c_void_p, [c_void_p]),
     "osp_group_worker_params": (c_void_p, [c_void_p, P(c_u64)]),

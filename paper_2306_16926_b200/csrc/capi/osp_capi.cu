@@ -846,6 +846,7 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (chunk < 0 || chunk >= g->n_chunks) return fail(OSP_ERR_INVALID, "chunk out of range");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    if (g->v.V) deltas = g->v.V, ld = g->v.ldP;  // momentum: stage 1 left v' there
     if (g->tma) OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, chunk, chunk + 1, as_stream(stream)));
     else OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, chunk + 1, g->grid, as_stream(stream)));
     return OSP_OK;
@@ -854,6 +855,7 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
 osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    if (g->v.V) deltas = g->v.V, ld = g->v.ldP;
     if (g->tma) OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, 0, g->n_chunks, as_stream(stream)));
     else OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, 0, g->n_chunks, g->grid, as_stream(stream)));
     return OSP_OK;
@@ -861,7 +863,34 @@ osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, 
 
 osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
+    if (g->v.V) deltas = g->v.V, ld = g->v.ldP;  // the exact fallback re-aggregates v'
     OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, as_stream(stream)));
+    return OSP_OK;
+}
+
+osp_status osp_group_set_momentum(osp_group* g, double mu, void* stream) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    if (!(mu >= 0.0 && mu < 1.0)) return fail(OSP_ERR_CONFIG, "momentum must be in [0, 1)");
+    cudaStream_t s = as_stream(stream);
+    if (mu == 0.0) {  // plain sgd_delta (bit-identical to a group that never had momentum)
+        if (g->v.V) {
+            OSP_CUDA(cudaStreamSynchronize(s));
+            auto it = std::find(g->owned.begin(), g->owned.end(), static_cast<void*>(g->v.V));
+            if (it != g->owned.end()) g->owned.erase(it);
+            cudaFree(g->v.V);
+        }
+        g->v.V = nullptr;
+        g->v.mu = 0.0f;
+        return OSP_OK;
+    }
+    if (!(g->sgd_lr > 0)) return fail(OSP_ERR_CONFIG, "momentum needs gradient inputs (sgd_lr > 0)");
+    if (!g->tma) return fail(OSP_ERR_INVALID, "momentum needs the TMA-staged stage kernels");
+    if (!g->v.V) {
+        osp_status st = dalloc(g, &g->v.V, g->v.ldP * g->N);
+        if (st != OSP_OK) return st;
+        OSP_CUDA(cudaMemsetAsync(g->v.V, 0, g->v.ldP * g->N * 4, s));
+    }
+    g->v.mu = static_cast<float>(mu);
     return OSP_OK;
 }
 
@@ -880,6 +909,7 @@ osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t 
     // carry: every tile partial is known after stage 1, so the resolve goes
     // first and the stage-2 broadcast runs beside it (joined before it retires)
     cudaStream_t s = as_stream(stream);
+    if (g->v.V) deltas = g->v.V, ld = g->v.ldP;
     OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, s));
     OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, 0, g->n_chunks, s, 1));
     return OSP_OK;

@@ -71,6 +71,24 @@ __device__ void tab_seq(const TileTab& tab, int u, int& l, int& k) {
 
 // ---- consumer bodies ----------------------------------------------------------
 
+// Stage-1 momentum (g.V set): v' = mu*v + grad per element (separately rounded
+// fp32 mul and add), stored back; the step then uses v' as the gradient.
+__device__ __forceinline__ float4 momentum4(const GroupView& g, int w, uint64_t f, float4 x) {
+    float4* vp = reinterpret_cast<float4*>(g.V + static_cast<uint64_t>(w) * g.ldP + f);
+    const float4 v = *vp;
+    const float4 vn = make_float4(__fadd_rn(__fmul_rn(g.mu, v.x), x.x), __fadd_rn(__fmul_rn(g.mu, v.y), x.y),
+                                  __fadd_rn(__fmul_rn(g.mu, v.z), x.z), __fadd_rn(__fmul_rn(g.mu, v.w), x.w));
+    *vp = vn;
+    return vn;
+}
+
+__device__ __forceinline__ float momentum1(const GroupView& g, int w, uint64_t f, float x) {
+    float* vp = g.V + static_cast<uint64_t>(w) * g.ldP + f;
+    const float vn = __fadd_rn(__fmul_rn(g.mu, *vp), x);
+    *vp = vn;
+    return vn;
+}
+
 template <int NS>
 __device__ __forceinline__ void consume_agg_quad(const GroupView& g, const AggParams& ap,
                                                  const float4* xs, float4 go, uint64_t f,
@@ -175,7 +193,7 @@ __device__ __forceinline__ void consume_bcast_quad(const GroupView& g, float4 gn
 // Unstaged tile (unaligned layer): per-element from global memory.
 template <int NS, int CW>
 __device__ void consume_direct(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
-                               const StageMeta& m, int ctid, double& acc) {
+                               const StageMeta& m, int ctid, double& acc, bool mom) {
     for (uint64_t f = m.s + ctid; f < m.e; f += CW * 32) {
         if (m.kind == 2) {
             const float gn = g.C[f];
@@ -186,6 +204,7 @@ __device__ void consume_direct(const GroupView& g, const AggParams& ap, const fl
             double s = 0.0;
             for (int w = 0; w < NS; ++w) {
                 float x = X[static_cast<uint64_t>(w) * ldX + f];
+                if (mom) x = momentum1(g, w, f, x);
                 if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
                 g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
                 s = agg_acc(s, ap.w[w], x);
@@ -200,6 +219,7 @@ __device__ void consume_direct(const GroupView& g, const AggParams& ap, const fl
             double s = 0.0;
             for (int w = 0; w < NS; ++w) {
                 float x = X[static_cast<uint64_t>(w) * ldX + f];
+                if (mom) x = momentum1(g, w, f, x);
                 if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
                 s = agg_acc(s, ap.w[w], x);
             }
@@ -215,7 +235,7 @@ __device__ void consume_direct(const GroupView& g, const AggParams& ap, const fl
 // STAGE 1: all tiles (RS aggregate / ICS local estimate, + the ICS carry when
 // g.C is set); STAGE 2: ICS chunks [c0, c1) from the deltas; STAGE 3: ICS
 // chunks [c0, c1) from the carry (one staged row per tile instead of N + 1).
-template <int NS, int STAGE, int CW, int kStages>
+template <int NS, int STAGE, int CW, int kStages, bool MOM>
 __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggParams ap,
                                                            const float* __restrict__ X,
                                                            uint64_t ldX, int c0, int c1, int ovl) {
@@ -428,12 +448,16 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                     xs[w] = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(w) * T + 4 * q);
                 const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(NS) * T + 4 * q);
                 const uint64_t f = m.s + 4ull * q;
+                if (MOM) {
+#pragma unroll
+                    for (int w = 0; w < NS; ++w) xs[w] = momentum4(g, w, f, xs[w]);
+                }
                 if (m.kind == 0) consume_agg_quad<NS>(g, ap, xs, go, f, acc);
                 else if (g.C) consume_split_quad<NS>(g, ap, xs, go, f, acc);
                 else consume_local_quad<NS>(g, ap, xs, go, f);
             }
         } else {
-            consume_direct<NS, CW>(g, ap, X, ldX, m, ctid, acc);
+            consume_direct<NS, CW>(g, ap, X, ldX, m, ctid, acc, MOM);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
@@ -459,7 +483,13 @@ template <int STAGE, int NS, int CW, int KS>
 cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int c0, int c1, int ovl, cudaStream_t s) {
     const size_t sm = tma_smem_bytes(STAGE == 3 ? 1 : NS + 1, g.T, g.L, CW, KS);
-    auto kern = k_stage_tma<NS, STAGE, CW, KS>;
+    // momentum is a separate stage-1 instantiation: its velocity traffic would
+    // otherwise cost the default kernel registers (and a CTA per SM)
+    void (*kern)(GroupView, AggParams, const float*, uint64_t, int, int, int) =
+        k_stage_tma<NS, STAGE, CW, KS, false>;
+    if constexpr (STAGE == 1) {
+        if (g.V) kern = k_stage_tma<NS, STAGE, CW, KS, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sm));

@@ -86,6 +86,11 @@ struct GroupView {
     // chunks, [1] the resolve epoch stage 2 joins on, [4..] chunk_begin
     // [n_chunks+1], ics_layers [L], ics_tile_prefix [L+1]. Null without carry.
     int* snap;
+    // Heavy-ball momentum on the gradient inputs (extension, TMA family, sgd only):
+    // per worker v <- mu*v + g (fp32, no FMA) in stage 1, delta = sgd_delta(v).
+    // V [N][ldP] holds the updated velocities after stage 1. Null = plain SGD.
+    float* V;
+    float mu;
     // resolve's per-layer sums are split into items of <= kSumChunk tiles so a
     // huge layer is summed by many blocks (fixed order: items ascending)
     const int* sum_items;        // [n_sum_items][3] layer, first tile, end tile

@@ -557,6 +557,11 @@ class OspGroup:
         _check(lib().osp_group_set_gib_wire(self._h, b.ctypes.data_as(P(ctypes.c_uint8)), b.size,
                                             _stream(stream)))
 
+    def set_momentum(self, mu: float, stream=None):
+        """Heavy-ball momentum on gradient inputs, fused into stage 1 (extension;
+        include/osp_c.h osp_group_set_momentum)."""
+        _check(lib().osp_group_set_momentum(self._h, float(mu), _stream(stream)))
+
     def stage2_resolve(self, deltas: torch.Tensor, stream=None):
         """stage2_all + resolve (overlapped with the ICS carry)."""
         p, ld = self._deltas(deltas)

@@ -437,6 +437,58 @@ def test_group_step_captured_in_cuda_graph(osp, carry):
         assert np.array_equal(ra["order"], rb["order"]) and np.array_equal(ra["flags"], rb["flags"])
 
 
+@pytest.mark.parametrize("carry", [True, False])
+def test_momentum_matches_oracle_on_momentum_deltas(osp, carry):
+    """Momentum (extension): v <- fl(fl(mu*v) + g), delta = sgd_delta(v), fused
+    into stage 1. Pinned to the oracle step fed with deltas from the same rule
+    restated in numpy (fp32 multiply then add, as in the kernel); mu = 0 is the
+    plain sgd_delta path bit for bit."""
+    rng = np.random.default_rng(17)
+    counts = [int(c) for c in rng.integers(1, 7000, 23)] + [4096, 8192, 12]
+    M, N, lr, mu = sum(counts), 4, 0.05, 0.9
+    part = osp.Partition(counts)
+    grp = osp.OspGroup(part, N, [0.25] * N, n_chunks=3, sgd_lr=lr, carry=carry)
+    plain = osp.OspGroup(part, N, [0.25] * N, n_chunks=3, sgd_lr=lr, carry=carry)
+    grp.set_momentum(mu)
+    plain.set_momentum(0.0)
+    G = np.zeros(M, np.float32)
+    Pw = np.zeros((N, M), np.float32)
+    V = np.zeros((N, M), np.float32)
+    flags, order = np.zeros(len(counts), np.uint8), np.zeros(0, np.int32)
+    budget = int(0.5 * M * 4)
+    X = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    for it in range(4):
+        osp.synth_deltas(41, N, it, M, out=X)
+        X.mul_(29.0)  # gradients
+        g = X.cpu().numpy()
+        V = (np.float32(mu) * V).astype(np.float32) + g          # fp32 mul, then fp32 add
+        deltas = np.stack([oracle.sgd_delta(V[w], lr) for w in range(N)])
+        r = oracle.step(counts, 4, [0.25] * N, deltas, G, Pw, flags, order, 3, budget)
+        for grp_ in (grp, plain):
+            grp_.set_budget(budget)
+            grp_.step(X)
+        assert np.array_equal(bits(grp.global_params), bits(G)), f"global, it {it}"
+        assert np.array_equal(bits(grp.worker_params), bits(Pw)), f"workers, it {it}"
+        nxt = grp.read_gib()
+        assert np.array_equal(nxt["flags"], r["flags_out"]) and np.array_equal(nxt["order"], r["order_out"])
+        flags, order = r["flags_out"], r["order_out"]
+    # mu = 0: the group that never had momentum and one that turned it off agree
+    ref0 = osp.OspGroup(part, N, [0.25] * N, n_chunks=3, sgd_lr=lr, carry=carry)
+    for it in range(4):
+        osp.synth_deltas(41, N, it, M, out=X)
+        X.mul_(29.0)
+        ref0.set_budget(budget)
+        ref0.step(X)
+    assert np.array_equal(bits(ref0.global_params), bits(plain.global_params))
+    assert np.array_equal(bits(ref0.worker_params), bits(plain.worker_params))
+    with pytest.raises(osp.ConfigError):
+        osp.OspGroup(part, N, [0.25] * N).set_momentum(0.9)       # deltas, not gradients
+    with pytest.raises(osp.ConfigError):
+        grp.set_momentum(1.5)
+    with pytest.raises(osp.InvalidArgument):
+        osp.OspGroup(part, N, [0.25] * N, sgd_lr=lr, tma=False).set_momentum(0.9)
+
+
 def test_group_device_memory_released_without_gc(osp):
     """Dropping a group (and its zero-copy views) frees its device memory at
     once: the views keep a handle holder alive, not the group, so there is no
