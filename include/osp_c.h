@@ -398,6 +398,12 @@ osp_status osp_shard_step(osp_shard* s, int buf, void* stream);
  * stage-1 apply fused with the stage-2 aggregate, stage-2 apply, resolve (each
  * including its in-kernel cross-GPU wait). Unused entries are 0. */
 osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream);
+/* Diagnostics: this rank's part of a stage's push/pull (k_shard_agg: peers'
+ * rows over NVLink, fixed-order aggregate, stores into every rank) launched
+ * alone, without the cross-GPU ordering, so a profiler that serialises kernels
+ * (ncu) can replay it. The peers must be idle with their rows in place; the
+ * results are those of a normal stage only if nothing else runs. */
+osp_status osp_shard_solo_agg(osp_shard* s, int stage, int buf, void* stream);
 /* 1 if the shard runs the streaming kernels, 0 for barrier mode. */
 int osp_shard_streaming(const osp_shard* s);
 /* ProtocolError if a cross-GPU wait timed out (synchronises `stream`). */

@@ -139,6 +139,7 @@ _SIGS = {
     "osp_shard_check": (c_int, [c_void_p, c_void_p]),
     "osp_shard_streaming": (c_int, [c_void_p]),
     "osp_shard_profile": (c_int, [c_void_p, c_int, P(ctypes.c_float), c_void_p]),
+    "osp_shard_solo_agg": (c_int, [c_void_p, c_int, c_int, c_void_p]),
     "osp_synth_deltas_range": (c_int, [c_u64, c_int, c_int, c_u64, c_u64, c_void_p, c_u64,
                                        c_void_p]),
 }

@@ -397,6 +397,15 @@ osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
     return osp_shard_resolve(s, buf, stream);
 }
 
+osp_status osp_shard_solo_agg(osp_shard* s, int stage, int buf, void* stream) {
+    OSP_TRY(check_ready(s, buf));
+    if (stage != 1 && stage != 2) return fail(OSP_ERR_INVALID, "stage must be 1 or 2");
+    osp_group* g = s->grp;
+    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], stage, 0, s->n_chunks, g->grid, XSync{},
+                              as_stream(stream)));
+    return OSP_OK;
+}
+
 osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream) {
     OSP_TRY(check_ready(s, buf));
     if (!ms) return fail(OSP_ERR_INVALID, "null output");

@@ -119,6 +119,10 @@ class ShardGroup:
         """True: streaming kernels (per-tile flags); False: barrier mode."""
         return bool(lib().osp_shard_streaming(self._h))
 
+    def solo_agg(self, stage: int, buf: int, stream=None):
+        """Diagnostics: this rank's push/pull of a stage alone (osp_shard_solo_agg)."""
+        _check(lib().osp_shard_solo_agg(self._h, stage, buf, _stream(stream)))
+
     def check(self, stream=None):
         _check(lib().osp_shard_check(self._h, _stream(stream)))
 
