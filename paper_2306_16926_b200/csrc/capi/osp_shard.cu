@@ -385,14 +385,12 @@ osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
-    osp_group* g = s->grp;
     if (s->stream) {
         s->iter += 1;
         OSP_CUDA(stream_stage(s, buf, 1, 0, 0, st));
         OSP_CUDA(stream_stage(s, buf, 2, 0, s->n_chunks, st));
         return osp_shard_resolve(s, buf, stream);
     }
-    float* Xb = s->X + buf * s->buf_stride;
     OSP_CUDA(barrier_step_kernels(s, buf, st));
     return osp_shard_resolve(s, buf, stream);
 }

@@ -776,12 +776,6 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggP
     xsync_end(g, pt, sy);
 }
 
-__device__ __forceinline__ uint64_t global_ns() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
 bool vec_ok(const GroupView& g, const float* X, uint64_t ldX) {
     return (ldX % 4 == 0) && (g.ldP % 4 == 0) &&
            (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
