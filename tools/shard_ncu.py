@@ -35,7 +35,29 @@ def main():
     sh.fill_synth(11, 0, 0)
     torch.cuda.synchronize()
     dist.barrier()
-    if rank == 0:
+    if os.environ.get("BOTH") == "1":
+        # every rank launches its solo push/pull at once: the bidirectional
+        # exchange without the step's cross-GPU ordering
+        reps = int(os.environ.get("REPS", "5"))
+        res = []
+        for r in range(reps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            sh.solo_agg(1, 0)
+            b.record()
+            torch.cuda.synchronize()
+            res.append(a.elapsed_time(b))
+        t = torch.tensor([min(res)], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        if rank == 0:
+            P, nl = world, N // world
+            per_dir = 4.0 * M * ((N - nl) / P + (P - 1) / P)
+            print(json.dumps({"layout": layout, "P": P, "both_solo_agg_ms_max": float(t[0]),
+                              "per_direction_GBps": per_dir / (float(t[0]) * 1e-3) / 1e9}),
+                  flush=True)
+    elif rank == 0:
         reps = int(os.environ.get("REPS", "3"))
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
         for r in range(reps):
