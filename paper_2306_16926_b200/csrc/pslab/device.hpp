@@ -19,6 +19,16 @@ inline void check(osp_status s) {
     if (s != OSP_OK) throw_status(s);
 }
 
+// Caching device allocator for the façade's buffers (device.cpp). The reference
+// API creates and drops per-iteration state (an OspServer round holds N
+// contribution vectors of the whole model); cudaMalloc / cudaFree per round
+// cost milliseconds and cudaFree synchronises the device. Freed blocks are
+// kept per size class and handed out again. Safe because all façade work is
+// ordered on the legacy default stream: a block's next owner can only enqueue
+// work after everything its previous owner enqueued.
+void* pool_alloc(size_t bytes, size_t* cls);
+void pool_free(void* p, size_t cls);
+
 // Device float buffer. All façade work runs on the legacy default stream, so a
 // download is ordered after every kernel that produced the data.
 class DevBuf {
@@ -27,12 +37,14 @@ public:
     explicit DevBuf(size_t n) { reset(n); }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)) {}
+    DevBuf(DevBuf&& o) noexcept
+        : p_(std::exchange(o.p_, nullptr)), n_(std::exchange(o.n_, 0)), cls_(std::exchange(o.cls_, 0)) {}
     DevBuf& operator=(DevBuf&& o) noexcept {
         if (this != &o) {
             release();
             p_ = std::exchange(o.p_, nullptr);
             n_ = std::exchange(o.n_, 0);
+            cls_ = std::exchange(o.cls_, 0);
         }
         return *this;
     }
@@ -40,9 +52,7 @@ public:
 
     void reset(size_t n) {
         release();
-        void* p = nullptr;
-        check(osp_device_alloc(std::max<size_t>(n, 1) * sizeof(float), &p));
-        p_ = static_cast<float*>(p);
+        p_ = static_cast<float*>(pool_alloc(std::max<size_t>(n, 1) * sizeof(float), &cls_));
         n_ = n;
     }
     void zero() { check(osp_memset(p_, 0, std::max<size_t>(n_, 1) * sizeof(float), nullptr)); }
@@ -63,12 +73,13 @@ public:
 
 private:
     void release() {
-        if (p_) osp_device_free(p_);
+        if (p_) pool_free(p_, cls_);
         p_ = nullptr;
         n_ = 0;
     }
     float* p_ = nullptr;
     size_t n_ = 0;
+    size_t cls_ = 0;
 };
 
 }  // namespace pslab_b200
