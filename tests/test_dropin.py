@@ -56,3 +56,28 @@ def test_reference_unit_tests_through_facade():
     res = subprocess.run([exe], capture_output=True, text=True, timeout=1500)
     print(res.stdout[-4000:])
     assert res.returncode == 0, res.stdout[-4000:] + res.stderr[-2000:]
+
+
+def test_reference_flow_fullsize_goldens_through_facade(tmp_path):
+    """oracle/ref_driver.cpp (OspWorker x 8 + OspServer driven through the
+    reference C++ API) built against the reference engines and against the
+    façade: at the full ResNet-50 layout every per-iteration artefact (GIB
+    bytes, rank orders, chunk maps, stage-1 and final worker rows, global
+    vector, aggregate, PGP scores, budgets) must be byte-identical."""
+    _load_check()
+    ref, dev = _exe("ref_driver"), _exe("dropin_driver")
+    from paper_2306_16926_b200 import layouts
+    lf = tmp_path / "layers.txt"
+    lf.write_text(",".join(map(str, layouts.resnet50())))
+    args = ["golden", "--layers-file", str(lf), "--workers", "8", "--budget-frac", "0.5",
+            "--chunks", "4", "--seed", "11", "--iters", "3"]
+    for exe, d in ((ref, "ref"), (dev, "dev")):
+        (tmp_path / d).mkdir()
+        res = subprocess.run([exe] + args + ["--out", str(tmp_path / d)], capture_output=True,
+                             text=True, timeout=1500)
+        assert res.returncode == 0, res.stderr[-2000:]
+    names = sorted(os.listdir(tmp_path / "ref"))
+    assert len(names) >= 40 and names == sorted(os.listdir(tmp_path / "dev"))
+    diff = [n for n in names
+            if not filecmp.cmp(tmp_path / "ref" / n, tmp_path / "dev" / n, shallow=False)]
+    assert not diff, diff
