@@ -59,7 +59,9 @@ struct osp_shard {
     StreamArgs sa{};           // peer tables of tflag/pbuf
     int vec[2]{};              // per delta buffer: 16-byte aligned rows
     unsigned iter = 0;         // iterations started (stage-1 launches)
-    unsigned xep[3] = {0, 0, 0};  // barrier mode: epochs of the in-kernel cross-GPU syncs
+    unsigned xep[4] = {0, 0, 0, 0};  // barrier mode: epochs of the in-kernel cross-GPU syncs
+                                     // (kinds 0, 1, 2 and 4)
+    bool pipe = false;               // pipelined step (OSP_SHARD_PIPE, barrier mode)
     unsigned long long* dbg = nullptr;  // [2 stages][3 roles][16] diagnostics counters (OSP_SS_DEBUG=1)
 };
 
@@ -98,6 +100,8 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     const uint32_t Ts = cfg->tile_elems ? cfg->tile_elems : 2048u;
     s->stream = (se && se[0] == '1') &&
                 shard_stream_supported(s->N, static_cast<int>(Ts), static_cast<int>(part->counts.size()));
+    const char* pe = std::getenv("OSP_SHARD_PIPE");
+    s->pipe = !s->stream && pe && pe[0] == '1';
     osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks,
                         s->stream ? Ts : cfg->tile_elems, cfg->sgd_lr, OSP_GROUP_REGISTER};
     osp_status st = osp_group_create(part, &gc, init_params, stream, &s->grp);
@@ -317,6 +321,42 @@ static cudaError_t barrier_step_kernels(osp_shard* s, int buf, cudaStream_t st,
     ++s->xep[1];
     ++s->xep[2];
     cudaError_t e;
+    if (s->pipe) {
+        // agg1 (first half of the RS exchange) -> [apply: RS first half + local
+        // estimates || agg: RS second half] -> [apply: RS second half || agg:
+        // ICS] -> apply2; cross-GPU kinds 1, 4, 2 in that order
+        ++s->xep[3];
+        if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
+        if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st,
+                                  1)) != cudaSuccess)
+            return e;
+        if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+        XSync ya = sync_wait(1, s->xep[1]);
+        ya.signal_end = 4;
+        ya.ep_end = s->xep[3];
+        FusedLists la;
+        la.apply_mode = 1;
+        la.agg_stage = 1;
+        la.agg_part = 2;
+        if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0, 0, g->grid,
+                                    ya, st, la)) != cudaSuccess)
+            return e;
+        XSync yb = sync_wait(4, s->xep[3]);
+        yb.signal_end = 2;
+        yb.ep_end = s->xep[2];
+        FusedLists lb;
+        lb.apply_mode = 2;
+        lb.agg_stage = 2;
+        if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0,
+                                    s->n_chunks, g->grid, yb, st, lb)) != cudaSuccess)
+            return e;
+        if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
+        if ((e = launch_shard_apply(g->v, s->ap_loc, s->pt[buf], Xb, s->ldX, 2, 0, s->n_chunks,
+                                    g->grid, sync_wait(2, s->xep[2]), st)) != cudaSuccess)
+            return e;
+        if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
+        return cudaSuccess;
+    }
     if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
     if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st)) !=
         cudaSuccess)

@@ -439,6 +439,35 @@ __device__ __forceinline__ Tab stage_tab(const GroupView& g, unsigned char* sm, 
     return load_tab(g, sm, g.ics_layers, g.ics_tile_prefix, jb, je);
 }
 
+// Pipelined sharded step: the stage-1 (RS) tile sequence is exchanged in two
+// halves so the first half's apply overlaps the second half's exchange.
+// part 0 = the whole sequence [U0, U0+U), 1 = its first half, 2 = its second.
+__device__ __forceinline__ void seq_part(int part, int& U0, int& U) {
+    if (part == 1) {
+        U = U / 2;
+    } else if (part == 2) {
+        U0 += U / 2;
+        U -= U / 2;
+    }
+}
+
+// Global index of the tile at the middle of the RS sequence (RS layers ascend
+// by id, so "RS position < middle" <=> "global tile index < this"). NT when
+// there is no RS tile.
+__device__ int rs_mid_tile(const GroupView& g) {
+    const int n_rs = g.meta[META_N_RS];
+    const int U = n_rs > 0 ? g.rs_tile_prefix[n_rs] : 0;
+    if (U == 0) return g.NT;
+    const int mid = U / 2;
+    int a = 0, b = n_rs - 1;  // last p with prefix[p] <= mid
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (g.rs_tile_prefix[m] <= mid) a = m;
+        else b = m - 1;
+    }
+    return g.tile_base[g.rs_layers[a]] + (mid - g.rs_tile_prefix[a]);
+}
+
 // The owner's part of the push/pull for elements [s, e): read every worker's
 // row (local or peer HBM over NVLink), aggregate in the fixed worker order,
 // store the fp32 aggregate into every rank's agg buffer.
@@ -580,14 +609,15 @@ __device__ void xsync_end(const GroupView& g, const PeerTable& pt, const XSync& 
 template <int NS>
 __global__ void __launch_bounds__(kStageThreads) k_shard_agg(GroupView g, AggParams ap,
                                                              PeerTable pt, int stage, int c0,
-                                                             int c1, int vec, XSync sy) {
+                                                             int c1, int vec, XSync sy, int part) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
     xsync_start(pt, sy);
     const int lane = threadIdx.x & 31;
     int* next = g.sched + SCHED_AGG_NEXT;
     const Tab tab = stage_tab(g, smem_tab, stage, c0, c1);
-    const int U0 = tab.n > 0 ? tab.sp[0] : 0;
-    const int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
+    int U0 = tab.n > 0 ? tab.sp[0] : 0;
+    int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
+    seq_part(part, U0, U);
     const int lo = U0 + static_cast<int>((static_cast<int64_t>(U) * pt.rank) / pt.world);
     const int hi = U0 + static_cast<int>((static_cast<int64_t>(U) * (pt.rank + 1)) / pt.world);
     int u = lo + grab(next, lane);
@@ -707,20 +737,26 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggP
                                                                const float* __restrict__ X,
                                                                uint64_t ldX, int c0, int c1,
                                                                int vec_apply, int vec_agg,
-                                                               int apply_every, XSync sy) {
+                                                               int apply_every, XSync sy,
+                                                               FusedLists fl) {
     extern __shared__ __align__(16) unsigned char smem_tab[];
     xsync_start(pt, sy);
     const int lane = threadIdx.x & 31;
-    const Tab tab = stage_tab(g, smem_tab, 2, c0, c1);
-    const int U0 = tab.n > 0 ? tab.sp[0] : 0;
-    const int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
+    const Tab tab = stage_tab(g, smem_tab, fl.agg_stage, c0, c1);
+    int U0 = tab.n > 0 ? tab.sp[0] : 0;
+    int U = tab.n > 0 ? tab.sp[tab.n] - U0 : 0;
+    seq_part(fl.agg_part, U0, U);
+    // apply list: mode 0 every tile; 1 RS tiles before the RS middle + every
+    // deferred tile (local estimate); 2 RS tiles from the middle on
+    const int t_mid = fl.apply_mode ? rs_mid_tile(g) : 0;
+    const int t_first = fl.apply_mode == 2 ? t_mid : 0;
     const int lo = U0 + static_cast<int>((static_cast<int64_t>(U) * pt.rank) / pt.world);
     const int hi = U0 + static_cast<int>((static_cast<int64_t>(U) * (pt.rank + 1)) / pt.world);
     int* next_apply = g.sched + SCHED_S1_NEXT;
     int* next_agg = g.sched + SCHED_AGG_NEXT;
     auto fetch = [&](int list) -> int {
         if (list == 0) {
-            const int t = grab(next_apply, lane);
+            const int t = t_first + grab(next_apply, lane);
             return t < g.NT ? t : -1;
         }
         const int u = lo + grab(next_agg, lane);
@@ -748,7 +784,10 @@ __global__ void __launch_bounds__(kStageThreads) k_shard_fused(GroupView g, AggP
             const int l = tab_layer_of_tile(tab, t);
             uint64_t s, e;
             tab_range(tab, g, l, t - tab.tb[l], s, e);
-            if (tab.flag[l]) {
+            const bool skip = (fl.apply_mode == 1 && !tab.flag[l] && t >= t_mid) ||
+                              (fl.apply_mode == 2 && tab.flag[l]);
+            if (skip) {
+            } else if (tab.flag[l]) {
                 warp_tile_local<0>(g, ap_loc, X, ldX, s, e, vec_apply != 0, lane);
             } else {
                 double acc = 0.0;
@@ -849,7 +888,8 @@ cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* 
 }
 
 cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
-                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s) {
+                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s,
+                             int part) {
     bool vec = (g.ldP % 4 == 0);
     for (int w = 0; w < ap.n; ++w) vec = vec && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
     for (int r = 0; r < pt.world; ++r) vec = vec && (reinterpret_cast<uintptr_t>(pt.agg[r]) % 16 == 0);
@@ -859,7 +899,8 @@ cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const Peer
         constexpr int NS = decltype(nc)::value;
         cudaError_t e = allow_tab_smem(reinterpret_cast<const void*>(k_shard_agg<NS>));
         if (e != cudaSuccess) return e;
-        k_shard_agg<NS><<<grid, kStageThreads, sm, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0, sy);
+        k_shard_agg<NS><<<grid, kStageThreads, sm, s>>>(g, ap, pt, stage, c0, c1, vec ? 1 : 0, sy,
+                                                        part);
         return cudaGetLastError();
     });
 }
@@ -883,7 +924,7 @@ cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, cons
 
 cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
                                const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
-                               int grid, const XSync& sy, cudaStream_t s) {
+                               int grid, const XSync& sy, cudaStream_t s, FusedLists fl) {
     const bool vec_apply =
         vec_ok(g, Xloc, ldX) && (reinterpret_cast<uintptr_t>(g.agg_full) % 16 == 0);
     bool vec_agg = true;
@@ -905,7 +946,8 @@ cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, cons
             return e != 0 ? e : -4;
         }();
         k_shard_fused<NS><<<grid, kStageThreads, sm, s>>>(g, ap_all, ap_loc, pt, Xloc, ldX, c0, c1,
-                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0, every, sy);
+                                                          vec_apply ? 1 : 0, vec_agg ? 1 : 0, every, sy,
+                                                          fl);
         return cudaGetLastError();
     });
 }

@@ -136,7 +136,7 @@ constexpr int kResolveThreads = 1024;
 
 // ---- sharded (multi-GPU) path: peer tables ---------------------------------
 constexpr int kMaxRanks = 8;      // one NVLink/NVSwitch node
-constexpr int kBarKinds = 4;      // flag-slot kinds: deltas ready, stage-1 aggregate done, stage-2 aggregate done, streaming deltas ready
+constexpr int kBarKinds = 5;      // flag-slot kinds: deltas ready, stage-1 aggregate done, stage-2 aggregate done, streaming deltas ready, stage-1 second-half aggregate done (pipelined)
 
 struct PeerTable {
     int world;
@@ -158,8 +158,10 @@ struct XSync {
     int signal_end = -1;    // when the last CTA finishes: signal slot[signal_end] = ep_end
     unsigned ep_wait = 0, ep_start = 0, ep_end = 0;
 };
+// part: 0 the stage's whole tile sequence, 1 / 2 its first / second half
 cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
-                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s);
+                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s,
+                             int part = 0);
 cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const PeerTable& pt,
                                const float* Xloc, uint64_t ldX, int stage, int c0, int c1, int grid,
                                const XSync& sy, cudaStream_t s);
@@ -179,9 +181,19 @@ bool shard_stream_supported(int n_workers, int T, int L);
 cudaError_t launch_shard_stream(const GroupView& g, const AggParams& ap, const PeerTable& pt,
                                 const StreamArgs& sa, cudaStream_t s);
 // stage-1 apply + stage-2 aggregate of chunks [c0, c1) in one launch
+// Which lists a fused launch runs: the apply list (mode 0: every stage-1 tile;
+// 1: RS tiles before the RS sequence's middle + all local estimates; 2: RS
+// tiles from the middle on) beside the aggregate of agg_stage's sequence
+// (agg_part as launch_shard_agg's part).
+struct FusedLists {
+    int apply_mode = 0;
+    int agg_stage = 2;
+    int agg_part = 0;
+};
 cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
                                const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
-                               int grid, const XSync& sy, cudaStream_t s);
+                               int grid, const XSync& sy, cudaStream_t s,
+                               FusedLists fl = FusedLists{});
 
 // ---- payload wire codec (kernels/codec.cu) -----------------------------------
 struct CodecSeg {

@@ -34,6 +34,8 @@ def _worker(rank, world, port, cfg, q):
 
         if "stream" in cfg:
             os.environ["OSP_SHARD_STREAM"] = "1" if cfg["stream"] else "0"
+        if "pipe" in cfg:
+            os.environ["OSP_SHARD_PIPE"] = "1" if cfg["pipe"] else "0"
         torch.cuda.set_device(rank % torch.cuda.device_count())
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
@@ -147,6 +149,23 @@ def test_shard_four_gpus_stream_ragged():
     w = [float(x) for x in 0.1 + rng.random(8)]
     run_world(dict(counts=counts, N=8, weights=w, chunks=4, budget_frac=0.5, iters=3, seed=3,
                    p0_seed=5, stream=True), world=4)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_shard_pipelined_step(world):
+    """Pipelined barrier mode: the RS exchange in two halves, each half's apply
+    beside the next exchange (OSP_SHARD_PIPE=1); ragged layers, unequal weights,
+    budget edges, per-iteration GIB changes."""
+    from paper_2306_16926_b200 import layouts
+    run_world(dict(counts=layouts.resnet50()[:70], N=8, weights=[0.125] * 8, chunks=4,
+                   budget_frac=0.5, iters=4, seed=11, p0_seed=3, stream=False, pipe=True),
+              world=world)
+    rng = np.random.default_rng(21)
+    counts = [int(c) for c in rng.integers(1, 9000, 33)]
+    w = [float(x) for x in 0.1 + rng.random(4)]
+    for frac in (0.0, 0.6, 1.0):
+        run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=frac, iters=3, seed=8,
+                       p0_seed=2, stream=False, pipe=True), world=2)
 
 
 @pytest.mark.skipif(os.environ.get("OSP_TEST_OVERSUB") != "1",
