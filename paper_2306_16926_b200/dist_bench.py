@@ -200,6 +200,12 @@ def run(args, metric: str, unit: str):
                          "frac": nvl_gbs / nvl_peak, "traffic": None,
                          "note": "per-GPU NVLink bytes each direction / step time; peak = measured "
                                  "peer copy 770 GB/s (B200_PROFILING.md)",
+                         "nvlink_bytes_per_gpu_per_direction": nvl_bytes,
+                         "collective_bus_gbs": nvl_gbs,
+                         "frac_vs_bidirectional_667": nvl_gbs / 667.0,
+                         "ncu": "profiles/r1_ncu_full_shard_agg_solo.csv (k_shard_agg alone: NVLink "
+                                "rx user bytes == algorithmic; a profiled multi-rank step cannot "
+                                "run under ncu, see profiles/r1_multi_gpu_notes.md)",
                          "hbm_gbs_per_gpu": hbm_gbs, "hbm_frac": hbm_gbs / hbm_peak},
             "breakdown_ms": ({"stage1": s1_max, "stage2": s2_max,
                               "resolve": ms_step - s1_max - s2_max} if args.per_chunk
