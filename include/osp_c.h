@@ -288,7 +288,8 @@ osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void
  * mu = 0 returns to plain sgd_delta (bit-identical). Needs sgd_lr > 0
  * (ConfigError) and the TMA family (OSP_ERR_INVALID); velocities start at 0. */
 osp_status osp_group_set_momentum(osp_group* g, double mu, void* stream);
-/* stage2_all + resolve, same results. With the ICS carry the resolve needs
+/* stage2_all + resolve, same results (on_push_ics_chunk + check_resolution,
+ * protocol.cpp:326-353, 384-439). With the ICS carry the resolve needs
  * nothing from stage 2 (every PGP partial is published by stage 1), so it is
  * launched first and the stage-2 broadcast runs beside it, reading a stage-1
  * snapshot of the ICS lists the resolve rewrites; the stage-2 grid retires only
