@@ -82,6 +82,15 @@ __device__ __forceinline__ float4 momentum4(const GroupView& g, int w, uint64_t 
     return vn;
 }
 
+// staged form: v read from shared memory, v' streamed out
+__device__ __forceinline__ float4 momentum4s(const GroupView& g, int w, uint64_t f, float4 v,
+                                             float4 x) {
+    const float4 vn = make_float4(__fadd_rn(__fmul_rn(g.mu, v.x), x.x), __fadd_rn(__fmul_rn(g.mu, v.y), x.y),
+                                  __fadd_rn(__fmul_rn(g.mu, v.z), x.z), __fadd_rn(__fmul_rn(g.mu, v.w), x.w));
+    st_stream4(g.V + static_cast<uint64_t>(w) * g.ldP + f, vn);
+    return vn;
+}
+
 __device__ __forceinline__ float momentum1(const GroupView& g, int w, uint64_t f, float x) {
     float* vp = g.V + static_cast<uint64_t>(w) * g.ldP + f;
     const float vn = __fadd_rn(__fmul_rn(g.mu, *vp), x);
@@ -248,7 +257,8 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int T = g.T;
-    constexpr int kRows = STAGE == 3 ? 1 : NS + 1;
+    // slot rows: N delta rows + G (+ N velocity rows with momentum); 1 for stage 3
+    constexpr int kRows = STAGE == 3 ? 1 : (MOM ? 2 * NS + 1 : NS + 1);
     const size_t stage_floats = static_cast<size_t>(kRows) * T;
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + kStages * stage_floats);
@@ -394,6 +404,11 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                             bulk_g2s(dst + static_cast<size_t>(w) * T,
                                      X + static_cast<uint64_t>(w) * ldX + m.s, bytes, &full[s]);
                         bulk_g2s(dst + static_cast<size_t>(NS) * T, g.G + m.s, bytes, &full[s]);
+                        if (MOM)
+                            for (int w = 0; w < NS; ++w)
+                                bulk_g2s(dst + static_cast<size_t>(NS + 1 + w) * T,
+                                         g.V + static_cast<uint64_t>(w) * g.ldP + m.s, bytes,
+                                         &full[s]);
                     }
                 } else {
                     mbar_arrive(&full[s]);
@@ -448,9 +463,13 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                     xs[w] = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(w) * T + 4 * q);
                 const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(NS) * T + 4 * q);
                 const uint64_t f = m.s + 4ull * q;
-                if (MOM) {
+                if (MOM) {  // velocities staged in the slot after G
 #pragma unroll
-                    for (int w = 0; w < NS; ++w) xs[w] = momentum4(g, w, f, xs[w]);
+                    for (int w = 0; w < NS; ++w) {
+                        const float4 v = *reinterpret_cast<const float4*>(
+                            buf + static_cast<size_t>(NS + 1 + w) * T + 4 * q);
+                        xs[w] = momentum4s(g, w, f, v, xs[w]);
+                    }
                 }
                 if (m.kind == 0) consume_agg_quad<NS>(g, ap, xs, go, f, acc);
                 else if (g.C) consume_split_quad<NS>(g, ap, xs, go, f, acc);
@@ -482,13 +501,16 @@ size_t tma_smem_bytes(int rows, int T, int L, int CW, int kStages) {
 template <int STAGE, int NS, int CW, int KS>
 cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int c0, int c1, int ovl, cudaStream_t s) {
-    const size_t sm = tma_smem_bytes(STAGE == 3 ? 1 : NS + 1, g.T, g.L, CW, KS);
-    // momentum is a separate stage-1 instantiation: its velocity traffic would
-    // otherwise cost the default kernel registers (and a CTA per SM)
+    size_t sm = tma_smem_bytes(STAGE == 3 ? 1 : NS + 1, g.T, g.L, CW, KS);
+    // momentum is a separate stage-1 instantiation (velocity rows staged in the
+    // ring too): its traffic would otherwise cost the default kernel registers
     void (*kern)(GroupView, AggParams, const float*, uint64_t, int, int, int) =
         k_stage_tma<NS, STAGE, CW, KS, false>;
     if constexpr (STAGE == 1) {
-        if (g.V) kern = k_stage_tma<NS, STAGE, CW, KS, true>;
+        if (g.V) {
+            kern = k_stage_tma<NS, STAGE, CW, KS, true>;
+            sm = tma_smem_bytes(2 * NS + 1, g.T, g.L, CW, KS);
+        }
     }
     cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -563,6 +585,12 @@ bool tma_supported(int n_workers, int T, int L) {
     if (T < 512 || T > 4096) return false;
     const TmaShape sh = tma_shape(T);
     return tma_smem_bytes(n_workers + 1, T, L, sh.cw, sh.ks) <= 220 * 1024;
+}
+
+bool tma_momentum_supported(int n_workers, int T, int L) {
+    if (!tma_supported(n_workers, T, L)) return false;
+    const TmaShape sh = tma_shape(T);
+    return tma_smem_bytes(2 * n_workers + 1, T, L, sh.cw, sh.ks) <= 220 * 1024;
 }
 
 cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,

@@ -224,6 +224,8 @@ cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order
 int stage_blocks_per_sm(int n_workers, int n_layers);
 // TMA-staged stage kernels (stage_tma.cu)
 bool tma_supported(int n_workers, int T, int L);
+// momentum stages N velocity rows beside the N delta rows + G
+bool tma_momentum_supported(int n_workers, int T, int L);
 cudaError_t launch_stage1_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                               cudaStream_t s);
 // overlap = 1 (carry only): launched after the resolve of the same iteration,
