@@ -887,7 +887,7 @@ osp_status osp_group_set_momentum(osp_group* g, double mu, void* stream) {
     if (!g->tma) return fail(OSP_ERR_INVALID, "momentum needs the TMA-staged stage kernels");
     if (!tma_momentum_supported(g->N, g->v.T, g->v.L))
         return fail(OSP_ERR_INVALID, "momentum: the velocity rows do not fit the shared-memory "
-                                     "ring at this tile size (tile_elems <= 2048 for 8 workers)");
+                                     "ring at this tile size (tile_elems <= 1024 for 8 workers)");
     if (!g->v.V) {
         osp_status st = dalloc(g, &g->v.V, g->v.ldP * g->N);
         if (st != OSP_OK) return st;

@@ -487,8 +487,8 @@ def test_momentum_matches_oracle_on_momentum_deltas(osp, carry):
         grp.set_momentum(1.5)
     with pytest.raises(osp.InvalidArgument):
         osp.OspGroup(part, N, [0.25] * N, sgd_lr=lr, tma=False).set_momentum(0.9)
-    with pytest.raises(osp.InvalidArgument):  # 17 rows x 16 KB x 2 slots: no room for the ring
-        osp.OspGroup(part, 8, [0.125] * 8, sgd_lr=lr, tile_elems=4096).set_momentum(0.9)
+    with pytest.raises(osp.InvalidArgument):  # 17 rows x 8 KB x 2 slots: no room for the ring
+        osp.OspGroup(part, 8, [0.125] * 8, sgd_lr=lr, tile_elems=2048).set_momentum(0.9)
 
 
 def test_group_device_memory_released_without_gc(osp):
