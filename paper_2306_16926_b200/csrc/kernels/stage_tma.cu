@@ -428,7 +428,8 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                         reinterpret_cast<volatile unsigned long long*>(g.meta64 + META64_RESOLVE_DONE);
                     uint64_t t0;
                     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-                    while ((*dn & 0xffffffffull) != want) {
+                    // reached or passed (a repeated stage2_resolve must not hang)
+                    while (static_cast<int>(static_cast<unsigned>(*dn) - static_cast<unsigned>(want)) < 0) {
                         __nanosleep(64);
                         uint64_t t;
                         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

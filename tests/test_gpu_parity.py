@@ -491,6 +491,27 @@ def test_momentum_matches_oracle_on_momentum_deltas(osp, carry):
         osp.OspGroup(part, 8, [0.125] * 8, sgd_lr=lr, tile_elems=2048).set_momentum(0.9)
 
 
+def test_repeated_stage2_resolve_does_not_hang(osp):
+    """Misuse guard for the carry's device-side join: a second stage2_resolve
+    without a stage 1 in between re-broadcasts the same carry (idempotent) and
+    resolves again; it must complete (the join waits for 'reached or passed')."""
+    counts = [4096, 1000, 8192, 12, 2048]
+    M, N = sum(counts), 4
+    grp = osp.OspGroup(osp.Partition(counts), N, [0.25] * N, n_chunks=2)
+    grp.set_budget(M * 2)
+    X = osp.synth_deltas(3, N, 0, M)
+    grp.step(X)
+    grp.step(osp.synth_deltas(3, N, 1, M))
+    torch.cuda.synchronize()
+    G = grp.global_params.clone()
+    P = grp.worker_params.clone()
+    tag = grp.read_gib()["tag"]
+    grp.stage2_resolve(X)
+    torch.cuda.synchronize()
+    assert torch.equal(G, grp.global_params) and torch.equal(P, grp.worker_params)
+    assert grp.read_gib()["tag"] == tag + 1
+
+
 def test_group_device_memory_released_without_gc(osp):
     """Dropping a group (and its zero-copy views) frees its device memory at
     once: the views keep a handle holder alive, not the group, so there is no
