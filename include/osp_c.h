@@ -239,7 +239,7 @@ typedef struct osp_group_config {
 
 /* Stage-kernel family. Default (flags 0): the TMA-staged kernels (tiles moved
  * global->shared by cp.async.bulk into an mbarrier ring, tile_elems default 1024)
- * when the shape allows them (N in {1,2,4,8}, tile_elems in [512, 4096]), else
+ * when the shape allows them (N in 1..8, tile_elems in [512, 4096]), else
  * the register-staged kernels (tile_elems default 512). OSP_GROUP_TMA requires
  * the TMA family (OSP_ERR_INVALID if unsupported); OSP_GROUP_REGISTER forces the
  * register-staged one. Both produce identical results. */

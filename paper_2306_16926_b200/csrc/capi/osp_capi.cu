@@ -657,7 +657,7 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         const uint32_t Tt = cfg->tile_elems ? cfg->tile_elems : kDefaultTmaTile;
         use_tma = tma_supported(N, static_cast<int>(Tt), static_cast<int>(L));
         if (want_tma && !use_tma)
-            return fail(OSP_ERR_INVALID, "OSP_GROUP_TMA needs N in {1,2,4,8}, tile_elems in "
+            return fail(OSP_ERR_INVALID, "OSP_GROUP_TMA needs N in 1..8, tile_elems in "
                                          "[512, 4096] and the ring + layer tables within "
                                          "shared memory");
     }

@@ -567,13 +567,31 @@ cudaError_t launch_tma_n(const GroupView& g, const AggParams& ap, const float* X
     }
 }
 
+// N in {3, 5, 6, 7}: the default shape only (2-slot ring, T/128 <= 8 consumer
+// warps), no sweep overrides, to bound the number of instantiations
+int default_cw(int T) { return T / 128 > 8 ? 8 : T / 128; }
+
+template <int STAGE, int NS>
+cudaError_t launch_tma_n_default(const GroupView& g, const AggParams& ap, const float* X,
+                                 uint64_t ldX, int c0, int c1, int ovl, cudaStream_t s) {
+    switch (default_cw(g.T)) {
+        case 4: return launch_tma_cw<STAGE, NS, 4, 2>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 8: return launch_tma_cw<STAGE, NS, 8, 2>(g, ap, X, ldX, c0, c1, ovl, s);
+        default: return cudaErrorNotSupported;
+    }
+}
+
 template <int STAGE>
 cudaError_t launch_tma(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                        int c0, int c1, int ovl, cudaStream_t s) {
     switch (ap.n) {
         case 1: return launch_tma_n<STAGE, 1>(g, ap, X, ldX, c0, c1, ovl, s);
         case 2: return launch_tma_n<STAGE, 2>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 3: return launch_tma_n_default<STAGE, 3>(g, ap, X, ldX, c0, c1, ovl, s);
         case 4: return launch_tma_n<STAGE, 4>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 5: return launch_tma_n_default<STAGE, 5>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 6: return launch_tma_n_default<STAGE, 6>(g, ap, X, ldX, c0, c1, ovl, s);
+        case 7: return launch_tma_n_default<STAGE, 7>(g, ap, X, ldX, c0, c1, ovl, s);
         case 8: return launch_tma_n<STAGE, 8>(g, ap, X, ldX, c0, c1, ovl, s);
         default: return cudaErrorNotSupported;
     }
@@ -581,16 +599,23 @@ cudaError_t launch_tma(const GroupView& g, const AggParams& ap, const float* X, 
 
 }  // namespace
 
+namespace {
+TmaShape shape_for(int n_workers, int T) {
+    const bool pow2 = n_workers == 1 || n_workers == 2 || n_workers == 4 || n_workers == 8;
+    return pow2 ? tma_shape(T) : TmaShape{default_cw(T), 2};
+}
+}  // namespace
+
 bool tma_supported(int n_workers, int T, int L) {
-    if (!(n_workers == 1 || n_workers == 2 || n_workers == 4 || n_workers == 8)) return false;
+    if (n_workers < 1 || n_workers > 8) return false;
     if (T < 512 || T > 4096) return false;
-    const TmaShape sh = tma_shape(T);
+    const TmaShape sh = shape_for(n_workers, T);
     return tma_smem_bytes(n_workers + 1, T, L, sh.cw, sh.ks) <= 220 * 1024;
 }
 
 bool tma_momentum_supported(int n_workers, int T, int L) {
     if (!tma_supported(n_workers, T, L)) return false;
-    const TmaShape sh = tma_shape(T);
+    const TmaShape sh = shape_for(n_workers, T);
     return tma_smem_bytes(2 * n_workers + 1, T, L, sh.cw, sh.ks) <= 220 * 1024;
 }
 

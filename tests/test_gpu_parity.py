@@ -304,8 +304,10 @@ def test_group_odd_workers_unequal_weights(osp):
     counts = rng.integers(1, 20000, 57)
     w = list(0.1 + rng.random(5))
     p0 = rng.uniform(-1, 1, int(counts.sum())).astype(np.float32)
+    grp = oracle_vs_group(osp, counts, 5, w, 0.6, 3, 4, seed=3, p0=p0, tile_elems=2048, tma=False)
+    assert grp.stage_kernels == "register-staged"
     grp = oracle_vs_group(osp, counts, 5, w, 0.6, 3, 4, seed=3, p0=p0, tile_elems=2048)
-    assert grp.stage_kernels == "register-staged"  # N=5: no TMA family
+    assert grp.stage_kernels == "tma-staged"  # N=5: default TMA shape
 
 
 def test_group_fused_sgd(osp):
@@ -592,7 +594,7 @@ def test_step_host_matches_device_step(osp):
 @pytest.mark.parametrize("carry", [True, False])
 @pytest.mark.parametrize("pad_ld", [0, 1])
 def test_tma_group_matches_reference_engine(osp, golden, pad_ld, carry):
-    if golden.N not in (1, 2, 4, 8):
+    if golden.N > 8:
         with pytest.raises(osp.InvalidArgument):
             osp.OspGroup(osp.Partition(golden.counts, golden.bpe), golden.N,
                          list(golden.weights), tma=True)
@@ -615,8 +617,9 @@ def test_default_group_is_tma_staged(osp):
     part = osp.Partition([1000, 5000])
     assert osp.OspGroup(part, 8).geometry()["tile_elems"] == 1024
     assert osp.OspGroup(part, 8).stage_kernels == "tma-staged"
-    assert osp.OspGroup(part, 3).stage_kernels == "register-staged"
-    assert osp.OspGroup(part, 3).geometry()["tile_elems"] == 512
+    assert osp.OspGroup(part, 3).stage_kernels == "tma-staged"   # default shape for N = 3..7
+    assert osp.OspGroup(part, 9).stage_kernels == "register-staged"
+    assert osp.OspGroup(part, 9).geometry()["tile_elems"] == 512
     with pytest.raises(osp.InvalidArgument):
         osp.OspGroup(part, 8, tile_elems=256, tma=True)
 
@@ -637,11 +640,22 @@ def test_carry_flag_reported(osp):
     part = osp.Partition([1000, 5000])
     assert lib_flags(osp, osp.OspGroup(part, 8)) & 4 == 0
     assert lib_flags(osp, osp.OspGroup(part, 8, carry=False)) & 4 == 4
-    assert lib_flags(osp, osp.OspGroup(part, 3)) & 4 == 4  # register family: no carry
+    assert lib_flags(osp, osp.OspGroup(part, 9)) & 4 == 4  # register family: no carry
 
 
 def lib_flags(osp, grp):
     return osp.lib().osp_group_flags(grp._h)
+
+
+@pytest.mark.parametrize("n", [3, 5, 6, 7])
+def test_tma_group_non_power_of_two_workers(osp, n):
+    """N in {3,5,6,7}: TMA family (default shape), ICS carry and the overlapped
+    resolve, against the oracle on ragged layers with unequal weights."""
+    rng = np.random.default_rng(40 + n)
+    counts = [int(c) for c in rng.integers(1, 9000, 29)] + [8192, 4096]
+    w = [float(x) for x in 0.1 + rng.random(n)]
+    grp = oracle_vs_group(osp, counts, n, w, 0.55, 3, 3, seed=50 + n, tma=True)
+    assert grp.stage_kernels == "tma-staged"
 
 
 def test_tma_matches_default_kernels(osp):
