@@ -1,4 +1,4 @@
-"""CPU (gloo, world_size 2) test of the multi-GPU decomposition's host logic.
+"""CPU (gloo, world_size 2/4/8) test of the multi-GPU decomposition's host logic.
 
 Mirrors what osp_shard_* does on the device, with torch.distributed over gloo as
 the transport: per stage, the tile sequence (RS layers ascending for stage 1,
@@ -130,17 +130,23 @@ def _rank_main(rank, world, port, cfg, q):
         q.put((rank, traceback.format_exc()))
 
 
-@pytest.mark.parametrize("cfg", [
-    dict(counts=[700, 64, 1000, 3, 2048, 129, 512, 77], N=4, weights=[0.25] * 4, chunks=3,
-         budget_frac=0.5, iters=3, seed=11, T=256),
-    dict(counts=[100, 7, 300, 33, 64, 5, 17, 999], N=2, weights=[0.3, 0.9], chunks=4,
-         budget_frac=0.8, iters=3, seed=5, T=64),
+@pytest.mark.parametrize("world,cfg", [
+    (2, dict(counts=[700, 64, 1000, 3, 2048, 129, 512, 77], N=4, weights=[0.25] * 4, chunks=3,
+             budget_frac=0.5, iters=3, seed=11, T=256)),
+    (2, dict(counts=[100, 7, 300, 33, 64, 5, 17, 999], N=2, weights=[0.3, 0.9], chunks=4,
+             budget_frac=0.8, iters=3, seed=5, T=64)),
+    # the bench's N = 8 logical workers at P = 4 (2 per rank) and P = 8 (1 per rank),
+    # the shapes the driver's scaling run launches but no 2/4-GPU box test reaches at P = 8
+    (4, dict(counts=[700, 64, 1000, 3, 2048, 129, 512, 77, 33], N=8, weights=[0.125] * 8,
+             chunks=4, budget_frac=0.5, iters=3, seed=11, T=128)),
+    (8, dict(counts=[300, 64, 1000, 3, 517, 129, 12, 77], N=8, weights=[0.125] * 8,
+             chunks=4, budget_frac=0.5, iters=2, seed=7, T=64)),
 ])
-def test_sharded_decomposition_gloo(cfg):
+def test_sharded_decomposition_gloo(world, cfg):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, cfg, q)) for r in range(2)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, cfg, q)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=300) for _ in procs)
