@@ -21,6 +21,10 @@
 // stable (score, id) order. Exact zeros (s^ == 0 <=> every term is 0) are
 // exact and never marked.
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 
 namespace osp {
@@ -569,9 +573,22 @@ __global__ void __launch_bounds__(kResolveThreads) k_rank_gib(const double* scor
     }
 }
 
+// Raise a kernel's dynamic shared-memory opt-in only when a launch needs more
+// than any before it on this device (never lowered, so groups of different L
+// can interleave): saves a host API call per launch on the launch-bound layouts.
 cudaError_t set_smem(const void* fn, size_t bytes) {
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(bytes));
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> opted;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& cur = opted[std::make_pair(dev, fn)];
+    if (bytes <= cur) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(bytes));
+    if (e == cudaSuccess) cur = bytes;
+    return e;
 }
 
 }  // namespace

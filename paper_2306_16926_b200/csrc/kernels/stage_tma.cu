@@ -17,6 +17,9 @@
 // Every mbarrier wait is bounded (20 s) and traps instead of hanging.
 
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "tma.cuh"
@@ -499,6 +502,38 @@ size_t tma_smem_bytes(int rows, int T, int L, int CW, int kStages) {
     return ring + bars + metas + red + tab;
 }
 
+// Opt the kernel into its shared-memory size and query its occupancy once per
+// (device, kernel, smem bytes): both are host API calls the launch-bound small
+// layouts would otherwise pay on every launch.
+cudaError_t tma_blocks_per_sm(const void* kern, int threads, size_t sm, int* per_sm) {
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void*, size_t>, int> cache;
+    static std::map<std::pair<int, const void*>, size_t> opted;  // attribute = max asked
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const auto key = std::make_tuple(dev, kern, sm);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *per_sm = it->second;
+        return cudaSuccess;
+    }
+    // never lower the opt-in: a smaller layout must not break a cached larger one
+    size_t& cur = opted[std::make_pair(dev, kern)];
+    if (sm > cur) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+        cur = sm;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, sm);
+    if (e != cudaSuccess) return e;
+    if (*per_sm < 1) return cudaErrorInvalidConfiguration;
+    cache.emplace(key, *per_sm);
+    return cudaSuccess;
+}
+
 template <int STAGE, int NS, int CW, int KS>
 cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                           int c0, int c1, int ovl, cudaStream_t s) {
@@ -513,14 +548,13 @@ cudaError_t launch_tma_cw(const GroupView& g, const AggParams& ap, const float* 
             sm = tma_smem_bytes(2 * NS + 1, g.T, g.L, CW, KS);
         }
     }
-    cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(kern),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(sm));
-    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (CW + 1) * 32, sm);
+    cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), (CW + 1) * 32, sm,
+                                      &per_sm);
     if (e != cudaSuccess) return e;
-    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    // grid stays one wave even when a small layout has fewer tiles: clamping it
+    // to the tile count measured no faster for the 420-parameter MLP (18.4 ->
+    // 20.5 us per graph-replayed step; profiles/r1_mlp_launch_notes.md)
     const int grid = sm_count() * per_sm;
     return launch_pdl(kern, dim3(grid), dim3((CW + 1) * 32), sm, s, g, ap, X, ldX, c0, c1, ovl);
 }
