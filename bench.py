@@ -158,29 +158,59 @@ def host_cpu():
     return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
+_CONFIG_INDEX = {"mlp": 0, "mlp_acc": 0, "resnet50": 1, "resnet152": 2, "vgg16": 3, "llama1b": 4}
+
+
+def workload_config(args, counts) -> dict:
+    """The workload both arms run (identical dict in the b200 and the reference
+    line; arm-specific keys live under "arm")."""
+    M = sum(counts)
+    idx = _CONFIG_INDEX.get(args.layout)
+    return {"workload": f"{args.layout}-size OSP sync+LGP step, {args.workers} logical workers "
+                        f"+ PS" + (f" (BASELINE configs[{idx}])" if idx is not None else ""),
+            "layout": args.layout, "params": M, "layers": len(counts), "workers": args.workers,
+            "budget_frac": args.budget_frac, "chunks": args.chunks,
+            "deltas": f"reference synth generator (runner.cpp:312-321), seed {args.seed}, "
+                      "generated outside the timed region",
+            "l2": (f"inputs larger than L2 ({args.workers * M * 4 / 1e6:.0f} MB of delta rows per "
+                   "step against the 126 MB L2), no flush" if args.workers * M * 4 > 126e6 else
+                   f"{args.workers * M * 4 / 1e6:.3f} MB of delta rows per step: L2-resident, "
+                   "launch-bound case")}
+
+
 def run_reference_cpu(layout: str, workers: int, budget_frac: float, chunks: int, seed: int,
-                      iters: int, warmup: int, threads: int):
-    """Time the UNMODIFIED reference engine (oracle/_ref/ref_driver) on host cores."""
+                      iters: int, warmup: int, threads: int, allow_port: bool = True):
+    """Time the UNMODIFIED reference engine (oracle/_ref/ref_driver) on host cores.
+    Without a runnable oracle/_ref the C restatement is timed instead and the
+    result says kind "port" (allow_port=False raises instead)."""
     from paper_2306_16926_b200 import layouts
     drv = os.path.join(REPO, "oracle", "_ref", "ref_driver")
     counts = layouts.get(layout)
-    path = os.path.join("/tmp", f"osp_layers_{layout}.txt")
+    path = os.path.join("/tmp", f"osp_layers_{layout}_{os.getpid()}.txt")
     with open(path, "w") as f:
         f.write(",".join(map(str, counts)))
+    why = "oracle/_ref/ref_driver missing"
     if os.path.exists(drv):
         cmd = [drv, "bench", "--layers-file", path, "--workers", str(workers), "--budget-frac",
                str(budget_frac), "--chunks", str(chunks), "--seed", str(seed), "--iters",
                str(iters), "--warmup", str(warmup), "--threads", str(threads)]
-        res = subprocess.run(cmd, capture_output=True, text=True, timeout=1800)
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=3600)
         if res.returncode == 0:
             d = json.loads(res.stdout.strip().splitlines()[-1])
             return {"value": d["params_per_s"], "unit": UNIT, "cores": threads,
                     "kind": "reference", "ms_per_step": d["median_ms"],
+                    "mean_ms": d["mean_ms"], "total_ms": d.get("total_ms"), "steps_timed": d["steps"],
                     "sample": (f"reference pslab OspWorker/OspServer engine (oracle/_ref, g++ -O3), "
                                f"{layout} layout, {workers} workers, budget {budget_frac} x model, "
-                               f"{chunks} chunks, median of {iters} steps after {warmup} warm-up; "
-                               f"synth delta generation excluded")}
-    # fallback: the C restatement (oracle/osp_oracle.c), single thread
+                               f"{chunks} chunks, {iters} timed steps after {warmup} warm-up, "
+                               f"{threads} host thread(s) for the worker-side calls; synth delta "
+                               f"generation excluded")}
+        why = f"oracle/_ref/ref_driver exited {res.returncode}: {res.stderr.strip()[-200:]}"
+    if not allow_port:
+        raise RuntimeError(why)
+    print(f"bench.py: reference engine unavailable ({why}); timing the C restatement",
+          file=sys.stderr)
+    # the C restatement (oracle/osp_oracle.c), single thread
     import numpy as np
     from oracle import oracle
     M = sum(counts)
@@ -200,37 +230,56 @@ def run_reference_cpu(layout: str, workers: int, budget_frac: float, chunks: int
             times.append(t1 - t0)
     med = statistics.median(times)
     return {"value": M / med, "unit": UNIT, "cores": 1, "kind": "port", "ms_per_step": med * 1e3,
+            "mean_ms": statistics.mean(times) * 1e3, "total_ms": sum(times) * 1e3,
+            "steps_timed": len(times), "unavailable_reason": why,
             "sample": f"C restatement (oracle/osp_oracle.c), {layout}, {workers} workers, "
-                      f"median of {iters} steps"}
+                      f"{iters} timed steps"}
 
 
 def reference_arm(args, rank: int):
+    """--impl reference: the reference engine on this box's host cores, all
+    threads for the worker-side calls, the b200 arm's config / metric / unit.
+    Times exactly --steps steps after --warmup warm-up steps; a 1-thread sample
+    (the reference as shipped is single-threaded) is reported beside it."""
     if rank != 0:
         return
+    from paper_2306_16926_b200 import layouts
     threads = os.cpu_count() or 1
     t0 = time.time()
-    k_run = max(1, args.steps if args.steps <= 5 else 5)  # bounded CPU sample
-    w_run = max(1, min(args.warmup, 2))
+    counts = layouts.get(args.layout)
+    M = sum(counts)
     cb = run_reference_cpu(args.layout, args.workers, args.budget_frac, args.chunks, args.seed,
-                           k_run, w_run, threads)
-    from paper_2306_16926_b200 import layouts
-    M = sum(layouts.get(args.layout))
-    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cb["ms_per_step"], "higher_is_better": True,
+                           args.steps, args.warmup, threads)
+    # whole-run throughput over the timed steps (mean, as the b200 arm's total / K)
+    mean_ms = cb["mean_ms"]
+    value = M / (mean_ms * 1e-3)
+    one = None
+    if threads > 1 and cb["kind"] == "reference":
+        k1 = max(1, min(3, args.steps))
+        c1 = run_reference_cpu(args.layout, args.workers, args.budget_frac, args.chunks,
+                               args.seed, k1, 1, 1)
+        one = {"value": M / (c1["mean_ms"] * 1e-3), "unit": UNIT, "cores": 1,
+               "ms_per_step": c1["mean_ms"], "steps_timed": c1["steps_timed"],
+               "sample": c1["sample"]}
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": cb["steps_timed"], "warmup": args.warmup,
+            "ms_per_step": mean_ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
-            "config": {"workload": f"{args.layout}-size OSP sync+LGP step (BASELINE configs[1])",
-                       "params": M, "layers": len(layouts.get(args.layout)),
-                       "workers": args.workers, "budget_frac": args.budget_frac,
-                       "chunks": args.chunks, "deltas": "reference synth generator, seed "
-                       f"{args.seed} (generated outside the timed region)",
-                       "parallelism": "host threads (reference CPU engine)"},
-            "cpu_baseline": dict({k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                                 **host_cpu()),
-            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+            "config": workload_config(args, counts),
+            "arm": {"engine": "reference pslab OspWorker/OspServer (oracle/_ref)"
+                    if cb["kind"] == "reference" else "C restatement (oracle/osp_oracle.c)",
+                    "host_threads": cb["cores"], "median_ms": cb["ms_per_step"],
+                    "total_timed_ms": cb.get("total_ms"),
+                    "deltas": "regenerated per iteration by the reference generator"},
+            "cpu_baseline": dict({k: cb[k] for k in ("unit", "cores", "kind", "sample")},
+                                 value=value, **host_cpu()),
+            "cpu_baseline_1thread": one,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
-            "cpu_steps_timed": k_run, "cpu_warmup_run": w_run,
+            "gpu_launches": 0,
             "wall_s": round(time.time() - t0, 2)}
+    if cb["kind"] != "reference":
+        line["reference_unavailable"] = cb.get("unavailable_reason")
     print(json.dumps(line), flush=True)
 
 
@@ -265,6 +314,9 @@ def b200_single(args):
         # ICS carry); the breakdown pass (full=True) runs stage 2 and the resolve
         # one after the other to time each
         x = X[k % 2]
+        if evs is None and not full and not args.per_chunk:
+            grp.step(x)  # stage 1 + stage2_resolve (one launch on launch-bound layouts)
+            return
         if evs is not None:
             evs[0].record(stream)
         grp.stage1(x)
@@ -395,7 +447,14 @@ def b200_single(args):
     # the step time the SURVEY byte model allows at the measured peak
     survey_ms = (sum(b_survey) / K) / (peak * 1e9) * 1e3
     stats = grp.stats()
-    launches_per_step = 1 + (args.chunks if args.per_chunk else 1) + 1  # stage1, stage2, resolve
+    # stage1, stage2, resolve (the sampled evented steps always take this path);
+    # single-launch layouts: one launch on the unevented steps
+    launches_3 = 1 + (args.chunks if args.per_chunk else 1) + 1
+    n_evented = 0 if graph is not None else len(sampled)
+    if grp.single_launch and not args.per_chunk:
+        gpu_launches = n_evented * launches_3 + (K - n_evented)
+    else:
+        gpu_launches = K * launches_3
 
     # ---- stage 2 overlapped with the next iteration's (synthetic) compute
     ovl = None
@@ -409,15 +468,18 @@ def b200_single(args):
         ovl = overlap.run(lambda i: grp.stage1(X[i % 2]), s2r, comp, K=min(K, 50), W=3)
         ovl["t_c_ms"] = comp.ms
 
-    # ---- e2e through the C-ABI with host buffers (pinned), H2D + step + D2H of the GIB
-    # one pinned host set for small layouts two; the 1B layout's 40 GB set is pinned once
+    # ---- e2e through the C-ABI with host buffers (pinned): H2D of the step's N
+    # delta rows, the step, D2H of the next GIB and of the updated global vector
+    # (every worker's parameters at the boundary), all inside the timed call.
+    # One pinned host set for small layouts two; the 1B layout's 40 GB set is pinned once
     n_sets = 2 if N * M * 4 <= (8 << 30) else 1
     host = [X[i].cpu().pin_memory() for i in range(n_sets)]
+    params_host = torch.empty(M, dtype=torch.float32).pin_memory()
     e2e_ms = []
     for k in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        grp.step_host(host[k % n_sets])
+        grp.step_host(host[k % n_sets], params_out=params_host)
         t1 = time.perf_counter()
         if k > 0:
             e2e_ms.append((t1 - t0) * 1e3)
@@ -429,18 +491,14 @@ def b200_single(args):
         "metric": METRIC, "value": M / (ms_step * 1e-3), "unit": UNIT, "n_gpus": 1,
         "steps": K, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
-        "config": {"workload": f"{args.layout}-size OSP sync+LGP step (BASELINE configs[1])",
-                   "params": M, "layers": L, "workers": N, "budget_frac": args.budget_frac,
-                   "chunks": args.chunks, "deltas": "reference synth generator, seed "
-                   f"{args.seed}, 2 sets alternating ("
-                   + (f"{2 * N * M * 4 / 1e9:.2f} GB > the 126 MB L2, no flush)"
-                      if 2 * N * M * 4 > 126e6 else
-                      f"{2 * N * M * 4 / 1e6:.3f} MB, L2-resident: launch-bound case)"),
-                   "tile_elems": grp.geometry()["tile_elems"], "parallelism": "single GPU",
-                   "stage_kernels": grp.stage_kernels, "ics_carry": carry,
-                   "inputs": (f"gradients, sgd_delta lr {args.sgd_lr}" if args.sgd_lr > 0 else "deltas")
-                   + (f", momentum {args.momentum}" if args.momentum > 0 else ""),
-                   "launch": "CUDA graph (2 steps per replay)" if graph is not None else "stream"},
+        "config": workload_config(args, counts),
+        "arm": {"parallelism": "single GPU", "tile_elems": grp.geometry()["tile_elems"],
+                "stage_kernels": grp.stage_kernels, "ics_carry": carry,
+                "deltas": "2 device-resident sets (iterations 0 and 1) alternating",
+                "inputs": (f"gradients, sgd_delta lr {args.sgd_lr}" if args.sgd_lr > 0 else "deltas")
+                + (f", momentum {args.momentum}" if args.momentum > 0 else ""),
+                "launch": "CUDA graph (2 steps per replay)" if graph is not None else "stream",
+                "single_launch_step": grp.single_launch},
         "hbm_gbs_step": ach_step,
         "roofline": {"bound": "hbm",
                      "kernel": s1_kernel + (" (barrier: RS agg/apply + LGP + ICS carry)" if carry
@@ -467,9 +525,10 @@ def b200_single(args):
                                  "pass of min(K, 50) steps"},
         "u_mean": float(u.mean()),
         "e2e": {"value": M / (e2e_step * 1e-3), "unit": UNIT, "ms_per_step": e2e_step,
-                "h2d_bytes_per_step": N * M * 4, "d2h_bytes_per_step": gib_bytes,
-                "path": "osp_group_step_host (C-ABI, pinned host deltas)"},
-        "gpu_launches": launches_per_step * K,
+                "h2d_bytes_per_step": N * M * 4, "d2h_bytes_per_step": gib_bytes + 4 * M,
+                "path": "osp_group_step_host (C-ABI): pinned host delta rows in, next GIB and "
+                        "the updated global vector (= every worker's params) out"},
+        "gpu_launches": gpu_launches,
         "certificate": stats,
         "graph": graph_pass,
         "step_ms_percentiles": step_pct,

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define OSP_ABI_VERSION 1
+#define OSP_ABI_VERSION 2
 /* Workers per aggregation call / group (kernel-parameter weights table). */
 #define OSP_MAX_WORKERS 64
 
@@ -253,6 +253,13 @@ typedef struct osp_group_config {
  * protocol.cpp:122-166): stage 2 ignores its `deltas` argument then.
  * OSP_GROUP_NO_CARRY keeps the re-reading stage 2 (identical results). */
 #define OSP_GROUP_NO_CARRY 4u
+/* Launch-bound layouts (L <= 32 layers, M <= 32768 parameters, with the carry
+ * and without momentum): osp_group_step runs the whole iteration — stage 1,
+ * the carry broadcast and a single-warp resolve — as ONE launch of ONE CTA
+ * (identical results). OSP_GROUP_NO_SMALL keeps the three-launch step;
+ * osp_group_flags reports OSP_GROUP_SMALL when the single-launch step is used. */
+#define OSP_GROUP_NO_SMALL 8u
+#define OSP_GROUP_SMALL 16u
 
 /* init_params: DEVICE pointer to M floats (P0), or NULL for zeros. Every worker
  * and the server start from it (runner.cpp:214-231). */
@@ -299,10 +306,14 @@ osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t 
 /* stage1 + stage2_resolve. */
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream);
 /* End-to-end step from HOST (pinned or pageable) deltas: H2D copy of the N rows
- * into the group's staging buffer, the step, and a D2H read of the encoded next
- * GIB into gib_out (osp_gib_encoded_size(L) bytes, may be NULL). Synchronous. */
+ * into the group's staging buffer, the step, a D2H read of the encoded next GIB
+ * into gib_out (osp_gib_encoded_size(L) bytes, may be NULL) and of the updated
+ * global vector into params_out (HOST, M floats, may be NULL) — at the iteration
+ * boundary every worker's parameters equal it bit for bit, so it is the
+ * step's result as OspServer::global_params() / OspWorker::params() return it
+ * (protocol.hpp). Synchronous. */
 osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,
-                               uint8_t* gib_out, void* stream);
+                               uint8_t* gib_out, float* params_out, void* stream);
 
 /* Device pointers into the group state (valid until destroy). */
 float* osp_group_global(osp_group* g);

@@ -47,6 +47,7 @@ def lib():
         L.oo_aggregate_layer.argtypes = [ctypes.c_int, ctypes.POINTER(_f32p), _f64p,
                                          ctypes.c_uint64, _f32p]
         L.oo_pgp.argtypes = [ctypes.c_int64, _u64p, _f32p, _f32p, _f64p]
+        L.oo_pgp_accum.argtypes = [ctypes.c_uint64, _f32p, _f32p, _f64p]
         L.oo_rank.argtypes = [ctypes.c_int64, _f64p, _i32p]
         L.oo_build_gib.argtypes = [ctypes.c_int64, _f64p, _u64p, ctypes.c_uint32,
                                    ctypes.c_uint64, _u8p]
@@ -131,6 +132,15 @@ def pgp(counts, params, grads) -> np.ndarray:
     out = np.empty(c.size, dtype=np.float64)
     lib().oo_pgp(c.size, _p(c, _u64p), _p(p, _f32p), _p(g, _f32p), _p(out, _f64p))
     return out
+
+
+def pgp_accum(params, grads, acc: float) -> float:
+    """importance.cpp:20-25, continued: acc + the sequential sum over this piece"""
+    p = _c(params, np.float32)
+    g = _c(grads, np.float32)
+    a = ctypes.c_double(acc)
+    lib().oo_pgp_accum(p.size, _p(p, _f32p), _p(g, _f32p), ctypes.byref(a))
+    return a.value
 
 
 def rank(scores) -> np.ndarray:

@@ -102,6 +102,15 @@ void oo_pgp(int64_t n_layers, const uint64_t* counts, const float* params, const
     }
 }
 
+/* importance.cpp:20-25 continued over a stream: the same sequential sum of one
+ * layer, fed in consecutive pieces (acc carries the running sum). Used by the
+ * 1B-parameter parity test, whose layers do not fit the host in one piece. */
+void oo_pgp_accum(uint64_t n, const float* params, const float* grads, double* acc) {
+    double sum = *acc;
+    for (uint64_t j = 0; j < n; ++j) sum += fabs((double)grads[j] * (double)params[j]);
+    *acc = sum;
+}
+
 static const double* g_rank_scores;
 
 static int rank_cmp(const void* a, const void* b) {
@@ -182,7 +191,7 @@ int oo_split(int64_t n_layers, const uint64_t* counts, uint32_t bpe, const uint8
     *n_rs = nr;
     /* deferred order: rank order filtered by the bitmap, then missing ids ascending */
     int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n_layers + n_order + 1));
-    uint8_t* seen = (uint8_t*)calloc((size_t)(n_layers ? n_layers : 1), 1);
+    uint8_t* seen = (uint8_t*)calloc(n_layers > 0 ? (size_t)n_layers : 1u, 1);
     int64_t no = 0;
     for (int64_t i = 0; i < n_order; ++i) {
         int32_t id = ics_order[i];

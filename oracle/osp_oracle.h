@@ -10,7 +10,7 @@
  * /root/reference/proj) on flat arrays. Parity pinning: tests/test_oracle.py
  * checks it against (1) the hand vectors of the reference unit tests and
  * (2) golden dumps produced by the unmodified reference engine
- * (oracle/_ref/ref_driver, committed as tests/golden/*.npz by
+ * (oracle/_ref/ref_driver, committed as tests/golden/ (npz) by
  * oracle/gen_golden.py).
  */
 #ifndef OSP_ORACLE_H
@@ -42,6 +42,7 @@ int oo_aggregate_layer(int n_workers, const float* const* contribs, const double
                        uint64_t n, float* out);
 
 /* importance.cpp:11-28 — scores[l] = sequential sum_j |(double)g_j * (double)p_j| */
+void oo_pgp_accum(uint64_t n, const float* params, const float* grads, double* acc);
 void oo_pgp(int64_t n_layers, const uint64_t* counts, const float* params, const float* grads,
             double* scores);
 /* importance.cpp:30-40 — stable ascending, ties by id */

@@ -28,6 +28,8 @@ class osp_group_config(ctypes.Structure):
 GROUP_TMA = 1
 GROUP_REGISTER = 2
 GROUP_NO_CARRY = 4
+GROUP_NO_SMALL = 8
+GROUP_SMALL = 16
 
 
 class osp_shard_config(ctypes.Structure):
@@ -114,7 +116,8 @@ _SIGS = {
     "osp_group_stages": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_stage2_resolve": (c_int, [c_void_p, c_void_p, c_u64, c_void_p]),
     "osp_group_set_momentum": (c_int, [c_void_p, c_dbl, c_void_p]),
-    "osp_group_step_host": (c_int, [c_void_p, c_void_p, c_u64, P(ctypes.c_uint8), c_void_p]),
+    "osp_group_step_host": (c_int, [c_void_p, c_void_p, c_u64, P(ctypes.c_uint8), c_void_p,
+                                    c_void_p]),
     "osp_group_global": (c_void_p, [c_void_p]),
     "osp_group_worker_params": (c_void_p, [c_void_p, P(c_u64)]),
     "osp_group_scores": (c_void_p, [c_void_p]),

@@ -27,6 +27,11 @@ struct osp_group {
     int grid = 1;
     int blocks_per_sm = 1;
     bool tma = false;  // OSP_GROUP_TMA
+    // stage 1 issued and the iteration not yet resolved: stage 2 needs it (the
+    // carry and its list snapshot are written by stage 1), a GIB install must
+    // not land between the two (the overlapped stage 2 joins on the snapshot)
+    bool s1_open = false;
+    bool small = false;  // osp_group_step runs as one launch (kernels/step_small.cu)
     // owned device buffers
     std::vector<void*> owned;
     int* d_order_tmp = nullptr;

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -42,6 +43,34 @@ int sm_count() {
             cached = 148;
     });
     return cached;
+}
+
+unsigned long long current_ctx_id() {
+    using GetCurrent = int (*)(void**);
+    using GetId = int (*)(void*, unsigned long long*);
+    static GetCurrent get_current = nullptr;
+    static GetId get_id = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_current = reinterpret_cast<GetCurrent>(f);
+        f = nullptr;
+        if (cudaGetDriverEntryPoint("cuCtxGetId", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            get_id = reinterpret_cast<GetId>(f);
+    });
+    void* ctx = nullptr;
+    unsigned long long id = 0;
+    if (get_current && get_current(&ctx) == 0 && ctx) {
+        if (get_id && get_id(ctx, &id) == 0) return id;
+        return reinterpret_cast<unsigned long long>(ctx);
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return 0xffff000000000000ull | static_cast<unsigned>(dev);
 }
 
 AggParams make_agg_params(int n, const double* weights, double sgd_lr) {
@@ -652,6 +681,8 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     const bool force_reg = (cfg->flags & OSP_GROUP_REGISTER) != 0;
     if (want_tma && force_reg)
         return fail(OSP_ERR_INVALID, "OSP_GROUP_TMA and OSP_GROUP_REGISTER are exclusive");
+    if (cfg->flags & ~(OSP_GROUP_TMA | OSP_GROUP_REGISTER | OSP_GROUP_NO_CARRY | OSP_GROUP_NO_SMALL))
+        return fail(OSP_ERR_INVALID, "unknown osp_group_config flags");
     bool use_tma = false;
     if (!force_reg) {
         const uint32_t Tt = cfg->tile_elems ? cfg->tile_elems : kDefaultTmaTile;
@@ -791,9 +822,13 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
         return cleanup(st);
     if (use_tma && !(cfg->flags & OSP_GROUP_NO_CARRY)) {
         if ((st = dalloc(g, &v.C, M)) != OSP_OK) return cleanup(st);
-        if ((st = dalloc(g, &v.snap, snap_ints(static_cast<int>(L), cfg->n_chunks))) != OSP_OK)
+        const int ns = snap_ints(static_cast<int>(L), cfg->n_chunks);
+        if ((st = dalloc(g, &v.snap, ns)) != OSP_OK) return cleanup(st);
+        if ((st = cu(cudaMemsetAsync(v.snap, 0, ns * sizeof(int), s), "snap")) != OSP_OK)
             return cleanup(st);
     }
+    g->small = v.C != nullptr && small_step_supported(N, static_cast<int>(L), M) &&
+               !(cfg->flags & OSP_GROUP_NO_SMALL);
     g->blocks_per_sm = stage_blocks_per_sm(N, static_cast<int>(L));
     g->tma = use_tma;
     g->grid = sm_count() * g->blocks_per_sm;
@@ -819,6 +854,8 @@ osp_status osp_group_set_budget(osp_group* g, uint64_t budget, void* stream) {
 osp_status osp_group_set_gib(osp_group* g, const uint8_t* flags, const int32_t* order,
                              int64_t n_order, uint32_t tag, void* stream) {
     if (!g || !flags) return fail(OSP_ERR_INVALID, "null argument");
+    if (g->s1_open)
+        return fail(OSP_ERR_PROTOCOL, "GIB install between stage 1 and the resolve of an iteration");
     if (n_order < 0 || n_order > g->v.L)
         return fail(OSP_ERR_INVALID, "rank order longer than the layer count");
     cudaStream_t s = as_stream(stream);
@@ -838,6 +875,13 @@ osp_status osp_group_stage1(osp_group* g, const float* deltas, uint64_t ld, void
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
     if (g->tma) OSP_CUDA(launch_stage1_tma(g->v, g->ap, deltas, ld, as_stream(stream)));
     else OSP_CUDA(launch_stage1(g->v, g->ap, deltas, ld, g->grid, as_stream(stream)));
+    g->s1_open = true;
+    return OSP_OK;
+}
+
+static osp_status need_stage1(const osp_group* g) {
+    if (!g->s1_open)
+        return fail(OSP_ERR_PROTOCOL, "stage 2 before stage 1 of this iteration");
     return OSP_OK;
 }
 
@@ -846,6 +890,7 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (chunk < 0 || chunk >= g->n_chunks) return fail(OSP_ERR_INVALID, "chunk out of range");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    OSP_TRY(need_stage1(g));
     if (g->v.V) deltas = g->v.V, ld = g->v.ldP;  // momentum: stage 1 left v' there
     if (g->tma) OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, chunk, chunk + 1, as_stream(stream)));
     else OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, chunk, chunk + 1, g->grid, as_stream(stream)));
@@ -855,6 +900,7 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
 osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    OSP_TRY(need_stage1(g));
     if (g->v.V) deltas = g->v.V, ld = g->v.ldP;
     if (g->tma) OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, 0, g->n_chunks, as_stream(stream)));
     else OSP_CUDA(launch_stage2(g->v, g->ap, deltas, ld, 0, g->n_chunks, g->grid, as_stream(stream)));
@@ -865,6 +911,7 @@ osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, voi
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (g->v.V) deltas = g->v.V, ld = g->v.ldP;  // the exact fallback re-aggregates v'
     OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, as_stream(stream)));
+    g->s1_open = false;
     return OSP_OK;
 }
 
@@ -905,6 +952,7 @@ osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void
 osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    OSP_TRY(need_stage1(g));
     if (!g->v.C) {
         OSP_TRY(osp_group_stage2_all(g, deltas, ld, stream));
         return osp_group_resolve(g, deltas, ld, stream);
@@ -915,16 +963,22 @@ osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t 
     if (g->v.V) deltas = g->v.V, ld = g->v.ldP;
     OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, s));
     OSP_CUDA(launch_stage2_tma(g->v, g->ap, deltas, ld, 0, g->n_chunks, s, 1));
+    g->s1_open = false;
     return OSP_OK;
 }
 
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    if (g && deltas && g->small && !g->v.V && !g->s1_open) {
+        if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+        OSP_CUDA(launch_step_small(g->v, g->ap, deltas, ld, as_stream(stream)));
+        return OSP_OK;
+    }
     OSP_TRY(osp_group_stage1(g, deltas, ld, stream));
     return osp_group_stage2_resolve(g, deltas, ld, stream);
 }
 
 osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,
-                               uint8_t* gib_out, void* stream) {
+                               uint8_t* gib_out, float* params_out, void* stream) {
     if (!g || !host_deltas) return fail(OSP_ERR_INVALID, "null argument");
     const uint64_t M = g->part->total;
     if (host_ld < M) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
@@ -936,6 +990,8 @@ osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t 
     if (gib_out)
         OSP_CUDA(cudaMemcpyAsync(gib_out, g->v.gib_bytes, osp_gib_encoded_size(g->v.L),
                                  cudaMemcpyDeviceToHost, s));
+    if (params_out)
+        OSP_CUDA(cudaMemcpyAsync(params_out, g->v.G, M * 4, cudaMemcpyDeviceToHost, s));
     OSP_CUDA(cudaStreamSynchronize(s));
     return OSP_OK;
 }
@@ -1039,7 +1095,8 @@ osp_status osp_group_deferred_history(osp_group* g, uint32_t first_tag, int n, u
 
 uint32_t osp_group_flags(const osp_group* g) {
     if (!g) return 0;
-    return (g->tma ? OSP_GROUP_TMA : OSP_GROUP_REGISTER) | (g->v.C ? 0u : OSP_GROUP_NO_CARRY);
+    return (g->tma ? OSP_GROUP_TMA : OSP_GROUP_REGISTER) | (g->v.C ? 0u : OSP_GROUP_NO_CARRY) |
+           (g->small && !g->v.V ? OSP_GROUP_SMALL : 0u);
 }
 
 osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_tiles,

@@ -574,16 +574,16 @@ __global__ void __launch_bounds__(kResolveThreads) k_rank_gib(const double* scor
 }
 
 // Raise a kernel's dynamic shared-memory opt-in only when a launch needs more
-// than any before it on this device (never lowered, so groups of different L
+// than any before it in this context (never lowered, so groups of different L
 // can interleave): saves a host API call per launch on the launch-bound layouts.
+// Keyed on the context (attributes do not survive a recreated context).
 cudaError_t set_smem(const void* fn, size_t bytes) {
     static std::mutex mu;
-    static std::map<std::pair<int, const void*>, size_t> opted;
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
+    static std::map<std::pair<unsigned long long, const void*>, size_t> opted;
+    cudaError_t e = cudaSuccess;
+    const unsigned long long ctx = current_ctx_id();
     std::lock_guard<std::mutex> lock(mu);
-    size_t& cur = opted[std::make_pair(dev, fn)];
+    size_t& cur = opted[std::make_pair(ctx, fn)];
     if (bytes <= cur) return cudaSuccess;
     e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(bytes));

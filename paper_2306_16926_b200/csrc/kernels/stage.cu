@@ -29,6 +29,7 @@
 
 #include <mutex>
 #include <set>
+#include <utility>
 
 #include "common.cuh"
 
@@ -835,15 +836,17 @@ cudaError_t dispatch_n(int n, K1&& k) {
 
 }  // namespace
 
-// Opt a kernel into the largest table size once (dynamic smem above 48 KB).
+// Opt a kernel into the largest table size once per context (dynamic smem
+// above 48 KB; the attribute belongs to the context).
 cudaError_t allow_tab_smem(const void* fn) {
     static std::mutex mu;
-    static std::set<const void*> done;
+    static std::set<std::pair<unsigned long long, const void*>> done;
+    const auto key = std::make_pair(current_ctx_id(), fn);
     std::lock_guard<std::mutex> lock(mu);
-    if (done.count(fn)) return cudaSuccess;
+    if (done.count(key)) return cudaSuccess;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(tab_smem_bytes(kSmemLayers)));
-    if (e == cudaSuccess) done.insert(fn);
+    if (e == cudaSuccess) done.insert(key);
     return e;
 }
 

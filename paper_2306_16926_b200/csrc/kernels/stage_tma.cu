@@ -503,15 +503,15 @@ size_t tma_smem_bytes(int rows, int T, int L, int CW, int kStages) {
 }
 
 // Opt the kernel into its shared-memory size and query its occupancy once per
-// (device, kernel, smem bytes): both are host API calls the launch-bound small
-// layouts would otherwise pay on every launch.
+// (context, kernel, smem bytes): both are host API calls the launch-bound small
+// layouts would otherwise pay on every launch. Keyed on the context, not the
+// device: a recreated context starts without the opt-in.
 cudaError_t tma_blocks_per_sm(const void* kern, int threads, size_t sm, int* per_sm) {
     static std::mutex mu;
-    static std::map<std::tuple<int, const void*, size_t>, int> cache;
-    static std::map<std::pair<int, const void*>, size_t> opted;  // attribute = max asked
-    int dev = 0;
-    cudaError_t e = cudaGetDevice(&dev);
-    if (e != cudaSuccess) return e;
+    static std::map<std::tuple<unsigned long long, const void*, size_t>, int> cache;
+    static std::map<std::pair<unsigned long long, const void*>, size_t> opted;  // attribute = max asked
+    cudaError_t e = cudaSuccess;
+    const unsigned long long dev = current_ctx_id();
     const auto key = std::make_tuple(dev, kern, sm);
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);

@@ -1,0 +1,314 @@
+// Whole OSP iteration in ONE launch of ONE CTA for launch-bound layouts (the
+// small MLP of BASELINE config #1: L <= 32 layers, a few thousand parameters).
+// The big-layout step is three launches (stage 1 over every SM, the resolve,
+// the stage-2 broadcast); for a 420-parameter model those launches, their
+// table loads and the resolve's ~15 block-wide phases are the whole cost, so
+// here every phase of the iteration runs in one 1024-thread CTA and the
+// resolve is done by a single warp with shuffles (one layer per lane):
+//
+//   stage 1   (OspServer::try_close_barrier + finish_layer, protocol.cpp:292-307,
+//             361-382; OspWorker::apply_pull -> lgp_partial, protocol.cpp:69-97):
+//             per element agg = float(sum_w w_k*(double)x_k / W) in the fixed worker
+//             order; RS layers: G' = G + agg, every worker row = G'; ICS layers:
+//             worker rows = G + x_w (local estimate), the carry C = G + agg.
+//   stage 2   (on_push_ics_chunk / lgp_correct, protocol.cpp:99-116, 326-353):
+//             ICS layers: G = C, every worker row = C (base + agg, base == G_old).
+//   resolve   (check_resolution, protocol.cpp:384-439): PGP per layer
+//             (importance.cpp:11-28) as tile partials summed in a fixed order,
+//             certified against the reference's sequential sum (resolve.cu's
+//             interval rule; touching intervals are recomputed sequentially),
+//             rank (importance.cpp:30-40), prefix rule (importance.cpp:42-59),
+//             chunk map (split_for_sync, protocol.cpp:145-164), and every device
+//             list / counter / GIB byte the regular kernels keep, so the group
+//             can continue on either path.
+//
+// Results are bit-identical to stage1 + stage2_resolve (tests/test_gpu_parity.py).
+
+#include "common.cuh"
+
+namespace osp {
+namespace {
+
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallWarps = kSmallThreads / 32;
+constexpr int kSmallTile = 32;  // PGP tile: one term per lane, then 5 shuffles
+constexpr double kU = 1.1102230246251565404e-16;  // 2^-53
+
+struct SmallSmem {
+    uint64_t off[kSmallMaxLayers + 1];
+    uint64_t cnt[kSmallMaxLayers];
+    int tb[kSmallMaxLayers + 1];       // the group's tile geometry (lists for the big kernels)
+    int ptb[kSmallMaxLayers + 1];      // PGP tiles of this kernel per layer (prefix)
+    int flag[kSmallMaxLayers];         // current GIB
+    double part[kSmallMaxTiles];       // PGP tile partials
+    int n_marked;
+};
+
+__device__ __forceinline__ int layer_of_ptile(const SmallSmem& s, int L, int t) {
+    int l = 0;
+    while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
+    return l;
+}
+
+// rank of lane l's (key, id) among lanes 0..L-1 (stable: ties by id)
+__device__ __forceinline__ int warp_rank(double key, int lane, int L) {
+    int r = 0;
+    for (int j = 0; j < L; ++j) {
+        const double kj = __shfl_sync(0xffffffffu, key, j);
+        r += (kj < key) || (kj == key && j < lane);
+    }
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const T u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+    k_step_small(GroupView g, AggParams ap, const float* __restrict__ X, uint64_t ldX) {
+    __shared__ SmallSmem s;
+    pdl_wait();
+    pdl_trigger();
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int L = g.L, n = ap.n;
+    if (tid <= L) {
+        s.tb[tid] = g.tile_base[tid];
+        if (tid < L) {
+            s.off[tid] = g.offsets[tid];
+            s.cnt[tid] = g.counts[tid];
+            s.flag[tid] = g.flags[tid];
+        }
+    }
+    if (tid == 0) s.n_marked = 0;
+    __syncthreads();
+    if (tid == 0) {
+        int t = 0;
+        for (int l = 0; l < L; ++l) {
+            s.ptb[l] = t;
+            t += static_cast<int>((s.cnt[l] + kSmallTile - 1) / kSmallTile);
+        }
+        s.ptb[L] = t;
+        s.off[L] = s.off[L - 1] + s.cnt[L - 1];
+    }
+    __syncthreads();
+    const int n_ptiles = s.ptb[L];
+
+    // ---- stage 1: one warp per PGP tile (one element per lane)
+    for (int t = warp; t < n_ptiles; t += kSmallWarps) {
+        const int l = layer_of_ptile(s, L, t);
+        const uint64_t b = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile;
+        const uint64_t e = min(b + kSmallTile, s.off[l] + s.cnt[l]);
+        const bool ics = s.flag[l] != 0;
+        double acc = 0.0;
+#pragma unroll
+        for (int j = 0; j < kSmallTile / 32; ++j) {
+            const uint64_t f = b + j * 32 + lane;
+            if (f < e) {
+                const float go = g.G[f];
+                double sum = 0.0;
+                for (int w = 0; w < n; ++w) {
+                    float x = X[static_cast<uint64_t>(w) * ldX + f];
+                    if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                    sum = agg_acc(sum, ap.w[w], x);
+                    if (ics) g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
+                }
+                const float a = agg_finish(ap, sum);
+                const float gn = __fadd_rn(go, a);
+                if (ics) {
+                    g.C[f] = gn;
+                } else {
+                    g.G[f] = gn;
+                    for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+                }
+                acc = __dadd_rn(acc, pgp_term(a, gn));
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (lane == 0) s.part[t] = acc;
+    }
+    __syncthreads();
+
+    // ---- stage 2: the carry broadcast on the deferred layers
+    for (int l = 0; l < L; ++l) {
+        if (!s.flag[l]) continue;
+        for (uint64_t f = s.off[l] + tid; f < s.off[l] + s.cnt[l]; f += kSmallThreads) {
+            const float gn = g.C[f];
+            g.G[f] = gn;
+            for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+        }
+    }
+    __syncthreads();  // G final (the exact fallback reads it)
+
+    // ---- resolve: scores + certificate (warp 0, lane = layer)
+    double key = __longlong_as_double(0x7ff0000000000000ll), rad = 0.0;
+    bool marked = false;
+    if (warp == 0) {
+        if (lane < L) {
+            double sc = 0.0;
+            for (int t = s.ptb[lane]; t < s.ptb[lane + 1]; ++t) sc = __dadd_rn(sc, s.part[t]);
+            const double nt = static_cast<double>(s.ptb[lane + 1] - s.ptb[lane]);
+            // depth: 5 shuffle levels + the in-order tile sum (+ slack)
+            const double D = 5.0 + nt + 2.0;
+            key = sc;
+            rad = sc * (kU * (1.01 * (static_cast<double>(s.cnt[lane]) - 1.0 + D) + 8.0));
+            g.scores[lane] = sc;
+            g.lscore[lane] = sc;
+        }
+        for (int j = 0; j < L; ++j) {
+            const double kj = __shfl_sync(0xffffffffu, key, j);
+            const double rj = __shfl_sync(0xffffffffu, rad, j);
+            if (lane < L && j != lane && key != 0.0 && kj + rj >= key - rad && kj - rj <= key + rad)
+                marked = true;
+        }
+        if (lane < L) g.marked[lane] = marked ? 1 : 0;
+        const unsigned mm = __ballot_sync(0xffffffffu, marked);
+        if (lane == 0) s.n_marked = __popc(mm);
+    }
+    __syncthreads();
+    if (s.n_marked > 0) {
+        // exact sequential PGP of the marked layers (importance.cpp:20-25 order),
+        // one warp each, with agg recomputed as stage 1 computed it
+        const unsigned mm = [&] {
+            unsigned m = 0;
+            for (int l = 0; l < L; ++l) m |= g.marked[l] ? (1u << l) : 0u;
+            return m;
+        }();
+        int slot = 0;
+        for (int l = 0; l < L; ++l) {
+            if (!((mm >> l) & 1u)) continue;
+            if (slot++ % kSmallWarps != warp) continue;
+            const uint64_t b0 = s.off[l], e0 = b0 + s.cnt[l];
+            double sum = 0.0;
+            for (uint64_t b = b0; b < e0; b += 32) {
+                const uint64_t f = b + lane;
+                double t = 0.0;
+                if (f < e0) {
+                    double a = 0.0;
+                    for (int w = 0; w < n; ++w) {
+                        float x = X[static_cast<uint64_t>(w) * ldX + f];
+                        if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                        a = agg_acc(a, ap.w[w], x);
+                    }
+                    t = pgp_term(agg_finish(ap, a), g.G[f]);
+                }
+                const int valid = static_cast<int>((e0 - b) < 32 ? (e0 - b) : 32);
+                for (int i = 0; i < valid; ++i) sum = __dadd_rn(sum, __shfl_sync(0xffffffffu, t, i));
+            }
+            if (lane == 0) {
+                g.exact[l] = sum;
+                s.part[l] = sum;  // tile partials are consumed: reuse as exact keys
+            }
+        }
+        __syncthreads();
+        if (warp == 0 && marked) key = s.part[lane];
+        if (tid == 0) {
+            g.meta64[META64_FB_LAYERS] += static_cast<uint64_t>(s.n_marked);
+            g.meta64[META64_FB_RESOLVES] += 1;
+        }
+    }
+    if (warp != 0) return;
+
+    // rank, prefix rule, chunk map, lists (lane = rank position r or layer id)
+    const int my_rank = lane < L ? warp_rank(key, lane, L) : 32;
+    // sorted[r]: the lane whose rank is r
+    int sorted = 0;
+    for (int j = 0; j < L; ++j) {
+        const int rj = __shfl_sync(0xffffffffu, my_rank, j);
+        if (rj == lane) sorted = j;
+    }
+    const uint64_t bpe = g.bpe;
+    const uint64_t bytes_r = lane < L ? s.cnt[sorted] * bpe : 0ull;
+    const uint64_t pre = warp_incl_scan<unsigned long long>(bytes_r, lane);
+    const uint64_t budget = g.meta64[META64_BUDGET];
+    const unsigned fit = __ballot_sync(0xffffffffu, lane < L && pre <= budget);
+    const int k = __popc(fit);  // pre is nondecreasing: the fitting ranks are a prefix
+    const uint64_t total = k > 0 ? __shfl_sync(0xffffffffu, pre, k - 1) : 0ull;
+    const uint64_t nc = static_cast<uint64_t>(g.n_chunks);
+    const bool in_ics = lane < k;
+    uint64_t idx = 0;
+    if (in_ics) {
+        const uint64_t cum = pre - bytes_r;
+        idx = total == 0 ? 0 : (cum * nc) / total;
+        if (idx > nc - 1) idx = nc - 1;
+    }
+    const uint64_t prev_idx = __shfl_up_sync(0xffffffffu, idx, 1);
+    const int is_new = in_ics && (lane == 0 || idx != prev_idx) ? 1 : 0;
+    const int chunk_no = warp_incl_scan<int>(is_new, lane);  // 1-based in the compacted map
+    const int n_used = k > 0 ? __shfl_sync(0xffffffffu, chunk_no, k - 1) : 0;
+    const int ics_tiles = in_ics ? s.tb[sorted + 1] - s.tb[sorted] : 0;
+    const int ics_tp = warp_incl_scan<int>(ics_tiles, lane);
+    // per layer (lane = id): deferred?  rank < k
+    const int deferred = lane < L && my_rank < k ? 1 : 0;
+    const int rs = lane < L && !deferred ? 1 : 0;
+    const int rs_pos = warp_incl_scan<int>(rs, lane);
+    const int rs_tiles = rs ? s.tb[lane + 1] - s.tb[lane] : 0;
+    const int rs_tp = warp_incl_scan<int>(rs_tiles, lane);
+    const uint32_t tag = static_cast<uint32_t>(g.meta64[META64_RESOLVED] + 1);
+    if (in_ics) {
+        g.chunk_of[sorted] = chunk_no - 1;
+        g.ics_layers[lane] = sorted;
+        if (is_new) g.chunk_begin[chunk_no - 1] = lane;
+        g.ics_tile_prefix[lane + 1] = ics_tp;
+    }
+    if (lane < L) {
+        g.flags[lane] = static_cast<uint8_t>(deferred);
+        if (rs) {
+            g.chunk_of[lane] = -1;
+            if (g.rs_layers) {
+                g.rs_layers[rs_pos - 1] = lane;
+                g.rs_tile_prefix[rs_pos] = rs_tp;
+            }
+        }
+    }
+    const unsigned dmask = __ballot_sync(0xffffffffu, deferred);
+    uint8_t* gb = g.gib_bytes;
+    const int nbm = (L + 7) / 8;
+    if (lane < 4) {
+        gb[lane] = (tag >> (8 * lane)) & 0xff;
+        gb[4 + lane] = (static_cast<uint32_t>(L) >> (8 * lane)) & 0xff;
+        gb[8 + nbm + lane] = (static_cast<uint32_t>(k) >> (8 * lane)) & 0xff;
+    }
+    if (lane < nbm) gb[8 + lane] = static_cast<uint8_t>((dmask >> (8 * lane)) & 0xffu);
+    if (in_ics)
+        for (int i = 0; i < 4; ++i)
+            gb[8 + nbm + 4 + 4 * lane + i] = (static_cast<uint32_t>(sorted) >> (8 * i)) & 0xff;
+    if (lane == 0) {
+        g.ics_tile_prefix[0] = 0;
+        if (g.rs_layers) g.rs_tile_prefix[0] = 0;
+        g.chunk_begin[n_used] = k;
+        g.meta[META_N_ICS] = k;
+        g.meta[META_N_USED] = n_used;
+        g.meta[META_N_RS] = L - k;
+        g.meta64[META64_DEFERRED] = total;
+        g.meta64[META64_TAG] = tag;
+        if (g.hist) g.hist[tag % kHist] = total;
+        g.meta64[META64_RESOLVED] = tag;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence();
+        atomicExch(reinterpret_cast<unsigned long long*>(g.meta64 + META64_RESOLVE_DONE),
+                   static_cast<unsigned long long>(tag));
+    }
+}
+
+}  // namespace
+
+bool small_step_supported(int n_workers, int L, uint64_t M) {
+    return n_workers >= 1 && n_workers <= OSP_MAX_WORKERS && L >= 1 && L <= kSmallMaxLayers &&
+           M <= static_cast<uint64_t>(kSmallMaxTiles - kSmallMaxLayers) * kSmallTile;
+}
+
+cudaError_t launch_step_small(const GroupView& g, const AggParams& ap, const float* X,
+                              uint64_t ldX, cudaStream_t s) {
+    return launch_pdl(k_step_small, dim3(1), dim3(kSmallThreads), 0, s, g, ap, X, ldX);
+}
+
+}  // namespace osp

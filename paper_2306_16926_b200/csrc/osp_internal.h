@@ -30,6 +30,11 @@ osp_status cuda_fail(cudaError_t e, const char* what);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count();
+// Identity of the calling thread's current CUDA context (cuCtxGetId through the
+// runtime's driver entry point). Function attributes such as the dynamic
+// shared-memory opt-in belong to a context, so launch-side caches key on this:
+// a recreated primary context (cudaDeviceReset) gets a new id.
+unsigned long long current_ctx_id();
 
 // ---- aggregation parameters (kernel argument, by value) ---------------------
 struct AggParams {
@@ -222,6 +227,14 @@ cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t 
 cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,
                                cudaStream_t s);
 int stage_blocks_per_sm(int n_workers, int n_layers);
+// Whole iteration (stage 1, carry broadcast, warp-level resolve) in one launch
+// of one CTA for launch-bound layouts (kernels/step_small.cu). Needs the carry
+// buffer C, no momentum, L <= kSmallMaxLayers and M within the tile table.
+constexpr int kSmallMaxLayers = 32;
+constexpr int kSmallMaxTiles = 1056;
+bool small_step_supported(int n_workers, int L, uint64_t M);
+cudaError_t launch_step_small(const GroupView& g, const AggParams& ap, const float* X,
+                              uint64_t ldX, cudaStream_t s);
 // TMA-staged stage kernels (stage_tma.cu)
 bool tma_supported(int n_workers, int T, int L);
 // momentum stages N velocity rows beside the N delta rows + G

@@ -16,7 +16,7 @@ import torch.distributed as dist
 
 from . import _capi
 from ._capi import P, c_dbl, c_u64, c_void_p
-from .osp import (ConfigError, OspGroup, Partition, _check, _dev_f32, _Handle, _ptr, _stream,
+from .osp import (ConfigError, OspGroup, ShapeError, Partition, _check, _dev_f32, _Handle, _ptr, _stream,
                   _view, lib)
 
 
@@ -43,6 +43,8 @@ class ShardGroup:
         init = None
         if init_params is not None:
             _dev_f32(init_params, "init_params")
+            if init_params.numel() != self.M:
+                raise ShapeError("init params do not match the partition")
             init = _ptr(init_params)
         h = c_void_p()
         _check(lib().osp_shard_create(part.handle, ctypes.byref(cfg), init, _stream(stream),
@@ -113,6 +115,11 @@ class ShardGroup:
         else:
             names = ["agg1", "apply1+agg2", "apply2", "resolve"]
         return {n: float(v) for n, v in zip(names, out) if n}
+
+    @property
+    def mode(self) -> str:
+        return ("streaming (per-tile flags)" if self.streaming
+                else "barrier (agg / barrier / apply)")
 
     @property
     def streaming(self) -> bool:

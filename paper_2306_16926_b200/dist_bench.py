@@ -18,6 +18,8 @@ import torch.distributed as dist
 
 
 def run(args, metric: str, unit: str):
+    from bench import workload_config
+
     from . import layouts, osp
     from .dist import ShardGroup
 
@@ -155,7 +157,7 @@ def run(args, metric: str, unit: str):
 
     # ---- e2e: pinned host deltas -> device (this rank's rows), step, GIB read-back
     host = [sh.deltas(b).cpu().pin_memory() for b in range(2)]
-    gib = torch.empty(8 + (L + 7) // 8, dtype=torch.uint8).pin_memory()
+    params_host = torch.empty(M, dtype=torch.float32).pin_memory()
     e2e = []
     for k in range(args.e2e_steps + 1):
         dist.barrier()
@@ -163,7 +165,9 @@ def run(args, metric: str, unit: str):
         t0 = time.perf_counter()
         sh.deltas(k % 2).copy_(host[k % 2], non_blocking=True)
         step(k)
-        st = sh.read_gib()  # synchronising D2H of the next GIB
+        if rank == 0:  # the step's result: the updated global vector (= every worker's params)
+            params_host.copy_(sh.global_params, non_blocking=True)
+        sh.read_gib()  # synchronising D2H of the next GIB
         t1 = time.perf_counter()
         if k > 0:
             e2e.append((t1 - t0) * 1e3)
@@ -186,15 +190,11 @@ def run(args, metric: str, unit: str):
             "metric": metric, "value": M / (ms_step * 1e-3), "unit": unit, "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
-            "config": {"workload": f"{args.layout}-size OSP sync+LGP step, PS sharded over "
-                                   f"{world} GPUs (NVLink peer memory)",
-                       "params": M, "layers": L, "workers": N, "workers_per_gpu": n_loc,
-                       "budget_frac": args.budget_frac, "chunks": args.chunks,
-                       "deltas": "reference synth generator, 2 sets alternating (> L2)",
-                       "parallelism": f"ps-shard{world}",
-                       "shard_kernels": "streaming (per-tile flags)" if sh.streaming
-                       else "barrier (agg / barrier / apply)",
-                       "tile_elems": sh.local.geometry()["tile_elems"]},
+            "config": workload_config(args, counts),
+            "arm": {"parallelism": f"ps-shard{world}", "workers_per_gpu": n_loc,
+                    "shard_kernels": sh.mode,
+                    "deltas": "2 device-resident sets (iterations 0 and 1) alternating",
+                    "tile_elems": sh.local.geometry()["tile_elems"]},
             "roofline": {"bound": "nvlink" if nvl_bytes / nvl_peak > hbm_bytes / hbm_peak else "hbm",
                          "achieved": nvl_gbs, "peak": nvl_peak, "unit": "GB/s",
                          "frac": nvl_gbs / nvl_peak, "traffic": None,
@@ -215,8 +215,9 @@ def run(args, metric: str, unit: str):
             "u_mean": u_mean,
             "e2e": {"value": M / (e2e_ms * 1e-3), "unit": unit, "ms_per_step": e2e_ms,
                     "h2d_bytes_per_step": n_loc * M * 4 * world,
-                    "d2h_bytes_per_step": (8 + (L + 7) // 8) * world,
-                    "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read"},
+                    "d2h_bytes_per_step": (8 + (L + 7) // 8) * world + 4 * M,
+                    "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read on "
+                            "every rank, updated global vector read on rank 0"},
             # streaming: stage1, stage2, resolve per step (per chunk: one stage-2 launch
             # each); barrier mode: agg1, apply1+agg2, apply2, resolve (per chunk: agg1,
             # apply1, agg2 + apply2 per chunk, resolve)

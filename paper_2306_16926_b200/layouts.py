@@ -61,6 +61,8 @@ LAYOUTS = {
     "vgg16": vgg16,
     "llama1b": llama1b,
     "mlp": small_mlp,
+    # the accuracy check's wider MLP (checks.cpp:346): [16, 64, 64, 4]
+    "mlp_acc": lambda: small_mlp((16, 64, 64, 4)),
 }
 
 

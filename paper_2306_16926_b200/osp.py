@@ -441,11 +441,13 @@ class OspGroup:
     def __init__(self, part: Partition, n_workers: int, weights: Optional[Sequence[float]] = None,
                  n_chunks: int = 4, init_params: Optional[torch.Tensor] = None,
                  tile_elems: int = 0, sgd_lr: float = 0.0, tma: Optional[bool] = None,
-                 carry: bool = True, stream=None):
+                 carry: bool = True, small: bool = True, stream=None):
         """tma: None = TMA-staged stage kernels when the shape allows them, True =
         require them, False = register-staged kernels (identical results).
         carry: with the TMA family, stage 1 also keeps the ICS aggregate so stage 2
-        only broadcasts it (OSP_GROUP_NO_CARRY when False; identical results)."""
+        only broadcasts it (OSP_GROUP_NO_CARRY when False; identical results).
+        small: launch-bound layouts step in one single-CTA launch
+        (OSP_GROUP_NO_SMALL when False; identical results)."""
         self.part = part
         self.N = n_workers
         self.M = part.total_count()
@@ -459,7 +461,8 @@ class OspGroup:
                                      tile_elems, sgd_lr,
                                      {None: 0, True: _capi.GROUP_TMA,
                                       False: _capi.GROUP_REGISTER}[tma]
-                                     | (0 if carry else _capi.GROUP_NO_CARRY))
+                                     | (0 if carry else _capi.GROUP_NO_CARRY)
+                                     | (0 if small else _capi.GROUP_NO_SMALL))
         init = 0
         if init_params is not None:
             _dev_f32(init_params, "init_params")
@@ -512,6 +515,8 @@ class OspGroup:
             raise InvalidArgument("deltas must be a [N, >=M] float32 CUDA tensor")
         if deltas.shape[0] != self.N or deltas.stride(1) != 1:
             raise ShapeError("deltas must have one unit-stride row per worker")
+        if deltas.shape[1] < self.M:
+            raise ShapeError(f"delta rows hold {deltas.shape[1]} elements, the partition {self.M}")
         return _ptr(deltas), deltas.stride(0)
 
     def set_budget(self, budget_bytes: int, stream=None):
@@ -519,6 +524,8 @@ class OspGroup:
 
     def set_gib(self, ics_flags, ics_order, tag: int, stream=None):
         f, fp = _u8(ics_flags)
+        if f.size != self.L:
+            raise ShapeError(f"gib covers {f.size} layers, the partition {self.L}")
         o, op = _i32(ics_order)
         _check(lib().osp_group_set_gib(self._h, fp, op, len(ics_order), tag, _stream(stream)))
 
@@ -571,17 +578,43 @@ class OspGroup:
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_step(self._h, p, ld, _stream(stream)))
 
-    def step_host(self, host_deltas: np.ndarray, stream=None) -> bytes:
-        """End-to-end step from host memory (H2D + step + D2H of the next GIB)."""
+    def step_host(self, host_deltas, stream=None, params_out=None) -> bytes:
+        """End-to-end step from host memory: H2D copy of the N delta rows, the
+        step, and D2H of the next GIB and of the updated global vector (every
+        worker's parameters at the iteration boundary; OspServer::global_params /
+        OspWorker::params). params_out: a host float32 array of M elements to
+        receive it, or None to skip that copy."""
         if isinstance(host_deltas, torch.Tensor):
-            assert host_deltas.device.type == "cpu" and host_deltas.dtype == torch.float32
+            if host_deltas.device.type != "cpu" or host_deltas.dtype != torch.float32:
+                raise InvalidArgument("host deltas must be a float32 CPU tensor")
+            if host_deltas.dim() != 2 or host_deltas.stride(1) != 1:
+                raise ShapeError("host deltas must be [N, >=M] with unit inner stride")
+            shape = tuple(host_deltas.shape)
             ptr, ld = host_deltas.data_ptr(), host_deltas.stride(0)
         else:
-            assert host_deltas.dtype == np.float32 and host_deltas.flags.c_contiguous
-            ptr, ld = host_deltas.ctypes.data, host_deltas.shape[1]
+            if not (isinstance(host_deltas, np.ndarray) and host_deltas.dtype == np.float32):
+                raise InvalidArgument("host deltas must be a float32 numpy array")
+            if host_deltas.ndim != 2 or host_deltas.strides[1] != 4 or host_deltas.strides[0] % 4:
+                raise ShapeError("host deltas must be [N, >=M] with unit inner stride")
+            shape = host_deltas.shape
+            ptr, ld = host_deltas.ctypes.data, host_deltas.strides[0] // 4
+        if shape[0] != self.N or shape[1] < self.M:
+            raise ShapeError(f"host deltas are {list(shape)}, need [{self.N}, >={self.M}]")
+        pout = None
+        if params_out is not None:
+            if isinstance(params_out, torch.Tensor):
+                if not (params_out.device.type == "cpu" and params_out.dtype == torch.float32
+                        and params_out.is_contiguous() and params_out.numel() == self.M):
+                    raise ShapeError("params_out must be a contiguous float32 CPU tensor of M")
+                pout = params_out.data_ptr()
+            else:
+                if not (isinstance(params_out, np.ndarray) and params_out.dtype == np.float32
+                        and params_out.flags.c_contiguous and params_out.size == self.M):
+                    raise ShapeError("params_out must be a contiguous float32 array of M")
+                pout = params_out.ctypes.data
         out = np.empty(int(lib().osp_gib_encoded_size(self.L)), dtype=np.uint8)
         _check(lib().osp_group_step_host(self._h, ptr, ld, out.ctypes.data_as(P(ctypes.c_uint8)),
-                                         _stream(stream)))
+                                         pout, _stream(stream)))
         return out.tobytes()
 
     def read_gib(self, stream=None) -> dict:
@@ -619,6 +652,11 @@ class OspGroup:
                                         ctypes.byref(gb), ctypes.byref(bt)))
         return dict(tile_elems=int(t.value), n_tiles=int(nt.value), grid_blocks=int(gb.value),
                     block_threads=int(bt.value), stage_kernels=self.stage_kernels)
+
+    @property
+    def single_launch(self) -> bool:
+        """True when step() runs as one single-CTA launch (OSP_GROUP_SMALL)."""
+        return bool(lib().osp_group_flags(self._h) & _capi.GROUP_SMALL)
 
     @property
     def stage_kernels(self) -> str:

@@ -41,7 +41,7 @@ def test_host_only_entry_points_without_gpu():
     """GIB codec and tuning are host logic; they run without a device."""
     from paper_2306_16926_b200 import _capi
     lib = _capi.load()
-    assert lib.osp_abi_version() == 1
+    assert lib.osp_abi_version() == 2
     assert lib.osp_gib_encoded_size(1000) == 133
     assert lib.osp_status_name(7) == b"ProtocolError"
     out = ctypes.c_uint64()

@@ -493,13 +493,13 @@ def test_momentum_matches_oracle_on_momentum_deltas(osp, carry):
         osp.OspGroup(part, 8, [0.125] * 8, sgd_lr=lr, tile_elems=2048).set_momentum(0.9)
 
 
-def test_repeated_stage2_resolve_does_not_hang(osp):
+def test_repeated_stage2_resolve_is_refused(osp):
     """Misuse guard for the carry's device-side join: a second stage2_resolve
-    without a stage 1 in between re-broadcasts the same carry (idempotent) and
-    resolves again; it must complete (the join waits for 'reached or passed')."""
+    without a stage 1 in between is a ProtocolError raised on the host (no
+    launch, no hang, state untouched); the group then continues normally."""
     counts = [4096, 1000, 8192, 12, 2048]
     M, N = sum(counts), 4
-    grp = osp.OspGroup(osp.Partition(counts), N, [0.25] * N, n_chunks=2)
+    grp = osp.OspGroup(osp.Partition(counts), N, [0.25] * N, n_chunks=2, small=False)
     grp.set_budget(M * 2)
     X = osp.synth_deltas(3, N, 0, M)
     grp.step(X)
@@ -508,9 +508,12 @@ def test_repeated_stage2_resolve_does_not_hang(osp):
     G = grp.global_params.clone()
     P = grp.worker_params.clone()
     tag = grp.read_gib()["tag"]
-    grp.stage2_resolve(X)
+    with pytest.raises(osp.ProtocolError):
+        grp.stage2_resolve(X)
     torch.cuda.synchronize()
     assert torch.equal(G, grp.global_params) and torch.equal(P, grp.worker_params)
+    assert grp.read_gib()["tag"] == tag
+    grp.step(osp.synth_deltas(3, N, 2, M))
     assert grp.read_gib()["tag"] == tag + 1
 
 
@@ -583,10 +586,45 @@ def test_step_host_matches_device_step(osp):
         a.set_budget(M * 2)
         b.set_budget(M * 2)
         a.step(X)
-        gib = b.step_host(host)
+        params = np.empty(M, np.float32)
+        gib = b.step_host(host, params_out=params)
         assert np.array_equal(bits(a.global_params), bits(b.global_params))
+        assert np.array_equal(params.view(np.uint32), a.global_params.cpu().numpy().view(np.uint32))
         ra = a.read_gib()
         assert gib == oracle.gib_encode(ra["tag"], ra["flags"])
+    # shape errors are raised before any copy (no host out-of-bounds read)
+    with pytest.raises(osp.ShapeError):
+        b.step_host(np.zeros((N - 1, M), np.float32))
+    with pytest.raises(osp.ShapeError):
+        b.step_host(np.zeros((N, M - 1), np.float32))
+    with pytest.raises(osp.ShapeError):
+        b.step_host(np.zeros((N, M), np.float32), params_out=np.zeros(M - 1, np.float32))
+    with pytest.raises(osp.ShapeError):
+        b.set_gib(np.zeros(len(counts) - 1, np.uint8), [], 0)
+    with pytest.raises(osp.ShapeError):
+        b.stage1(torch.zeros((N, 2 * M), device="cuda")[:, : M - 4])
+
+
+def test_stage2_needs_stage1_and_gib_install_waits(osp):
+    """stage 2 before stage 1 of an iteration and a GIB install between stage 1
+    and the resolve are protocol errors (the carry and its list snapshot are
+    written by stage 1)."""
+    counts = [4096, 64, 2048, 1000]
+    M, N = sum(counts), 4
+    part = osp.Partition(counts)
+    g = osp.OspGroup(part, N, [0.25] * N, n_chunks=2)
+    X = osp.synth_deltas(3, N, 0, M)
+    with pytest.raises(osp.ProtocolError):
+        g.stage2_all(X)
+    with pytest.raises(osp.ProtocolError):
+        g.stage2_resolve(X)
+    g.stage1(X)
+    with pytest.raises(osp.ProtocolError):
+        g.set_gib([0, 1, 0, 0], [1], 5)
+    g.stage2_resolve(X)
+    g.set_gib([0, 1, 0, 0], [1], 5)
+    g.step(X)
+    torch.cuda.synchronize()
 
 
 # ---- TMA-staged stage kernels (OSP_GROUP_TMA): same results --------------------
@@ -714,3 +752,144 @@ def test_group_more_than_max_workers_refused(osp):
     part = osp.Partition([100, 200])
     with pytest.raises(osp.InvalidArgument, match="OSP_MAX_WORKERS"):
         osp.OspGroup(part, 65, [1.0 / 65] * 65)
+
+
+# ---- the single-launch step of launch-bound layouts (kernels/step_small.cu) -----
+
+def test_small_step_matches_reference_engine(osp, golden):
+    """osp_group_step as ONE single-CTA launch against the reference-engine
+    goldens whose layout qualifies (L <= 32): every vector, the scores, the
+    next GIB, its rank order and the device-written wire."""
+    g = golden
+    part = osp.Partition(g.counts, g.bpe)
+    grp = osp.OspGroup(part, g.N, list(g.weights), n_chunks=g.n_chunks, init_params=cuda(g.p0))
+    if not (g.L <= 32 and g.M <= 32768 and g.N <= 8):
+        assert not grp.single_launch
+        pytest.skip("layout above the single-launch limits")
+    assert grp.single_launch
+    for it in range(g.iters):
+        X = cuda(g.deltas(it))
+        grp.set_budget(int(g.get(it, "budget")[0]))
+        grp.step(X)
+        G = grp.global_params.cpu().numpy()
+        assert np.array_equal(bits(G), bits(g.get(it, "global"))), f"global, it {it}"
+        P = grp.worker_params.cpu().numpy()
+        for w in range(g.N):
+            assert np.array_equal(bits(P[w]), bits(G)), f"worker {w}, it {it}"
+        np.testing.assert_allclose(grp.scores.cpu().numpy(), g.get(it, "scores"), rtol=SCORE_RTOL,
+                                   atol=0)
+        nxt = grp.read_gib()
+        tag_out, flags_out = oracle.gib_decode(bytes(g.get(it, "gib_out")))
+        assert nxt["tag"] == tag_out == it + 1
+        assert np.array_equal(nxt["flags"], flags_out), f"GIB flags, it {it}"
+        assert np.array_equal(nxt["order"], g.get(it, "order_out")), f"ICS order, it {it}"
+        order_out = np.asarray(g.get(it, "order_out"), dtype="<u4")
+        assert grp.gib_wire() == (bytes(g.get(it, "gib_out")) + struct.pack("<I", order_out.size)
+                                  + order_out.tobytes()), f"GIB wire, it {it}"
+        if it + 1 < g.iters:  # the chunk map the next split uses
+            chunks_ref = Golden.decode_chunks(g.get(it + 1, "chunks"))
+            assert nxt["n_used"] == len(chunks_ref)
+            for c, ids in enumerate(chunks_ref):
+                assert sorted(np.flatnonzero(nxt["chunk_of"] == c).tolist()) == ids
+
+
+@pytest.mark.parametrize("N,L,frac,chunks,sgd", [(8, 4, 0.5, 4, 0.0), (4, 6, 0.9, 3, 0.0),
+                                                  (1, 1, 1.0, 2, 0.0), (3, 32, 0.33, 7, 0.0),
+                                                  (5, 17, 0.0, 4, 0.05), (8, 32, 0.6, 9, 0.0)])
+def test_small_step_vs_oracle_and_three_launch_step(osp, N, L, frac, chunks, sgd):
+    """Random small layouts (odd sizes, unequal weights, random P0, budget edges,
+    fused sgd): the single-launch step equals the oracle and the three-launch
+    step bit for bit over 5 iterations, the two groups mixed freely."""
+    rng = np.random.default_rng(1000 + 7 * N + L)
+    counts = rng.integers(1, max(2, 32768 // L // 2), L)
+    w = list(0.1 + rng.random(N))
+    p0 = rng.uniform(-1, 1, int(counts.sum())).astype(np.float32)
+    grp = oracle_vs_group(osp, counts, N, w, frac, chunks, 5, seed=L, p0=p0, sgd_lr=sgd)
+    assert grp.single_launch
+    M = int(counts.sum())
+    part = osp.Partition(counts)
+    a = osp.OspGroup(part, N, w, n_chunks=chunks, init_params=cuda(p0), sgd_lr=sgd)
+    b = osp.OspGroup(part, N, w, n_chunks=chunks, init_params=cuda(p0), sgd_lr=sgd, small=False)
+    assert a.single_launch and not b.single_launch
+    X = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    for it in range(6):
+        osp.synth_deltas(L, N, it, M, out=X)
+        for grp in (a, b):
+            grp.set_budget(int(frac * M * 4))
+        a.step(X)
+        if it % 2:  # the per-stage API on the small group continues from its lists
+            b.step(X)
+        else:
+            b.stage1(X)
+            b.stage2_resolve(X)
+        assert np.array_equal(bits(a.global_params), bits(b.global_params)), f"it {it}"
+        assert np.array_equal(bits(a.worker_params), bits(b.worker_params)), f"it {it}"
+        ra, rb = a.read_gib(), b.read_gib()
+        for k in ("flags", "order", "chunk_of", "n_used", "tag", "deferred_bytes"):
+            assert np.array_equal(ra[k], rb[k]), f"{k} it {it}"
+        assert a.gib_wire() == b.gib_wire()
+        assert np.array_equal(a.deferred_history(ra["tag"], 1), b.deferred_history(rb["tag"], 1))
+    a.stage1(X)  # the per-stage path after single-launch steps
+    a.stage2_resolve(X)
+    b.step(X)
+    assert np.array_equal(bits(a.global_params), bits(b.global_params))
+
+
+def test_small_step_certificate_fallback(osp):
+    """Exact ties (identical layers) in a small layout: the warp resolve cannot
+    certify the order from tile sums, recomputes the tied layers sequentially
+    and reproduces the reference's stable order."""
+    counts = [700, 700, 33, 700]
+    M, N = sum(counts), 4
+    part = osp.Partition(counts)
+    grp = osp.OspGroup(part, N, [0.25] * N, n_chunks=2)
+    assert grp.single_launch
+    G = np.zeros(M, np.float32)
+    P = np.zeros((N, M), np.float32)
+    flags, order = np.zeros(4, np.uint8), np.zeros(0, np.int32)
+    budget = int(0.6 * M * 4)
+    X = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    for it in range(3):
+        osp.synth_deltas(7, N, it, M, out=X)
+        X[:, 700:1400] = X[:, :700]
+        X[:, 1433:] = X[:, :700]
+        r = oracle.step(counts, 4, [0.25] * N, X.cpu().numpy(), G, P, flags, order, 2, budget)
+        grp.set_budget(budget)
+        grp.step(X)
+        assert np.array_equal(bits(grp.global_params), bits(G)), f"global, it {it}"
+        assert np.array_equal(bits(grp.worker_params), bits(P)), f"workers, it {it}"
+        nxt = grp.read_gib()
+        assert np.array_equal(nxt["flags"], r["flags_out"]), f"flags, it {it}"
+        assert np.array_equal(nxt["order"], r["order_out"]), f"order, it {it}"
+        flags, order = r["flags_out"], r["order_out"]
+    st = grp.stats()
+    assert st["fallback_resolves"] == 3 and st["fallback_layers"] >= 9
+
+
+def test_small_step_in_cuda_graph(osp):
+    """The single-launch step replayed from a CUDA graph equals direct steps."""
+    counts = [256, 32, 128, 4]
+    M, N = sum(counts), 8
+    part = osp.Partition(counts)
+    X = [osp.synth_deltas(11, N, i, M) for i in range(2)]
+    a = osp.OspGroup(part, N, n_chunks=4)
+    b = osp.OspGroup(part, N, n_chunks=4)
+    assert b.single_launch
+    for grp in (a, b):
+        grp.set_budget(M * 2)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.graph(graph, stream=cs, capture_error_mode="thread_local"):
+        b.step(X[0])
+        b.step(X[1])
+    torch.cuda.synchronize()
+    for r in range(3):
+        a.step(X[0])
+        a.step(X[1])
+        graph.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(a.global_params), bits(b.global_params)), f"replay {r}"
+        assert np.array_equal(bits(a.worker_params), bits(b.worker_params)), f"replay {r}"
+        assert a.gib_wire() == b.gib_wire()
