@@ -467,6 +467,23 @@ def b200_single(args):
 
         ovl = overlap.run(lambda i: grp.stage1(X[i % 2]), s2r, comp, K=min(K, 50), W=3)
         ovl["t_c_ms"] = comp.ms
+        ovl["budget_frac"] = args.budget_frac
+        # closed-loop budget (runner.cpp:364-376, protocol.cpp:396-405): the SGU
+        # budget per epoch from the measured compute time and the measured rate
+        # of the synchronization traffic (HBM bytes of the step on one GPU)
+        from paper_2306_16926_b200.budget import BudgetLoop
+        ipe = 5
+        loop = BudgetLoop(ipe, N, model_bytes)
+        tag_cl = grp.read_gib()["tag"]
+
+        def link_bytes(j):
+            uj = float(grp.deferred_history(tag_cl + j, 1)[0]) / model_bytes
+            return 4.0 * M * ((2 * N + 2) + uj * ((N + 2) if carry else (2 * N + 1)))
+
+        ovl["closed_loop"] = overlap.run_closed_loop(lambda i: grp.stage1(X[i % 2]), s2r,
+                                                     grp.set_budget, comp, loop, link_bytes,
+                                                     K=30, ipe=ipe)
+        grp.set_budget(budget)
 
     # ---- e2e through the C-ABI with host buffers (pinned): H2D of the step's N
     # delta rows, the step, D2H of the next GIB and of the updated global vector

@@ -141,6 +141,20 @@ osp_status osp_rank_and_gib(const osp_partition* part, const double* scores_host
                             uint64_t budget_bytes, int32_t* order_host, uint8_t* ics_flags_host,
                             void* stream);
 
+/* The resolution's importance -> GIB step (OspServer::check_resolution,
+ * protocol.cpp:407-419: pgp_layer_importance + rank_layers + build_gib) on
+ * DEVICE vectors, the way the group path does it: per-tile tree sums of
+ * |grads * params|, a per-layer interval certificate against the reference's
+ * sequential sum, the exact sequential sum only for layers whose intervals
+ * touch, then the stable (score, id) rank and the prefix rule under
+ * budget_bytes. The deferred set and its rank order equal the reference's
+ * bit for bit. HOST outputs (any may be NULL): scores [L] (the tree sums, exact
+ * where recomputed), the deferred ids in rank order (*n_ics of them, capacity
+ * L), flags [L]. Synchronises `stream`. */
+osp_status osp_pgp_rank_gib(const osp_partition* part, const float* params, const float* grads,
+                            uint64_t budget_bytes, double* scores_host, int32_t* ics_order_host,
+                            int64_t* n_ics, uint8_t* ics_flags_host, void* stream);
+
 /* split_for_sync (protocol.cpp:122-166) index lists (payload copies are not
  * made: the device path works on segment lists). HOST in/out. rs_ids gets the
  * RS layer ids ascending; chunk_of[l] the compacted chunk of each deferred layer
@@ -353,22 +367,24 @@ osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_ti
 /* ------------------------------------------------------------------------
  * Shard: the multi-GPU path, one process per GPU (PS sharded one shard per
  * GPU). Rank r hosts workers [r*N/P, (r+1)*N/P) and a full
- * replica of the global vector. Per stage, the owner of each tile of the
- * stage's tile sequence reads every worker's delta rows from the peers' HBM
- * over NVLink (CUDA IPC), aggregates them in the reference's fixed worker
- * order in fp64 (push = reduce-scatter, bit-exact) and stores the result
- * into every rank's buffer (pull = all-gather); each rank applies locally and
- * resolves the identical next GIB.
+ * replica of the global vector. A stage's exchanged tile sequence is cut into
+ * P owner ranges; the owner of a tile reads every worker's delta rows (its own
+ * from HBM, the peers' straight out of their HBM over NVLink, CUDA IPC),
+ * aggregates them in the reference's fixed worker order in fp64 (push =
+ * reduce-scatter, bit-exact), applies locally and stores the aggregate into
+ * every rank's pull buffer (pull = all-gather), then raises the tile's flag on
+ * every peer, which applies it as soon as it lands. Push, aggregate, pull and
+ * apply are ONE kernel per stage (kernels/shard_x.cu); the cross-GPU ordering
+ * is per tile inside it, and every rank resolves the identical next GIB.
  *
- * Default (barrier) mode: per stage an aggregate kernel (the owners' push +
- * pull) and an apply kernel, ordered across GPUs by epoch flags the kernels
- * signal and wait on themselves (no barrier launches); stage 1's apply runs in
- * the same launch as stage 2's aggregate. Streaming mode (opt-in with
- * OSP_SHARD_STREAM=1 in the environment at create; N in {1,2,4,8}, tile_elems
- * 1024/2048, default 2048): one kernel per stage, tiles dealt round-robin to
- * owners, each owner publishes a tile with a per-tile ready flag and the other
- * ranks apply it as the flag lands — no grid-wide barrier. Both are
- * bit-identical; barrier mode is faster on the measured configurations.
+ * Modes. Default: ONE exchange per iteration — stage 1 moves every tile, the
+ * deferred (ICS) layers' aggregate is kept in the carry (the payload split at
+ * stage 1, as split_for_sync copies it, protocol.cpp:122-166) and the
+ * worker rows get the LGP local estimate; stage 2 is then a local broadcast of
+ * the carry (no NVLink traffic). OSP_SHARD_DEFER_ICS: stage 1 exchanges the
+ * barrier (RS) layers only and stage 2 exchanges the deferred chunks — the
+ * OSP schedule in which the ICS traffic runs beside the next iteration's
+ * compute on a side stream. Both are bit-identical to the oracle.
  *
  * Setup: create on every rank, export a handle, exchange the handles (e.g.
  * torch.distributed all_gather), connect with all of them (rank order).
@@ -377,6 +393,7 @@ osp_status osp_group_geometry(osp_group* g, uint32_t* tile_elems, uint64_t* n_ti
  * fill one while stage 2 still reads the other).
  * ---------------------------------------------------------------------- */
 #define OSP_SHARD_HANDLE_BYTES 512
+#define OSP_SHARD_DEFER_ICS 1u
 typedef struct osp_shard osp_shard;
 typedef struct osp_shard_config {
     int world;              /* ranks (GPUs), <= 8 */
@@ -384,8 +401,9 @@ typedef struct osp_shard_config {
     int n_workers;          /* N total logical workers, N % world == 0 */
     const double* weights;  /* HOST, N weights (all workers) */
     int n_chunks;
-    uint32_t tile_elems;    /* 0 = default */
+    uint32_t tile_elems;    /* 0 = default 1024; power of two in [512, 4096] */
     double sgd_lr;          /* 0 = deltas; > 0 fused sgd_delta */
+    uint32_t flags;         /* OSP_SHARD_* bits */
 } osp_shard_config;
 
 osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* cfg,
@@ -400,24 +418,21 @@ float* osp_shard_deltas(osp_shard* s, int buf, uint64_t* ld);
 /* The rank-local state (global replica, worker rows, GIB, stats): use the
  * osp_group_* getters on it. Do not step it directly. */
 osp_group* osp_shard_group(osp_shard* s);
+/* 1 when stage 2 exchanges the deferred layers (OSP_SHARD_DEFER_ICS, or a
+ * local group without the carry buffer), 0 for the single-exchange default. */
+int osp_shard_deferred_ics(const osp_shard* s);
 osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream);
+/* ProtocolError before stage 1 of the iteration. */
 osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream);
 osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream);
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream);
-/* One osp_shard_step with CUDA events between the kernels (synchronises
- * `stream`). Streaming mode: ms[0..2] = stage 1, stage 2 (all chunks),
- * resolve. Barrier mode: ms[0..3] = stage-1 aggregate (with the entry wait),
- * stage-1 apply fused with the stage-2 aggregate, stage-2 apply, resolve (each
- * including its in-kernel cross-GPU wait). Unused entries are 0. */
+/* One step with CUDA events between the phases (synchronises `stream`):
+ * ms[0] = stage 1 (exchange kernel), ms[1] = stage 2, ms[2] = resolve. */
 osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream);
-/* Diagnostics: this rank's part of a stage's push/pull (k_shard_agg: peers'
- * rows over NVLink, fixed-order aggregate, stores into every rank) launched
- * alone, without the cross-GPU ordering, so a profiler that serialises kernels
- * (ncu) can replay it. The peers must be idle with their rows in place; the
- * results are those of a normal stage only if nothing else runs. */
+/* Diagnostics: this rank's own tiles of a stage's exchange launched alone (no
+ * cross-GPU waits, no flags), so a profiler that serialises kernels (ncu) can
+ * replay it. The peers must be idle with their rows in place. */
 osp_status osp_shard_solo_agg(osp_shard* s, int stage, int buf, void* stream);
-/* 1 if the shard runs the streaming kernels, 0 for barrier mode. */
-int osp_shard_streaming(const osp_shard* s);
 /* ProtocolError if a cross-GPU wait timed out (synchronises `stream`). */
 osp_status osp_shard_check(osp_shard* s, void* stream);
 /* Synthetic deltas of workers [worker0, worker0+n_workers) into [n_workers][ld]. */

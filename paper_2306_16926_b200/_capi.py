@@ -34,10 +34,11 @@ GROUP_SMALL = 16
 
 class osp_shard_config(ctypes.Structure):
     _fields_ = [("world", c_int), ("rank", c_int), ("n_workers", c_int), ("weights", P(c_dbl)),
-                ("n_chunks", c_int), ("tile_elems", c_u32), ("sgd_lr", c_dbl)]
+                ("n_chunks", c_int), ("tile_elems", c_u32), ("sgd_lr", c_dbl), ("flags", c_u32)]
 
 
 SHARD_HANDLE_BYTES = 512
+SHARD_DEFER_ICS = 1
 
 
 class osp_sgu_schedule(ctypes.Structure):
@@ -78,6 +79,8 @@ _SIGS = {
     "osp_lgp_correct": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(ctypes.c_int32),
                                 c_i64, c_void_p]),
     "osp_pgp_layer_importance": (c_int, [c_void_p, c_void_p, c_void_p, P(c_dbl), c_void_p]),
+    "osp_pgp_rank_gib": (c_int, [c_void_p, c_void_p, c_void_p, c_u64, P(c_dbl), P(ctypes.c_int32),
+                                 P(c_i64), P(ctypes.c_uint8), c_void_p]),
     "osp_rank_and_gib": (c_int, [c_void_p, P(c_dbl), c_u64, P(ctypes.c_int32),
                                  P(ctypes.c_uint8), c_void_p]),
     "osp_split_for_sync": (c_int, [c_void_p, P(ctypes.c_uint8), P(ctypes.c_int32), c_i64,
@@ -140,7 +143,7 @@ _SIGS = {
     "osp_shard_resolve": (c_int, [c_void_p, c_int, c_void_p]),
     "osp_shard_step": (c_int, [c_void_p, c_int, c_void_p]),
     "osp_shard_check": (c_int, [c_void_p, c_void_p]),
-    "osp_shard_streaming": (c_int, [c_void_p]),
+    "osp_shard_deferred_ics": (c_int, [c_void_p]),
     "osp_shard_profile": (c_int, [c_void_p, c_int, P(ctypes.c_float), c_void_p]),
     "osp_shard_solo_agg": (c_int, [c_void_p, c_int, c_int, c_void_p]),
     "osp_synth_deltas_range": (c_int, [c_u64, c_int, c_int, c_u64, c_u64, c_void_p, c_u64,

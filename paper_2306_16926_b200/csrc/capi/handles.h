@@ -14,6 +14,9 @@ struct osp_partition {
     uint32_t bpe = 4;
     uint64_t* d_offsets = nullptr;
     uint64_t* d_counts = nullptr;
+    // lazily created one-worker group whose tile tables, lists and resolve
+    // buffers serve osp_pgp_rank_gib (the certified resolve of given vectors)
+    struct osp_group* scratch = nullptr;
 };
 
 struct osp_group {

@@ -240,6 +240,7 @@ osp_status osp_partition_create(const uint64_t* layer_counts, uint64_t n_layers,
 
 void osp_partition_destroy(osp_partition* p) {
     if (!p) return;
+    if (p->scratch) osp_group_destroy(p->scratch);
     if (p->d_offsets) cudaFree(p->d_offsets);
     if (p->d_counts) cudaFree(p->d_counts);
     delete p;
@@ -444,6 +445,52 @@ osp_status osp_rank_and_gib(const osp_partition* part, const double* scores_host
     cudaFreeAsync(dfl, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return cuda_fail(e, "rank_and_gib");
+    return OSP_OK;
+}
+
+osp_status osp_pgp_rank_gib(const osp_partition* part, const float* params, const float* grads,
+                            uint64_t budget_bytes, double* scores_host, int32_t* ics_order_host,
+                            int64_t* n_ics, uint8_t* ics_flags_host, void* stream) {
+    if (!part || !params || !grads) return fail(OSP_ERR_INVALID, "null argument");
+    const int L = static_cast<int>(part->counts.size());
+    if (L > kMaxLayers)
+        return fail(OSP_ERR_INVALID, "more than " + std::to_string(kMaxLayers) + " layers");
+    cudaStream_t s = as_stream(stream);
+    auto* mp = const_cast<osp_partition*>(part);
+    if (!mp->scratch) {
+        const double w1 = 1.0;
+        osp_group_config gc{1, &w1, 1, 0, 0.0, OSP_GROUP_REGISTER};
+        OSP_TRY(osp_group_create(part, &gc, nullptr, stream, &mp->scratch));
+    }
+    // the group's resolve over the caller's vectors: tile partials of
+    // |grads * params|, tree sums, certificate, exact sequential fallback on
+    // touching intervals (reading agg_full = grads, G = params), rank, prefix rule
+    GroupView v = mp->scratch->v;
+    v.G = const_cast<float*>(params);
+    v.agg_full = grads;
+    v.C = nullptr;
+    OSP_CUDA(launch_pgp_tiles(v, params, grads, s));
+    OSP_CUDA(launch_set_budget(v, budget_bytes, s));
+    OSP_CUDA(launch_resolve(v, mp->scratch->ap, grads, part->total, s));
+    int meta[8];
+    std::vector<double> sc(L), ex(L);
+    std::vector<uint8_t> mk(L);
+    OSP_CUDA(cudaMemcpyAsync(meta, v.meta, sizeof meta, cudaMemcpyDeviceToHost, s));
+    if (scores_host) {
+        OSP_CUDA(cudaMemcpyAsync(sc.data(), v.scores, L * sizeof(double), cudaMemcpyDeviceToHost, s));
+        OSP_CUDA(cudaMemcpyAsync(ex.data(), v.exact, L * sizeof(double), cudaMemcpyDeviceToHost, s));
+        OSP_CUDA(cudaMemcpyAsync(mk.data(), v.marked, L, cudaMemcpyDeviceToHost, s));
+    }
+    if (ics_flags_host) OSP_CUDA(cudaMemcpyAsync(ics_flags_host, v.flags, L, cudaMemcpyDeviceToHost, s));
+    std::vector<int32_t> ord(L);
+    if (ics_order_host)
+        OSP_CUDA(cudaMemcpyAsync(ord.data(), v.ics_layers, L * 4, cudaMemcpyDeviceToHost, s));
+    OSP_CUDA(cudaStreamSynchronize(s));
+    const int k = meta[META_N_ICS];
+    if (n_ics) *n_ics = k;
+    if (ics_order_host) std::copy(ord.begin(), ord.begin() + k, ics_order_host);
+    if (scores_host)
+        for (int l = 0; l < L; ++l) scores_host[l] = mk[l] ? ex[l] : sc[l];
     return OSP_OK;
 }
 

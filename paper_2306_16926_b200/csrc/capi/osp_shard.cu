@@ -2,12 +2,13 @@
 //
 // One process per GPU. Rank r hosts workers [r*N/P, (r+1)*N/P), a full replica
 // of the global vector, and the PS shard of every stage's tile sequence. The
-// push (reduce-scatter) and the pull (all-gather) are fused into k_shard_agg
-// over CUDA-IPC peer mappings of the other ranks' delta rows and agg buffers;
-// cross-GPU ordering uses epoch flags on peer-mapped slots that the kernels
-// signal and wait on themselves (XSync in stage.cu). The local state
-// (G replica, worker rows, PGP partials, GIB lists) is an osp_group with the
-// rank's workers, so resolve and every read-back reuse the group code.
+// push (reduce-scatter), fixed-order aggregation, pull (all-gather) and local
+// apply of a stage run in ONE kernel (kernels/shard_x.cu) over CUDA-IPC peer
+// mappings of the other ranks' delta rows, pull buffers, partials and flags;
+// the cross-GPU ordering is per tile inside that kernel. The local state
+// (G replica, worker rows, carry, PGP partials, GIB lists) is an osp_group with
+// the rank's workers, so the stage-2 broadcast, the resolve and every read-back
+// reuse the group code.
 
 #include <cuda_runtime.h>
 
@@ -22,16 +23,13 @@ using namespace osp;
 
 namespace {
 
-constexpr uint32_t kMagic = 0x0500b200u;
+constexpr uint32_t kMagic = 0x0600b200u;
 
 struct ShardHandle {
     uint32_t magic;
-    int32_t rank, world, n_loc;
-    uint64_t M, L, ldX, buf_stride;
-    cudaIpcMemHandle_t hx, hagg, hflags;
-    int32_t stream;      // streaming kernel in use
-    uint64_t NT;         // tiles (streaming mode)
-    cudaIpcMemHandle_t htf, hpart;
+    int32_t rank, world, n_loc, deferred;
+    uint64_t M, L, NT, ldX, buf_stride;
+    cudaIpcMemHandle_t hx, hagg, hpart, htflag, hready;
 };
 static_assert(sizeof(ShardHandle) <= OSP_SHARD_HANDLE_BYTES, "handle too large");
 
@@ -41,28 +39,20 @@ struct osp_shard {
     osp_group* grp = nullptr;  // local state: rank's workers
     const osp_partition* part = nullptr;
     int world = 1, rank = 0, n_loc = 1, N = 1, n_chunks = 1;
+    bool deferred = false;     // OSP_SHARD_DEFER_ICS (or no carry buffer): stage 2 exchanges
     AggParams ap_all{};        // every worker, global weights (aggregation)
-    AggParams ap_loc{};        // local workers (sgd conversion on the local estimate)
     float* X = nullptr;        // [2][n_loc][ldX] local delta rows, IPC-exported
     uint64_t ldX = 0, buf_stride = 0;
-    float* agg = nullptr;      // [ldX] agg_full, IPC-exported
-    unsigned* flags = nullptr; // [kBarKinds][kMaxRanks], IPC-exported
+    float* agg = nullptr;      // [ldX] pull buffer, IPC-exported (the group's agg_full)
+    unsigned* tflag = nullptr; // [NT] per-tile ready flags, IPC-exported
+    unsigned* ready = nullptr; // [kMaxRanks] deltas-ready slots, IPC-exported
     unsigned* error = nullptr; // [1] local
-    PeerTable pt[2]{};         // per delta buffer
+    XArgs xa[2]{};             // per delta buffer
     std::vector<void*> opened; // peer mappings to close
     bool connected = false;
-    // streaming mode (kernels/shard_stream.cu)
-    bool stream = false;
-    uint64_t NT = 0;
-    unsigned* tflag = nullptr; // [NT] per-tile ready flags, IPC-exported
-    double* pbuf = nullptr;    // [NT] per-tile PGP partials (the group's), IPC-exported
-    StreamArgs sa{};           // peer tables of tflag/pbuf
-    int vec[2]{};              // per delta buffer: 16-byte aligned rows
-    unsigned iter = 0;         // iterations started (stage-1 launches)
-    unsigned xep[4] = {0, 0, 0, 0};  // barrier mode: epochs of the in-kernel cross-GPU syncs
-                                     // (kinds 0, 1, 2 and 4)
-    bool pipe = false;               // pipelined step (OSP_SHARD_PIPE, barrier mode)
-    unsigned long long* dbg = nullptr;  // [2 stages][3 roles][16] diagnostics counters (OSP_SS_DEBUG=1)
+    unsigned iter = 0;         // iterations started (stage-1 launches) = tile-flag epoch
+    bool s1_open = false;      // stage 1 issued, iteration not yet resolved
+    int lag = 2;
 };
 
 extern "C" {
@@ -78,11 +68,17 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
         return fail(OSP_ERR_CONFIG, "worker count out of range");
     if (cfg->n_workers % cfg->world != 0)
         return fail(OSP_ERR_CONFIG, "workers must split evenly across ranks");
+    if (cfg->flags & ~OSP_SHARD_DEFER_ICS) return fail(OSP_ERR_INVALID, "unknown osp_shard_config flags");
     for (int w = 0; w < cfg->n_workers; ++w)
         if (cfg->weights[w] <= 0) return fail(OSP_ERR_CONFIG, "subset weight must be positive");
     double tw = 0.0;
     for (int w = 0; w < cfg->n_workers; ++w) tw += cfg->weights[w];
     if (!(tw > 0.0)) return fail(OSP_ERR_PROTOCOL, "aggregation weights must sum > 0");
+    const uint32_t T = cfg->tile_elems ? cfg->tile_elems : kDefaultTmaTile;
+    if (T < 512 || T > 4096 || (T & (T - 1)))
+        return fail(OSP_ERR_INVALID, "shard tile_elems must be a power of two in [512, 4096]");
+    if (!shard_x_supported(cfg->n_workers, static_cast<int>(T), static_cast<int>(part->counts.size())))
+        return fail(OSP_ERR_INVALID, "shard exchange ring and layer tables exceed shared memory");
 
     auto* s = new osp_shard();
     s->part = part;
@@ -92,54 +88,37 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     s->n_loc = cfg->n_workers / cfg->world;
     s->n_chunks = cfg->n_chunks;
     s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
-    s->ap_loc = make_agg_params(s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->sgd_lr);
-    // streaming kernel (opt-in: OSP_SHARD_STREAM=1) when the shape supports it;
-    // barrier mode is the default (faster on the measured configurations, see
-    // DESIGN.md "Multi-GPU")
-    const char* se = std::getenv("OSP_SHARD_STREAM");
-    const uint32_t Ts = cfg->tile_elems ? cfg->tile_elems : 2048u;
-    s->stream = (se && se[0] == '1') &&
-                shard_stream_supported(s->N, static_cast<int>(Ts), static_cast<int>(part->counts.size()));
-    const char* pe = std::getenv("OSP_SHARD_PIPE");
-    s->pipe = !s->stream && pe && pe[0] == '1';
-    osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks,
-                        s->stream ? Ts : cfg->tile_elems, cfg->sgd_lr, OSP_GROUP_REGISTER};
+    if (const char* lg = std::getenv("OSP_SHARD_LAG")) s->lag = std::max(0, std::atoi(lg));
+    // the local group: default (TMA-staged, carry) so the stage-2 broadcast and
+    // the overlapped resolve are the single-GPU kernels; no single-launch step
+    osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks, T, cfg->sgd_lr,
+                        OSP_GROUP_NO_SMALL};
     osp_status st = osp_group_create(part, &gc, init_params, stream, &s->grp);
     if (st != OSP_OK) {
         delete s;
         return st;
     }
+    s->deferred = (cfg->flags & OSP_SHARD_DEFER_ICS) || s->grp->v.C == nullptr;
     const uint64_t M = part->total;
     s->ldX = (M + 3) & ~uint64_t(3);
     s->buf_stride = s->ldX * s->n_loc;
+    const uint64_t NT = static_cast<uint64_t>(s->grp->v.NT);
     cudaError_t e = cudaMalloc(&s->X, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&s->agg, s->ldX * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&s->flags, kBarKinds * kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->tflag, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->ready, kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&s->error, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->X, 0, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(s->agg, 0, s->ldX * sizeof(float));
-    if (e == cudaSuccess) e = cudaMemset(s->flags, 0, kBarKinds * kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->ready, 0, kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
-    if (s->stream) {
-        const char* de = std::getenv("OSP_SS_DEBUG");
-        if (de && de[0] == '1') {
-            if (e == cudaSuccess) e = cudaMalloc(&s->dbg, 96 * sizeof(unsigned long long));
-            if (e == cudaSuccess) e = cudaMemset(s->dbg, 0, 96 * sizeof(unsigned long long));
-        }
-        s->NT = static_cast<uint64_t>(s->grp->v.NT);
-        const uint64_t nt = s->NT ? s->NT : 1;
-        if (e == cudaSuccess) e = cudaMalloc(&s->tflag, nt * sizeof(unsigned));
-        if (e == cudaSuccess) e = cudaMalloc(&s->pbuf, nt * sizeof(double));
-        if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, nt * sizeof(unsigned));
-        if (e == cudaSuccess) e = cudaMemset(s->pbuf, 0, nt * sizeof(double));
-    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         osp_shard_destroy(s);
         return cuda_fail(e, "shard buffers");
     }
-    s->grp->v.agg_full = s->agg;
-    if (s->stream) s->grp->v.partials = s->pbuf;  // resolve reads the exchanged partials
+    s->grp->v.agg_full = s->agg;  // the resolve's exact fallback reads the applied aggregate
     *out = s;
     return OSP_OK;
 }
@@ -150,11 +129,9 @@ void osp_shard_destroy(osp_shard* s) {
     for (void* p : s->opened) cudaIpcCloseMemHandle(p);
     if (s->X) cudaFree(s->X);
     if (s->agg) cudaFree(s->agg);
-    if (s->flags) cudaFree(s->flags);
-    if (s->error) cudaFree(s->error);
     if (s->tflag) cudaFree(s->tflag);
-    if (s->dbg) cudaFree(s->dbg);
-    if (s->pbuf) cudaFree(s->pbuf);
+    if (s->ready) cudaFree(s->ready);
+    if (s->error) cudaFree(s->error);
     if (s->grp) osp_group_destroy(s->grp);
     delete s;
 }
@@ -168,19 +145,17 @@ osp_status osp_shard_export(osp_shard* s, uint8_t* handle) {
     h.rank = s->rank;
     h.world = s->world;
     h.n_loc = s->n_loc;
+    h.deferred = s->deferred ? 1 : 0;
     h.M = s->part->total;
     h.L = s->part->counts.size();
+    h.NT = static_cast<uint64_t>(s->grp->v.NT);
     h.ldX = s->ldX;
     h.buf_stride = s->buf_stride;
     OSP_CUDA(cudaIpcGetMemHandle(&h.hx, s->X));
     OSP_CUDA(cudaIpcGetMemHandle(&h.hagg, s->agg));
-    OSP_CUDA(cudaIpcGetMemHandle(&h.hflags, s->flags));
-    h.stream = s->stream ? 1 : 0;
-    h.NT = s->NT;
-    if (s->stream) {
-        OSP_CUDA(cudaIpcGetMemHandle(&h.htf, s->tflag));
-        OSP_CUDA(cudaIpcGetMemHandle(&h.hpart, s->pbuf));
-    }
+    OSP_CUDA(cudaIpcGetMemHandle(&h.hpart, s->grp->v.partials));
+    OSP_CUDA(cudaIpcGetMemHandle(&h.htflag, s->tflag));
+    OSP_CUDA(cudaIpcGetMemHandle(&h.hready, s->ready));
     std::memset(handle, 0, OSP_SHARD_HANDLE_BYTES);
     std::memcpy(handle, &h, sizeof h);
     return OSP_OK;
@@ -190,68 +165,57 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     if (!s || !handles) return fail(OSP_ERR_INVALID, "null argument");
     if (s->connected) return fail(OSP_ERR_PROTOCOL, "shard already connected");
     std::vector<const float*> xbase(s->world);
-    std::vector<float*> aggs(s->world);
-    std::vector<unsigned*> flags(s->world);
+    XArgs base{};
     for (int q = 0; q < s->world; ++q) {
         ShardHandle h;
         std::memcpy(&h, handles + static_cast<size_t>(q) * OSP_SHARD_HANDLE_BYTES, sizeof h);
         if (h.magic != kMagic || h.rank != q || h.world != s->world || h.n_loc != s->n_loc ||
-            h.M != s->part->total || h.L != s->part->counts.size() || h.ldX != s->ldX ||
-            h.buf_stride != s->buf_stride || h.stream != (s->stream ? 1 : 0) || h.NT != s->NT)
+            h.M != s->part->total || h.L != s->part->counts.size() ||
+            h.NT != static_cast<uint64_t>(s->grp->v.NT) || h.ldX != s->ldX ||
+            h.buf_stride != s->buf_stride || h.deferred != (s->deferred ? 1 : 0))
             return fail(OSP_ERR_CONFIG, "rank " + std::to_string(q) +
-                                            " exported an incompatible shard (partition, worker "
-                                            "split or world size differ)");
+                                            " exported an incompatible shard (partition, tiles, "
+                                            "worker split, mode or world size differ)");
         if (q == s->rank) {
             xbase[q] = s->X;
-            aggs[q] = s->agg;
-            flags[q] = s->flags;
-            s->sa.tflag[q] = s->tflag;
-            s->sa.part[q] = s->pbuf;
+            base.agg[q] = s->agg;
+            base.part[q] = s->grp->v.partials;
+            base.tflag[q] = s->tflag;
+            base.ready[q] = s->ready;
             continue;
         }
-        if (s->stream) {
-            void *pt = nullptr, *pp = nullptr;
-            OSP_CUDA(cudaIpcOpenMemHandle(&pt, h.htf, cudaIpcMemLazyEnablePeerAccess));
-            s->opened.push_back(pt);
-            OSP_CUDA(cudaIpcOpenMemHandle(&pp, h.hpart, cudaIpcMemLazyEnablePeerAccess));
-            s->opened.push_back(pp);
-            s->sa.tflag[q] = static_cast<unsigned*>(pt);
-            s->sa.part[q] = static_cast<double*>(pp);
+        void* p[5] = {};
+        const cudaIpcMemHandle_t* hs[5] = {&h.hx, &h.hagg, &h.hpart, &h.htflag, &h.hready};
+        for (int k = 0; k < 5; ++k) {
+            OSP_CUDA(cudaIpcOpenMemHandle(&p[k], *hs[k], cudaIpcMemLazyEnablePeerAccess));
+            s->opened.push_back(p[k]);
         }
-        void *px = nullptr, *pa = nullptr, *pf = nullptr;
-        OSP_CUDA(cudaIpcOpenMemHandle(&px, h.hx, cudaIpcMemLazyEnablePeerAccess));
-        s->opened.push_back(px);
-        OSP_CUDA(cudaIpcOpenMemHandle(&pa, h.hagg, cudaIpcMemLazyEnablePeerAccess));
-        s->opened.push_back(pa);
-        OSP_CUDA(cudaIpcOpenMemHandle(&pf, h.hflags, cudaIpcMemLazyEnablePeerAccess));
-        s->opened.push_back(pf);
-        xbase[q] = static_cast<const float*>(px);
-        aggs[q] = static_cast<float*>(pa);
-        flags[q] = static_cast<unsigned*>(pf);
+        xbase[q] = static_cast<const float*>(p[0]);
+        base.agg[q] = static_cast<float*>(p[1]);
+        base.part[q] = static_cast<double*>(p[2]);
+        base.tflag[q] = static_cast<unsigned*>(p[3]);
+        base.ready[q] = static_cast<unsigned*>(p[4]);
     }
+    base.error = s->error;
+    base.world = s->world;
+    base.rank = s->rank;
+    base.n_loc = s->n_loc;
+    base.slot_rows = x_slot_rows(s->N);
+    base.lag = s->lag;
     for (int b = 0; b < 2; ++b) {
-        PeerTable& pt = s->pt[b];
-        pt = PeerTable{};
-        pt.world = s->world;
-        pt.rank = s->rank;
-        pt.n_loc = s->n_loc;
-        const char* lm = std::getenv("OSP_PEER_LOAD");
-        pt.ldmode = lm ? std::atoi(lm) : 2;  // default-cached peer loads measured fastest
-        for (int w = 0; w < s->N; ++w) {
-            const int q = w / s->n_loc, i = w % s->n_loc;
-            pt.xrow[w] = xbase[q] + b * s->buf_stride + static_cast<uint64_t>(i) * s->ldX;
-        }
-        for (int q = 0; q < s->world; ++q) {
-            pt.agg[q] = aggs[q];
-            pt.flags[q] = flags[q];
-        }
-        pt.error = s->error;
+        XArgs& xa = s->xa[b];
+        xa = base;
         bool vec = (s->ldX % 4 == 0) && (s->grp->v.ldP % 4 == 0) &&
                    (reinterpret_cast<uintptr_t>(s->grp->v.G) % 16 == 0) &&
-                   (reinterpret_cast<uintptr_t>(s->grp->v.P) % 16 == 0);
-        for (int w = 0; w < s->N; ++w) vec = vec && (reinterpret_cast<uintptr_t>(pt.xrow[w]) % 16 == 0);
-        for (int q = 0; q < s->world; ++q) vec = vec && (reinterpret_cast<uintptr_t>(pt.agg[q]) % 16 == 0);
-        s->vec[b] = vec ? 1 : 0;
+                   (reinterpret_cast<uintptr_t>(s->grp->v.P) % 16 == 0) &&
+                   (!s->grp->v.C || reinterpret_cast<uintptr_t>(s->grp->v.C) % 16 == 0);
+        for (int w = 0; w < s->N; ++w) {
+            const int q = w / s->n_loc, i = w % s->n_loc;
+            xa.xrow[w] = xbase[q] + b * s->buf_stride + static_cast<uint64_t>(i) * s->ldX;
+            vec = vec && (reinterpret_cast<uintptr_t>(xa.xrow[w]) % 16 == 0);
+        }
+        for (int q = 0; q < s->world; ++q) vec = vec && (reinterpret_cast<uintptr_t>(xa.agg[q]) % 16 == 0);
+        xa.vec = vec ? 1 : 0;
     }
     s->connected = true;
     return OSP_OK;
@@ -265,6 +229,8 @@ float* osp_shard_deltas(osp_shard* s, int buf, uint64_t* ld) {
 
 osp_group* osp_shard_group(osp_shard* s) { return s ? s->grp : nullptr; }
 
+int osp_shard_deferred_ics(const osp_shard* s) { return s && s->deferred ? 1 : 0; }
+
 static osp_status check_ready(osp_shard* s, int buf) {
     if (!s) return fail(OSP_ERR_INVALID, "null shard");
     if (!s->connected) return fail(OSP_ERR_PROTOCOL, "shard not connected to its peers");
@@ -272,175 +238,81 @@ static osp_status check_ready(osp_shard* s, int buf) {
     return OSP_OK;
 }
 
-static cudaError_t stream_stage(osp_shard* s, int buf, int stage, int c0, int c1, cudaStream_t st) {
-    StreamArgs a = s->sa;
-    a.stage = stage;
-    a.c0 = c0;
-    a.c1 = c1;
-    a.tepoch = 2u * s->iter + static_cast<unsigned>(stage) - 2u;
-    a.xepoch = s->iter;
-    a.vec = s->vec[buf];
-    a.dbg = s->dbg ? s->dbg + (stage - 1) * 48 : nullptr;
-    return launch_shard_stream(s->grp->v, s->ap_all, s->pt[buf], a, st);
+static cudaError_t launch_x(osp_shard* s, int buf, int mode, int c0, int c1, int solo,
+                            cudaStream_t st) {
+    XArgs xa = s->xa[buf];
+    xa.epoch = s->iter;
+    xa.mode = mode;
+    xa.c0 = c0;
+    xa.c1 = c1;
+    xa.solo = solo;
+    return launch_shard_x(s->grp->v, s->ap_all, xa, st);
 }
 
-static XSync sync_wait(int kind, unsigned ep) {
-    XSync y;
-    y.wait = kind;
-    y.ep_wait = ep;
-    return y;
+// stage 1: SINGLE mode exchanges every tile (the carry keeps the deferred
+// layers' aggregate), deferred-ICS mode the barrier layers (local estimates for
+// the rest)
+static cudaError_t stage1_kernels(osp_shard* s, int buf, cudaStream_t st) {
+    s->iter += 1;
+    return launch_x(s, buf, s->deferred ? XM_RS : XM_SINGLE, 0, 0, 0, st);
 }
 
-static XSync sync_signal_end(int kind, unsigned ep) {
-    XSync y;
-    y.signal_end = kind;
-    y.ep_end = ep;
-    return y;
-}
-
-// agg1: announce "deltas ready, previous iteration done" and wait for every
-// peer's announcement before touching peer memory; signal kind 1 at the end
-static XSync sync_agg1(const osp_shard* s) {
-    XSync y;
-    y.signal_start = 0;
-    y.ep_start = s->xep[0];
-    y.wait = 0;
-    y.ep_wait = s->xep[0];
-    y.signal_end = 1;
-    y.ep_end = s->xep[1];
-    return y;
-}
-
-// Barrier-mode kernels of one step (no resolve); ev (optional) gets 4 records:
-// before agg1, before the fused launch, before apply2, after apply2.
-static cudaError_t barrier_step_kernels(osp_shard* s, int buf, cudaStream_t st,
-                                        cudaEvent_t* ev = nullptr) {
+static cudaError_t stage2_kernels(osp_shard* s, int buf, int c0, int c1, cudaStream_t st) {
     osp_group* g = s->grp;
-    float* Xb = s->X + buf * s->buf_stride;
-    ++s->xep[0];
-    ++s->xep[1];
-    ++s->xep[2];
-    cudaError_t e;
-    if (s->pipe) {
-        // agg1 (first half of the RS exchange) -> [apply: RS first half + local
-        // estimates || agg: RS second half] -> [apply: RS second half || agg:
-        // ICS] -> apply2; cross-GPU kinds 1, 4, 2 in that order
-        ++s->xep[3];
-        if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st,
-                                  1)) != cudaSuccess)
-            return e;
-        if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
-        XSync ya = sync_wait(1, s->xep[1]);
-        ya.signal_end = 4;
-        ya.ep_end = s->xep[3];
-        FusedLists la;
-        la.apply_mode = 1;
-        la.agg_stage = 1;
-        la.agg_part = 2;
-        if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0, 0, g->grid,
-                                    ya, st, la)) != cudaSuccess)
-            return e;
-        XSync yb = sync_wait(4, s->xep[3]);
-        yb.signal_end = 2;
-        yb.ep_end = s->xep[2];
-        FusedLists lb;
-        lb.apply_mode = 2;
-        lb.agg_stage = 2;
-        if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0,
-                                    s->n_chunks, g->grid, yb, st, lb)) != cudaSuccess)
-            return e;
-        if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-        if ((e = launch_shard_apply(g->v, s->ap_loc, s->pt[buf], Xb, s->ldX, 2, 0, s->n_chunks,
-                                    g->grid, sync_wait(2, s->xep[2]), st)) != cudaSuccess)
-            return e;
-        if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
-        return cudaSuccess;
-    }
-    if (ev && (e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-    if ((e = launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st)) !=
-        cudaSuccess)
-        return e;
-    if (ev && (e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
-    XSync yf = sync_wait(1, s->xep[1]);
-    yf.signal_end = 2;
-    yf.ep_end = s->xep[2];
-    if ((e = launch_shard_fused(g->v, s->ap_all, s->ap_loc, s->pt[buf], Xb, s->ldX, 0, s->n_chunks,
-                                g->grid, yf, st)) != cudaSuccess)
-        return e;
-    if (ev && (e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-    if ((e = launch_shard_apply(g->v, s->ap_loc, s->pt[buf], Xb, s->ldX, 2, 0, s->n_chunks, g->grid,
-                                sync_wait(2, s->xep[2]), st)) != cudaSuccess)
-        return e;
-    if (ev && (e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
-    return cudaSuccess;
+    if (s->deferred) return launch_x(s, buf, XM_ICS, c0, c1, 0, st);
+    return launch_stage2_tma(g->v, g->ap, s->X + buf * s->buf_stride, s->ldX, c0, c1, st, 0);
 }
 
 osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
-    cudaStream_t st = as_stream(stream);
-    osp_group* g = s->grp;
-    if (s->stream) {
-        s->iter += 1;
-        OSP_CUDA(stream_stage(s, buf, 1, 0, 0, st));
-        return OSP_OK;
-    }
-    // kind 0: deltas ready / previous iteration's reads done (agg1 entry);
-    // kind 1: every shard's stage-1 aggregate landed here (apply1 entry)
-    ++s->xep[0];
-    ++s->xep[1];
-    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 1, 0, 0, g->grid, sync_agg1(s), st));
-    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->pt[buf], s->X + buf * s->buf_stride, s->ldX, 1,
-                                0, 0, g->grid, sync_wait(1, s->xep[1]), st));
+    OSP_CUDA(stage1_kernels(s, buf, as_stream(stream)));
+    s->s1_open = true;
     return OSP_OK;
 }
 
 osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     if (c0 < 0 || c1 > s->n_chunks || c0 > c1) return fail(OSP_ERR_INVALID, "chunk range");
-    cudaStream_t st = as_stream(stream);
-    osp_group* g = s->grp;
-    if (s->stream) {
-        if (s->iter == 0) return fail(OSP_ERR_PROTOCOL, "stage 2 before any stage 1");
-        OSP_CUDA(stream_stage(s, buf, 2, c0, c1, st));
-        return OSP_OK;
-    }
-    ++s->xep[2];  // kind 2: every shard's aggregate of these chunks landed here
-    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], 2, c0, c1, g->grid,
-                              sync_signal_end(2, s->xep[2]), st));
-    OSP_CUDA(launch_shard_apply(g->v, s->ap_loc, s->pt[buf], s->X + buf * s->buf_stride, s->ldX, 2,
-                                c0, c1, g->grid, sync_wait(2, s->xep[2]), st));
+    if (!s->s1_open) return fail(OSP_ERR_PROTOCOL, "stage 2 before stage 1 of this iteration");
+    OSP_CUDA(stage2_kernels(s, buf, c0, c1, as_stream(stream)));
     return OSP_OK;
 }
 
 osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
-    return osp_group_resolve(s->grp, s->X + buf * s->buf_stride, s->ldX, stream);
+    osp_group* g = s->grp;
+    OSP_CUDA(launch_resolve(g->v, g->ap, s->X + buf * s->buf_stride, s->ldX, as_stream(stream)));
+    s->s1_open = false;
+    return OSP_OK;
 }
 
-// Whole iteration with stage 2's push/pull running inside the stage-1 apply
-// launch (k_shard_fused): agg1, apply1 || agg2, apply2, resolve — four
-// launches, the cross-GPU ordering inside them (XSync). Same results as
-// stage1 + stage2 + resolve.
+// Whole iteration: stage 1, then (SINGLE) the resolve with the local stage-2
+// broadcast beside it (joined on the device, as osp_group_stage2_resolve), or
+// (deferred ICS) the stage-2 exchange of every chunk and the resolve.
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
-    if (s->stream) {
-        s->iter += 1;
-        OSP_CUDA(stream_stage(s, buf, 1, 0, 0, st));
-        OSP_CUDA(stream_stage(s, buf, 2, 0, s->n_chunks, st));
-        return osp_shard_resolve(s, buf, stream);
+    osp_group* g = s->grp;
+    float* Xb = s->X + buf * s->buf_stride;
+    OSP_CUDA(stage1_kernels(s, buf, st));
+    if (s->deferred) {
+        OSP_CUDA(launch_x(s, buf, XM_ICS, 0, s->n_chunks, 0, st));
+        OSP_CUDA(launch_resolve(g->v, g->ap, Xb, s->ldX, st));
+    } else {
+        OSP_CUDA(launch_resolve(g->v, g->ap, Xb, s->ldX, st));
+        OSP_CUDA(launch_stage2_tma(g->v, g->ap, Xb, s->ldX, 0, s->n_chunks, st, 1));
     }
-    OSP_CUDA(barrier_step_kernels(s, buf, st));
-    return osp_shard_resolve(s, buf, stream);
+    s->s1_open = false;
+    return OSP_OK;
 }
 
 osp_status osp_shard_solo_agg(osp_shard* s, int stage, int buf, void* stream) {
     OSP_TRY(check_ready(s, buf));
     if (stage != 1 && stage != 2) return fail(OSP_ERR_INVALID, "stage must be 1 or 2");
-    osp_group* g = s->grp;
-    OSP_CUDA(launch_shard_agg(g->v, s->ap_all, s->pt[buf], stage, 0, s->n_chunks, g->grid, XSync{},
-                              as_stream(stream)));
+    if (stage == 2 && !s->deferred)
+        return fail(OSP_ERR_PROTOCOL, "stage 2 exchanges nothing in single-exchange mode");
+    const int mode = stage == 2 ? XM_ICS : (s->deferred ? XM_RS : XM_SINGLE);
+    OSP_CUDA(launch_x(s, buf, mode, 0, s->n_chunks, 1, as_stream(stream)));
     return OSP_OK;
 }
 
@@ -449,40 +321,29 @@ osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream) {
     if (!ms) return fail(OSP_ERR_INVALID, "null output");
     cudaStream_t st = as_stream(stream);
     osp_group* g = s->grp;
-    cudaEvent_t ev[9];
+    float* Xb = s->X + buf * s->buf_stride;
+    cudaEvent_t ev[4];
     for (auto& e : ev) OSP_CUDA(cudaEventCreate(&e));
-    osp_status rc = OSP_OK;
-    auto step = [&]() -> cudaError_t {
+    auto run = [&]() -> cudaError_t {
         cudaError_t e;
-        float* Xb = s->X + buf * s->buf_stride;
-        if (s->stream) {
-            s->iter += 1;
-            for (int i = 0; i < 8; ++i) ms[i] = 0.f;
-            if ((e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
-            if ((e = stream_stage(s, buf, 1, 0, 0, st)) != cudaSuccess) return e;
-            if ((e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
-            if ((e = stream_stage(s, buf, 2, 0, s->n_chunks, st)) != cudaSuccess) return e;
-            if ((e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
-            if ((e = launch_resolve(g->v, g->ap, Xb, s->ldX, st)) != cudaSuccess) return e;
-            if ((e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
-            if ((e = cudaEventSynchronize(ev[3])) != cudaSuccess) return e;
-            for (int i = 0; i < 3; ++i)
-                if ((e = cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1])) != cudaSuccess) return e;
-            return cudaSuccess;
-        }
         for (int i = 0; i < 8; ++i) ms[i] = 0.f;
-        if ((e = barrier_step_kernels(s, buf, st, ev)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[0], st)) != cudaSuccess) return e;
+        if ((e = stage1_kernels(s, buf, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[1], st)) != cudaSuccess) return e;
+        if ((e = stage2_kernels(s, buf, 0, s->n_chunks, st)) != cudaSuccess) return e;
+        if ((e = cudaEventRecord(ev[2], st)) != cudaSuccess) return e;
         if ((e = launch_resolve(g->v, g->ap, Xb, s->ldX, st)) != cudaSuccess) return e;
-        if ((e = cudaEventRecord(ev[4], st)) != cudaSuccess) return e;
-        if ((e = cudaEventSynchronize(ev[4])) != cudaSuccess) return e;
-        for (int i = 0; i < 4; ++i)
+        if ((e = cudaEventRecord(ev[3], st)) != cudaSuccess) return e;
+        if ((e = cudaEventSynchronize(ev[3])) != cudaSuccess) return e;
+        for (int i = 0; i < 3; ++i)
             if ((e = cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1])) != cudaSuccess) return e;
         return cudaSuccess;
     };
-    cudaError_t e = step();
-    if (e != cudaSuccess) rc = cuda_fail(e, "shard profile");
+    cudaError_t e = run();
+    s->s1_open = false;
     for (auto& x : ev) cudaEventDestroy(x);
-    return rc;
+    if (e != cudaSuccess) return cuda_fail(e, "shard profile");
+    return OSP_OK;
 }
 
 osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
@@ -495,27 +356,13 @@ osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uin
     return OSP_OK;
 }
 
-int osp_shard_streaming(const osp_shard* s) { return s && s->stream ? 1 : 0; }
-
-// Diagnostics of the streaming kernel (OSP_SS_DEBUG=1 at create): 96 counters
-// accumulated since create, [stage 1 | stage 2][48]: producer empty-wait
-// cycles, peer-flag wait cycles, 0, A/B/C items, producer cycles, 0, consumer
-// warp-0 full-wait cycles, consumer warp-0 processing cycles, 0, 0, producers,
-// max producer cycles (atomicMax, never reset), 0... Returns 0 when disabled.
-int osp_shard_debug_counters(osp_shard* s, unsigned long long* out96) {
-    if (!s || !s->dbg || !out96) return 0;
-    if (cudaMemcpy(out96, s->dbg, 96 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
-        return 0;
-    return 1;
-}
-
 osp_status osp_shard_check(osp_shard* s, void* stream) {
     if (!s) return fail(OSP_ERR_INVALID, "null shard");
     unsigned err = 0;
     cudaStream_t st = as_stream(stream);
     OSP_CUDA(cudaMemcpyAsync(&err, s->error, sizeof err, cudaMemcpyDeviceToHost, st));
     OSP_CUDA(cudaStreamSynchronize(st));
-    if (err) return fail(OSP_ERR_PROTOCOL, "cross-GPU barrier timed out (a peer did not arrive)");
+    if (err) return fail(OSP_ERR_PROTOCOL, "cross-GPU wait timed out (a peer did not arrive)");
     return OSP_OK;
 }
 

@@ -537,6 +537,27 @@ __global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const 
 
 __global__ void k_set_budget(uint64_t* meta64, uint64_t budget) { meta64[META64_BUDGET] = budget; }
 
+// Per-tile PGP partials of (params, grads) in the group's tile geometry for the
+// certified resolve of arbitrary vectors: one warp per tile, lane-strided terms
+// summed in order, then the fixed shuffle tree (depth <= T/32 + 5, inside
+// tile_depth's bound).
+__global__ void __launch_bounds__(256) k_pgp_tiles(GroupView g, const float* __restrict__ params,
+                                                   const float* __restrict__ grads) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int t = gw; t < g.NT; t += nw) {
+        const int l = g.tile_layer[t];
+        const uint64_t s = g.offsets[l] + static_cast<uint64_t>(t - g.tile_base[l]) * g.T;
+        const uint64_t e = min(s + static_cast<uint64_t>(g.T), g.offsets[l] + g.counts[l]);
+        double acc = 0.0;
+        for (uint64_t f = s + lane; f < e; f += 32) acc = __dadd_rn(acc, pgp_term(grads[f], params[f]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (lane == 0) g.partials[t] = acc;
+    }
+}
+
 // Per-function API: exact sequential PGP of (params, grads) per layer.
 __global__ void k_pgp_exact(const float* __restrict__ P, const float* __restrict__ Gr,
                             const uint64_t* offsets, const uint64_t* counts, double* scores) {
@@ -609,6 +630,14 @@ cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order
     cudaError_t e = set_smem(reinterpret_cast<const void*>(k_install), sm);
     if (e != cudaSuccess) return e;
     k_install<<<1, kResolveThreads, sm, st>>>(g, order, n_order, tag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pgp_tiles(const GroupView& g, const float* params, const float* grads,
+                             cudaStream_t st) {
+    if (g.NT < 1) return cudaSuccess;
+    const int blocks = min((g.NT + 7) / 8, sm_count() * 8);
+    k_pgp_tiles<<<blocks, 256, 0, st>>>(g, params, grads);
     return cudaGetLastError();
 }
 

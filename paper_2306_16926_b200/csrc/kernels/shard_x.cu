@@ -1,0 +1,533 @@
+// The sharded (multi-GPU) exchange kernel: one launch does a stage's push
+// (reduce-scatter), fixed-order aggregation, pull (all-gather) and the local
+// apply, with per-tile ready flags over NVLink peer memory instead of grid-wide
+// cross-GPU barriers (one process per GPU, CUDA-IPC mappings).
+//
+// The exchanged tile sequence (mode SINGLE: every tile, the ICS payload split at
+// stage-1 time as split_for_sync copies it, protocol.cpp:122-166; mode RS: the
+// barrier layers; mode ICS: the deferred layers of chunks [c0, c1)) is cut into
+// P contiguous owner ranges, and each owner range into one slice per CTA. Three
+// kinds of work item per CTA:
+//
+//   A  a tile of this rank's own slice: bulk-copy (cp.async.bulk, SASS UBLKCP)
+//      every worker's delta rows into shared memory — the local ones from HBM,
+//      the others straight out of the peers' HBM over NVLink — plus the G slice;
+//      aggregate in fp64 in the reference's ascending worker order
+//      (protocol.cpp:9-30, bit-exact, unlike an fp32 NCCL reduce-scatter);
+//      apply locally (RS: G' = G + agg, local rows = G'; ICS in SINGLE mode:
+//      local rows = G + x_w, the LGP local estimate, and the carry C = G + agg);
+//      store agg into every rank's pull buffer (NVLink stores); the publisher
+//      warp then writes the tile's PGP partial into every rank's partials and,
+//      after a system-scope fence, the tile's flag on every peer.
+//   B  the same slice position of a peer's range: wait for its flag, bulk-copy
+//      agg (written by the owner into the local pull buffer), the G slice and,
+//      for a deferred layer in SINGLE mode, the local delta rows; apply as A.
+//   L  (mode RS) a deferred layer's tile: the local estimate only, no exchange.
+//
+// CTA c of every rank works on slice c of every owner range at the same pace,
+// so B items are scheduled by due time a few A items behind (lag): the peer's
+// CTA c has published them by then. A merge by due time interleaves the
+// NVLink-bound A items with the HBM-bound B / L items so both links stay busy.
+//
+// Ordering across GPUs: at launch every CTA signals "this iteration's delta rows
+// are ready" (epoch) into every peer's ready slots and waits for every peer's
+// before its first A item; a rank at iteration i has finished iteration i-1's
+// kernels, so the pull buffer, partials and flags need no double buffering.
+// Tile flags carry the iteration number (each tile is exchanged once per
+// iteration) and are never reset. Every wait is bounded (20 s) and records an
+// error instead of hanging.
+
+#include "common.cuh"
+#include "tma.cuh"
+
+namespace osp {
+namespace {
+
+enum XItem { XI_A = 0, XI_B = 1, XI_L = 2 };
+
+struct XMeta {
+    uint64_t s, e;  // element range
+    int t;          // global tile id, -1 = stop
+    int kind;       // XItem
+    int staged;     // rows in shared memory (else consumers read global memory)
+    int ics;        // tile of a deferred layer
+};
+
+__device__ __forceinline__ void xseq_lookup(const int* lp, const int* ll, int n, int u, int& l,
+                                            int& k) {
+    int a = 0, b = n - 1;
+    while (a < b) {
+        const int m = (a + b + 1) >> 1;
+        if (lp[m] <= u) a = m;
+        else b = m - 1;
+    }
+    l = ll ? ll[a] : a;
+    k = u - lp[a];
+}
+
+__device__ __forceinline__ bool xspin(const unsigned* p, unsigned want, unsigned* error) {
+    if (static_cast<int>(ld_acquire_sys(p) - want) >= 0) return true;
+    const uint64_t t0 = now_ns();
+    while (static_cast<int>(ld_acquire_sys(p) - want) < 0) {
+        __nanosleep(64);
+        if (now_ns() - t0 > 20000000000ull) {
+            atomicExch(error, 1u);
+            return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ float4 cvt4x(const AggParams& ap, float4 v) {
+    if (ap.sgd) {
+        v.x = sgd_conv(ap.neg_lr, v.x);
+        v.y = sgd_conv(ap.neg_lr, v.y);
+        v.z = sgd_conv(ap.neg_lr, v.z);
+        v.w = sgd_conv(ap.neg_lr, v.w);
+    }
+    return v;
+}
+
+__device__ __forceinline__ float4 add4x(float4 a, float4 b) {
+    return make_float4(__fadd_rn(a.x, b.x), __fadd_rn(a.y, b.y), __fadd_rn(a.z, b.z),
+                       __fadd_rn(a.w, b.w));
+}
+
+// Per-CTA item order: A items at due time i, the peers' B items
+// (j + 1) * nA / nB + lag - 1 (behind the A item the peer's CTA is on), L items
+// spread evenly; ties go to A. Deterministic and identical on every lane.
+struct XSched {
+    int nA, nL, nB[kMaxRanks];
+    int ia, il, ib[kMaxRanks];
+    int P, R, lag;
+
+    __device__ double dueA() const { return ia < nA ? static_cast<double>(ia) : 1e30; }
+    __device__ double dueL() const {
+        if (il >= nL) return 1e30;
+        return nA > 0 ? (static_cast<double>(il) + 0.5) * nA / nL : 0.0;
+    }
+    __device__ double dueB(int q) const {
+        if (ib[q] >= nB[q]) return 1e30;
+        return nA > 0 ? (static_cast<double>(ib[q]) + 1.0) * nA / nB[q] + lag - 1 : 0.0;
+    }
+    // next (kind, peer, index); kind -1 = done
+    __device__ void next(int& kind, int& q, int& k) {
+        double best = dueA();
+        kind = ia < nA ? XI_A : -1;
+        q = R;
+        k = ia;
+        const double dl = dueL();
+        if (dl < best) {
+            best = dl;
+            kind = XI_L;
+            k = il;
+        }
+        for (int p = 0; p < P; ++p) {
+            if (p == R) continue;
+            const double db = dueB(p);
+            if (db < best) {
+                best = db;
+                kind = XI_B;
+                q = p;
+                k = ib[p];
+            }
+        }
+        if (kind == XI_A) ++ia;
+        else if (kind == XI_L) ++il;
+        else if (kind == XI_B) ++ib[q];
+    }
+};
+
+// Slot layout: A: rows 0..N-1 = every worker's deltas, row N = G.
+//              B: row 0 = agg, row 1 = G, rows 2.. = local deltas (ICS, SINGLE).
+//              L: rows 0..NL-1 = local deltas, row NL = G.
+template <int NS, int CW>
+__global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParams ap, XArgs xa) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int KS = 2;  // ring stages
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int T = g.T;
+    const int P = xa.world, R = xa.rank, NL = xa.n_loc, N = ap.n;
+    const size_t SF = static_cast<size_t>(xa.slot_rows) * T;
+
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + KS * SF);
+    uint64_t* done = full + KS;
+    uint64_t* empty = done + KS;
+    XMeta* meta = reinterpret_cast<XMeta*>(empty + KS);
+    double* red = reinterpret_cast<double*>(meta + KS);  // [KS][CW]
+    unsigned char* tabmem = reinterpret_cast<unsigned char*>(red + KS * CW);
+
+    // ---- tables: layer geometry, exchange sequence, local-estimate sequence
+    const int L = g.L;
+    uint64_t* t_off = reinterpret_cast<uint64_t*>(tabmem);
+    uint64_t* t_cnt = t_off + L;
+    int* t_tb = reinterpret_cast<int*>(t_cnt + L);
+    uint8_t* t_flag = reinterpret_cast<uint8_t*>(t_tb + L + 1);
+    int* xl = reinterpret_cast<int*>(t_flag + ((L + 15) & ~15));
+    int* xp = xl + L;
+    int* cl = xp + L + 1;
+    int* cp = cl + L;
+    int nx = 0, nc = 0, xb = 0;
+    const int* XL = nullptr;
+    const int* XP = g.tile_base;
+    const int used = g.meta[META_N_USED];
+    if (xa.mode == XM_SINGLE) {
+        nx = L;
+    } else if (xa.mode == XM_RS) {
+        XL = g.rs_layers;
+        XP = g.rs_tile_prefix;
+        nx = g.meta[META_N_RS];
+        nc = used > 0 ? g.chunk_begin[used] : 0;
+    } else {
+        XL = g.ics_layers;
+        XP = g.ics_tile_prefix;
+        const int cc1 = xa.c1 > used ? used : xa.c1;
+        if (xa.c0 < cc1) {
+            xb = g.chunk_begin[xa.c0];
+            nx = g.chunk_begin[cc1] - xb;
+        }
+    }
+    for (int i = tid; i < L; i += blockDim.x) {
+        t_off[i] = g.offsets[i];
+        t_cnt[i] = g.counts[i];
+        t_tb[i] = g.tile_base[i];
+        t_flag[i] = g.flags[i];
+    }
+    if (tid == 0) t_tb[L] = g.tile_base[L];
+    if (XL)
+        for (int i = tid; i < nx; i += blockDim.x) xl[i] = XL[xb + i];
+    for (int i = tid; nx > 0 && i <= nx; i += blockDim.x) xp[i] = XP[xb + i];
+    for (int i = tid; i < nc; i += blockDim.x) cl[i] = g.ics_layers[i];
+    for (int i = tid; nc > 0 && i <= nc; i += blockDim.x) cp[i] = g.ics_tile_prefix[i];
+    // SINGLE mode is this iteration's stage 1: block 0 snapshots the ICS lists
+    // the stage-3 broadcast walks (as k_stage_tma's stage 1 does)
+    if (xa.mode == XM_SINGLE && g.snap && blockIdx.x == 0 && !xa.solo) {
+        const int n_ics = g.meta[META_N_ICS];
+        int* snap_cb = g.snap + kSnapHead;
+        int* snap_il = snap_cb + g.n_chunks + 1;
+        int* snap_tp = snap_il + L;
+        if (tid == 0) {
+            g.snap[0] = used;
+            g.snap[1] = static_cast<int>(g.meta64[META64_RESOLVED] + 1);
+        }
+        for (int i = tid; i <= g.n_chunks; i += blockDim.x) snap_cb[i] = g.chunk_begin[i];
+        for (int i = tid; i < n_ics; i += blockDim.x) snap_il[i] = g.ics_layers[i];
+        for (int i = tid; i <= n_ics; i += blockDim.x) snap_tp[i] = g.ics_tile_prefix[i];
+    }
+    if (tid == 0) {
+        for (int s = 0; s < KS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&done[s], CW);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init_fence();
+    }
+    __syncthreads();
+
+    const int C = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+    const int U0 = nx > 0 ? xp[0] : 0;
+    const int U = nx > 0 ? xp[nx] - U0 : 0;
+    const int V = nc > 0 ? cp[nc] - cp[0] : 0;
+    // owner range of rank q, and CTA c's slice of it
+    auto range_lo = [&](int q) { return static_cast<int>((static_cast<int64_t>(U) * q) / P); };
+    auto slice_lo = [&](int q, int cc) {
+        const int lo = range_lo(q), len = range_lo(q + 1) - lo;
+        return lo + static_cast<int>((static_cast<int64_t>(len) * cc) / C);
+    };
+    const int lcl_lo = static_cast<int>((static_cast<int64_t>(V) * c) / C);
+
+    auto locate = [&](int kind, int u, XMeta& m) {
+        int l, kk;
+        if (kind == XI_L) xseq_lookup(cp, cl, nc, (nc > 0 ? cp[0] : 0) + u, l, kk);
+        else xseq_lookup(xp, XL ? xl : nullptr, nx, U0 + u, l, kk);
+        m.t = t_tb[l] + kk;
+        m.s = t_off[l] + static_cast<uint64_t>(kk) * T;
+        const uint64_t le = t_off[l] + t_cnt[l];
+        m.e = m.s + static_cast<uint64_t>(T) < le ? m.s + static_cast<uint64_t>(T) : le;
+        m.kind = kind;
+        m.ics = t_flag[l];
+        m.staged = xa.vec && NS > 0 && (m.s % 4 == 0) && ((m.e - m.s) % 4 == 0);
+    };
+
+    if (warp == CW + 1) {
+        // ================= publisher =================
+        for (int i = 0;; ++i) {
+            const int s = i % KS;
+            mbar_wait(&done[s], (i / KS) & 1);
+            const XMeta m = meta[s];
+            double tot = 0.0;
+            if (m.t >= 0 && m.kind == XI_A)
+                for (int w = 0; w < CW; ++w) tot = __dadd_rn(tot, red[s * CW + w]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (m.t < 0) break;
+            if (m.kind != XI_A) continue;
+            // partial everywhere, then (system-scope fence, cumulative over the
+            // consumers' pull stores acquired through the done barrier and these
+            // partials) the tile flag on every peer; one lane does all of it
+            if (lane == 0) {
+                for (int r = 0; r < P; ++r) xa.part[r][m.t] = tot;
+                if (!xa.solo) {
+                    __threadfence_system();
+                    for (int r = 0; r < P; ++r)
+                        if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + m.t) = xa.epoch;
+                }
+            }
+            __syncwarp();
+        }
+        return;
+    }
+
+    if (warp == CW) {
+        // ================= producer (whole warp; lane j issues row j) =================
+        XSched sc;
+        sc.P = P;
+        sc.R = R;
+        sc.lag = xa.lag;
+        sc.ia = sc.il = 0;
+        sc.nA = slice_lo(R, c + 1) - slice_lo(R, c);
+        sc.nL = xa.mode == XM_RS ? static_cast<int>((static_cast<int64_t>(V) * (c + 1)) / C) - lcl_lo : 0;
+        for (int q = 0; q < kMaxRanks; ++q) {
+            sc.ib[q] = 0;
+            sc.nB[q] = (q < P && q != R && !xa.solo) ? slice_lo(q, c + 1) - slice_lo(q, c) : 0;
+        }
+        // this iteration's delta rows are ready here; peers' before the first A item
+        if (lane == 0 && xa.mode != XM_ICS && !xa.solo) {
+            __threadfence_system();
+            for (int q = 0; q < P; ++q)
+                if (q != R) st_release_sys(xa.ready[q] + R, xa.epoch);
+        }
+        bool peers_ready = xa.mode == XM_ICS || xa.solo;
+        for (int i = 0;; ++i) {
+            const int s = i % KS;
+            const int use = i / KS;
+            if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+            int kind, q, k;
+            sc.next(kind, q, k);  // every lane, same result
+            XMeta m{};
+            if (kind < 0) {
+                if (lane == 0) {
+                    m.t = -1;
+                    meta[s] = m;
+                    mbar_arrive(&full[s]);
+                }
+                break;
+            }
+            const int u = kind == XI_A ? slice_lo(R, c) + k
+                        : kind == XI_B ? slice_lo(q, c) + k
+                                       : lcl_lo + k;
+            locate(kind, u, m);
+            if (kind == XI_A && !peers_ready) {
+                if (lane == 0)
+                    for (int p = 0; p < P; ++p)
+                        if (p != R) xspin(xa.ready[R] + p, xa.epoch, xa.error);
+                __syncwarp();
+                fence_proxy_async();
+                peers_ready = true;
+            }
+            if (kind == XI_B) {
+                if (lane == 0) xspin(xa.tflag[R] + m.t, xa.epoch, xa.error);
+                __syncwarp();
+                fence_proxy_async();
+            }
+            const bool local_rows = kind == XI_L || (kind == XI_B && m.ics && xa.mode == XM_SINGLE);
+            const int nrows = kind == XI_A ? N + 1 : kind == XI_L ? NL + 1 : (local_rows ? 2 + NL : 2);
+            const unsigned bytes = static_cast<unsigned>((m.e - m.s) * 4);
+            if (lane == 0) {
+                meta[s] = m;
+                if (m.staged) mbar_arrive_tx(&full[s], bytes * nrows);
+            }
+            __syncwarp();
+            if (m.staged) {
+                float* dst = ring + s * SF;
+                for (int r = lane; r < nrows; r += 32) {
+                    const float* src;
+                    if (kind == XI_A) src = r < N ? xa.xrow[r] + m.s : g.G + m.s;
+                    else if (kind == XI_L) src = r < NL ? xa.xrow[R * NL + r] + m.s : g.G + m.s;
+                    else src = r == 0 ? xa.agg[R] + m.s : r == 1 ? g.G + m.s : xa.xrow[R * NL + r - 2] + m.s;
+                    bulk_g2s(dst + static_cast<size_t>(r) * T, src, bytes, &full[s]);
+                }
+            } else if (lane == 0) {
+                mbar_arrive(&full[s]);
+            }
+        }
+        return;
+    }
+
+    // ================= consumers =================
+    const int ctid = tid;
+    for (int i = 0;; ++i) {
+        const int s = i % KS;
+        mbar_wait(&full[s], (i / KS) & 1);
+        const XMeta m = meta[s];
+        if (m.t < 0) {
+            if (lane == 0) mbar_arrive(&done[s]);
+            break;
+        }
+        const float* buf = ring + s * SF;
+        // ICS tile of SINGLE mode: local estimate + carry; otherwise G' and rows
+        const bool carry = m.ics && xa.mode == XM_SINGLE;
+        double acc = 0.0;
+        if (m.staged) {
+            const int nq = static_cast<int>((m.e - m.s) >> 2);
+            for (int qd = ctid; qd < nq; qd += CW * 32) {
+                const uint64_t f = m.s + 4ull * qd;
+                if (m.kind == XI_A) {
+                    if constexpr (NS > 0) {
+                        const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(NS) * T + 4 * qd);
+                        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+                        for (int w = 0; w < NS; ++w) {
+                            const float4 v = cvt4x(ap, *reinterpret_cast<const float4*>(
+                                                           buf + static_cast<size_t>(w) * T + 4 * qd));
+                            s0 = agg_acc(s0, ap.w[w], v.x);
+                            s1 = agg_acc(s1, ap.w[w], v.y);
+                            s2 = agg_acc(s2, ap.w[w], v.z);
+                            s3 = agg_acc(s3, ap.w[w], v.w);
+                        }
+                        const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1),
+                                                     agg_finish(ap, s2), agg_finish(ap, s3));
+                        const float4 gn = add4x(go, a);
+                        for (int r = 0; r < P; ++r) *reinterpret_cast<float4*>(xa.agg[r] + f) = a;
+                        if (carry) {
+                            st_stream4(g.C + f, gn);
+                            for (int w = 0; w < NL; ++w) {
+                                const float4 v = cvt4x(ap, *reinterpret_cast<const float4*>(
+                                                               buf + static_cast<size_t>(R * NL + w) * T + 4 * qd));
+                                st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, add4x(go, v));
+                            }
+                        } else {
+                            *reinterpret_cast<float4*>(g.G + f) = gn;
+                            for (int w = 0; w < NL; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+                        }
+                        acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
+                        acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
+                        acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
+                        acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
+                    }
+                } else if (m.kind == XI_B) {
+                    const float4 a = *reinterpret_cast<const float4*>(buf + 4 * qd);
+                    const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(T) + 4 * qd);
+                    const float4 gn = add4x(go, a);
+                    if (carry) {
+                        st_stream4(g.C + f, gn);
+                        for (int w = 0; w < NL; ++w) {
+                            const float4 v = cvt4x(ap, *reinterpret_cast<const float4*>(
+                                                           buf + static_cast<size_t>(2 + w) * T + 4 * qd));
+                            st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, add4x(go, v));
+                        }
+                    } else {
+                        *reinterpret_cast<float4*>(g.G + f) = gn;
+                        for (int w = 0; w < NL; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+                    }
+                } else {
+                    const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(NL) * T + 4 * qd);
+                    for (int w = 0; w < NL; ++w) {
+                        const float4 v = cvt4x(ap, *reinterpret_cast<const float4*>(
+                                                       buf + static_cast<size_t>(w) * T + 4 * qd));
+                        st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, add4x(go, v));
+                    }
+                }
+            }
+        } else {
+            // unstaged tile (unaligned layer, or more workers than the slot holds):
+            // per element from global memory (peer rows over NVLink)
+            for (uint64_t f = m.s + ctid; f < m.e; f += CW * 32) {
+                const float go = g.G[f];
+                if (m.kind == XI_L) {
+                    for (int w = 0; w < NL; ++w) {
+                        float x = xa.xrow[R * NL + w][f];
+                        if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                        g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
+                    }
+                    continue;
+                }
+                float a;
+                if (m.kind == XI_A) {
+                    double sum = 0.0;
+                    for (int w = 0; w < N; ++w) {
+                        float x = xa.xrow[w][f];
+                        if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                        sum = agg_acc(sum, ap.w[w], x);
+                    }
+                    a = agg_finish(ap, sum);
+                    for (int r = 0; r < P; ++r) xa.agg[r][f] = a;
+                } else {
+                    a = __ldcg(xa.agg[R] + f);
+                }
+                const float gn = __fadd_rn(go, a);
+                if (carry) {
+                    g.C[f] = gn;
+                    for (int w = 0; w < NL; ++w) {
+                        float x = xa.xrow[R * NL + w][f];
+                        if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                        g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
+                    }
+                } else {
+                    g.G[f] = gn;
+                    for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+                }
+                if (m.kind == XI_A) acc = __dadd_rn(acc, pgp_term(a, gn));
+            }
+        }
+        if (m.kind == XI_A) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        }
+        __syncwarp();
+        if (lane == 0) {
+            if (m.kind == XI_A) red[s * CW + warp] = acc;
+            mbar_arrive(&done[s]);
+        }
+    }
+}
+
+constexpr int kXCW = 8;
+
+size_t x_smem_bytes(int slot_rows, int T, int L) {
+    const size_t ring = static_cast<size_t>(2) * slot_rows * T * sizeof(float);
+    const size_t ctl = 3 * 2 * sizeof(uint64_t) + 2 * sizeof(XMeta) + 2 * kXCW * sizeof(double);
+    const size_t tab = static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + L * 4 +
+                       (L + 1) * 4 + L * 4 + (L + 1) * 4 + 128;
+    return ring + ctl + tab;
+}
+
+template <int NS>
+cudaError_t launch_x_ns(const GroupView& g, const AggParams& ap, const XArgs& xa_in, cudaStream_t s) {
+    auto kern = k_shard_x<NS, kXCW>;
+    XArgs xa = xa_in;
+    const size_t sm = x_smem_bytes(xa.slot_rows, g.T, g.L);
+    int per_sm = 0;
+    cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), (kXCW + 2) * 32, sm, &per_sm);
+    if (e != cudaSuccess) return e;
+    const int grid = sm_count() * (per_sm > 2 ? 2 : per_sm);
+    kern<<<grid, (kXCW + 2) * 32, sm, s>>>(g, ap, xa);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+int x_slot_rows(int n_workers) { return n_workers <= kXMaxStagedWorkers ? n_workers + 1 : 2; }
+
+bool shard_x_supported(int n_workers, int T, int L) {
+    if (T < 512 || T > 4096) return false;
+    return x_smem_bytes(x_slot_rows(n_workers), T, L) <= 220 * 1024;
+}
+
+cudaError_t launch_shard_x(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
+    switch (ap.n <= kXMaxStagedWorkers ? ap.n : 0) {
+        case 1: return launch_x_ns<1>(g, ap, xa, s);
+        case 2: return launch_x_ns<2>(g, ap, xa, s);
+        case 3: return launch_x_ns<3>(g, ap, xa, s);
+        case 4: return launch_x_ns<4>(g, ap, xa, s);
+        case 5: return launch_x_ns<5>(g, ap, xa, s);
+        case 6: return launch_x_ns<6>(g, ap, xa, s);
+        case 7: return launch_x_ns<7>(g, ap, xa, s);
+        case 8: return launch_x_ns<8>(g, ap, xa, s);
+        default: return launch_x_ns<0>(g, ap, xa, s);
+    }
+}
+
+}  // namespace osp

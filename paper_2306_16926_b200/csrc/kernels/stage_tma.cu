@@ -25,6 +25,38 @@
 #include "tma.cuh"
 
 namespace osp {
+// Opt the kernel into its shared-memory size and query its occupancy once per
+// (context, kernel, smem bytes): both are host API calls the launch-bound small
+// layouts would otherwise pay on every launch. Keyed on the context, not the
+// device: a recreated context starts without the opt-in.
+cudaError_t tma_blocks_per_sm(const void* kern, int threads, size_t sm, int* per_sm) {
+    static std::mutex mu;
+    static std::map<std::tuple<unsigned long long, const void*, size_t>, int> cache;
+    static std::map<std::pair<unsigned long long, const void*>, size_t> opted;  // attribute = max asked
+    cudaError_t e = cudaSuccess;
+    const unsigned long long dev = current_ctx_id();
+    const auto key = std::make_tuple(dev, kern, sm);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *per_sm = it->second;
+        return cudaSuccess;
+    }
+    // never lower the opt-in: a smaller layout must not break a cached larger one
+    size_t& cur = opted[std::make_pair(dev, kern)];
+    if (sm > cur) {
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(sm));
+        if (e != cudaSuccess) return e;
+        cur = sm;
+    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, sm);
+    if (e != cudaSuccess) return e;
+    if (*per_sm < 1) return cudaErrorInvalidConfiguration;
+    cache.emplace(key, *per_sm);
+    return cudaSuccess;
+}
+
 namespace {
 
 // Shapes: CW consumer warps (each thread T/(CW*128) quads per tile) and a KS-deep
@@ -500,38 +532,6 @@ size_t tma_smem_bytes(int rows, int T, int L, int CW, int kStages) {
     const size_t tab = static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + L * 4 +
                        (L + 1) * 4 + 64;
     return ring + bars + metas + red + tab;
-}
-
-// Opt the kernel into its shared-memory size and query its occupancy once per
-// (context, kernel, smem bytes): both are host API calls the launch-bound small
-// layouts would otherwise pay on every launch. Keyed on the context, not the
-// device: a recreated context starts without the opt-in.
-cudaError_t tma_blocks_per_sm(const void* kern, int threads, size_t sm, int* per_sm) {
-    static std::mutex mu;
-    static std::map<std::tuple<unsigned long long, const void*, size_t>, int> cache;
-    static std::map<std::pair<unsigned long long, const void*>, size_t> opted;  // attribute = max asked
-    cudaError_t e = cudaSuccess;
-    const unsigned long long dev = current_ctx_id();
-    const auto key = std::make_tuple(dev, kern, sm);
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find(key);
-    if (it != cache.end()) {
-        *per_sm = it->second;
-        return cudaSuccess;
-    }
-    // never lower the opt-in: a smaller layout must not break a cached larger one
-    size_t& cur = opted[std::make_pair(dev, kern)];
-    if (sm > cur) {
-        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(sm));
-        if (e != cudaSuccess) return e;
-        cur = sm;
-    }
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, sm);
-    if (e != cudaSuccess) return e;
-    if (*per_sm < 1) return cudaErrorInvalidConfiguration;
-    cache.emplace(key, *per_sm);
-    return cudaSuccess;
 }
 
 template <int STAGE, int NS, int CW, int KS>

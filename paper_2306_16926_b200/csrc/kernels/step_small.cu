@@ -216,7 +216,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     if (warp != 0) return;
 
     // rank, prefix rule, chunk map, lists (lane = rank position r or layer id)
-    const int my_rank = lane < L ? warp_rank(key, lane, L) : 32;
+    const int rk = warp_rank(key, lane, L);  // every lane takes part in the shuffles
+    const int my_rank = lane < L ? rk : 32;
     // sorted[r]: the lane whose rank is r
     int sorted = 0;
     for (int j = 0; j < L; ++j) {

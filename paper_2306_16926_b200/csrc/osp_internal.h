@@ -110,14 +110,7 @@ enum SchedIdx {
     SCHED_S1_DONE = 1,
     SCHED_S2_NEXT = 2,
     SCHED_S2_DONE = 3,
-    SCHED_RESOLVE_DONE = 4,
-    SCHED_AGG_NEXT = 5,
-    SCHED_AGG_DONE = 6,
-    SCHED_SS_A = 8,     // streaming shard kernel: own exchange tiles
-    SCHED_SS_B = 9,     //   peers' exchange tiles
-    SCHED_SS_C = 10,    //   local-estimate tiles (stage 1)
-    SCHED_SS_DONE = 11,
-    SCHED_XSYNC_TICKET = 12  // last-CTA ticket of the in-kernel cross-GPU signal
+    SCHED_RESOLVE_DONE = 4
 };
 enum MetaIdx { META_N_ICS = 0, META_N_USED = 1, META_NEED_FB = 2, META_N_RS = 3 };
 enum Meta64Idx {
@@ -139,66 +132,39 @@ constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profil
 constexpr uint32_t kDefaultTmaTile = 1024;  // TMA-staged kernels (tools/tma_sweep.sh)
 constexpr int kResolveThreads = 1024;
 
-// ---- sharded (multi-GPU) path: peer tables ---------------------------------
-constexpr int kMaxRanks = 8;      // one NVLink/NVSwitch node
-constexpr int kBarKinds = 5;      // flag-slot kinds: deltas ready, stage-1 aggregate done, stage-2 aggregate done, streaming deltas ready, stage-1 second-half aggregate done (pipelined)
+// ---- sharded (multi-GPU) path (kernels/shard_x.cu) ---------------------------
+constexpr int kMaxRanks = 8;           // one NVLink/NVSwitch node
+constexpr int kXMaxStagedWorkers = 8;  // A items stage every worker's row in shared memory
 
-struct PeerTable {
-    int world;
-    int rank;
-    int n_loc;                                   // workers hosted per rank
-    int ldmode;                                  // peer load flavour (common.cuh ld_peer4)
-    const float* xrow[OSP_MAX_WORKERS];          // delta row of every worker (peer or local)
-    float* agg[kMaxRanks];                       // every rank's agg_full buffer
-    unsigned* flags[kMaxRanks];                  // every rank's barrier slots [kBarKinds][kMaxRanks]
-    unsigned* error;                             // local: set on barrier timeout
-};
+// Exchange modes: SINGLE = every tile in one exchange (the ICS payload split at
+// stage 1, kept in the carry, broadcast locally by stage 2); RS = the barrier
+// layers only, local estimates for the deferred ones; ICS = the deferred layers
+// of chunks [c0, c1) (stage 2 of the deferred-ICS mode).
+enum XMode { XM_SINGLE = 0, XM_RS = 1, XM_ICS = 2 };
 
-// In-kernel cross-GPU ordering of the barrier-mode shard kernels (stage.cu):
-// kinds index PeerTable flag slots; -1 = none. Epochs are host counters that
-// every rank advances identically.
-struct XSync {
-    int wait = -1;          // at start: wait for every peer's slot[wait] >= ep_wait
-    int signal_start = -1;  // at start: signal slot[signal_start] = ep_start
-    int signal_end = -1;    // when the last CTA finishes: signal slot[signal_end] = ep_end
-    unsigned ep_wait = 0, ep_start = 0, ep_end = 0;
+struct XArgs {
+    const float* xrow[OSP_MAX_WORKERS];  // every worker's delta row (local HBM or peer)
+    float* agg[kMaxRanks];               // every rank's pull buffer [ldX]
+    double* part[kMaxRanks];             // every rank's per-tile PGP partials [NT]
+    unsigned* tflag[kMaxRanks];          // every rank's per-tile ready flags [NT]
+    unsigned* ready[kMaxRanks];          // every rank's deltas-ready slots [kMaxRanks]
+    unsigned* error;                     // local: set when a bounded wait timed out
+    int world, rank, n_loc;
+    unsigned epoch;                      // iteration number (1-based)
+    int mode;                            // XMode
+    int c0, c1;                          // XM_ICS chunk range
+    int solo;                            // diagnostics: own tiles only, no waits or flags
+    int vec;                             // every row and buffer 16-byte aligned
+    int slot_rows;                       // shared-memory rows per ring slot
+    int lag;                             // B items' due-time lag behind the A items
 };
-// part: 0 the stage's whole tile sequence, 1 / 2 its first / second half
-cudaError_t launch_shard_agg(const GroupView& g, const AggParams& ap, const PeerTable& pt,
-                             int stage, int c0, int c1, int grid, const XSync& sy, cudaStream_t s,
-                             int part = 0);
-cudaError_t launch_shard_apply(const GroupView& g, const AggParams& ap_loc, const PeerTable& pt,
-                               const float* Xloc, uint64_t ldX, int stage, int c0, int c1, int grid,
-                               const XSync& sy, cudaStream_t s);
-// Streaming shard kernel (kernels/shard_stream.cu): push, aggregate, pull and
-// apply of one stage in one launch, per-tile flags instead of grid barriers.
-struct StreamArgs {
-    unsigned* tflag[kMaxRanks];  // every rank's per-tile ready flags [NT]
-    double* part[kMaxRanks];     // every rank's per-tile PGP partials [NT]
-    unsigned tepoch;             // tile-flag value of this launch (2*iteration + stage - 2)
-    unsigned xepoch;             // deltas-ready value of this iteration
-    int stage, c0, c1;
-    int vec;                     // rows, G, P and pull buffers 16-byte aligned
-    unsigned long long* dbg;     // optional counters (diagnostics), or null
-    size_t ring_bytes;           // shared-memory ring per CTA (set by the launcher)
-};
-bool shard_stream_supported(int n_workers, int T, int L);
-cudaError_t launch_shard_stream(const GroupView& g, const AggParams& ap, const PeerTable& pt,
-                                const StreamArgs& sa, cudaStream_t s);
-// stage-1 apply + stage-2 aggregate of chunks [c0, c1) in one launch
-// Which lists a fused launch runs: the apply list (mode 0: every stage-1 tile;
-// 1: RS tiles before the RS sequence's middle + all local estimates; 2: RS
-// tiles from the middle on) beside the aggregate of agg_stage's sequence
-// (agg_part as launch_shard_agg's part).
-struct FusedLists {
-    int apply_mode = 0;
-    int agg_stage = 2;
-    int agg_part = 0;
-};
-cudaError_t launch_shard_fused(const GroupView& g, const AggParams& ap_all, const AggParams& ap_loc,
-                               const PeerTable& pt, const float* Xloc, uint64_t ldX, int c0, int c1,
-                               int grid, const XSync& sy, cudaStream_t s,
-                               FusedLists fl = FusedLists{});
+int x_slot_rows(int n_workers);
+bool shard_x_supported(int n_workers, int T, int L);
+cudaError_t launch_shard_x(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s);
+
+// Opt a kernel into `smem` bytes of dynamic shared memory and return its
+// occupancy, cached per (context, kernel, bytes) (stage_tma.cu).
+cudaError_t tma_blocks_per_sm(const void* kern, int threads, size_t smem, int* per_sm);
 
 // ---- payload wire codec (kernels/codec.cu) -----------------------------------
 struct CodecSeg {
@@ -223,6 +189,9 @@ cudaError_t launch_stage2(const GroupView& g, const AggParams& ap, const float* 
 cudaError_t launch_resolve(const GroupView& g, const AggParams& ap, const float* X, uint64_t ldX,
                            cudaStream_t s);
 cudaError_t launch_set_budget(const GroupView& g, uint64_t budget, cudaStream_t s);
+// Per-tile PGP partials |grads * params| in g's tile geometry (g.partials).
+cudaError_t launch_pgp_tiles(const GroupView& g, const float* params, const float* grads,
+                             cudaStream_t s);
 // Rebuild device lists from g.flags + the given rank-ordered ICS ids (device).
 cudaError_t launch_install_gib(const GroupView& g, const int* order, int n_order, uint32_t tag,
                                cudaStream_t s);

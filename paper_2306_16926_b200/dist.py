@@ -26,7 +26,11 @@ class ShardGroup:
     def __init__(self, part: Partition, n_workers: int, weights: Optional[Sequence[float]] = None,
                  n_chunks: int = 4, init_params: Optional[torch.Tensor] = None,
                  tile_elems: int = 0, sgd_lr: float = 0.0, rank: Optional[int] = None,
-                 world: Optional[int] = None, group=None, stream=None):
+                 world: Optional[int] = None, group=None, defer_ics: bool = False, stream=None):
+        """defer_ics: stage 1 exchanges the barrier layers only and stage 2 the
+        deferred chunks (OSP_SHARD_DEFER_ICS: the ICS traffic can run beside the
+        next iteration's compute); default: one exchange per iteration in stage 1,
+        stage 2 a local broadcast of the carry. Identical results."""
         self.rank = dist.get_rank(group) if rank is None else rank
         self.world = dist.get_world_size(group) if world is None else world
         if n_workers % self.world:
@@ -39,7 +43,8 @@ class ShardGroup:
         w = list(weights) if weights is not None else [1.0 / n_workers] * n_workers
         self._w = (c_dbl * n_workers)(*w)
         cfg = _capi.osp_shard_config(self.world, self.rank, n_workers, ctypes.cast(self._w, P(c_dbl)),
-                                     n_chunks, tile_elems, sgd_lr)
+                                     n_chunks, tile_elems, sgd_lr,
+                                     _capi.SHARD_DEFER_ICS if defer_ics else 0)
         init = None
         if init_params is not None:
             _dev_f32(init_params, "init_params")
@@ -107,24 +112,21 @@ class ShardGroup:
         _check(lib().osp_shard_step(self._h, buf, _stream(stream)))
 
     def profile(self, buf: int, stream=None) -> dict:
-        """One step with events between the kernels (ms per phase)."""
+        """One step with events between the phases (ms per phase)."""
         out = (ctypes.c_float * 8)()
         _check(lib().osp_shard_profile(self._h, buf, out, _stream(stream)))
-        if self.streaming:
-            names = ["stage1", "stage2", "resolve"]
-        else:
-            names = ["agg1", "apply1+agg2", "apply2", "resolve"]
-        return {n: float(v) for n, v in zip(names, out) if n}
+        return {n: float(v) for n, v in zip(["stage1", "stage2", "resolve"], out)}
+
+    @property
+    def deferred_ics(self) -> bool:
+        """True: stage 2 exchanges the deferred layers; False: single exchange."""
+        return bool(lib().osp_shard_deferred_ics(self._h))
 
     @property
     def mode(self) -> str:
-        return ("streaming (per-tile flags)" if self.streaming
-                else "barrier (agg / barrier / apply)")
-
-    @property
-    def streaming(self) -> bool:
-        """True: streaming kernels (per-tile flags); False: barrier mode."""
-        return bool(lib().osp_shard_streaming(self._h))
+        return ("deferred ICS: stage 1 exchanges the RS layers, stage 2 the ICS chunks"
+                if self.deferred_ics else
+                "single exchange: every tile in stage 1 (ICS carry), stage 2 local")
 
     def solo_agg(self, stage: int, buf: int, stream=None):
         """Diagnostics: this rank's push/pull of a stage alone (osp_shard_solo_agg)."""

@@ -3,7 +3,10 @@
 N_w = 8 logical workers spread N_w/N per GPU (strong scaling: the job is one
 OSP iteration over the whole model per step, whatever N). Timing: W warm-up
 steps, barrier + synchronize, K steps bracketed by CUDA events on the launching
-stream, max over ranks.
+stream, max over ranks. The timed step is the single-exchange mode (one
+exchange kernel, the resolve and the local stage-2 broadcast); the overlap
+report runs the deferred-ICS mode (stage 2's exchange beside the next
+iteration's compute) with a fixed budget and with the closed-loop budget.
 """
 from __future__ import annotations
 
@@ -15,6 +18,12 @@ import time
 import numpy as np
 import torch
 import torch.distributed as dist
+
+
+def _max(vals, device="cuda"):
+    t = torch.tensor(vals, dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.tolist()]
 
 
 def run(args, metric: str, unit: str):
@@ -37,8 +46,10 @@ def run(args, metric: str, unit: str):
         dist.init_process_group("gloo")
     else:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = "cpu" if oversub else "cuda"
     counts = layouts.get(args.layout)
     N, M, L = args.workers, sum(counts), len(counts)
+    n_loc = N // world
     model_bytes = 4 * M
     budget = int(args.budget_frac * model_bytes)
     part = osp.Partition(counts)
@@ -49,26 +60,16 @@ def run(args, metric: str, unit: str):
     sh.set_budget(budget)
     stream = torch.cuda.current_stream()
 
-    def step(k, evs=None):
+    def step(k):
         buf = k % 2
-        if evs is not None:
-            evs[0].record(stream)
         if args.per_chunk:
-            # message-by-message shape: barrier stage, then one launch set per chunk
+            # message-by-message shape: stage 1, one stage-2 launch per chunk, resolve
             sh.stage1(buf)
-            if evs is not None:
-                evs[1].record(stream)
             for c in range(args.chunks):
                 sh.stage2(buf, c, c + 1)
-            if evs is not None:
-                evs[2].record(stream)
             sh.resolve(buf)
         else:
-            # fused step: stage-2 push/pull inside the stage-1 apply launch
             sh.step(buf)
-            if evs is not None:
-                evs[1].record(stream)
-                evs[2].record(stream)
 
     for k in range(args.warmup):
         step(k)
@@ -76,7 +77,6 @@ def run(args, metric: str, unit: str):
     torch.cuda.synchronize()
     tag0 = sh.read_gib()["tag"]
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
     clocks = None
@@ -88,74 +88,33 @@ def run(args, metric: str, unit: str):
     dist.barrier()
     torch.cuda.synchronize()
     start.record(stream)
-    ev_every = max(1, getattr(args, "event_every", 4))
-    sampled = [k for k in range(K) if k % ev_every == 0]
     for k in range(K):
-        step(args.warmup + k, evs[k] if k % ev_every == 0 else None)
+        step(args.warmup + k)
     end.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop() if clocks else None
     sh.check()
-    local_ms = start.elapsed_time(end)
-    s1 = sum(evs[k][0].elapsed_time(evs[k][1]) for k in sampled) / len(sampled)
-    s2 = sum(evs[k][1].elapsed_time(evs[k][2]) for k in sampled) / len(sampled)
-    t = torch.tensor([local_ms, s1, s2], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, s1_max, s2_max = (float(x) for x in t.tolist())
+    total_ms, = _max([start.elapsed_time(end)], dev)
     ms_step = total_ms / K
     u = sh.local.deferred_history(tag0, K).astype(np.float64) / model_bytes
-    n_loc = N // world
     u_mean = float(u.mean())
-    # per-GPU algorithmic HBM bytes per step
-    if sh.streaming:
-        # local rows read once (by this rank or an owner), G read + written, agg
-        # written into the pull buffer (own tiles locally, the rest by the peers)
-        # and read back on the peers' tiles, worker rows, local estimate on ICS
-        # layers
-        hbm_bytes = 4.0 * M * (2 * n_loc + 2 + 1 + (world - 1.0) / world
-                               + u_mean * (2 * n_loc + 1))
-    else:
-        # own rows served to the shard owners, agg written + read, G read + written,
-        # worker rows (+ local estimate on ICS layers)
-        hbm_bytes = 4.0 * M * (4 + n_loc * (2 + 2 * u_mean))
-    # per-GPU NVLink bytes per step (each direction): remote delta rows read by this
-    # rank's shard + its aggregate stored to the other ranks
+    # per-GPU NVLink bytes per step, each direction: the peers' delta rows this
+    # rank's shard reads + its aggregate stored into the other ranks
     nvl_bytes = 4.0 * M * ((N - n_loc) / world + (world - 1) / world)
+    # per-GPU algorithmic HBM bytes per step (single exchange): local rows read
+    # once (by this rank or a peer) and written once, G read, the pull buffer
+    # written everywhere and read back on the peers' tiles, G (RS) / carry (ICS)
+    # written, the local rows re-read for the peers' deferred tiles, and the
+    # stage-2 broadcast (carry read, G + local rows written)
+    hbm_bytes = 4.0 * M * (2 * n_loc + 1 + 1 + (world - 1) / world + 1
+                           + u_mean * (n_loc * (world - 1) / world + 2 + n_loc))
 
     # ---- per-phase breakdown (events between kernels, 5 profiled steps, max over ranks)
-    phases = None
     prof = [sh.profile(k % 2) for k in range(5)]
     keys = list(prof[0])
-    pt = torch.tensor([sum(p[k] for p in prof) / len(prof) for k in keys], dtype=torch.float64,
-                      device="cuda")
-    dist.all_reduce(pt, op=dist.ReduceOp.MAX)
-    phases = {k: float(v) for k, v in zip(keys, pt.tolist())}
+    phases = dict(zip(keys, _max([sum(p[k] for p in prof) / len(prof) for k in keys], dev)))
 
-    # ---- stage 2 overlapped with the next iteration's (synthetic) compute
-    ovl = None
-    if args.overlap_ms > 0:
-        from . import overlap
-        comp = overlap.SyntheticCompute(args.overlap_ms)
-
-        def s2r(i):
-            sh.stage2(i % 2)
-            sh.resolve(i % 2)
-
-        res = overlap.run(lambda i: sh.stage1(i % 2), s2r, comp, K=min(K, 50), W=3)
-        sh.check()
-        keys = ["iter_ms_overlapped", "iter_ms_serial", "exposed_stage2_ms_mean",
-                "exposed_stage2_ms_max", "stage2_plus_resolve_ms_mean"]
-        ot = torch.tensor([res[k] for k in keys] + [comp.ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(ot, op=dist.ReduceOp.MAX)
-        ovl = {k: float(v) for k, v in zip(keys + ["t_c_ms"], ot.tolist())}
-        # Eq. 5 budget from the measured compute time and the measured per-GPU
-        # NVLink rate of this run (runner.cpp:364-376 umax_measured, on hardware)
-        nvl_bps = nvl_bytes / (total_ms / K * 1e-3)
-        ovl["umax_measured_bytes"] = osp.compute_umax(nvl_bps, ovl["t_c_ms"] * 1e-3, N,
-                                                      model_bytes)
-        ovl["umax_frac_of_model"] = ovl["umax_measured_bytes"] / model_bytes
-
-    # ---- e2e: pinned host deltas -> device (this rank's rows), step, GIB read-back
+    # ---- e2e: pinned host deltas -> device (this rank's rows), step, result read-back
     host = [sh.deltas(b).cpu().pin_memory() for b in range(2)]
     params_host = torch.empty(M, dtype=torch.float32).pin_memory()
     e2e = []
@@ -171,19 +130,60 @@ def run(args, metric: str, unit: str):
         t1 = time.perf_counter()
         if k > 0:
             e2e.append((t1 - t0) * 1e3)
-    e2e_t = torch.tensor([statistics.median(e2e)], dtype=torch.float64, device="cuda")
-    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(e2e_t.item())
-    peaks = {}
-    try:
-        with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
-                               "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except Exception:
-        pass
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    nvl_peak = 770.0
+    e2e_ms, = _max([statistics.median(e2e)], dev)
+    geometry = sh.local.geometry()
+    mode = sh.mode
+    sh.close()
+    del host
+    torch.cuda.empty_cache()
+
+    # ---- OSP overlap: the deferred-ICS mode, stage 2's exchange on a side stream
+    # beside the next iteration's (synthetic) compute; fixed budget, then the
+    # closed-loop budget from the measured t_c and NVLink rate
+    ovl = None
+    if args.overlap_ms > 0:
+        from . import overlap
+        from .budget import BudgetLoop
+        sd = ShardGroup(part, N, None, n_chunks=args.chunks, tile_elems=args.tile, defer_ics=True)
+        sd.connect_via()
+        for b in range(2):
+            sd.fill_synth(args.seed, b, b)
+        sd.set_budget(budget)
+        comp = overlap.SyntheticCompute(args.overlap_ms)
+
+        def s2r(i):
+            sd.stage2(i % 2)
+            sd.resolve(i % 2)
+
+        res = overlap.run(lambda i: sd.stage1(i % 2), s2r, comp, K=min(K, 50), W=3)
+        sd.check()
+        keys = ["iter_ms_overlapped", "iter_ms_serial", "exposed_stage2_ms_mean",
+                "exposed_stage2_ms_max", "stage2_plus_resolve_ms_mean"]
+        ovl = dict(zip(keys + ["t_c_ms"], _max([res[k] for k in keys] + [comp.ms], dev)))
+        ovl["mode"] = sd.mode
+        ovl["budget_frac"] = args.budget_frac
+        # closed loop (runner.cpp:364-376, protocol.cpp:396-405): budgets start
+        # at 0 and follow Eq. 5 / Alg. 1 from the measured t_c and NVLink rate
+        # (the per-GPU NVLink bytes of an iteration do not depend on its split:
+        # every element crosses the links once, in stage 1 or in stage 2)
+        ipe = 5
+        loop = BudgetLoop(ipe, N, model_bytes)
+        cl = overlap.run_closed_loop(lambda i: sd.stage1(i % 2), s2r, sd.set_budget, comp, loop,
+                                     lambda j: nvl_bytes, K=30, ipe=ipe)
+        sd.check()
+        ovl["closed_loop"] = cl
+        sd.close()
+
     if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")) as f:
+                peaks = json.load(f)
+        except Exception:
+            pass
+        hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+        nvl_peak = 770.0
         hbm_gbs = hbm_bytes / (ms_step * 1e-3) / 1e9
         nvl_gbs = nvl_bytes / (ms_step * 1e-3) / 1e9
         line = {
@@ -192,24 +192,21 @@ def run(args, metric: str, unit: str):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
             "config": workload_config(args, counts),
             "arm": {"parallelism": f"ps-shard{world}", "workers_per_gpu": n_loc,
-                    "shard_kernels": sh.mode,
+                    "shard_mode": mode, "tile_elems": geometry["tile_elems"],
                     "deltas": "2 device-resident sets (iterations 0 and 1) alternating",
-                    "tile_elems": sh.local.geometry()["tile_elems"]},
+                    "per_chunk": bool(args.per_chunk)},
             "roofline": {"bound": "nvlink" if nvl_bytes / nvl_peak > hbm_bytes / hbm_peak else "hbm",
+                         "kernel": "k_shard_x (exchange + apply, one launch per step)",
                          "achieved": nvl_gbs, "peak": nvl_peak, "unit": "GB/s",
                          "frac": nvl_gbs / nvl_peak, "traffic": None,
                          "note": "per-GPU NVLink bytes each direction / step time; peak = measured "
-                                 "peer copy 770 GB/s (B200_PROFILING.md)",
+                                 "one-way peer copy 770 GB/s (B200_PROFILING.md); both directions "
+                                 "load at once, where the measured ceiling is 667 GB/s",
                          "nvlink_bytes_per_gpu_per_direction": nvl_bytes,
                          "collective_bus_gbs": nvl_gbs,
                          "frac_vs_bidirectional_667": nvl_gbs / 667.0,
-                         "ncu": "profiles/r1_ncu_full_shard_agg_solo.csv (k_shard_agg alone: NVLink "
-                                "rx user bytes == algorithmic; a profiled multi-rank step cannot "
-                                "run under ncu, see profiles/r1_multi_gpu_notes.md)",
-                         "hbm_gbs_per_gpu": hbm_gbs, "hbm_frac": hbm_gbs / hbm_peak},
-            "breakdown_ms": ({"stage1": s1_max, "stage2": s2_max,
-                              "resolve": ms_step - s1_max - s2_max} if args.per_chunk
-                             else {"step": s1_max}),
+                         "hbm_gbs_per_gpu": hbm_gbs, "hbm_frac": hbm_gbs / hbm_peak,
+                         "hbm_alg_bytes_per_gpu": hbm_bytes},
             "phase_ms": phases,
             "overlap": ovl,
             "u_mean": u_mean,
@@ -218,11 +215,9 @@ def run(args, metric: str, unit: str):
                     "d2h_bytes_per_step": (8 + (L + 7) // 8) * world + 4 * M,
                     "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read on "
                             "every rank, updated global vector read on rank 0"},
-            # streaming: stage1, stage2, resolve per step (per chunk: one stage-2 launch
-            # each); barrier mode: agg1, apply1+agg2, apply2, resolve (per chunk: agg1,
-            # apply1, agg2 + apply2 per chunk, resolve)
-            "gpu_launches": K * (((2 + args.chunks) if args.per_chunk else 3) if sh.streaming
-                                 else ((3 + 2 * args.chunks) if args.per_chunk else 4)),
+            # per step: the exchange kernel, the resolve, the stage-2 broadcast
+            # (per chunk: one broadcast launch per chunk)
+            "gpu_launches": K * (2 + (args.chunks if args.per_chunk else 1)),
             "clocks": clk,
         }
         if oversub:
@@ -230,5 +225,4 @@ def run(args, metric: str, unit: str):
                                       "code-path check, timings not meaningful")
         print(json.dumps(line), flush=True)
     dist.barrier()
-    sh.close()
     dist.destroy_process_group()

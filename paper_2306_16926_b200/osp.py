@@ -281,6 +281,27 @@ def rank_and_gib(part: Partition, scores, budget: int, stream=None):
     return order, flags
 
 
+def pgp_rank_gib(part: Partition, params: torch.Tensor, grads: torch.Tensor, budget: int,
+                 stream=None):
+    """check_resolution's PGP -> rank -> GIB (protocol.cpp:407-419) on device
+    vectors, certified (osp_pgp_rank_gib) -> (scores, deferred ids in rank
+    order, flags)."""
+    _dev_f32(params, "params")
+    _dev_f32(grads, "grads")
+    if params.numel() != part.total_count() or grads.numel() != part.total_count():
+        raise ShapeError("vectors do not match the partition")
+    L = part.layer_count()
+    scores = np.empty(L, dtype=np.float64)
+    order = np.empty(L, dtype=np.int32)
+    flags = np.empty(L, dtype=np.uint8)
+    k = c_i64()
+    _check(lib().osp_pgp_rank_gib(part.handle, _ptr(params), _ptr(grads), int(budget),
+                                  scores.ctypes.data_as(P(c_dbl)),
+                                  order.ctypes.data_as(P(ctypes.c_int32)), ctypes.byref(k),
+                                  flags.ctypes.data_as(P(ctypes.c_uint8)), _stream(stream)))
+    return scores, order[: k.value].copy(), flags
+
+
 def split_for_sync(part: Partition, ics_flags, ics_order, n_chunks: int):
     """split_for_sync index lists (protocol.cpp:122-166) -> (rs_ids, chunk_of, n_used)."""
     f, fp = _u8(ics_flags)

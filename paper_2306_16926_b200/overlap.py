@@ -94,3 +94,63 @@ def run(stage1, stage2_resolve, compute, K: int, W: int):
     return {"t_c_ms": None, "iter_ms_overlapped": overlapped, "iter_ms_serial": serial,
             "exposed_stage2_ms_mean": sum(exposed) / K, "exposed_stage2_ms_max": max(exposed),
             "stage2_plus_resolve_ms_mean": sum(s2) / K}
+
+
+def run_closed_loop(stage1, stage2_resolve, set_budget, compute, loop, link_bytes, K: int,
+                    ipe: int):
+    """The overlapped schedule of run() with the SGU budget driven by the device
+    measurements (budget.BudgetLoop, runner.cpp:364-376 + protocol.cpp:396-405):
+    at every epoch end the host reads the epoch's compute-phase times and
+    stage-2 link rates from CUDA events (one host sync per epoch), and the
+    resolution of the epoch's last iteration builds the next GIB with the tuned
+    budget (set_budget is stream-ordered before it). link_bytes(i): the bytes
+    the synchronization of iteration i (stage 1 + stage 2) moves on its link;
+    the link rate is those bytes over the stage-1 time plus the stage-2 +
+    resolve time under the overlap. Returns the per-iteration budgets and the
+    loop's U_max history."""
+    from .budget import synthetic_loss
+    main = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    ev_s0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_s1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_c0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_c = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev_r = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    budgets = []
+    budget = loop.budget_for_epoch(1)
+    set_budget(budget)
+    torch.cuda.synchronize()
+    for i in range(K):
+        if i > 0:
+            main.wait_event(ev_r[i - 1])
+        ev_s0[i].record(main)
+        stage1(i)
+        ev_s1[i].record(main)
+        ev_c0[i].record(main)
+        compute()
+        ev_c[i].record(main)
+        side.wait_event(ev_s1[i])
+        if (i + 1) % ipe == 0:
+            # epoch end: this epoch's compute phases are measured (ev_c[i]
+            # implies every earlier stage 2 has finished: stage 1 waited on it)
+            ev_c[i].synchronize()
+            e0 = i + 1 - ipe
+            for j in range(e0, i + 1):
+                t_c = ev_c0[j].elapsed_time(ev_c[j]) * 1e-3
+                # sync time of the epoch's earlier iterations (j < i)
+                ts = ((ev_s0[j].elapsed_time(ev_s1[j]) + ev_s1[j].elapsed_time(ev_r[j])) * 1e-3
+                      if j < i else 0.0)
+                loop.record(j, t_c, link_bytes(j) if j < i else 0.0, ts,
+                            synthetic_loss(loop.epoch_of(j)))
+            loop.on_resolution(i)
+            budget = loop.budget_for_next(i)
+        with torch.cuda.stream(side):
+            set_budget(budget)
+            stage2_resolve(i)
+            ev_r[i].record(side)
+        budgets.append(budget)
+    main.wait_event(ev_r[K - 1])
+    torch.cuda.synchronize()
+    return {"iterations_per_epoch": ipe, "budgets_per_iteration": budgets,
+            "epoch_budgets": {str(k): v for k, v in sorted(loop.epoch_budget.items())},
+            "umax_per_epoch": loop.umax_history}

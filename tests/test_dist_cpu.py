@@ -1,14 +1,18 @@
 """CPU (gloo, world_size 2/4/8) test of the multi-GPU decomposition's host logic.
 
-Mirrors what osp_shard_* does on the device, with torch.distributed over gloo as
-the transport: per stage, the tile sequence (RS layers ascending for stage 1,
-ICS chunks in rank order for stage 2; tiles of T elements that never straddle a
-layer) is split into P equal tile-count ranges (k_shard_agg); the owner
-aggregates its range over ALL workers in the fixed ascending worker order
-(fp64, oracle.aggregate_layer); the aggregates are all-gathered; every rank
-applies G += agg and its own workers' rows. Asserts bit-equality with the
-single-process oracle step (global vector, every rank's worker rows, next GIB)
-and that the owner ranges cover every element of every stage exactly once.
+Mirrors what osp_shard_* does on the device (kernels/shard_x.cu), with
+torch.distributed over gloo as the transport. The exchanged tile sequence
+(single-exchange mode: every tile in layer order; deferred-ICS mode: the RS
+layers ascending for stage 1, the ICS chunks in rank order for stage 2; tiles of
+T elements that never straddle a layer) is split into P equal tile-count owner
+ranges, and each owner range into C per-CTA slices; the owner aggregates its
+range over ALL workers in the fixed ascending worker order (fp64,
+oracle.aggregate_layer); the aggregates are all-gathered; every rank applies
+G += agg and its own workers' rows (single exchange: the deferred layers get
+the local estimate and the carry G + agg, which stage 2 broadcasts). Asserts
+bit-equality with the single-process oracle step (global vector, every rank's
+worker rows, next GIB) and that the (owner, CTA slice) pieces cover every
+element of every stage exactly once.
 """
 import os
 import socket
@@ -31,7 +35,7 @@ def _free_port():
     return port
 
 
-def stage_sequences(counts, flags, order, n_chunks, bpe, T):
+def stage_sequences(counts, flags, order, n_chunks, bpe, T, single=False):
     """[(stage, [(layer, start, end), ...tiles in sequence order]), ...]"""
     from oracle import oracle
     offsets = np.concatenate([[0], np.cumsum(counts)[:-1]]).astype(np.int64)
@@ -43,6 +47,8 @@ def stage_sequences(counts, flags, order, n_chunks, bpe, T):
                 out.append((l, int(offsets[l]) + s, int(offsets[l]) + min(s + T, int(counts[l]))))
         return out
 
+    if single:
+        return [(0, tiles_of(range(len(counts))))]
     rs = [l for l in range(len(counts)) if not flags[l]]
     seqs = [(1, tiles_of(rs))]
     _, chunk_of, used = oracle.split(counts, bpe, flags, order, n_chunks)
@@ -79,13 +85,17 @@ def _rank_main(rank, world, port, cfg, q):
             X = np.concatenate([g.numpy() for g in gathered])
             agg = np.zeros(M, np.float32)
             covered = np.zeros(M, np.int32)
-            for stage, tiles in stage_sequences(counts, flags, order, nc, 4, T):
+            single = cfg.get("single", False)
+            C = cfg.get("ctas", 3)
+            for stage, tiles in stage_sequences(counts, flags, order, nc, 4, T, single):
                 U = len(tiles)
                 lo, hi = (U * rank) // world, (U * (rank + 1)) // world
                 part = np.zeros(M, np.float32)
-                for (l, s, e) in tiles[lo:hi]:
-                    part[s:e] = oracle.aggregate_layer([X[k][s:e] for k in range(N)], w)
-                    covered[s:e] += 1
+                for c in range(C):  # CTA c's slice of this rank's owner range
+                    a, b = lo + ((hi - lo) * c) // C, lo + ((hi - lo) * (c + 1)) // C
+                    for (l, s, e) in tiles[a:b]:
+                        part[s:e] = oracle.aggregate_layer([X[k][s:e] for k in range(N)], w)
+                        covered[s:e] += 1
                 got = [torch.zeros(M, dtype=torch.float32) for _ in range(world)]
                 dist.all_gather(got, torch.from_numpy(part))
                 cov = [torch.zeros(M, dtype=torch.int32) for _ in range(world)]
@@ -94,7 +104,24 @@ def _rank_main(rank, world, port, cfg, q):
                     lo_r, hi_r = (U * r) // world, (U * (r + 1)) // world
                     for (l, s, e) in tiles[lo_r:hi_r]:
                         agg[s:e] = t.numpy()[s:e]
-                if stage == 1:
+                if stage == 0:
+                    # single exchange: RS elements G' = G + agg; ICS elements the
+                    # local estimate and the carry, broadcast by stage 2
+                    ics = np.zeros(M, bool)
+                    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+                    for l in np.flatnonzero(flags):
+                        ics[offs[l]:offs[l + 1]] = True
+                    G_new = (G_mine + agg).astype(np.float32)
+                    for i in range(n_loc):
+                        P_mine[i] = np.where(ics, (G_mine + X[rank * n_loc + i]).astype(np.float32),
+                                             G_new)
+                    carry = G_new
+                    G_mine = np.where(ics, G_mine, G_new)
+                    # stage 2: the local broadcast of the carry
+                    G_mine = np.where(ics, carry, G_mine)
+                    for i in range(n_loc):
+                        P_mine[i][ics] = carry[ics]
+                elif stage == 1:
                     # barrier: RS elements G' = G + agg; ICS elements local estimate
                     rs_mask = np.zeros(M, bool)
                     for (l, s, e) in tiles:
@@ -141,6 +168,13 @@ def _rank_main(rank, world, port, cfg, q):
              chunks=4, budget_frac=0.5, iters=3, seed=11, T=128)),
     (8, dict(counts=[300, 64, 1000, 3, 517, 129, 12, 77], N=8, weights=[0.125] * 8,
              chunks=4, budget_frac=0.5, iters=2, seed=7, T=64)),
+    # the default single-exchange mode (every tile in stage 1, the ICS carry)
+    (2, dict(counts=[700, 64, 1000, 3, 2048, 129, 512, 77], N=4, weights=[0.25] * 4, chunks=3,
+             budget_frac=0.5, iters=3, seed=11, T=256, single=True, ctas=5)),
+    (4, dict(counts=[700, 64, 1000, 3, 2048, 129, 512, 77, 33], N=8, weights=[0.125] * 8,
+             chunks=4, budget_frac=0.6, iters=3, seed=11, T=128, single=True, ctas=7)),
+    (8, dict(counts=[300, 64, 1000, 3, 517, 129, 12, 77], N=8, weights=[0.125] * 8,
+             chunks=4, budget_frac=0.5, iters=2, seed=7, T=64, single=True)),
 ])
 def test_sharded_decomposition_gloo(world, cfg):
     ctx = mp.get_context("spawn")

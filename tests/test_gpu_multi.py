@@ -1,6 +1,8 @@
-"""Multi-GPU parity (>= 2 GPUs): the sharded path (osp_shard_*, NVLink peer
-memory) must be bit-identical to the oracle — global replica on every rank,
-every rank's worker rows, and the next GIB — for several iterations."""
+"""Multi-GPU parity: the sharded path (osp_shard_*, NVLink peer memory) must be
+bit-identical to the oracle — global replica on every rank, every rank's
+worker rows, and the next GIB — for several iterations, in both exchange modes
+(single exchange with the ICS carry; deferred ICS). The *_oversubscribed tests
+run on any box (ranks share the GPUs that exist), the others need world GPUs."""
 import os
 import socket
 import sys
@@ -32,10 +34,6 @@ def _worker(rank, world, port, cfg, q):
         from paper_2306_16926_b200 import dist as odist
         from paper_2306_16926_b200 import osp
 
-        if "stream" in cfg:
-            os.environ["OSP_SHARD_STREAM"] = "1" if cfg["stream"] else "0"
-        if "pipe" in cfg:
-            os.environ["OSP_SHARD_PIPE"] = "1" if cfg["pipe"] else "0"
         torch.cuda.set_device(rank % torch.cuda.device_count())
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
@@ -47,10 +45,9 @@ def _worker(rank, world, port, cfg, q):
         p0 = rng.uniform(-1, 1, M).astype(np.float32) if cfg["p0_seed"] else np.zeros(M, np.float32)
         part = osp.Partition(counts)
         sh = odist.ShardGroup(part, N, w, n_chunks=nc, init_params=torch.as_tensor(p0, device="cuda"),
-                              tile_elems=cfg.get("tile", 0))
+                              tile_elems=cfg.get("tile", 0), defer_ics=cfg.get("defer", False))
         sh.connect_via()
-        if "stream" in cfg:
-            assert sh.streaming == bool(cfg["stream"]), "shard kernel family"
+        assert sh.deferred_ics == bool(cfg.get("defer", False)), "shard exchange mode"
         G = p0.copy()
         P = np.tile(p0, (N, 1))
         flags = np.zeros(len(counts), np.uint8)
@@ -63,6 +60,12 @@ def _worker(rank, world, port, cfg, q):
             sh.set_budget(budget)
             if cfg.get("per_chunk"):
                 sh.stage1(buf)
+                sh.check()
+                # stage-1 state: RS layers G', deferred layers the local estimate
+                p1 = sh.worker_params.cpu().numpy()
+                mine1 = r["p_stage1"][rank * sh.n_loc:(rank + 1) * sh.n_loc]
+                assert np.array_equal(p1.view(np.uint32), mine1.view(np.uint32)), \
+                    f"stage-1 rows rank {rank} it {it}"
                 for c in range(nc):
                     sh.stage2(buf, c, c + 1)
                 sh.resolve(buf)
@@ -103,69 +106,55 @@ def run_world(cfg, world=2, oversubscribe=False):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("stream", [True, False])
-def test_shard_two_gpus_resnet_like(stream):
+@pytest.mark.parametrize("defer", [False, True])
+def test_shard_two_gpus_resnet_like(defer):
     from paper_2306_16926_b200 import layouts
     run_world(dict(counts=layouts.resnet50()[:60], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, stream=stream))
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, defer=defer))
 
 
-def test_shard_two_gpus_ragged_unequal_weights():
-    # tile 256: no streaming kernel for this shape, barrier mode
+@pytest.mark.parametrize("defer", [False, True])
+def test_shard_two_gpus_ragged_unequal_weights_per_chunk(defer):
+    # odd layer sizes: unstaged (scalar) tiles next to staged ones; per-chunk stage 2
     rng = np.random.default_rng(3)
     counts = [int(c) for c in rng.integers(1, 7000, 37)]
     w = [float(x) for x in 0.1 + rng.random(4)]
     run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=0.7, iters=4, seed=5,
-                   p0_seed=9, tile=256, per_chunk=True, stream=False))
-
-
-def test_shard_stream_ragged_per_chunk():
-    # odd layer sizes: unstaged (scalar) tiles next to staged ones; per-chunk stage 2
-    rng = np.random.default_rng(4)
-    counts = [int(c) for c in rng.integers(1, 9000, 41)]
-    w = [float(x) for x in 0.1 + rng.random(4)]
-    run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=0.6, iters=4, seed=6,
-                   p0_seed=2, per_chunk=True, stream=True))
+                   p0_seed=9, tile=512, per_chunk=True, defer=defer))
 
 
 @pytest.mark.parametrize("frac", [0.0, 1.0])
-def test_shard_stream_budget_edges(frac):
-    # 0.0: every layer in stage 1's exchange; 1.0: stage 1 only local estimates
+def test_shard_budget_edges(frac):
+    # 0.0: every layer in the barrier; 1.0: every layer deferred
     from paper_2306_16926_b200 import layouts
-    run_world(dict(counts=layouts.resnet50()[:50], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=frac, iters=3, seed=13, p0_seed=7, stream=True))
+    for defer in (False, True):
+        run_world(dict(counts=layouts.resnet50()[:50], N=8, weights=[0.125] * 8, chunks=4,
+                       budget_frac=frac, iters=3, seed=13, p0_seed=7, defer=defer))
 
 
-@pytest.mark.parametrize("stream", [True, False])
-def test_shard_four_gpus(stream):
+@pytest.mark.parametrize("defer", [False, True])
+def test_shard_four_gpus(defer):
     from paper_2306_16926_b200 import layouts
     run_world(dict(counts=layouts.resnet50()[:80], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, stream=stream), world=4)
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, defer=defer), world=4)
 
 
-def test_shard_four_gpus_stream_ragged():
+def test_shard_four_gpus_ragged_per_chunk():
     rng = np.random.default_rng(12)
     counts = [int(c) for c in rng.integers(1, 20000, 30)]
     w = [float(x) for x in 0.1 + rng.random(8)]
     run_world(dict(counts=counts, N=8, weights=w, chunks=4, budget_frac=0.5, iters=3, seed=3,
-                   p0_seed=5, stream=True), world=4)
+                   p0_seed=5, per_chunk=True), world=4)
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_shard_pipelined_step(world):
-    """Pipelined barrier mode: the RS exchange in two halves, each half's apply
-    beside the next exchange (OSP_SHARD_PIPE=1); ragged layers, unequal weights,
-    budget edges, per-iteration GIB changes."""
-    from paper_2306_16926_b200 import layouts
-    run_world(dict(counts=layouts.resnet50()[:70], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=0.5, iters=4, seed=11, p0_seed=3, stream=False, pipe=True),
-              world=world)
-    rng = np.random.default_rng(21)
-    counts = [int(c) for c in rng.integers(1, 9000, 33)]
-    w = [float(x) for x in 0.1 + rng.random(4)]
-    for frac in (0.0, 0.6, 1.0):
-        run_world(dict(counts=counts, N=4, weights=w, chunks=3, budget_frac=frac, iters=3, seed=8,
-                       p0_seed=2, stream=False, pipe=True), world=2)
+def test_shard_many_workers_unstaged():
+    """N = 16 workers (more rows than a ring slot holds): the exchange reads
+    every row straight from (peer) global memory."""
+    rng = np.random.default_rng(77)
+    counts = [int(c) for c in rng.integers(1, 3000, 19)]
+    w = [float(x) for x in 0.1 + rng.random(16)]
+    run_world(dict(counts=counts, N=16, weights=w, chunks=3, budget_frac=0.5, iters=3, seed=9,
+                   p0_seed=1), world=2, oversubscribe=True)
 
 
 # ---- runs on any box: ranks share the GPUs that exist (time-sliced contexts,
@@ -187,6 +176,7 @@ def test_shard_oversubscribed_ragged(world, N, frac):
     cfg = dict(counts=_ragged(7 + N, 23, 5000), N=N, weights=w, chunks=3, budget_frac=frac,
                iters=3, seed=5, p0_seed=4)
     run_world(cfg, world=world, oversubscribe=True)
+    run_world(dict(cfg, per_chunk=True, defer=True), world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True), world=world, oversubscribe=True)
 
 
@@ -199,4 +189,5 @@ def test_shard_eight_ranks_oversubscribed():
     rng = np.random.default_rng(8)
     w = [float(x) for x in 0.1 + rng.random(8)]
     run_world(dict(counts=_ragged(9, 17, 3000), N=8, weights=w, chunks=4, budget_frac=0.6,
-                   iters=2, seed=3, p0_seed=6), world=8, oversubscribe=True)
+                   iters=2, seed=3, p0_seed=6, defer=True, per_chunk=True), world=8,
+              oversubscribe=True)

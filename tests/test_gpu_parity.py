@@ -893,3 +893,34 @@ def test_small_step_in_cuda_graph(osp):
         assert np.array_equal(bits(a.global_params), bits(b.global_params)), f"replay {r}"
         assert np.array_equal(bits(a.worker_params), bits(b.worker_params)), f"replay {r}"
         assert a.gib_wire() == b.gib_wire()
+
+
+@pytest.mark.parametrize("case", ["random", "ties", "edges"])
+def test_pgp_rank_gib_certified_vs_oracle(osp, case):
+    """osp_pgp_rank_gib (the façade's resolution step): certified tree sums +
+    exact fallback reproduce the reference's deferred set and rank order
+    (importance.cpp:11-59) on arbitrary vectors, incl. exact ties."""
+    rng = np.random.default_rng({"random": 1, "ties": 2, "edges": 3}[case])
+    counts = [int(c) for c in rng.integers(1, 30000, 41)]
+    if case == "ties":
+        counts[5] = counts[9] = counts[20] = 4096
+    M = sum(counts)
+    p = rng.uniform(-1, 1, M).astype(np.float32)
+    g = rng.uniform(-1e-3, 1e-3, M).astype(np.float32)
+    offs = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    if case == "ties":
+        for l in (9, 20):
+            p[offs[l]:offs[l + 1]] = p[offs[5]:offs[6]]
+            g[offs[l]:offs[l + 1]] = g[offs[5]:offs[6]]
+    part = osp.Partition(counts)
+    ref_scores = oracle.pgp(counts, p, g)
+    budgets = [int(0.5 * M * 4)] if case != "edges" else [0, 1, M * 4, M * 4 - 1, int(0.37 * M * 4)]
+    for budget in budgets:
+        scores, order, flags = osp.pgp_rank_gib(part, cuda(p), cuda(g), budget)
+        want_flags = oracle.build_gib(ref_scores, counts, 4, budget)
+        want_order = oracle.rank(ref_scores)[: int(want_flags.sum())]
+        assert np.array_equal(flags, want_flags), f"flags at budget {budget}"
+        assert np.array_equal(order, want_order), f"order at budget {budget}"
+        np.testing.assert_allclose(scores, ref_scores, rtol=SCORE_RTOL, atol=0)
+        if case == "ties":
+            assert scores[5] == scores[9] == scores[20] == ref_scores[5]
