@@ -6,15 +6,19 @@
 // here every phase of the iteration runs in one 1024-thread CTA and the
 // resolve is done by a single warp with shuffles (one layer per lane):
 //
-//   stage 1   (OspServer::try_close_barrier + finish_layer, protocol.cpp:292-307,
-//             361-382; OspWorker::apply_pull -> lgp_partial, protocol.cpp:69-97):
-//             per element agg = float(sum_w w_k*(double)x_k / W) in the fixed worker
-//             order; RS layers: G' = G + agg, every worker row = G'; ICS layers:
-//             worker rows = G + x_w (local estimate), the carry C = G + agg.
-//   stage 2   (on_push_ics_chunk / lgp_correct, protocol.cpp:99-116, 326-353):
-//             ICS layers: G = C, every worker row = C (base + agg, base == G_old).
+//   stage 1+2 (OspServer::try_close_barrier + finish_layer, protocol.cpp:292-307,
+//             361-382, on_push_ics_chunk, :326-353; OspWorker::apply_pull ->
+//             lgp_partial and lgp_correct, protocol.cpp:69-116): per element
+//             agg = float(sum_w w_k*(double)x_k / W) in the fixed worker order,
+//             G' = G + agg, and every worker row ends at G' — on a barrier layer
+//             directly, on a deferred layer as base + agg with base == G. Inside
+//             one launch the stage-1 local estimate of a deferred element is
+//             overwritten by its stage-2 correction before anything can read it
+//             (the same thread writes both), so this kernel writes each row once
+//             with its final value; the per-stage API (osp_group_stage1 /
+//             stage2_*) materialises the intermediate state.
 //   resolve   (check_resolution, protocol.cpp:384-439): PGP per layer
-//             (importance.cpp:11-28) as tile partials summed in a fixed order,
+//             (importance.cpp:11-28) as tile partials summed in a fixed tree,
 //             certified against the reference's sequential sum (resolve.cu's
 //             interval rule; touching intervals are recomputed sequentially),
 //             rank (importance.cpp:30-40), prefix rule (importance.cpp:42-59),
@@ -22,6 +26,8 @@
 //             list / counter / GIB byte the regular kernels keep, so the group
 //             can continue on either path.
 //
+// Latency is the cost here, not bytes: one barrier after the table load, one
+// after the elementwise pass; each warp keeps kBatch tiles' loads in flight.
 // Results are bit-identical to stage1 + stage2_resolve (tests/test_gpu_parity.py).
 
 #include "common.cuh"
@@ -41,24 +47,10 @@ struct SmallSmem {
     int ptb[kSmallMaxLayers + 1];      // PGP tiles of this kernel per layer (prefix)
     int flag[kSmallMaxLayers];         // current GIB
     double part[kSmallMaxTiles];       // PGP tile partials
+    double exact[kSmallMaxLayers];     // exact sequential sums of marked layers
+    uint64_t budget, resolved;
     int n_marked;
 };
-
-__device__ __forceinline__ int layer_of_ptile(const SmallSmem& s, int L, int t) {
-    int l = 0;
-    while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
-    return l;
-}
-
-// rank of lane l's (key, id) among lanes 0..L-1 (stable: ties by id)
-__device__ __forceinline__ int warp_rank(double key, int lane, int L) {
-    int r = 0;
-    for (int j = 0; j < L; ++j) {
-        const double kj = __shfl_sync(0xffffffffu, key, j);
-        r += (kj < key) || (kj == key && j < lane);
-    }
-    return r;
-}
 
 template <typename T>
 __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
@@ -70,96 +62,150 @@ __device__ __forceinline__ T warp_incl_scan(T v, int lane) {
     return v;
 }
 
+// rank of lane l's (key, id) among lanes 0..L-1 (stable: ties by id); every
+// lane of the warp must call it
+__device__ __forceinline__ int warp_rank(double key, int lane, int L) {
+    int r = 0;
+    for (int j = 0; j < L; ++j) {
+        const double kj = __shfl_sync(0xffffffffu, key, j);
+        r += (kj < key) || (kj == key && j < lane);
+    }
+    return r;
+}
+
+// One element: fixed-order aggregate, G' = G + agg, every worker row = G';
+// returns the PGP term. xs: the NS deltas (NS > 0) or read here (NS == 0).
+template <int NS>
+__device__ __forceinline__ double small_elem(const GroupView& g, const AggParams& ap,
+                                             const float* __restrict__ X, uint64_t ldX,
+                                             uint64_t f, float go, const float* xs) {
+    const int n = NS > 0 ? NS : ap.n;
+    double sum = 0.0;
+#pragma unroll
+    for (int w = 0; w < (NS > 0 ? NS : 1); ++w) {
+        if (NS > 0) {
+            float x = xs[w];
+            if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+            sum = agg_acc(sum, ap.w[w], x);
+        }
+    }
+    if (NS == 0) {
+        for (int w = 0; w < n; ++w) {
+            float x = X[static_cast<uint64_t>(w) * ldX + f];
+            if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+            sum = agg_acc(sum, ap.w[w], x);
+        }
+    }
+    const float a = agg_finish(ap, sum);
+    const float gn = __fadd_rn(go, a);
+    g.G[f] = gn;
+    for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+    return pgp_term(a, gn);
+}
+
+template <int NS>
 __global__ void __launch_bounds__(kSmallThreads, 1)
     k_step_small(GroupView g, AggParams ap, const float* __restrict__ X, uint64_t ldX) {
     __shared__ SmallSmem s;
     pdl_wait();
     pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int L = g.L, n = ap.n;
-    if (tid <= L) {
-        s.tb[tid] = g.tile_base[tid];
-        if (tid < L) {
-            s.off[tid] = g.offsets[tid];
-            s.cnt[tid] = g.counts[tid];
-            s.flag[tid] = g.flags[tid];
+    const int L = g.L;
+    if (warp == 0) {
+        // tables, this kernel's PGP tile prefix (warp scan), the scalars the
+        // resolve needs — all loads issued together
+        uint64_t off = 0, cnt = 0;
+        int fl = 0, tb = 0;
+        if (lane < L) {
+            off = g.offsets[lane];
+            cnt = g.counts[lane];
+            fl = g.flags[lane];
         }
-    }
-    if (tid == 0) s.n_marked = 0;
-    __syncthreads();
-    if (tid == 0) {
-        int t = 0;
-        for (int l = 0; l < L; ++l) {
-            s.ptb[l] = t;
-            t += static_cast<int>((s.cnt[l] + kSmallTile - 1) / kSmallTile);
+        if (lane <= L) tb = g.tile_base[lane];
+        const uint64_t budget = g.meta64[META64_BUDGET], resolved = g.meta64[META64_RESOLVED];
+        const int nt = lane < L ? static_cast<int>((cnt + kSmallTile - 1) / kSmallTile) : 0;
+        const int incl = warp_incl_scan<int>(nt, lane);
+        const uint64_t end = warp_incl_scan<unsigned long long>(cnt, lane);
+        if (lane < L) {
+            s.off[lane] = off;
+            s.cnt[lane] = cnt;
+            s.flag[lane] = fl;
+            s.ptb[lane] = incl - nt;
         }
-        s.ptb[L] = t;
-        s.off[L] = s.off[L - 1] + s.cnt[L - 1];
+        if (lane <= L) s.tb[lane] = tb;
+        if (lane == L - 1) {
+            s.ptb[L] = incl;
+            s.off[L] = end;
+        }
+        if (lane == 0) {
+            s.budget = budget;
+            s.resolved = resolved;
+            s.n_marked = 0;
+        }
     }
     __syncthreads();
     const int n_ptiles = s.ptb[L];
 
-    // ---- stage 1: one warp per PGP tile (one element per lane)
-    for (int t = warp; t < n_ptiles; t += kSmallWarps) {
-        const int l = layer_of_ptile(s, L, t);
-        const uint64_t b = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile;
-        const uint64_t e = min(b + kSmallTile, s.off[l] + s.cnt[l]);
-        const bool ics = s.flag[l] != 0;
-        double acc = 0.0;
+    // ---- stages 1 + 2: one warp per 32-element PGP tile, kBatch tiles in flight
+    constexpr int kBatch = 4;
+    constexpr int kRows = NS > 0 ? NS : 1;
+    for (int t0 = warp; t0 < n_ptiles; t0 += kSmallWarps * kBatch) {
+        float go[kBatch], xs[kBatch][kRows];
+        uint64_t fe[kBatch];
+        bool ok[kBatch];
 #pragma unroll
-        for (int j = 0; j < kSmallTile / 32; ++j) {
-            const uint64_t f = b + j * 32 + lane;
-            if (f < e) {
-                const float go = g.G[f];
-                double sum = 0.0;
-                for (int w = 0; w < n; ++w) {
-                    float x = X[static_cast<uint64_t>(w) * ldX + f];
-                    if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
-                    sum = agg_acc(sum, ap.w[w], x);
-                    if (ics) g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
-                }
-                const float a = agg_finish(ap, sum);
-                const float gn = __fadd_rn(go, a);
-                if (ics) {
-                    g.C[f] = gn;
-                } else {
-                    g.G[f] = gn;
-                    for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
-                }
-                acc = __dadd_rn(acc, pgp_term(a, gn));
+        for (int j = 0; j < kBatch; ++j) {
+            const int t = t0 + j * kSmallWarps;
+            ok[j] = false;
+            fe[j] = 0;
+            if (t < n_ptiles) {
+                int l = 0;
+                while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
+                const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
+                ok[j] = f < s.off[l] + s.cnt[l];
+                fe[j] = f;
+            }
+            if (ok[j]) {
+                go[j] = g.G[fe[j]];
+#pragma unroll
+                for (int w = 0; w < kRows; ++w)
+                    if (NS > 0) xs[j][w] = X[static_cast<uint64_t>(w) * ldX + fe[j]];
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
-        if (lane == 0) s.part[t] = acc;
-    }
-    __syncthreads();
-
-    // ---- stage 2: the carry broadcast on the deferred layers
-    for (int l = 0; l < L; ++l) {
-        if (!s.flag[l]) continue;
-        for (uint64_t f = s.off[l] + tid; f < s.off[l] + s.cnt[l]; f += kSmallThreads) {
-            const float gn = g.C[f];
-            g.G[f] = gn;
-            for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+        for (int j = 0; j < kBatch; ++j) {
+            const int t = t0 + j * kSmallWarps;
+            if (t >= n_ptiles) break;  // warp-uniform
+            double acc = ok[j] ? small_elem<NS>(g, ap, X, ldX, fe[j], go[j], xs[j]) : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+            if (lane == 0) s.part[t] = acc;
         }
     }
-    __syncthreads();  // G final (the exact fallback reads it)
+    __syncthreads();  // G final, every tile partial in shared memory
 
-    // ---- resolve: scores + certificate (warp 0, lane = layer)
-    double key = __longlong_as_double(0x7ff0000000000000ll), rad = 0.0;
+    // ---- resolve (warp 0; lane = layer for the per-layer values)
+    double key = __longlong_as_double(0x7ff0000000000000ll);
     bool marked = false;
     if (warp == 0) {
+        // per-layer sums of the tile partials: lane-strided in order, then the
+        // fixed shuffle tree (depth <= ceil(nt / 32) + 5)
+        double rad = 0.0;
+        for (int l = 0; l < L; ++l) {
+            double acc = 0.0;
+            for (int t = s.ptb[l] + lane; t < s.ptb[l + 1]; t += 32) acc = __dadd_rn(acc, s.part[t]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+            acc = __shfl_sync(0xffffffffu, acc, 0);
+            if (lane == l) key = acc;
+        }
         if (lane < L) {
-            double sc = 0.0;
-            for (int t = s.ptb[lane]; t < s.ptb[lane + 1]; ++t) sc = __dadd_rn(sc, s.part[t]);
             const double nt = static_cast<double>(s.ptb[lane + 1] - s.ptb[lane]);
-            // depth: 5 shuffle levels + the in-order tile sum (+ slack)
-            const double D = 5.0 + nt + 2.0;
-            key = sc;
-            rad = sc * (kU * (1.01 * (static_cast<double>(s.cnt[lane]) - 1.0 + D) + 8.0));
-            g.scores[lane] = sc;
-            g.lscore[lane] = sc;
+            // depth: 5 (tile tree) + ceil(nt / 32) + 5 (layer tree) + slack
+            const double D = 5.0 + floor((nt + 31.0) / 32.0) + 5.0 + 2.0;
+            rad = key * (kU * (1.01 * (static_cast<double>(s.cnt[lane]) - 1.0 + D) + 8.0));
+            g.scores[lane] = key;
+            g.lscore[lane] = key;
         }
         for (int j = 0; j < L; ++j) {
             const double kj = __shfl_sync(0xffffffffu, key, j);
@@ -171,18 +217,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         const unsigned mm = __ballot_sync(0xffffffffu, marked);
         if (lane == 0) s.n_marked = __popc(mm);
     }
+    // warp 0 decides whether the exact fallback (every warp) runs
     __syncthreads();
-    if (s.n_marked > 0) {
+    const int n_marked = s.n_marked;
+    if (n_marked > 0) {
         // exact sequential PGP of the marked layers (importance.cpp:20-25 order),
-        // one warp each, with agg recomputed as stage 1 computed it
-        const unsigned mm = [&] {
-            unsigned m = 0;
-            for (int l = 0; l < L; ++l) m |= g.marked[l] ? (1u << l) : 0u;
-            return m;
-        }();
+        // one warp each, against the final G, with agg recomputed as above
         int slot = 0;
         for (int l = 0; l < L; ++l) {
-            if (!((mm >> l) & 1u)) continue;
+            if (!g.marked[l]) continue;
             if (slot++ % kSmallWarps != warp) continue;
             const uint64_t b0 = s.off[l], e0 = b0 + s.cnt[l];
             double sum = 0.0;
@@ -191,7 +234,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
                 double t = 0.0;
                 if (f < e0) {
                     double a = 0.0;
-                    for (int w = 0; w < n; ++w) {
+                    for (int w = 0; w < ap.n; ++w) {
                         float x = X[static_cast<uint64_t>(w) * ldX + f];
                         if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
                         a = agg_acc(a, ap.w[w], x);
@@ -203,23 +246,22 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             }
             if (lane == 0) {
                 g.exact[l] = sum;
-                s.part[l] = sum;  // tile partials are consumed: reuse as exact keys
+                s.exact[l] = sum;
             }
         }
         __syncthreads();
-        if (warp == 0 && marked) key = s.part[lane];
+        if (warp == 0 && marked) key = s.exact[lane];
         if (tid == 0) {
-            g.meta64[META64_FB_LAYERS] += static_cast<uint64_t>(s.n_marked);
+            g.meta64[META64_FB_LAYERS] += static_cast<uint64_t>(n_marked);
             g.meta64[META64_FB_RESOLVES] += 1;
         }
     }
     if (warp != 0) return;
 
     // rank, prefix rule, chunk map, lists (lane = rank position r or layer id)
-    const int rk = warp_rank(key, lane, L);  // every lane takes part in the shuffles
+    const int rk = warp_rank(key, lane, L);
     const int my_rank = lane < L ? rk : 32;
-    // sorted[r]: the lane whose rank is r
-    int sorted = 0;
+    int sorted = 0;  // sorted[r]: the lane whose rank is r
     for (int j = 0; j < L; ++j) {
         const int rj = __shfl_sync(0xffffffffu, my_rank, j);
         if (rj == lane) sorted = j;
@@ -227,31 +269,32 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     const uint64_t bpe = g.bpe;
     const uint64_t bytes_r = lane < L ? s.cnt[sorted] * bpe : 0ull;
     const uint64_t pre = warp_incl_scan<unsigned long long>(bytes_r, lane);
-    const uint64_t budget = g.meta64[META64_BUDGET];
+    const uint64_t budget = s.budget;
     const unsigned fit = __ballot_sync(0xffffffffu, lane < L && pre <= budget);
     const int k = __popc(fit);  // pre is nondecreasing: the fitting ranks are a prefix
-    const uint64_t total = k > 0 ? __shfl_sync(0xffffffffu, pre, k - 1) : 0ull;
+    const uint64_t total = __shfl_sync(0xffffffffu, pre, k > 0 ? k - 1 : 0);
+    const uint64_t tot = k > 0 ? total : 0ull;
     const uint64_t nc = static_cast<uint64_t>(g.n_chunks);
     const bool in_ics = lane < k;
     uint64_t idx = 0;
     if (in_ics) {
         const uint64_t cum = pre - bytes_r;
-        idx = total == 0 ? 0 : (cum * nc) / total;
+        idx = tot == 0 ? 0 : (cum * nc) / tot;
         if (idx > nc - 1) idx = nc - 1;
     }
     const uint64_t prev_idx = __shfl_up_sync(0xffffffffu, idx, 1);
     const int is_new = in_ics && (lane == 0 || idx != prev_idx) ? 1 : 0;
     const int chunk_no = warp_incl_scan<int>(is_new, lane);  // 1-based in the compacted map
-    const int n_used = k > 0 ? __shfl_sync(0xffffffffu, chunk_no, k - 1) : 0;
+    const int n_used_all = __shfl_sync(0xffffffffu, chunk_no, k > 0 ? k - 1 : 0);
+    const int n_used = k > 0 ? n_used_all : 0;
     const int ics_tiles = in_ics ? s.tb[sorted + 1] - s.tb[sorted] : 0;
     const int ics_tp = warp_incl_scan<int>(ics_tiles, lane);
-    // per layer (lane = id): deferred?  rank < k
     const int deferred = lane < L && my_rank < k ? 1 : 0;
     const int rs = lane < L && !deferred ? 1 : 0;
     const int rs_pos = warp_incl_scan<int>(rs, lane);
     const int rs_tiles = rs ? s.tb[lane + 1] - s.tb[lane] : 0;
     const int rs_tp = warp_incl_scan<int>(rs_tiles, lane);
-    const uint32_t tag = static_cast<uint32_t>(g.meta64[META64_RESOLVED] + 1);
+    const uint32_t tag = static_cast<uint32_t>(s.resolved + 1);
     if (in_ics) {
         g.chunk_of[sorted] = chunk_no - 1;
         g.ics_layers[lane] = sorted;
@@ -287,9 +330,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         g.meta[META_N_ICS] = k;
         g.meta[META_N_USED] = n_used;
         g.meta[META_N_RS] = L - k;
-        g.meta64[META64_DEFERRED] = total;
+        g.meta64[META64_DEFERRED] = tot;
         g.meta64[META64_TAG] = tag;
-        if (g.hist) g.hist[tag % kHist] = total;
+        if (g.hist) g.hist[tag % kHist] = tot;
         g.meta64[META64_RESOLVED] = tag;
     }
     __syncwarp();
@@ -309,7 +352,18 @@ bool small_step_supported(int n_workers, int L, uint64_t M) {
 
 cudaError_t launch_step_small(const GroupView& g, const AggParams& ap, const float* X,
                               uint64_t ldX, cudaStream_t s) {
-    return launch_pdl(k_step_small, dim3(1), dim3(kSmallThreads), 0, s, g, ap, X, ldX);
+    const dim3 grid(1), block(kSmallThreads);
+    switch (ap.n) {
+        case 1: return launch_pdl(k_step_small<1>, grid, block, 0, s, g, ap, X, ldX);
+        case 2: return launch_pdl(k_step_small<2>, grid, block, 0, s, g, ap, X, ldX);
+        case 3: return launch_pdl(k_step_small<3>, grid, block, 0, s, g, ap, X, ldX);
+        case 4: return launch_pdl(k_step_small<4>, grid, block, 0, s, g, ap, X, ldX);
+        case 5: return launch_pdl(k_step_small<5>, grid, block, 0, s, g, ap, X, ldX);
+        case 6: return launch_pdl(k_step_small<6>, grid, block, 0, s, g, ap, X, ldX);
+        case 7: return launch_pdl(k_step_small<7>, grid, block, 0, s, g, ap, X, ldX);
+        case 8: return launch_pdl(k_step_small<8>, grid, block, 0, s, g, ap, X, ldX);
+        default: return launch_pdl(k_step_small<0>, grid, block, 0, s, g, ap, X, ldX);
+    }
 }
 
 }  // namespace osp
