@@ -435,6 +435,14 @@ osp_status osp_shard_profile(osp_shard* s, int buf, float* ms, void* stream);
 osp_status osp_shard_solo_agg(osp_shard* s, int stage, int buf, void* stream);
 /* ProtocolError if a cross-GPU wait timed out (synchronises `stream`). */
 osp_status osp_shard_check(osp_shard* s, void* stream);
+/* Diagnostics (OSP_SHARD_DEBUG=1 in the environment at create): the exchange
+ * kernel's counters summed over CTAs since the last read, then reset —
+ * [0] producer cycles blocked on a peer's tile flag, [1] producer cycles
+ * waiting for a free ring slot, [2] consumer (warp 0) cycles waiting for data,
+ * [3] publisher cycles in the system-scope fence + flag stores, [4] producer
+ * cycles in total, [5] blocking B waits, [6..8] A / B / L items, [9] flag
+ * batches. Returns 1 when filled, 0 when disabled. */
+int osp_shard_debug_counters(osp_shard* s, unsigned long long* out16);
 /* Synthetic deltas of workers [worker0, worker0+n_workers) into [n_workers][ld]. */
 osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
                                   uint64_t n, float* out, uint64_t ld, void* stream);

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <vector>
 
@@ -40,6 +41,17 @@ struct osp_group {
     int* d_order_tmp = nullptr;
     float* d_staging = nullptr;
 };
+
+// NVTX range over a C-ABI call (header-only NVTX3: a no-op unless a tool such as
+// nsys or ncu --nvtx is attached), so a host profile shows the sync path's
+// phases by their reference names.
+struct OspRange {
+    explicit OspRange(const char* name) { nvtxRangePushA(name); }
+    ~OspRange() { nvtxRangePop(); }
+    OspRange(const OspRange&) = delete;
+    OspRange& operator=(const OspRange&) = delete;
+};
+#define OSP_RANGE(name) OspRange osp_range_guard_(name)
 
 #define OSP_TRY(expr)                \
     do {                             \

@@ -918,6 +918,7 @@ osp_status osp_group_set_gib(osp_group* g, const uint8_t* flags, const int32_t* 
 }
 
 osp_status osp_group_stage1(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_RANGE("osp_group_stage1 (barrier: RS + LGP partial)");
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
     if (g->tma) OSP_CUDA(launch_stage1_tma(g->v, g->ap, deltas, ld, as_stream(stream)));
@@ -934,6 +935,7 @@ static osp_status need_stage1(const osp_group* g) {
 
 osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, uint64_t ld,
                                   void* stream) {
+    OSP_RANGE("osp_group_stage2_chunk (ICS)");
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (chunk < 0 || chunk >= g->n_chunks) return fail(OSP_ERR_INVALID, "chunk out of range");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
@@ -945,6 +947,7 @@ osp_status osp_group_stage2_chunk(osp_group* g, int chunk, const float* deltas, 
 }
 
 osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_RANGE("osp_group_stage2_all (ICS)");
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
     OSP_TRY(need_stage1(g));
@@ -955,6 +958,7 @@ osp_status osp_group_stage2_all(osp_group* g, const float* deltas, uint64_t ld, 
 }
 
 osp_status osp_group_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_RANGE("osp_group_resolve (PGP -> GIB)");
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (g->v.V) deltas = g->v.V, ld = g->v.ldP;  // the exact fallback re-aggregates v'
     OSP_CUDA(launch_resolve(g->v, g->ap, deltas, ld, as_stream(stream)));
@@ -997,6 +1001,7 @@ osp_status osp_group_stages(osp_group* g, const float* deltas, uint64_t ld, void
 }
 
 osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_RANGE("osp_group_stage2_resolve");
     if (!g || !deltas) return fail(OSP_ERR_INVALID, "null argument");
     if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
     OSP_TRY(need_stage1(g));
@@ -1015,6 +1020,7 @@ osp_status osp_group_stage2_resolve(osp_group* g, const float* deltas, uint64_t 
 }
 
 osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* stream) {
+    OSP_RANGE("osp_group_step");
     if (g && deltas && g->small && !g->v.V && !g->s1_open) {
         if (ld < g->part->total) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
         OSP_CUDA(launch_step_small(g->v, g->ap, deltas, ld, as_stream(stream)));
@@ -1026,6 +1032,7 @@ osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* 
 
 osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,
                                uint8_t* gib_out, float* params_out, void* stream) {
+    OSP_RANGE("osp_group_step_host");
     if (!g || !host_deltas) return fail(OSP_ERR_INVALID, "null argument");
     const uint64_t M = g->part->total;
     if (host_ld < M) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");

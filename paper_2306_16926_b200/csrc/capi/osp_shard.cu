@@ -52,7 +52,9 @@ struct osp_shard {
     bool connected = false;
     unsigned iter = 0;         // iterations started (stage-1 launches) = tile-flag epoch
     bool s1_open = false;      // stage 1 issued, iteration not yet resolved
-    int lag = 2;
+    int lag = 2;               // OSP_SHARD_LAG: B items' due-time lag (A items)
+    int stages = 2;            // OSP_SHARD_STAGES: exchange ring depth (2 or 3)
+    unsigned long long* dbg = nullptr;  // OSP_SHARD_DEBUG=1: kernel counters [16]
 };
 
 extern "C" {
@@ -89,6 +91,7 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     s->n_chunks = cfg->n_chunks;
     s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
     if (const char* lg = std::getenv("OSP_SHARD_LAG")) s->lag = std::max(0, std::atoi(lg));
+    if (const char* ks = std::getenv("OSP_SHARD_STAGES")) s->stages = std::atoi(ks) == 3 ? 3 : 2;
     // the local group: default (TMA-staged, carry) so the stage-2 broadcast and
     // the overlapped resolve are the single-GPU kernels; no single-launch step
     osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks, T, cfg->sgd_lr,
@@ -113,6 +116,10 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->ready, 0, kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
+    if (const char* d = std::getenv("OSP_SHARD_DEBUG"); d && d[0] == '1') {
+        if (e == cudaSuccess) e = cudaMalloc(&s->dbg, 16 * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(s->dbg, 0, 16 * sizeof(unsigned long long));
+    }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         osp_shard_destroy(s);
@@ -132,6 +139,7 @@ void osp_shard_destroy(osp_shard* s) {
     if (s->tflag) cudaFree(s->tflag);
     if (s->ready) cudaFree(s->ready);
     if (s->error) cudaFree(s->error);
+    if (s->dbg) cudaFree(s->dbg);
     if (s->grp) osp_group_destroy(s->grp);
     delete s;
 }
@@ -202,6 +210,8 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.n_loc = s->n_loc;
     base.slot_rows = x_slot_rows(s->N);
     base.lag = s->lag;
+    base.stages = s->stages;
+    base.dbg = s->dbg;
     for (int b = 0; b < 2; ++b) {
         XArgs& xa = s->xa[b];
         xa = base;
@@ -264,6 +274,7 @@ static cudaError_t stage2_kernels(osp_shard* s, int buf, int c0, int c1, cudaStr
 }
 
 osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
+    OSP_RANGE("osp_shard_stage1");
     OSP_TRY(check_ready(s, buf));
     OSP_CUDA(stage1_kernels(s, buf, as_stream(stream)));
     s->s1_open = true;
@@ -271,6 +282,7 @@ osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream) {
 }
 
 osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream) {
+    OSP_RANGE("osp_shard_stage2");
     OSP_TRY(check_ready(s, buf));
     if (c0 < 0 || c1 > s->n_chunks || c0 > c1) return fail(OSP_ERR_INVALID, "chunk range");
     if (!s->s1_open) return fail(OSP_ERR_PROTOCOL, "stage 2 before stage 1 of this iteration");
@@ -279,6 +291,7 @@ osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream)
 }
 
 osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
+    OSP_RANGE("osp_shard_resolve");
     OSP_TRY(check_ready(s, buf));
     osp_group* g = s->grp;
     OSP_CUDA(launch_resolve(g->v, g->ap, s->X + buf * s->buf_stride, s->ldX, as_stream(stream)));
@@ -290,6 +303,7 @@ osp_status osp_shard_resolve(osp_shard* s, int buf, void* stream) {
 // broadcast beside it (joined on the device, as osp_group_stage2_resolve), or
 // (deferred ICS) the stage-2 exchange of every chunk and the resolve.
 osp_status osp_shard_step(osp_shard* s, int buf, void* stream) {
+    OSP_RANGE("osp_shard_step");
     OSP_TRY(check_ready(s, buf));
     cudaStream_t st = as_stream(stream);
     osp_group* g = s->grp;
@@ -354,6 +368,15 @@ osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uin
     OSP_CUDA(launch_synth(seed, n_workers, iteration, 0, n, out, ld,
                           static_cast<uint64_t>(worker0), as_stream(stream)));
     return OSP_OK;
+}
+
+int osp_shard_debug_counters(osp_shard* s, unsigned long long* out16) {
+    if (!s || !s->dbg || !out16) return 0;
+    if (cudaMemcpy(out16, s->dbg, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) !=
+        cudaSuccess)
+        return 0;
+    cudaMemset(s->dbg, 0, 16 * sizeof(unsigned long long));
+    return 1;
 }
 
 osp_status osp_shard_check(osp_shard* s, void* stream) {

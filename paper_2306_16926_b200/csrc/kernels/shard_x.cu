@@ -95,7 +95,10 @@ __device__ __forceinline__ float4 add4x(float4 a, float4 b) {
 
 // Per-CTA item order: A items at due time i, the peers' B items
 // (j + 1) * nA / nB + lag - 1 (behind the A item the peer's CTA is on), L items
-// spread evenly; ties go to A. Deterministic and identical on every lane.
+// spread evenly; ties go to A. A B item whose flag has not landed yet is passed
+// over while A / L items remain (the producer never blocks the ring on a peer
+// while it has local work to issue). Identical on every lane: the readiness
+// probe is lane 0's, broadcast.
 struct XSched {
     int nA, nL, nB[kMaxRanks];
     int ia, il, ib[kMaxRanks];
@@ -110,41 +113,62 @@ struct XSched {
         if (ib[q] >= nB[q]) return 1e30;
         return nA > 0 ? (static_cast<double>(ib[q]) + 1.0) * nA / nB[q] + lag - 1 : 0.0;
     }
-    // next (kind, peer, index); kind -1 = done
-    __device__ void next(int& kind, int& q, int& k) {
-        double best = dueA();
-        kind = ia < nA ? XI_A : -1;
-        q = R;
-        k = ia;
-        const double dl = dueL();
-        if (dl < best) {
-            best = dl;
-            kind = XI_L;
-            k = il;
-        }
+    // the earliest-due B item: (peer, index) or q = -1
+    __device__ void headB(int& q, int& k, double& due) const {
+        q = -1;
+        due = 1e30;
         for (int p = 0; p < P; ++p) {
             if (p == R) continue;
-            const double db = dueB(p);
-            if (db < best) {
-                best = db;
-                kind = XI_B;
+            const double d = dueB(p);
+            if (d < due) {
+                due = d;
                 q = p;
-                k = ib[p];
             }
         }
-        if (kind == XI_A) ++ia;
-        else if (kind == XI_L) ++il;
-        else if (kind == XI_B) ++ib[q];
+        k = q >= 0 ? ib[q] : 0;
+    }
+    // next (kind, peer, index) given whether the head B item is ready; kind -1 = done
+    __device__ void next(bool b_ready, int& kind, int& q, int& k) {
+        int bq, bk;
+        double bd;
+        headB(bq, bk, bd);
+        const double da = dueA(), dl = dueL();
+        const bool local_left = ia < nA || il < nL;
+        kind = -1;
+        if (bq >= 0 && (b_ready || !local_left) && bd < da && bd < dl) {
+            kind = XI_B;
+            q = bq;
+            k = bk;
+            ++ib[bq];
+            return;
+        }
+        if (ia < nA && da <= dl) {
+            kind = XI_A;
+            q = R;
+            k = ia++;
+            return;
+        }
+        if (il < nL) {
+            kind = XI_L;
+            q = R;
+            k = il++;
+            return;
+        }
+        if (bq >= 0) {
+            kind = XI_B;
+            q = bq;
+            k = bk;
+            ++ib[bq];
+        }
     }
 };
 
 // Slot layout: A: rows 0..N-1 = every worker's deltas, row N = G.
 //              B: row 0 = agg, row 1 = G, rows 2.. = local deltas (ICS, SINGLE).
 //              L: rows 0..NL-1 = local deltas, row NL = G.
-template <int NS, int CW>
+template <int NS, int CW, int KS>
 __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParams ap, XArgs xa) {
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int KS = 2;  // ring stages
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int T = g.T;
@@ -253,29 +277,54 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
 
     if (warp == CW + 1) {
         // ================= publisher =================
+        // A tiles' partials go out as they complete; their flags are published
+        // in batches of up to kPubBatch under one system-scope fence (cumulative
+        // over the consumers' pull stores, acquired through the done barrier,
+        // and the partials), or at once when no further item is done yet
+        constexpr int kPubBatch = 4;
+        int pend[kPubBatch];
+        int np = 0;
+        long long t_fence = 0, n_flush = 0;
+        auto flush = [&]() {
+            if (np == 0) return;
+            if (lane == 0 && !xa.solo) {
+                const long long f0 = clock64();
+                __threadfence_system();
+                for (int j = 0; j < np; ++j)
+                    for (int r = 0; r < P; ++r)
+                        if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + pend[j]) = xa.epoch;
+                t_fence += clock64() - f0;
+                ++n_flush;
+            }
+            np = 0;
+            __syncwarp();
+        };
         for (int i = 0;; ++i) {
             const int s = i % KS;
-            mbar_wait(&done[s], (i / KS) & 1);
+            const unsigned par = (i / KS) & 1;
+            if (!mbar_try(&done[s], par)) {
+                flush();
+                mbar_wait(&done[s], par);
+            }
             const XMeta m = meta[s];
             double tot = 0.0;
             if (m.t >= 0 && m.kind == XI_A)
                 for (int w = 0; w < CW; ++w) tot = __dadd_rn(tot, red[s * CW + w]);
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
-            if (m.t < 0) break;
-            if (m.kind != XI_A) continue;
-            // partial everywhere, then (system-scope fence, cumulative over the
-            // consumers' pull stores acquired through the done barrier and these
-            // partials) the tile flag on every peer; one lane does all of it
-            if (lane == 0) {
-                for (int r = 0; r < P; ++r) xa.part[r][m.t] = tot;
-                if (!xa.solo) {
-                    __threadfence_system();
-                    for (int r = 0; r < P; ++r)
-                        if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + m.t) = xa.epoch;
-                }
+            if (m.t < 0) {
+                flush();
+                break;
             }
-            __syncwarp();
+            if (m.kind != XI_A) continue;
+            if (lane == 0)
+                for (int r = 0; r < P; ++r) xa.part[r][m.t] = tot;
+            pend[np++] = m.t;
+            if (np == kPubBatch) flush();
+        }
+        if (xa.dbg && lane == 0) {
+            atomicAdd(xa.dbg + 3, static_cast<unsigned long long>(t_fence));
+            atomicAdd(xa.dbg + 9, static_cast<unsigned long long>(n_flush));
         }
         return;
     }
@@ -300,12 +349,30 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
                 if (q != R) st_release_sys(xa.ready[q] + R, xa.epoch);
         }
         bool peers_ready = xa.mode == XM_ICS || xa.solo;
+        long long t_bspin = 0, t_empty = 0, n_block = 0, n_it[3] = {0, 0, 0};
+        const long long t_start = clock64();
         for (int i = 0;; ++i) {
             const int s = i % KS;
             const int use = i / KS;
-            if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+            if (use > 0) {
+                const long long e0 = clock64();
+                mbar_wait(&empty[s], (use - 1) & 1);
+                t_empty += clock64() - e0;
+            }
+            // probe the head B item's flag (lane 0), then choose
+            int bq, bk;
+            double bd;
+            sc.headB(bq, bk, bd);
+            int ready = 0;
+            if (bq >= 0) {
+                XMeta mb{};
+                locate(XI_B, slice_lo(bq, c) + bk, mb);
+                if (lane == 0)
+                    ready = static_cast<int>(ld_relaxed_sys(xa.tflag[R] + mb.t) - xa.epoch) >= 0 ? 1 : 0;
+                ready = __shfl_sync(0xffffffffu, ready, 0);
+            }
             int kind, q, k;
-            sc.next(kind, q, k);  // every lane, same result
+            sc.next(ready != 0, kind, q, k);  // every lane, same result
             XMeta m{};
             if (kind < 0) {
                 if (lane == 0) {
@@ -315,6 +382,7 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
                 }
                 break;
             }
+            ++n_it[kind];
             const int u = kind == XI_A ? slice_lo(R, c) + k
                         : kind == XI_B ? slice_lo(q, c) + k
                                        : lcl_lo + k;
@@ -328,9 +396,14 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
                 peers_ready = true;
             }
             if (kind == XI_B) {
+                const long long b0 = clock64();
                 if (lane == 0) xspin(xa.tflag[R] + m.t, xa.epoch, xa.error);
                 __syncwarp();
                 fence_proxy_async();
+                if (!ready) {
+                    t_bspin += clock64() - b0;
+                    ++n_block;
+                }
             }
             const bool local_rows = kind == XI_L || (kind == XI_B && m.ics && xa.mode == XM_SINGLE);
             const int nrows = kind == XI_A ? N + 1 : kind == XI_L ? NL + 1 : (local_rows ? 2 + NL : 2);
@@ -353,14 +426,24 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
                 mbar_arrive(&full[s]);
             }
         }
+        if (xa.dbg && lane == 0) {
+            atomicAdd(xa.dbg + 0, static_cast<unsigned long long>(t_bspin));
+            atomicAdd(xa.dbg + 1, static_cast<unsigned long long>(t_empty));
+            atomicAdd(xa.dbg + 4, static_cast<unsigned long long>(clock64() - t_start));
+            atomicAdd(xa.dbg + 5, static_cast<unsigned long long>(n_block));
+            for (int j = 0; j < 3; ++j) atomicAdd(xa.dbg + 6 + j, static_cast<unsigned long long>(n_it[j]));
+        }
         return;
     }
 
     // ================= consumers =================
     const int ctid = tid;
+    long long t_full = 0;
     for (int i = 0;; ++i) {
         const int s = i % KS;
+        const long long f0 = clock64();
         mbar_wait(&full[s], (i / KS) & 1);
+        t_full += clock64() - f0;
         const XMeta m = meta[s];
         if (m.t < 0) {
             if (lane == 0) mbar_arrive(&done[s]);
@@ -482,23 +565,23 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             mbar_arrive(&done[s]);
         }
     }
+    if (xa.dbg && tid == 0) atomicAdd(xa.dbg + 2, static_cast<unsigned long long>(t_full));
 }
 
 constexpr int kXCW = 8;
 
-size_t x_smem_bytes(int slot_rows, int T, int L) {
-    const size_t ring = static_cast<size_t>(2) * slot_rows * T * sizeof(float);
-    const size_t ctl = 3 * 2 * sizeof(uint64_t) + 2 * sizeof(XMeta) + 2 * kXCW * sizeof(double);
+size_t x_smem_bytes(int slot_rows, int T, int L, int ks) {
+    const size_t ring = static_cast<size_t>(ks) * slot_rows * T * sizeof(float);
+    const size_t ctl = 3 * ks * sizeof(uint64_t) + ks * sizeof(XMeta) + ks * kXCW * sizeof(double);
     const size_t tab = static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + L * 4 +
                        (L + 1) * 4 + L * 4 + (L + 1) * 4 + 128;
     return ring + ctl + tab;
 }
 
-template <int NS>
-cudaError_t launch_x_ns(const GroupView& g, const AggParams& ap, const XArgs& xa_in, cudaStream_t s) {
-    auto kern = k_shard_x<NS, kXCW>;
-    XArgs xa = xa_in;
-    const size_t sm = x_smem_bytes(xa.slot_rows, g.T, g.L);
+template <int NS, int KS>
+cudaError_t launch_x_ks(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
+    auto kern = k_shard_x<NS, kXCW, KS>;
+    const size_t sm = x_smem_bytes(xa.slot_rows, g.T, g.L, KS);
     int per_sm = 0;
     cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), (kXCW + 2) * 32, sm, &per_sm);
     if (e != cudaSuccess) return e;
@@ -507,13 +590,20 @@ cudaError_t launch_x_ns(const GroupView& g, const AggParams& ap, const XArgs& xa
     return cudaGetLastError();
 }
 
+template <int NS>
+cudaError_t launch_x_ns(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
+    if (xa.stages == 3 && x_smem_bytes(xa.slot_rows, g.T, g.L, 3) <= 220 * 1024)
+        return launch_x_ks<NS, 3>(g, ap, xa, s);
+    return launch_x_ks<NS, 2>(g, ap, xa, s);
+}
+
 }  // namespace
 
 int x_slot_rows(int n_workers) { return n_workers <= kXMaxStagedWorkers ? n_workers + 1 : 2; }
 
 bool shard_x_supported(int n_workers, int T, int L) {
     if (T < 512 || T > 4096) return false;
-    return x_smem_bytes(x_slot_rows(n_workers), T, L) <= 220 * 1024;
+    return x_smem_bytes(x_slot_rows(n_workers), T, L, 2) <= 220 * 1024;
 }
 
 cudaError_t launch_shard_x(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {

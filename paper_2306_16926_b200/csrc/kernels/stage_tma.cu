@@ -106,17 +106,6 @@ __device__ void tab_seq(const TileTab& tab, int u, int& l, int& k) {
 
 // ---- consumer bodies ----------------------------------------------------------
 
-// Stage-1 momentum (g.V set): v' = mu*v + grad per element (separately rounded
-// fp32 mul and add), stored back; the step then uses v' as the gradient.
-__device__ __forceinline__ float4 momentum4(const GroupView& g, int w, uint64_t f, float4 x) {
-    float4* vp = reinterpret_cast<float4*>(g.V + static_cast<uint64_t>(w) * g.ldP + f);
-    const float4 v = *vp;
-    const float4 vn = make_float4(__fadd_rn(__fmul_rn(g.mu, v.x), x.x), __fadd_rn(__fmul_rn(g.mu, v.y), x.y),
-                                  __fadd_rn(__fmul_rn(g.mu, v.z), x.z), __fadd_rn(__fmul_rn(g.mu, v.w), x.w));
-    *vp = vn;
-    return vn;
-}
-
 // staged form: v read from shared memory, v' streamed out
 __device__ __forceinline__ float4 momentum4s(const GroupView& g, int w, uint64_t f, float4 v,
                                              float4 x) {

@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             cnt = g.counts[lane];
             fl = g.flags[lane];
         }
-        if (lane <= L) tb = g.tile_base[lane];
+        if (lane < L) tb = g.tile_base[lane];
+        const int tb_end = g.tile_base[L];  // lane L does not exist when L == 32
         const uint64_t budget = g.meta64[META64_BUDGET], resolved = g.meta64[META64_RESOLVED];
         const int nt = lane < L ? static_cast<int>((cnt + kSmallTile - 1) / kSmallTile) : 0;
         const int incl = warp_incl_scan<int>(nt, lane);
@@ -132,10 +133,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             s.flag[lane] = fl;
             s.ptb[lane] = incl - nt;
         }
-        if (lane <= L) s.tb[lane] = tb;
+        if (lane < L) s.tb[lane] = tb;
         if (lane == L - 1) {
             s.ptb[L] = incl;
             s.off[L] = end;
+            s.tb[L] = tb_end;
         }
         if (lane == 0) {
             s.budget = budget;

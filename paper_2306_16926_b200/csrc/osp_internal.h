@@ -157,6 +157,8 @@ struct XArgs {
     int vec;                             // every row and buffer 16-byte aligned
     int slot_rows;                       // shared-memory rows per ring slot
     int lag;                             // B items' due-time lag behind the A items
+    int stages;                          // ring stages (2 or 3)
+    unsigned long long* dbg;             // diagnostics counters [16] or null
 };
 int x_slot_rows(int n_workers);
 bool shard_x_supported(int n_workers, int T, int L);

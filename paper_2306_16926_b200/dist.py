@@ -117,6 +117,15 @@ class ShardGroup:
         _check(lib().osp_shard_profile(self._h, buf, out, _stream(stream)))
         return {n: float(v) for n, v in zip(["stage1", "stage2", "resolve"], out)}
 
+    def debug_counters(self):
+        """Exchange-kernel counters (OSP_SHARD_DEBUG=1 at create) or None."""
+        out = (c_u64 * 16)()
+        if not lib().osp_shard_debug_counters(self._h, out):
+            return None
+        names = ["b_block_cycles", "empty_wait_cycles", "full_wait_cycles", "fence_cycles",
+                 "producer_cycles", "b_blocks", "a_items", "b_items", "l_items", "flushes"]
+        return {n: int(v) for n, v in zip(names, out)}
+
     @property
     def deferred_ics(self) -> bool:
         """True: stage 2 exchanges the deferred layers; False: single exchange."""

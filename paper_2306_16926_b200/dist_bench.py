@@ -168,8 +168,13 @@ def run(args, metric: str, unit: str):
         # every element crosses the links once, in stage 1 or in stage 2)
         ipe = 5
         loop = BudgetLoop(ipe, N, model_bytes)
+        def agree(vals):  # rank 0's measurements decide (every rank builds the same GIB)
+            t = torch.tensor(vals, dtype=torch.float64, device=dev)
+            dist.broadcast(t, 0)
+            return [float(x) for x in t.tolist()]
+
         cl = overlap.run_closed_loop(lambda i: sd.stage1(i % 2), s2r, sd.set_budget, comp, loop,
-                                     lambda j: nvl_bytes, K=30, ipe=ipe)
+                                     lambda j: nvl_bytes, K=30, ipe=ipe, agree=agree)
         sd.check()
         ovl["closed_loop"] = cl
         sd.close()

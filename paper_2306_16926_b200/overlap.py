@@ -97,7 +97,7 @@ def run(stage1, stage2_resolve, compute, K: int, W: int):
 
 
 def run_closed_loop(stage1, stage2_resolve, set_budget, compute, loop, link_bytes, K: int,
-                    ipe: int):
+                    ipe: int, agree=None):
     """The overlapped schedule of run() with the SGU budget driven by the device
     measurements (budget.BudgetLoop, runner.cpp:364-376 + protocol.cpp:396-405):
     at every epoch end the host reads the epoch's compute-phase times and
@@ -106,8 +106,11 @@ def run_closed_loop(stage1, stage2_resolve, set_budget, compute, loop, link_byte
     budget (set_budget is stream-ordered before it). link_bytes(i): the bytes
     the synchronization of iteration i (stage 1 + stage 2) moves on its link;
     the link rate is those bytes over the stage-1 time plus the stage-2 +
-    resolve time under the overlap. Returns the per-iteration budgets and the
-    loop's U_max history."""
+    resolve time under the overlap. agree(list) -> list: makes an epoch's
+    measurements identical on every rank (the sharded path resolves the same
+    GIB on every rank, so every rank must use the same budget; the reference
+    has one server). Returns the per-iteration budgets and the loop's U_max
+    history."""
     from .budget import synthetic_loss
     main = torch.cuda.current_stream()
     side = torch.cuda.Stream()
@@ -135,13 +138,18 @@ def run_closed_loop(stage1, stage2_resolve, set_budget, compute, loop, link_byte
             # implies every earlier stage 2 has finished: stage 1 waited on it)
             ev_c[i].synchronize()
             e0 = i + 1 - ipe
+            meas = []
             for j in range(e0, i + 1):
                 t_c = ev_c0[j].elapsed_time(ev_c[j]) * 1e-3
                 # sync time of the epoch's earlier iterations (j < i)
                 ts = ((ev_s0[j].elapsed_time(ev_s1[j]) + ev_s1[j].elapsed_time(ev_r[j])) * 1e-3
                       if j < i else 0.0)
-                loop.record(j, t_c, link_bytes(j) if j < i else 0.0, ts,
-                            synthetic_loss(loop.epoch_of(j)))
+                meas += [t_c, link_bytes(j) if j < i else 0.0, ts]
+            if agree is not None:
+                meas = agree(meas)
+            for n, j in enumerate(range(e0, i + 1)):
+                t_c, nb, ts = meas[3 * n: 3 * n + 3]
+                loop.record(j, t_c, nb, ts, synthetic_loss(loop.epoch_of(j)))
             loop.on_resolution(i)
             budget = loop.budget_for_next(i)
         with torch.cuda.stream(side):
