@@ -43,8 +43,10 @@ def parse():
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--stage-kernels", default="auto", choices=["auto", "tma", "register"],
                     help="stage-kernel family (OSP_GROUP_TMA / OSP_GROUP_REGISTER)")
+    ap.add_argument("--graph-steps", type=int, default=16,
+                    help="steps per captured CUDA graph (even: the two delta sets alternate)")
     ap.add_argument("--graph", action="store_true",
-                    help="capture two steps (both delta sets) in a CUDA graph and time replays "
+                    help="capture --graph-steps steps in a CUDA graph and time replays "
                          "(launch-bound layouts such as the MLP of config #1)")
     ap.add_argument("--sgd-lr", type=float, default=0.0,
                     help="> 0: the inputs are gradients, sgd_delta fused into the stage kernels")
@@ -349,23 +351,26 @@ def b200_single(args):
     time.sleep(0.3)
     graph = None
     if args.graph:
-        # the step has no host sync and fixed arguments: two steps (delta sets 0
-        # and 1, tags continue on the device) captured once, replayed K/2 times
-        K += K % 2
+        # the step has no host sync and fixed arguments: G steps (delta sets 0
+        # and 1 alternating, tags continue on the device) captured once and
+        # replayed K/G times, so the host's graph-launch cost is amortised over
+        # G device steps
+        n_graph = max(2, args.graph_steps + args.graph_steps % 2)
+        K += (-K) % n_graph
         graph = torch.cuda.CUDAGraph()
         cs = torch.cuda.Stream()
         cs.wait_stream(stream)
         with torch.cuda.graph(graph, stream=cs, capture_error_mode="thread_local"):
-            step(0)
-            step(1)
+            for j in range(n_graph):
+                step(j)
         torch.cuda.synchronize()
-        graph.replay()  # warm replay (2 more untimed steps)
+        graph.replay()  # warm replay (n_graph more untimed steps)
         torch.cuda.synchronize()
         tag0 = grp.read_gib()["tag"]
     torch.cuda.synchronize()
     start.record(stream)
     if graph is not None:
-        for _ in range(K // 2):
+        for _ in range(K // n_graph):
             graph.replay()
     else:
         for k in range(K):
@@ -514,7 +519,7 @@ def b200_single(args):
                 "deltas": "2 device-resident sets (iterations 0 and 1) alternating",
                 "inputs": (f"gradients, sgd_delta lr {args.sgd_lr}" if args.sgd_lr > 0 else "deltas")
                 + (f", momentum {args.momentum}" if args.momentum > 0 else ""),
-                "launch": "CUDA graph (2 steps per replay)" if graph is not None else "stream",
+                "launch": f"CUDA graph ({n_graph} steps per replay)" if graph is not None else "stream",
                 "single_launch_step": grp.single_launch},
         "hbm_gbs_step": ach_step,
         "roofline": {"bound": "hbm",

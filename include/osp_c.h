@@ -401,7 +401,7 @@ typedef struct osp_shard_config {
     int n_workers;          /* N total logical workers, N % world == 0 */
     const double* weights;  /* HOST, N weights (all workers) */
     int n_chunks;
-    uint32_t tile_elems;    /* 0 = default 1024; power of two in [512, 4096] */
+    uint32_t tile_elems;    /* 0 = default 2048; power of two in [512, 4096] */
     double sgd_lr;          /* 0 = deltas; > 0 fused sgd_delta */
     uint32_t flags;         /* OSP_SHARD_* bits */
 } osp_shard_config;

@@ -12,6 +12,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -52,8 +53,13 @@ struct osp_shard {
     bool connected = false;
     unsigned iter = 0;         // iterations started (stage-1 launches) = tile-flag epoch
     bool s1_open = false;      // stage 1 issued, iteration not yet resolved
-    int lag = 2;               // OSP_SHARD_LAG: B items' due-time lag (A items)
+    // exchange-kernel shape (profiles/r2_multi_gpu_notes.md, 2 B200, ResNet-50):
+    // role-split CTAs, flags published 4..8 per fence, B items 10 A items behind
+    int lag = 10;              // OSP_SHARD_LAG: B items' due-time lag (A items)
     int stages = 2;            // OSP_SHARD_STAGES: exchange ring depth (2 or 3)
+    int pub_batch = 8, pub_min = 4;  // OSP_SHARD_PUB="max,min": flags per fence
+    int diag = 0;              // OSP_SHARD_DIAG (timing experiments only)
+    int split = 1;             // OSP_SHARD_SPLIT=0: every CTA takes every item kind
     unsigned long long* dbg = nullptr;  // OSP_SHARD_DEBUG=1: kernel counters [16]
 };
 
@@ -76,7 +82,15 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     double tw = 0.0;
     for (int w = 0; w < cfg->n_workers; ++w) tw += cfg->weights[w];
     if (!(tw > 0.0)) return fail(OSP_ERR_PROTOCOL, "aggregation weights must sum > 0");
-    const uint32_t T = cfg->tile_elems ? cfg->tile_elems : kDefaultTmaTile;
+    // default 2048-element tiles (fewer per-tile flags for the same bytes,
+    // measured), smaller when the ring and the layer tables would not fit
+    uint32_t T = cfg->tile_elems;
+    if (!T) {
+        T = 2048u;
+        while (T > 512u && !shard_x_supported(cfg->n_workers, static_cast<int>(T),
+                                               static_cast<int>(part->counts.size())))
+            T /= 2;
+    }
     if (T < 512 || T > 4096 || (T & (T - 1)))
         return fail(OSP_ERR_INVALID, "shard tile_elems must be a power of two in [512, 4096]");
     if (!shard_x_supported(cfg->n_workers, static_cast<int>(T), static_cast<int>(part->counts.size())))
@@ -92,6 +106,15 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
     if (const char* lg = std::getenv("OSP_SHARD_LAG")) s->lag = std::max(0, std::atoi(lg));
     if (const char* ks = std::getenv("OSP_SHARD_STAGES")) s->stages = std::atoi(ks) == 3 ? 3 : 2;
+    if (const char* pb = std::getenv("OSP_SHARD_PUB")) {
+        int a = 0, b = 0;
+        if (std::sscanf(pb, "%d,%d", &a, &b) == 2 && a >= 1 && b >= 1 && b <= a) {
+            s->pub_batch = a;
+            s->pub_min = b;
+        }
+    }
+    if (const char* dg = std::getenv("OSP_SHARD_DIAG")) s->diag = std::atoi(dg);
+    if (const char* sp = std::getenv("OSP_SHARD_SPLIT")) s->split = std::atoi(sp) == 0 ? 0 : 1;
     // the local group: default (TMA-staged, carry) so the stage-2 broadcast and
     // the overlapped resolve are the single-GPU kernels; no single-launch step
     osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks, T, cfg->sgd_lr,
@@ -211,6 +234,10 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.slot_rows = x_slot_rows(s->N);
     base.lag = s->lag;
     base.stages = s->stages;
+    base.pub_batch = s->pub_batch;
+    base.pub_min = s->pub_min;
+    base.diag = s->diag;
+    base.split = s->split;
     base.dbg = s->dbg;
     for (int b = 0; b < 2; ++b) {
         XArgs& xa = s->xa[b];

@@ -44,6 +44,7 @@ namespace osp {
 namespace {
 
 enum XItem { XI_A = 0, XI_B = 1, XI_L = 2 };
+constexpr int kPQ = 16;  // publication queue entries per CTA
 
 struct XMeta {
     uint64_t s, e;  // element range
@@ -103,15 +104,16 @@ struct XSched {
     int nA, nL, nB[kMaxRanks];
     int ia, il, ib[kMaxRanks];
     int P, R, lag;
+    int pace;  // A items of this slice (or of the peers' slices when this CTA has none)
 
     __device__ double dueA() const { return ia < nA ? static_cast<double>(ia) : 1e30; }
     __device__ double dueL() const {
         if (il >= nL) return 1e30;
-        return nA > 0 ? (static_cast<double>(il) + 0.5) * nA / nL : 0.0;
+        return (static_cast<double>(il) + 0.5) * pace / nL;
     }
     __device__ double dueB(int q) const {
         if (ib[q] >= nB[q]) return 1e30;
-        return nA > 0 ? (static_cast<double>(ib[q]) + 1.0) * nA / nB[q] + lag - 1 : 0.0;
+        return (static_cast<double>(ib[q]) + 1.0) * pace / nB[q] + lag - 1;
     }
     // the earliest-due B item: (peer, index) or q = -1
     __device__ void headB(int& q, int& k, double& due) const {
@@ -177,11 +179,13 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
 
     float* ring = reinterpret_cast<float*>(smem);
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + KS * SF);
-    uint64_t* done = full + KS;
-    uint64_t* empty = done + KS;
-    XMeta* meta = reinterpret_cast<XMeta*>(empty + KS);
-    double* red = reinterpret_cast<double*>(meta + KS);  // [KS][CW]
-    unsigned char* tabmem = reinterpret_cast<unsigned char*>(red + KS * CW);
+    uint64_t* empty = full + KS;
+    uint64_t* pdone = empty + KS;                       // [kPQ] publication entries complete
+    XMeta* meta = reinterpret_cast<XMeta*>(pdone + kPQ);
+    double* red = reinterpret_cast<double*>(meta + KS);  // [kPQ][CW] warp partials
+    int* pq_t = reinterpret_cast<int*>(red + kPQ * CW);  // [kPQ] tile id (-1 stop, -2 no flag)
+    int* pub_head = pq_t + kPQ;                         // [1] entries the publisher consumed
+    unsigned char* tabmem = reinterpret_cast<unsigned char*>(pub_head + 4);
 
     // ---- tables: layer geometry, exchange sequence, local-estimate sequence
     const int L = g.L;
@@ -243,14 +247,21 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
     if (tid == 0) {
         for (int s = 0; s < KS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&done[s], CW);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CW);
         }
+        for (int j = 0; j < kPQ; ++j) mbar_init(&pdone[j], CW);
+        *pub_head = 0;
         mbar_init_fence();
     }
     __syncthreads();
 
-    const int C = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+    // role split (xa.split): even CTAs take the own slices (A items, NVLink-bound),
+    // odd CTAs the peers' slices and the local estimates (B / L items, HBM-bound),
+    // so waiting on a peer never takes a ring slot from the exchange
+    const bool split = xa.split != 0 && gridDim.x >= 2;
+    const int C = split ? static_cast<int>(gridDim.x) / 2 : static_cast<int>(gridDim.x);
+    const int c = split ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int role = split ? (static_cast<int>(blockIdx.x) & 1) + 1 : 0;  // 0 all, 1 A, 2 B/L
     const int U0 = nx > 0 ? xp[0] : 0;
     const int U = nx > 0 ? xp[nx] - U0 : 0;
     const int V = nc > 0 ? cp[nc] - cp[0] : 0;
@@ -277,19 +288,24 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
 
     if (warp == CW + 1) {
         // ================= publisher =================
-        // A tiles' partials go out as they complete; their flags are published
-        // in batches of up to kPubBatch under one system-scope fence (cumulative
-        // over the consumers' pull stores, acquired through the done barrier,
-        // and the partials), or at once when no further item is done yet
-        constexpr int kPubBatch = 4;
-        int pend[kPubBatch];
+        // Consumers hand every item to this warp through a kPQ-entry queue
+        // (warp partials + tile id) and free the ring slot themselves, so the
+        // system-scope fence below never holds a slot. A tiles' partials go out
+        // as their entries complete; their flags are published in batches under
+        // one fence (cumulative over the consumers' pull stores, acquired through
+        // the entry barrier, and the partials): when kPubBatch are pending or no
+        // further entry is complete yet.
+        constexpr int kPubMax = 16;
+        const int batch = xa.pub_batch < 1 ? 1 : (xa.pub_batch > kPubMax ? kPubMax : xa.pub_batch);
+        int pend[kPubMax];
         int np = 0;
         long long t_fence = 0, n_flush = 0;
         auto flush = [&]() {
             if (np == 0) return;
             if (lane == 0 && !xa.solo) {
                 const long long f0 = clock64();
-                __threadfence_system();
+                // acq_rel (not sc): a release pattern for the flag stores below
+                if (!(xa.diag & 1)) asm volatile("fence.acq_rel.sys;" ::: "memory");
                 for (int j = 0; j < np; ++j)
                     for (int r = 0; r < P; ++r)
                         if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + pend[j]) = xa.epoch;
@@ -300,27 +316,35 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             __syncwarp();
         };
         for (int i = 0;; ++i) {
-            const int s = i % KS;
-            const unsigned par = (i / KS) & 1;
-            if (!mbar_try(&done[s], par)) {
-                flush();
-                mbar_wait(&done[s], par);
+            const int j = i % kPQ;
+            const unsigned par = (i / kPQ) & 1;
+            if (!mbar_try(&pdone[j], par)) {
+                // nothing else to do: publish what is pending — at once when at
+                // least pub_min flags wait, else after 2 us (a peer may be
+                // blocked on exactly these tiles)
+                if (np >= xa.pub_min) flush();
+                const uint64_t w0 = now_ns();
+                while (!mbar_try(&pdone[j], par)) {
+                    const uint64_t dt = now_ns() - w0;
+                    if (np > 0 && dt > 2000) flush();
+                    if (dt > 20000000000ull) __trap();
+                }
             }
-            const XMeta m = meta[s];
+            const int t = pq_t[j];
             double tot = 0.0;
-            if (m.t >= 0 && m.kind == XI_A)
-                for (int w = 0; w < CW; ++w) tot = __dadd_rn(tot, red[s * CW + w]);
+            if (t >= 0)
+                for (int w = 0; w < CW; ++w) tot = __dadd_rn(tot, red[j * CW + w]);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-            if (m.t < 0) {
+            if (lane == 0) st_release_cta_s32(pub_head, i + 1);  // entry j may be reused
+            if (t == -1) {
                 flush();
                 break;
             }
-            if (m.kind != XI_A) continue;
+            if (t < 0) continue;  // B / L item: nothing to publish
             if (lane == 0)
-                for (int r = 0; r < P; ++r) xa.part[r][m.t] = tot;
-            pend[np++] = m.t;
-            if (np == kPubBatch) flush();
+                for (int r = 0; r < P; ++r) xa.part[r][t] = tot;
+            pend[np++] = t;
+            if (np >= batch) flush();
         }
         if (xa.dbg && lane == 0) {
             atomicAdd(xa.dbg + 3, static_cast<unsigned long long>(t_fence));
@@ -336,14 +360,19 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         sc.R = R;
         sc.lag = xa.lag;
         sc.ia = sc.il = 0;
-        sc.nA = slice_lo(R, c + 1) - slice_lo(R, c);
-        sc.nL = xa.mode == XM_RS ? static_cast<int>((static_cast<int64_t>(V) * (c + 1)) / C) - lcl_lo : 0;
+        const bool do_a = role != 2 && (c < C), do_bl = role != 1 && (c < C);
+        sc.nA = do_a ? slice_lo(R, c + 1) - slice_lo(R, c) : 0;
+        sc.nL = do_bl && xa.mode == XM_RS
+                    ? static_cast<int>((static_cast<int64_t>(V) * (c + 1)) / C) - lcl_lo : 0;
+        int pace = sc.nA;
         for (int q = 0; q < kMaxRanks; ++q) {
             sc.ib[q] = 0;
-            sc.nB[q] = (q < P && q != R && !xa.solo) ? slice_lo(q, c + 1) - slice_lo(q, c) : 0;
+            sc.nB[q] = (do_bl && q < P && q != R && !xa.solo) ? slice_lo(q, c + 1) - slice_lo(q, c) : 0;
+            if (q < P && q != R) pace = max(pace, slice_lo(q, c + 1) - slice_lo(q, c));
         }
+        sc.pace = pace > 0 ? pace : 1;
         // this iteration's delta rows are ready here; peers' before the first A item
-        if (lane == 0 && xa.mode != XM_ICS && !xa.solo) {
+        if (lane == 0 && xa.mode != XM_ICS && !xa.solo && role != 2) {
             __threadfence_system();
             for (int q = 0; q < P; ++q)
                 if (q != R) st_release_sys(xa.ready[q] + R, xa.epoch);
@@ -445,8 +474,14 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         mbar_wait(&full[s], (i / KS) & 1);
         t_full += clock64() - f0;
         const XMeta m = meta[s];
+        const int j = i % kPQ;
         if (m.t < 0) {
-            if (lane == 0) mbar_arrive(&done[s]);
+            if (lane == 0) {
+                // queue entry j is free once the publisher consumed item i - kPQ
+                while (ld_acquire_cta_s32(pub_head) < i - kPQ + 1) __nanosleep(32);
+                if (warp == 0) pq_t[j] = -1;
+                mbar_arrive(&pdone[j]);
+            }
             break;
         }
         const float* buf = ring + s * SF;
@@ -561,8 +596,11 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         }
         __syncwarp();
         if (lane == 0) {
-            if (m.kind == XI_A) red[s * CW + warp] = acc;
-            mbar_arrive(&done[s]);
+            mbar_arrive(&empty[s]);  // the slot's data has been read
+            while (ld_acquire_cta_s32(pub_head) < i - kPQ + 1) __nanosleep(32);
+            red[j * CW + warp] = acc;
+            if (warp == 0) pq_t[j] = m.kind == XI_A ? m.t : -2;
+            mbar_arrive(&pdone[j]);  // release: this warp's stores and partial
         }
     }
     if (xa.dbg && tid == 0) atomicAdd(xa.dbg + 2, static_cast<unsigned long long>(t_full));
@@ -572,7 +610,8 @@ constexpr int kXCW = 8;
 
 size_t x_smem_bytes(int slot_rows, int T, int L, int ks) {
     const size_t ring = static_cast<size_t>(ks) * slot_rows * T * sizeof(float);
-    const size_t ctl = 3 * ks * sizeof(uint64_t) + ks * sizeof(XMeta) + ks * kXCW * sizeof(double);
+    const size_t ctl = 2 * ks * sizeof(uint64_t) + kPQ * sizeof(uint64_t) + ks * sizeof(XMeta) +
+                       kPQ * kXCW * sizeof(double) + kPQ * sizeof(int) + 16;
     const size_t tab = static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + L * 4 +
                        (L + 1) * 4 + L * 4 + (L + 1) * 4 + 128;
     return ring + ctl + tab;

@@ -6,17 +6,15 @@
 // here every phase of the iteration runs in one 1024-thread CTA and the
 // resolve is done by a single warp with shuffles (one layer per lane):
 //
-//   stage 1+2 (OspServer::try_close_barrier + finish_layer, protocol.cpp:292-307,
-//             361-382, on_push_ics_chunk, :326-353; OspWorker::apply_pull ->
-//             lgp_partial and lgp_correct, protocol.cpp:69-116): per element
-//             agg = float(sum_w w_k*(double)x_k / W) in the fixed worker order,
-//             G' = G + agg, and every worker row ends at G' — on a barrier layer
-//             directly, on a deferred layer as base + agg with base == G. Inside
-//             one launch the stage-1 local estimate of a deferred element is
-//             overwritten by its stage-2 correction before anything can read it
-//             (the same thread writes both), so this kernel writes each row once
-//             with its final value; the per-stage API (osp_group_stage1 /
-//             stage2_*) materialises the intermediate state.
+//   stage 1   (OspServer::try_close_barrier + finish_layer, protocol.cpp:292-307,
+//             361-382; OspWorker::apply_pull -> lgp_partial, protocol.cpp:69-97):
+//             per element agg = float(sum_w w_k*(double)x_k / W) in the fixed worker
+//             order; RS layers: G' = G + agg, every worker row = G'; ICS layers:
+//             every worker row = G + x_w (the LGP local estimate) and the carry
+//             C = G + agg.
+//   stage 2   (on_push_ics_chunk / lgp_correct, protocol.cpp:99-116, 326-353),
+//             after a block barrier: ICS layers G = C, every worker row = C
+//             (base + agg, base == G_old).
 //   resolve   (check_resolution, protocol.cpp:384-439): PGP per layer
 //             (importance.cpp:11-28) as tile partials summed in a fixed tree,
 //             certified against the reference's sequential sum (resolve.cu's
@@ -26,8 +24,8 @@
 //             list / counter / GIB byte the regular kernels keep, so the group
 //             can continue on either path.
 //
-// Latency is the cost here, not bytes: one barrier after the table load, one
-// after the elementwise pass; each warp keeps kBatch tiles' loads in flight.
+// Latency is the cost here, not bytes: each warp keeps kBatch tiles' loads in
+// flight; block barriers after the table load, stage 1, stage 2 and the layer sums.
 // Results are bit-identical to stage1 + stage2_resolve (tests/test_gpu_parity.py).
 
 #include "common.cuh"
@@ -48,6 +46,7 @@ struct SmallSmem {
     int flag[kSmallMaxLayers];         // current GIB
     double part[kSmallMaxTiles];       // PGP tile partials
     double exact[kSmallMaxLayers];     // exact sequential sums of marked layers
+    double lsum[kSmallMaxLayers];      // per-layer tree sums of the tile partials
     uint64_t budget, resolved;
     int n_marked;
 };
@@ -73,12 +72,17 @@ __device__ __forceinline__ int warp_rank(double key, int lane, int L) {
     return r;
 }
 
-// One element: fixed-order aggregate, G' = G + agg, every worker row = G';
-// returns the PGP term. xs: the NS deltas (NS > 0) or read here (NS == 0).
+template <int NS>
+constexpr int kRowsOf() { return NS > 0 ? NS : 1; }
+
+// Stage 1 of one element: fixed-order aggregate, G' = G + agg; a barrier layer
+// ends there (G and every worker row = G'), a deferred one gets the local
+// estimates and the carry. Returns the PGP term. xs: the NS deltas (NS > 0) or
+// read here (NS == 0).
 template <int NS>
 __device__ __forceinline__ double small_elem(const GroupView& g, const AggParams& ap,
                                              const float* __restrict__ X, uint64_t ldX,
-                                             uint64_t f, float go, const float* xs) {
+                                             uint64_t f, float go, const float* xs, bool ics) {
     const int n = NS > 0 ? NS : ap.n;
     double sum = 0.0;
 #pragma unroll
@@ -98,8 +102,17 @@ __device__ __forceinline__ double small_elem(const GroupView& g, const AggParams
     }
     const float a = agg_finish(ap, sum);
     const float gn = __fadd_rn(go, a);
-    g.G[f] = gn;
-    for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+    if (ics) {  // LGP local estimate now, the carry for stage 2
+        for (int w = 0; w < n; ++w) {
+            float x = NS > 0 ? xs[w < kRowsOf<NS>() ? w : 0] : X[static_cast<uint64_t>(w) * ldX + f];
+            if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+            g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
+        }
+        g.C[f] = gn;
+    } else {
+        g.G[f] = gn;
+        for (int w = 0; w < n; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+    }
     return pgp_term(a, gn);
 }
 
@@ -148,24 +161,26 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     __syncthreads();
     const int n_ptiles = s.ptb[L];
 
-    // ---- stages 1 + 2: one warp per 32-element PGP tile, kBatch tiles in flight
+    // ---- stage 1: one warp per 32-element PGP tile, kBatch tiles in flight
     constexpr int kBatch = 4;
     constexpr int kRows = NS > 0 ? NS : 1;
     for (int t0 = warp; t0 < n_ptiles; t0 += kSmallWarps * kBatch) {
         float go[kBatch], xs[kBatch][kRows];
         uint64_t fe[kBatch];
-        bool ok[kBatch];
+        bool ok[kBatch], ics[kBatch];
 #pragma unroll
         for (int j = 0; j < kBatch; ++j) {
             const int t = t0 + j * kSmallWarps;
             ok[j] = false;
             fe[j] = 0;
+            ics[j] = false;
             if (t < n_ptiles) {
                 int l = 0;
                 while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
                 const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
                 ok[j] = f < s.off[l] + s.cnt[l];
                 fe[j] = f;
+                ics[j] = s.flag[l] != 0;
             }
             if (ok[j]) {
                 go[j] = g.G[fe[j]];
@@ -178,29 +193,41 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         for (int j = 0; j < kBatch; ++j) {
             const int t = t0 + j * kSmallWarps;
             if (t >= n_ptiles) break;  // warp-uniform
-            double acc = ok[j] ? small_elem<NS>(g, ap, X, ldX, fe[j], go[j], xs[j]) : 0.0;
+            double acc = ok[j] ? small_elem<NS>(g, ap, X, ldX, fe[j], go[j], xs[j], ics[j]) : 0.0;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
             if (lane == 0) s.part[t] = acc;
         }
     }
-    __syncthreads();  // G final, every tile partial in shared memory
+    __syncthreads();  // stage 1 complete: local estimates and the carry written
+
+    // ---- stage 2: the carry broadcast on the deferred layers
+    for (int l = 0; l < L; ++l) {
+        if (!s.flag[l]) continue;
+        for (uint64_t f = s.off[l] + tid; f < s.off[l] + s.cnt[l]; f += kSmallThreads) {
+            const float gn = g.C[f];
+            g.G[f] = gn;
+            for (int w = 0; w < (NS > 0 ? NS : ap.n); ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+        }
+    }
+    __syncthreads();  // G final (the exact fallback reads it), tile partials in shared memory
+    // per-layer sums of the tile partials, warp l for layer l: lane-strided in
+    // order, then the fixed shuffle tree (depth <= ceil(nt / 32) + 5)
+    if (warp < L) {
+        double acc = 0.0;
+        for (int t = s.ptb[warp] + lane; t < s.ptb[warp + 1]; t += 32) acc = __dadd_rn(acc, s.part[t]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        if (lane == 0) s.lsum[warp] = acc;
+    }
+    __syncthreads();
 
     // ---- resolve (warp 0; lane = layer for the per-layer values)
     double key = __longlong_as_double(0x7ff0000000000000ll);
     bool marked = false;
     if (warp == 0) {
-        // per-layer sums of the tile partials: lane-strided in order, then the
-        // fixed shuffle tree (depth <= ceil(nt / 32) + 5)
         double rad = 0.0;
-        for (int l = 0; l < L; ++l) {
-            double acc = 0.0;
-            for (int t = s.ptb[l] + lane; t < s.ptb[l + 1]; t += 32) acc = __dadd_rn(acc, s.part[t]);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
-            acc = __shfl_sync(0xffffffffu, acc, 0);
-            if (lane == l) key = acc;
-        }
+        if (lane < L) key = s.lsum[lane];
         if (lane < L) {
             const double nt = static_cast<double>(s.ptb[lane + 1] - s.ptb[lane]);
             // depth: 5 (tile tree) + ceil(nt / 32) + 5 (layer tree) + slack

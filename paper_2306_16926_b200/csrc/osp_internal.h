@@ -158,6 +158,10 @@ struct XArgs {
     int slot_rows;                       // shared-memory rows per ring slot
     int lag;                             // B items' due-time lag behind the A items
     int stages;                          // ring stages (2 or 3)
+    int pub_batch;                       // flags published under one fence, at most
+    int pub_min;                         // ... and at least, unless the stage ends
+    int diag;                            // diagnostics only: 1 = no fence (unordered flags)
+    int split;                           // CTA roles: even = own tiles, odd = peers' + local
     unsigned long long* dbg;             // diagnostics counters [16] or null
 };
 int x_slot_rows(int n_workers);
