@@ -60,6 +60,8 @@ struct osp_shard {
     int pub_batch = 8, pub_min = 4;  // OSP_SHARD_PUB="max,min": flags per fence
     int diag = 0;              // OSP_SHARD_DIAG (timing experiments only)
     int split = 1;             // OSP_SHARD_SPLIT=0: every CTA takes every item kind
+    int barrier = -1;          // OSP_SHARD_SYNC=tile|barrier; -1: by world size
+    unsigned* ticket = nullptr;  // [1] local, phase-1 last-CTA counter
     unsigned long long* dbg = nullptr;  // OSP_SHARD_DEBUG=1: kernel counters [16]
 };
 
@@ -115,6 +117,10 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     }
     if (const char* dg = std::getenv("OSP_SHARD_DIAG")) s->diag = std::atoi(dg);
     if (const char* sp = std::getenv("OSP_SHARD_SPLIT")) s->split = std::atoi(sp) == 0 ? 0 : 1;
+    if (const char* sy = std::getenv("OSP_SHARD_SYNC"))
+        s->barrier = std::strcmp(sy, "barrier") == 0 ? 1 : std::strcmp(sy, "tile") == 0 ? 0 : -1;
+    // measured: per-tile flags win at 2 ranks, own-tiles-then-barrier at 4
+    if (s->barrier < 0) s->barrier = cfg->world >= 4 ? 1 : 0;
     // the local group: default (TMA-staged, carry) so the stage-2 broadcast and
     // the overlapped resolve are the single-GPU kernels; no single-launch step
     osp_group_config gc{s->n_loc, cfg->weights + s->rank * s->n_loc, cfg->n_chunks, T, cfg->sgd_lr,
@@ -132,12 +138,14 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     cudaError_t e = cudaMalloc(&s->X, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&s->agg, s->ldX * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&s->tflag, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMalloc(&s->ready, kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->ready, 2 * kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->ticket, sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->ticket, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&s->error, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->X, 0, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(s->agg, 0, s->ldX * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
-    if (e == cudaSuccess) e = cudaMemset(s->ready, 0, kMaxRanks * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->ready, 0, 2 * kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
     if (const char* d = std::getenv("OSP_SHARD_DEBUG"); d && d[0] == '1') {
         if (e == cudaSuccess) e = cudaMalloc(&s->dbg, 16 * sizeof(unsigned long long));
@@ -163,6 +171,7 @@ void osp_shard_destroy(osp_shard* s) {
     if (s->ready) cudaFree(s->ready);
     if (s->error) cudaFree(s->error);
     if (s->dbg) cudaFree(s->dbg);
+    if (s->ticket) cudaFree(s->ticket);
     if (s->grp) osp_group_destroy(s->grp);
     delete s;
 }
@@ -238,6 +247,7 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.pub_min = s->pub_min;
     base.diag = s->diag;
     base.split = s->split;
+    base.ticket = s->ticket;
     base.dbg = s->dbg;
     for (int b = 0; b < 2; ++b) {
         XArgs& xa = s->xa[b];
@@ -283,6 +293,17 @@ static cudaError_t launch_x(osp_shard* s, int buf, int mode, int c0, int c1, int
     xa.c0 = c0;
     xa.c1 = c1;
     xa.solo = solo;
+    if (solo || !s->barrier) {
+        xa.phase = 0;
+        return launch_shard_x(s->grp->v, s->ap_all, xa, st);
+    }
+    // barrier form: own tiles (then a cross-GPU signal), then the peers' tiles;
+    // every CTA takes both kinds (no role split)
+    xa.split = 0;
+    xa.phase = 1;
+    cudaError_t e = launch_shard_x(s->grp->v, s->ap_all, xa, st);
+    if (e != cudaSuccess) return e;
+    xa.phase = 2;
     return launch_shard_x(s->grp->v, s->ap_all, xa, st);
 }
 

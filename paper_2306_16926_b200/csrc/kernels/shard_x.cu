@@ -302,7 +302,7 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         long long t_fence = 0, n_flush = 0;
         auto flush = [&]() {
             if (np == 0) return;
-            if (lane == 0 && !xa.solo) {
+            if (lane == 0 && !xa.solo && xa.phase == 0) {
                 const long long f0 = clock64();
                 // acq_rel (not sc): a release pattern for the flag stores below
                 if (!(xa.diag & 1)) asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -338,6 +338,17 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             if (lane == 0) st_release_cta_s32(pub_head, i + 1);  // entry j may be reused
             if (t == -1) {
                 flush();
+                if (xa.phase == 1 && !xa.solo && lane == 0) {
+                    // this CTA's pull stores (acquired through the queue) are
+                    // visible system-wide; the last CTA out signals every peer
+                    __threadfence_system();
+                    if (atomicAdd(xa.ticket, 1u) == gridDim.x - 1) {
+                        atomicExch(xa.ticket, 0u);
+                        __threadfence_system();
+                        for (int q = 0; q < P; ++q)
+                            if (q != R) st_release_sys(xa.ready[q] + kMaxRanks + R, xa.epoch);
+                    }
+                }
                 break;
             }
             if (t < 0) continue;  // B / L item: nothing to publish
@@ -360,19 +371,27 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         sc.R = R;
         sc.lag = xa.lag;
         sc.ia = sc.il = 0;
-        const bool do_a = role != 2 && (c < C), do_bl = role != 1 && (c < C);
+        // xa.phase: 0 = A, B and L items with per-tile flags; 1 = A and L items
+        // only (then a cross-GPU "own tiles done" signal); 2 = B items only,
+        // after every peer's signal (no per-tile waits)
+        const bool do_a = role != 2 && (c < C) && xa.phase != 2;
+        const bool do_bl = role != 1 && (c < C);
+        const bool do_b = do_bl && xa.phase != 1, do_l = do_bl && xa.phase != 2;
         sc.nA = do_a ? slice_lo(R, c + 1) - slice_lo(R, c) : 0;
-        sc.nL = do_bl && xa.mode == XM_RS
+        sc.nL = do_l && xa.mode == XM_RS
                     ? static_cast<int>((static_cast<int64_t>(V) * (c + 1)) / C) - lcl_lo : 0;
         int pace = sc.nA;
         for (int q = 0; q < kMaxRanks; ++q) {
             sc.ib[q] = 0;
-            sc.nB[q] = (do_bl && q < P && q != R && !xa.solo) ? slice_lo(q, c + 1) - slice_lo(q, c) : 0;
+            sc.nB[q] = (do_b && q < P && q != R && !xa.solo) ? slice_lo(q, c + 1) - slice_lo(q, c) : 0;
             if (q < P && q != R) pace = max(pace, slice_lo(q, c + 1) - slice_lo(q, c));
         }
         sc.pace = pace > 0 ? pace : 1;
         // this iteration's delta rows are ready here; peers' before the first A item
-        if (lane == 0 && xa.mode != XM_ICS && !xa.solo && role != 2) {
+        if (xa.phase == 2 && lane == 0)  // every peer's own tiles are in the pull buffer
+            for (int q = 0; q < P; ++q)
+                if (q != R) xspin(xa.ready[R] + kMaxRanks + q, xa.epoch, xa.error);
+        if (lane == 0 && xa.mode != XM_ICS && !xa.solo && role != 2 && xa.phase != 2) {
             __threadfence_system();
             for (int q = 0; q < P; ++q)
                 if (q != R) st_release_sys(xa.ready[q] + R, xa.epoch);
@@ -392,8 +411,8 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             int bq, bk;
             double bd;
             sc.headB(bq, bk, bd);
-            int ready = 0;
-            if (bq >= 0) {
+            int ready = xa.phase == 2 ? 1 : 0;
+            if (bq >= 0 && xa.phase != 2) {
                 XMeta mb{};
                 locate(XI_B, slice_lo(bq, c) + bk, mb);
                 if (lane == 0)
@@ -426,7 +445,7 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             }
             if (kind == XI_B) {
                 const long long b0 = clock64();
-                if (lane == 0) xspin(xa.tflag[R] + m.t, xa.epoch, xa.error);
+                if (lane == 0 && xa.phase != 2) xspin(xa.tflag[R] + m.t, xa.epoch, xa.error);
                 __syncwarp();
                 fence_proxy_async();
                 if (!ready) {

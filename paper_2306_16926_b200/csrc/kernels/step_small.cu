@@ -3,7 +3,7 @@
 // The big-layout step is three launches (stage 1 over every SM, the resolve,
 // the stage-2 broadcast); for a 420-parameter model those launches, their
 // table loads and the resolve's ~15 block-wide phases are the whole cost, so
-// here every phase of the iteration runs in one 1024-thread CTA and the
+// here every phase of the iteration runs in one 512-thread CTA and the
 // resolve is done by a single warp with shuffles (one layer per lane):
 //
 //   stage 1   (OspServer::try_close_barrier + finish_layer, protocol.cpp:292-307,
@@ -33,7 +33,7 @@
 namespace osp {
 namespace {
 
-constexpr int kSmallThreads = 1024;
+constexpr int kSmallThreads = 512;
 constexpr int kSmallWarps = kSmallThreads / 32;
 constexpr int kSmallTile = 32;  // PGP tile: one term per lane, then 5 shuffles
 constexpr double kU = 1.1102230246251565404e-16;  // 2^-53
@@ -82,7 +82,8 @@ constexpr int kRowsOf() { return NS > 0 ? NS : 1; }
 template <int NS>
 __device__ __forceinline__ double small_elem(const GroupView& g, const AggParams& ap,
                                              const float* __restrict__ X, uint64_t ldX,
-                                             uint64_t f, float go, const float* xs, bool ics) {
+                                             uint64_t f, float go, const float* xs, bool ics,
+                                             float& gn_out) {
     const int n = NS > 0 ? NS : ap.n;
     double sum = 0.0;
 #pragma unroll
@@ -102,6 +103,7 @@ __device__ __forceinline__ double small_elem(const GroupView& g, const AggParams
     }
     const float a = agg_finish(ap, sum);
     const float gn = __fadd_rn(go, a);
+    gn_out = gn;
     if (ics) {  // LGP local estimate now, the carry for stage 2
         for (int w = 0; w < n; ++w) {
             float x = NS > 0 ? xs[w < kRowsOf<NS>() ? w : 0] : X[static_cast<uint64_t>(w) * ldX + f];
@@ -164,6 +166,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     // ---- stage 1: one warp per 32-element PGP tile, kBatch tiles in flight
     constexpr int kBatch = 4;
     constexpr int kRows = NS > 0 ? NS : 1;
+    float gkeep[kBatch];  // this warp's first batch of G' values, kept for stage 2
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) gkeep[j] = 0.f;
     for (int t0 = warp; t0 < n_ptiles; t0 += kSmallWarps * kBatch) {
         float go[kBatch], xs[kBatch][kRows];
         uint64_t fe[kBatch];
@@ -193,7 +198,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         for (int j = 0; j < kBatch; ++j) {
             const int t = t0 + j * kSmallWarps;
             if (t >= n_ptiles) break;  // warp-uniform
-            double acc = ok[j] ? small_elem<NS>(g, ap, X, ldX, fe[j], go[j], xs[j], ics[j]) : 0.0;
+            float gn = 0.f;
+            double acc = ok[j] ? small_elem<NS>(g, ap, X, ldX, fe[j], go[j], xs[j], ics[j], gn) : 0.0;
+            if (t0 == warp) gkeep[j] = gn;
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
             if (lane == 0) s.part[t] = acc;
@@ -201,24 +208,44 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     }
     __syncthreads();  // stage 1 complete: local estimates and the carry written
 
-    // ---- stage 2: the carry broadcast on the deferred layers
-    for (int l = 0; l < L; ++l) {
-        if (!s.flag[l]) continue;
-        for (uint64_t f = s.off[l] + tid; f < s.off[l] + s.cnt[l]; f += kSmallThreads) {
-            const float gn = g.C[f];
-            g.G[f] = gn;
-            for (int w = 0; w < (NS > 0 ? NS : ap.n); ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+    // ---- stage 2: the carry broadcast on the deferred layers, in stage 1's
+    // element mapping (the first batch's values are still in registers, later
+    // batches read the carry back, kBatch loads in flight)
+    for (int t0 = warp; t0 < n_ptiles; t0 += kSmallWarps * kBatch) {
+        float cv[kBatch];
+        uint64_t fe[kBatch];
+        bool on[kBatch];
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            const int t = t0 + j * kSmallWarps;
+            on[j] = false;
+            fe[j] = 0;
+            if (t < n_ptiles) {
+                int l = 0;
+                while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
+                const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
+                on[j] = s.flag[l] != 0 && f < s.off[l] + s.cnt[l];
+                fe[j] = f;
+            }
+            cv[j] = t0 == warp ? gkeep[j] : (on[j] ? g.C[fe[j]] : 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < kBatch; ++j) {
+            if (!on[j]) continue;
+            g.G[fe[j]] = cv[j];
+            for (int w = 0; w < (NS > 0 ? NS : ap.n); ++w)
+                g.P[static_cast<uint64_t>(w) * g.ldP + fe[j]] = cv[j];
         }
     }
     __syncthreads();  // G final (the exact fallback reads it), tile partials in shared memory
     // per-layer sums of the tile partials, warp l for layer l: lane-strided in
     // order, then the fixed shuffle tree (depth <= ceil(nt / 32) + 5)
-    if (warp < L) {
+    for (int l = warp; l < L; l += kSmallWarps) {
         double acc = 0.0;
-        for (int t = s.ptb[warp] + lane; t < s.ptb[warp + 1]; t += 32) acc = __dadd_rn(acc, s.part[t]);
+        for (int t = s.ptb[l] + lane; t < s.ptb[l + 1]; t += 32) acc = __dadd_rn(acc, s.part[t]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
-        if (lane == 0) s.lsum[warp] = acc;
+        if (lane == 0) s.lsum[l] = acc;
     }
     __syncthreads();
 

@@ -147,7 +147,7 @@ struct XArgs {
     float* agg[kMaxRanks];               // every rank's pull buffer [ldX]
     double* part[kMaxRanks];             // every rank's per-tile PGP partials [NT]
     unsigned* tflag[kMaxRanks];          // every rank's per-tile ready flags [NT]
-    unsigned* ready[kMaxRanks];          // every rank's deltas-ready slots [kMaxRanks]
+    unsigned* ready[kMaxRanks];          // every rank's slots [2][kMaxRanks]: deltas ready, own tiles done
     unsigned* error;                     // local: set when a bounded wait timed out
     int world, rank, n_loc;
     unsigned epoch;                      // iteration number (1-based)
@@ -162,6 +162,8 @@ struct XArgs {
     int pub_min;                         // ... and at least, unless the stage ends
     int diag;                            // diagnostics only: 1 = no fence (unordered flags)
     int split;                           // CTA roles: even = own tiles, odd = peers' + local
+    int phase;                           // 0 per-tile flags; 1 own tiles + signal; 2 peers' tiles
+    unsigned* ticket;                    // local: last-CTA counter of phase 1
     unsigned long long* dbg;             // diagnostics counters [16] or null
 };
 int x_slot_rows(int n_workers);
