@@ -62,6 +62,7 @@ struct osp_shard {
     int split = 1;             // OSP_SHARD_SPLIT=0: every CTA takes every item kind
     int barrier = -1;          // OSP_SHARD_SYNC=tile|barrier; -1: by world size
     unsigned* ticket = nullptr;  // [1] local, phase-1 last-CTA counter
+    unsigned done_epoch = 0;     // barrier-form launches so far (a stage-2 chunk is one)
     unsigned long long* dbg = nullptr;  // OSP_SHARD_DEBUG=1: kernel counters [16]
 };
 
@@ -300,11 +301,12 @@ static cudaError_t launch_x(osp_shard* s, int buf, int mode, int c0, int c1, int
     // barrier form: own tiles (then a cross-GPU signal), then the peers' tiles;
     // every CTA takes both kinds (no role split)
     xa.split = 0;
+    xa.done_epoch = ++s->done_epoch;
     xa.phase = 1;
     cudaError_t e = launch_shard_x(s->grp->v, s->ap_all, xa, st);
     if (e != cudaSuccess) return e;
     xa.phase = 2;
-    return launch_shard_x(s->grp->v, s->ap_all, xa, st);
+    return launch_shard_peer_apply(s->grp->v, s->ap_all, xa, st);
 }
 
 // stage 1: SINGLE mode exchanges every tile (the carry keeps the deferred

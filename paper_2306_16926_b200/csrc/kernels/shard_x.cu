@@ -346,7 +346,7 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
                         atomicExch(xa.ticket, 0u);
                         __threadfence_system();
                         for (int q = 0; q < P; ++q)
-                            if (q != R) st_release_sys(xa.ready[q] + kMaxRanks + R, xa.epoch);
+                            if (q != R) st_release_sys(xa.ready[q] + kMaxRanks + R, xa.done_epoch);
                     }
                 }
                 break;
@@ -390,7 +390,7 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         // this iteration's delta rows are ready here; peers' before the first A item
         if (xa.phase == 2 && lane == 0)  // every peer's own tiles are in the pull buffer
             for (int q = 0; q < P; ++q)
-                if (q != R) xspin(xa.ready[R] + kMaxRanks + q, xa.epoch, xa.error);
+                if (q != R) xspin(xa.ready[R] + kMaxRanks + q, xa.done_epoch, xa.error);
         if (lane == 0 && xa.mode != XM_ICS && !xa.solo && role != 2 && xa.phase != 2) {
             __threadfence_system();
             for (int q = 0; q < P; ++q)
@@ -655,6 +655,123 @@ cudaError_t launch_x_ns(const GroupView& g, const AggParams& ap, const XArgs& xa
     return launch_x_ks<NS, 2>(g, ap, xa, s);
 }
 
+// Phase 2 of the barrier form: the peers' tiles of the exchanged sequence,
+// applied straight from the pull buffer with 128-bit loads (HBM-bound: one
+// warp per tile, two quads per lane in flight, no shared-memory staging), after
+// every peer has signalled that its own tiles are in this rank's pull buffer.
+__global__ void __launch_bounds__(256) k_shard_peer_apply(GroupView g, AggParams ap, XArgs xa) {
+    extern __shared__ __align__(16) unsigned char smem_tab[];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int P = xa.world, R = xa.rank, NL = xa.n_loc;
+    const int L = g.L;
+    uint64_t* t_off = reinterpret_cast<uint64_t*>(smem_tab);
+    uint64_t* t_cnt = t_off + L;
+    int* t_tb = reinterpret_cast<int*>(t_cnt + L);
+    uint8_t* t_flag = reinterpret_cast<uint8_t*>(t_tb + L + 1);
+    int* xl = reinterpret_cast<int*>(t_flag + ((L + 15) & ~15));
+    int* xp = xl + L;
+    int nx = 0, xb = 0;
+    const int* XL = nullptr;
+    const int* XP = g.tile_base;
+    const int used = g.meta[META_N_USED];
+    if (xa.mode == XM_SINGLE) {
+        nx = L;
+    } else if (xa.mode == XM_RS) {
+        XL = g.rs_layers;
+        XP = g.rs_tile_prefix;
+        nx = g.meta[META_N_RS];
+    } else {
+        XL = g.ics_layers;
+        XP = g.ics_tile_prefix;
+        const int cc1 = xa.c1 > used ? used : xa.c1;
+        if (xa.c0 < cc1) {
+            xb = g.chunk_begin[xa.c0];
+            nx = g.chunk_begin[cc1] - xb;
+        }
+    }
+    for (int i = tid; i < L; i += blockDim.x) {
+        t_off[i] = g.offsets[i];
+        t_cnt[i] = g.counts[i];
+        t_tb[i] = g.tile_base[i];
+        t_flag[i] = g.flags[i];
+    }
+    if (XL)
+        for (int i = tid; i < nx; i += blockDim.x) xl[i] = XL[xb + i];
+    for (int i = tid; nx > 0 && i <= nx; i += blockDim.x) xp[i] = XP[xb + i];
+    if (tid == 0) {
+        for (int q = 0; q < P; ++q)
+            if (q != R) xspin(xa.ready[R] + kMaxRanks + q, xa.done_epoch, xa.error);
+    }
+    __syncthreads();
+    const int U0 = nx > 0 ? xp[0] : 0;
+    const int U = nx > 0 ? xp[nx] - U0 : 0;
+    const int lo = static_cast<int>((static_cast<int64_t>(U) * R) / P);
+    const int hi = static_cast<int>((static_cast<int64_t>(U) * (R + 1)) / P);
+    const int n_peer = U - (hi - lo);
+    const bool carry_mode = xa.mode == XM_SINGLE;
+    const float* aggR = xa.agg[R];
+    const int gw = static_cast<int>((blockIdx.x * blockDim.x + tid) >> 5);
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    for (int k = gw; k < n_peer; k += nw) {
+        const int u = U0 + (k < lo ? k : k + (hi - lo));
+        int l, kk;
+        xseq_lookup(xp, XL ? xl : nullptr, nx, u, l, kk);
+        const uint64_t b = t_off[l] + static_cast<uint64_t>(kk) * g.T;
+        const uint64_t e = min(b + static_cast<uint64_t>(g.T), t_off[l] + t_cnt[l]);
+        const bool carry = carry_mode && t_flag[l];
+        const bool vec = xa.vec && (b % 4 == 0) && ((e - b) % 4 == 0);
+        if (vec) {
+            for (uint64_t f0 = b + 4ull * lane; f0 < e; f0 += 256) {
+                const uint64_t f1 = f0 + 128;
+                const bool has1 = f1 < e;
+                const float4 a0 = ld_stream4(aggR + f0), g0 = *reinterpret_cast<const float4*>(g.G + f0);
+                float4 a1 = a0, g1 = g0;
+                if (has1) {
+                    a1 = ld_stream4(aggR + f1);
+                    g1 = *reinterpret_cast<const float4*>(g.G + f1);
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    if (q == 1 && !has1) break;
+                    const uint64_t f = q == 0 ? f0 : f1;
+                    const float4 go = q == 0 ? g0 : g1;
+                    const float4 gn = add4x(go, q == 0 ? a0 : a1);
+                    if (carry) {
+                        st_stream4(g.C + f, gn);
+                        for (int w = 0; w < NL; ++w) {
+                            const float4 x = cvt4x(ap, ld_stream4(xa.xrow[R * NL + w] + f));
+                            st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, add4x(go, x));
+                        }
+                    } else {
+                        *reinterpret_cast<float4*>(g.G + f) = gn;
+                        for (int w = 0; w < NL; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+                    }
+                }
+            }
+        } else {
+            for (uint64_t f = b + lane; f < e; f += 32) {
+                const float go = g.G[f];
+                const float gn = __fadd_rn(go, aggR[f]);
+                if (carry) {
+                    g.C[f] = gn;
+                    for (int w = 0; w < NL; ++w) {
+                        float x = xa.xrow[R * NL + w][f];
+                        if (ap.sgd) x = sgd_conv(ap.neg_lr, x);
+                        g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x);
+                    }
+                } else {
+                    g.G[f] = gn;
+                    for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+                }
+            }
+        }
+    }
+}
+
+size_t peer_apply_smem(int L) {
+    return static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + L * 4 + (L + 1) * 4 + 64;
+}
+
 }  // namespace
 
 int x_slot_rows(int n_workers) { return n_workers <= kXMaxStagedWorkers ? n_workers + 1 : 2; }
@@ -662,6 +779,17 @@ int x_slot_rows(int n_workers) { return n_workers <= kXMaxStagedWorkers ? n_work
 bool shard_x_supported(int n_workers, int T, int L) {
     if (T < 512 || T > 4096) return false;
     return x_smem_bytes(x_slot_rows(n_workers), T, L, 2) <= 220 * 1024;
+}
+
+cudaError_t launch_shard_peer_apply(const GroupView& g, const AggParams& ap, const XArgs& xa,
+                                    cudaStream_t s) {
+    const size_t sm = peer_apply_smem(g.L);
+    int per_sm = 0;
+    cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(k_shard_peer_apply), 256, sm,
+                                      &per_sm);
+    if (e != cudaSuccess) return e;
+    k_shard_peer_apply<<<sm_count() * (per_sm < 4 ? per_sm : 4), 256, sm, s>>>(g, ap, xa);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_shard_x(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {

@@ -164,11 +164,15 @@ struct XArgs {
     int split;                           // CTA roles: even = own tiles, odd = peers' + local
     int phase;                           // 0 per-tile flags; 1 own tiles + signal; 2 peers' tiles
     unsigned* ticket;                    // local: last-CTA counter of phase 1
+    unsigned done_epoch;                 // phase 1/2: count of barrier-form launches (all ranks alike)
     unsigned long long* dbg;             // diagnostics counters [16] or null
 };
 int x_slot_rows(int n_workers);
 bool shard_x_supported(int n_workers, int T, int L);
 cudaError_t launch_shard_x(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s);
+// the barrier form's phase 2: the peers' tiles from the pull buffer (128-bit loads)
+cudaError_t launch_shard_peer_apply(const GroupView& g, const AggParams& ap, const XArgs& xa,
+                                    cudaStream_t s);
 
 // Opt a kernel into `smem` bytes of dynamic shared memory and return its
 // occupancy, cached per (context, kernel, bytes) (stage_tma.cu).
