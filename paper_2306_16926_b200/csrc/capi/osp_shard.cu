@@ -56,9 +56,7 @@ struct osp_shard {
     // exchange-kernel shape (profiles/r2_multi_gpu_notes.md, 2 B200, ResNet-50):
     // role-split CTAs, flags published 4..8 per fence, B items 10 A items behind
     int lag = 10;              // OSP_SHARD_LAG: B items' due-time lag (A items)
-    int stages = 2;            // OSP_SHARD_STAGES: exchange ring depth (2 or 3)
     int pub_batch = 8, pub_min = 4;  // OSP_SHARD_PUB="max,min": flags per fence
-    int diag = 0;              // OSP_SHARD_DIAG (timing experiments only)
     int split = 1;             // OSP_SHARD_SPLIT=0: every CTA takes every item kind
     int barrier = -1;          // OSP_SHARD_SYNC=tile|barrier; -1: by world size
     unsigned* ticket = nullptr;  // [1] local, phase-1 last-CTA counter
@@ -108,7 +106,6 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     s->n_chunks = cfg->n_chunks;
     s->ap_all = make_agg_params(s->N, cfg->weights, cfg->sgd_lr);
     if (const char* lg = std::getenv("OSP_SHARD_LAG")) s->lag = std::max(0, std::atoi(lg));
-    if (const char* ks = std::getenv("OSP_SHARD_STAGES")) s->stages = std::atoi(ks) == 3 ? 3 : 2;
     if (const char* pb = std::getenv("OSP_SHARD_PUB")) {
         int a = 0, b = 0;
         if (std::sscanf(pb, "%d,%d", &a, &b) == 2 && a >= 1 && b >= 1 && b <= a) {
@@ -116,7 +113,6 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
             s->pub_min = b;
         }
     }
-    if (const char* dg = std::getenv("OSP_SHARD_DIAG")) s->diag = std::atoi(dg);
     if (const char* sp = std::getenv("OSP_SHARD_SPLIT")) s->split = std::atoi(sp) == 0 ? 0 : 1;
     if (const char* sy = std::getenv("OSP_SHARD_SYNC"))
         s->barrier = std::strcmp(sy, "barrier") == 0 ? 1 : std::strcmp(sy, "tile") == 0 ? 0 : -1;
@@ -243,10 +239,8 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.n_loc = s->n_loc;
     base.slot_rows = x_slot_rows(s->N);
     base.lag = s->lag;
-    base.stages = s->stages;
     base.pub_batch = s->pub_batch;
     base.pub_min = s->pub_min;
-    base.diag = s->diag;
     base.split = s->split;
     base.ticket = s->ticket;
     base.dbg = s->dbg;

@@ -305,7 +305,7 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             if (lane == 0 && !xa.solo && xa.phase == 0) {
                 const long long f0 = clock64();
                 // acq_rel (not sc): a release pattern for the flag stores below
-                if (!(xa.diag & 1)) asm volatile("fence.acq_rel.sys;" ::: "memory");
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
                 for (int j = 0; j < np; ++j)
                     for (int r = 0; r < P; ++r)
                         if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + pend[j]) = xa.epoch;
@@ -650,9 +650,7 @@ cudaError_t launch_x_ks(const GroupView& g, const AggParams& ap, const XArgs& xa
 
 template <int NS>
 cudaError_t launch_x_ns(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
-    if (xa.stages == 3 && x_smem_bytes(xa.slot_rows, g.T, g.L, 3) <= 220 * 1024)
-        return launch_x_ks<NS, 3>(g, ap, xa, s);
-    return launch_x_ks<NS, 2>(g, ap, xa, s);
+    return launch_x_ks<NS, 2>(g, ap, xa, s);  // 3 stages measured slower (r2_multi_gpu_notes.md)
 }
 
 // Phase 2 of the barrier form: the peers' tiles of the exchanged sequence,

@@ -157,10 +157,8 @@ struct XArgs {
     int vec;                             // every row and buffer 16-byte aligned
     int slot_rows;                       // shared-memory rows per ring slot
     int lag;                             // B items' due-time lag behind the A items
-    int stages;                          // ring stages (2 or 3)
     int pub_batch;                       // flags published under one fence, at most
     int pub_min;                         // ... and at least, unless the stage ends
-    int diag;                            // diagnostics only: 1 = no fence (unordered flags)
     int split;                           // CTA roles: even = own tiles, odd = peers' + local
     int phase;                           // 0 per-tile flags; 1 own tiles + signal; 2 peers' tiles
     unsigned* ticket;                    // local: last-CTA counter of phase 1

@@ -4,9 +4,9 @@ run() { OSP_SHARD_DEBUG=1 timeout 300 python -m torch.distributed.run --nnodes=1
 run 29601 resnet50 1024
 OSP_SHARD_LAG=0 run 29602 resnet50 1024
 OSP_SHARD_LAG=4 run 29603 resnet50 1024
-OSP_SHARD_STAGES=3 run 29604 resnet50 1024
+run 29604 resnet50 1024
 run 29605 resnet50 2048
-OSP_SHARD_STAGES=3 run 29606 resnet50 2048
+run 29606 resnet50 2048
 run 29607 resnet50 512
 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q 2>&1 | tail -3 > gpurun_out/r2_multi3.log
 timeout 300 python -m pytest tests/test_gpu_parity.py -x -q -k "small" 2>&1 | tail -3 >> gpurun_out/r2_multi3.log
