@@ -28,7 +28,7 @@ FACADE_OBJS := $(patsubst $(CSRC)/%.cpp,build/%.o,$(FACADE_SRCS))
 FACADE_HDRS := $(wildcard include/pslab/*.hpp) $(CSRC)/pslab/device.hpp include/osp_c.h include/osp_engine.h
 CXXFLAGS_FACADE := -std=c++20 -O2 -fPIC -Wall -Wextra -ffp-contract=off -Iinclude -I$(CSRC)/pslab
 
-.PHONY: all lib facade oracle ref dropin clean
+.PHONY: all lib facade oracle ref dropin clean checked
 
 all: lib facade oracle
 
@@ -55,6 +55,19 @@ build/%.o: $(CSRC)/%.cu $(HDRS)
 $(LIB): $(CU_OBJS)
 	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS) -Xlinker -soname,libosp_b200.so
 
+# checked build: every kernel's indices bounds-checked (OSP_DCHECK, common.cuh);
+# the test suite runs against it with OSP_LIB_VARIANT=checked
+CHECKED := $(PKG)/libosp_b200_checked.so
+CU_OBJS_CHECKED := $(patsubst $(CSRC)/%.cu,build_checked/%.o,$(CU_SRCS))
+checked: $(CHECKED)
+
+build_checked/%.o: $(CSRC)/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -DOSP_CHECKED -c $< -o $@
+
+$(CHECKED): $(CU_OBJS_CHECKED)
+	$(NVCC) $(ARCH) -shared -o $@ $(CU_OBJS_CHECKED) -Xlinker -soname,libosp_b200_checked.so
+
 oracle:
 	$(MAKE) -s -C oracle liboracle.so
 
@@ -62,4 +75,4 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build build_checked $(LIB) $(CHECKED)

@@ -8,7 +8,10 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libosp_b200.so")
+# OSP_LIB_VARIANT=checked: the bounds-checked build (make checked), for the
+# test suite on the GPU pool, where compute-sanitizer is not available
+LIB_PATH = os.path.join(_HERE, "libosp_b200_checked.so"
+                        if os.environ.get("OSP_LIB_VARIANT") == "checked" else "libosp_b200.so")
 
 c_void_p = ctypes.c_void_p
 c_int = ctypes.c_int

@@ -5,11 +5,32 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdio>
 #include <stdint.h>
 
 #include "../osp_internal.h"
 
 namespace osp {
+
+// Checked build (make checked -> libosp_b200_checked.so, OSP_LIB_VARIANT=checked):
+// every kernel's indices are bounds-checked against the group geometry and a
+// violation prints its site and traps. compute-sanitizer is not available on
+// the GPU pool, so the test suite runs against this build instead
+// (tools/gpu_r2_checked.sh). Compiles to nothing in the product build.
+#ifdef OSP_CHECKED
+#define OSP_DCHECK(cond, what)                                                          \
+    do {                                                                                \
+        if (!(cond)) {                                                                  \
+            printf("OSP_DCHECK failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, \
+                   __LINE__, static_cast<int>(blockIdx.x), static_cast<int>(threadIdx.x)); \
+            __trap();                                                                   \
+        }                                                                               \
+    } while (0)
+#else
+#define OSP_DCHECK(cond, what) \
+    do {                       \
+    } while (0)
+#endif
 
 // Programmatic dependent launch: a kernel launched with launch_pdl may be
 // scheduled while its predecessor in the stream drains; it must call pdl_wait()

@@ -274,9 +274,12 @@ __device__ void finalize_lists(const GroupView& g, const Smem& s, const int* ord
     int* arrs[4] = {sc_new, sc_icst, sc_rsf, sc_rst};
     block_scan_multi<4, int>(arrs, L, 0, [](int a, int b) { return a + b; }, s.wtot);
     const int n_used = k > 0 ? sc_new[k - 1] : 0;
+    OSP_DCHECK(k >= 0 && k <= L, "resolve: deferred count outside [0, L]");
     for (int r = tid; r < k; r += B) {
         const int l = ord[r];
         const int c = sc_new[r] - 1;
+        OSP_DCHECK(l >= 0 && l < L, "resolve: ICS list id out of range");
+        OSP_DCHECK(c >= 0 && c < g.n_chunks, "resolve: chunk index out of range");
         g.chunk_of[l] = c;
         g.ics_layers[r] = l;
         if (r == 0 || sc_new[r] != sc_new[r - 1]) g.chunk_begin[c] = r;
@@ -377,6 +380,7 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
     //    tree, warps in order)
     for (int it = blockIdx.x; it < g.n_sum_items; it += gridDim.x) {
         const int t0 = g.sum_items[3 * it + 1], t1 = g.sum_items[3 * it + 2];
+        OSP_DCHECK(t0 >= 0 && t0 <= t1 && t1 <= g.NT, "resolve: sum item outside the tiles");
         double acc = 0.0;
         for (int t = t0 + tid; t < t1; t += blockDim.x) acc = __dadd_rn(acc, g.partials[t]);
 #pragma unroll

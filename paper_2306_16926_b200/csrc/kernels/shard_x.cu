@@ -283,6 +283,9 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
         m.e = m.s + static_cast<uint64_t>(T) < le ? m.s + static_cast<uint64_t>(T) : le;
         m.kind = kind;
         m.ics = t_flag[l];
+        OSP_DCHECK(l >= 0 && l < L, "shard: tile layer out of range");
+        OSP_DCHECK(m.t >= 0 && m.t < g.NT, "shard: tile id out of range");
+        OSP_DCHECK(m.s < m.e && m.e - m.s <= static_cast<uint64_t>(T), "shard: tile range");
         m.staged = xa.vec && NS > 0 && (m.s % 4 == 0) && ((m.e - m.s) % 4 == 0);
     };
 
@@ -455,6 +458,8 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             }
             const bool local_rows = kind == XI_L || (kind == XI_B && m.ics && xa.mode == XM_SINGLE);
             const int nrows = kind == XI_A ? N + 1 : kind == XI_L ? NL + 1 : (local_rows ? 2 + NL : 2);
+            OSP_DCHECK(!m.staged || nrows <= xa.slot_rows, "shard: item rows exceed the ring slot");
+            OSP_DCHECK(u >= 0 && u < (kind == XI_L ? V : U), "shard: sequence position out of range");
             const unsigned bytes = static_cast<unsigned>((m.e - m.s) * 4);
             if (lane == 0) {
                 meta[s] = m;
@@ -712,8 +717,10 @@ __global__ void __launch_bounds__(256) k_shard_peer_apply(GroupView g, AggParams
     const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
     for (int k = gw; k < n_peer; k += nw) {
         const int u = U0 + (k < lo ? k : k + (hi - lo));
+        OSP_DCHECK(u >= U0 && u < U0 + U && (u < U0 + lo || u >= U0 + hi), "peer apply: position");
         int l, kk;
         xseq_lookup(xp, XL ? xl : nullptr, nx, u, l, kk);
+        OSP_DCHECK(l >= 0 && l < L && kk >= 0, "peer apply: tile lookup");
         const uint64_t b = t_off[l] + static_cast<uint64_t>(kk) * g.T;
         const uint64_t e = min(b + static_cast<uint64_t>(g.T), t_off[l] + t_cnt[l]);
         const bool carry = carry_mode && t_flag[l];

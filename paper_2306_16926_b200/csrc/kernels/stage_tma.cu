@@ -411,6 +411,11 @@ __global__ void __launch_bounds__((CW + 1) * 32) k_stage_tma(GroupView g, AggPar
                 m.s = lo + static_cast<uint64_t>(k) * T;
                 m.e = min(m.s + static_cast<uint64_t>(T), lo + tab.cnt[l]);
                 const uint64_t n = m.e - m.s;
+                OSP_DCHECK(l >= 0 && l < tab.L, "stage tile layer out of range");
+                OSP_DCHECK(m.t >= 0 && m.t < g.NT, "stage tile id out of range");
+                OSP_DCHECK(m.s < m.e && m.e <= tab.off[tab.L - 1] + tab.cnt[tab.L - 1],
+                           "stage tile range outside the partition");
+                OSP_DCHECK(n <= static_cast<uint64_t>(T), "stage tile longer than the ring slot");
                 m.staged = (m.s % 4 == 0) && (n % 4 == 0) &&
                            (STAGE == 3 || ((ldX % 4 == 0) &&
                                            (reinterpret_cast<uintptr_t>(X) % 16 == 0)));

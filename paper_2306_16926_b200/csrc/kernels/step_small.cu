@@ -45,6 +45,7 @@ struct SmallSmem {
     int ptb[kSmallMaxLayers + 1];      // PGP tiles of this kernel per layer (prefix)
     int flag[kSmallMaxLayers];         // current GIB
     double part[kSmallMaxTiles];       // PGP tile partials
+    unsigned char tile_layer[kSmallMaxTiles];  // layer of each PGP tile
     double exact[kSmallMaxLayers];     // exact sequential sums of marked layers
     double lsum[kSmallMaxLayers];      // per-layer tree sums of the tile partials
     uint64_t budget, resolved;
@@ -147,6 +148,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             s.cnt[lane] = cnt;
             s.flag[lane] = fl;
             s.ptb[lane] = incl - nt;
+            for (int t = incl - nt; t < incl && t < kSmallMaxTiles; ++t)
+                s.tile_layer[t] = static_cast<unsigned char>(lane);
         }
         if (lane < L) s.tb[lane] = tb;
         if (lane == L - 1) {
@@ -162,10 +165,15 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     }
     __syncthreads();
     const int n_ptiles = s.ptb[L];
+    OSP_DCHECK(L >= 1 && L <= kSmallMaxLayers && n_ptiles <= kSmallMaxTiles,
+               "small step: layout above the single-launch limits");
 
     // ---- stage 1: one warp per 32-element PGP tile, kBatch tiles in flight
     constexpr int kBatch = 4;
     constexpr int kRows = NS > 0 ? NS : 1;
+    const float* xrow[kRows];  // row bases, computed once
+#pragma unroll
+    for (int w = 0; w < kRows; ++w) xrow[w] = X + static_cast<uint64_t>(w) * ldX;
     float gkeep[kBatch];  // this warp's first batch of G' values, kept for stage 2
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) gkeep[j] = 0.f;
@@ -180,18 +188,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             fe[j] = 0;
             ics[j] = false;
             if (t < n_ptiles) {
-                int l = 0;
-                while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
+                const int l = s.tile_layer[t];
                 const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
                 ok[j] = f < s.off[l] + s.cnt[l];
                 fe[j] = f;
                 ics[j] = s.flag[l] != 0;
+                OSP_DCHECK(!ok[j] || f < s.off[L], "small step: element outside the partition");
             }
             if (ok[j]) {
                 go[j] = g.G[fe[j]];
 #pragma unroll
                 for (int w = 0; w < kRows; ++w)
-                    if (NS > 0) xs[j][w] = X[static_cast<uint64_t>(w) * ldX + fe[j]];
+                    if (NS > 0) xs[j][w] = xrow[w][fe[j]];
             }
         }
 #pragma unroll
@@ -221,8 +229,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             on[j] = false;
             fe[j] = 0;
             if (t < n_ptiles) {
-                int l = 0;
-                while (l + 1 < L && s.ptb[l + 1] <= t) ++l;
+                const int l = s.tile_layer[t];
                 const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
                 on[j] = s.flag[l] != 0 && f < s.off[l] + s.cnt[l];
                 fe[j] = f;
