@@ -534,6 +534,7 @@ osp_status osp_split_for_sync(const osp_partition* part, const uint8_t* ics_flag
     if (e == cudaSuccess) e = al(&v.meta64, 8 * sizeof(uint64_t));
     if (e == cudaSuccess) e = al(&v.chunk_of, L * sizeof(int));
     if (e == cudaSuccess) e = al(&v.gib_bytes, osp_gib_wire_size(L, L));
+    if (e == cudaSuccess && L > kSmemResolveLayers) e = al(&v.rscratch, resolve_scratch_bytes(L));
     v.tile_base = d_tb;
     if (e == cudaSuccess) e = cudaMemcpy(d_tb, tb.data(), (L + 1) * sizeof(int), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(v.flags, f.data(), L, cudaMemcpyHostToDevice);
@@ -804,6 +805,9 @@ osp_status osp_group_create(const osp_partition* part, const osp_group_config* c
     if ((st = dalloc(g, &v.lscore, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.rs_layers, L)) != OSP_OK) return cleanup(st);
     if ((st = dalloc(g, &v.rs_tile_prefix, L + 1)) != OSP_OK) return cleanup(st);
+    if (L > static_cast<uint64_t>(kSmemResolveLayers) &&
+        (st = dalloc(g, &v.rscratch, resolve_scratch_bytes(static_cast<int>(L)))) != OSP_OK)
+        return cleanup(st);
     // resolve sum items: each layer's tiles in chunks of <= kSumChunk
     std::vector<int> items, layer_items(L + 1);
     for (uint64_t l = 0; l < L; ++l) {

@@ -3,8 +3,8 @@
 // (importance.cpp:30-40) -> prefix-rule GIB (importance.cpp:42-59) -> the
 // rank-ordered ICS list, its byte-balanced chunk map (split_for_sync,
 // protocol.cpp:122-166) and the tile lists the next iteration's stage-2
-// kernels walk. One CTA of 1024 threads, one launch; L <= kMaxLayers (shared
-// memory: ~60 B per layer).
+// kernels walk. One CTA of 1024 threads, one launch; ~60 B per layer of
+// shared memory up to kSmemResolveLayers layers, a global scratch buffer above.
 //
 // Bit-exact ranking from a parallel sum (SURVEY.md §7 hard part 1). The
 // reference sums |g*p| sequentially in double; a parallel tree rounds
@@ -46,33 +46,44 @@ struct Smem {
     int* pos;
     int* i1;
     int* i2;
-    double* wtot;  // [4 * kWarps] scan scratch (8-byte slots)
+    double* wtot;  // [4 * kWarps] scan scratch (8-byte slots), always shared memory
     uint64_t* cnt; // [L] layer element counts (staged from global)
     int* tb;       // [L+1] tile_base (staged from global)
-    int* flag;     // [8]
+    int* flag;     // [8], always shared memory
 };
 
-__device__ Smem carve(char* base, int L) {
+// Per-layer arrays of the single-CTA phases: dynamic shared memory up to
+// kSmemResolveLayers layers, above that a global scratch buffer owned by the
+// group (g.rscratch) — one CTA reads it, so block barriers order it as well.
+// The scan scratch and the flags stay in shared memory either way (every block
+// of k_resolve's first phase uses them).
+__device__ Smem carve(char* base, int L, double* wtot, int* flag) {
     Smem s;
     s.key = reinterpret_cast<double*>(base);
     s.rad = s.key + L;
     s.a1 = s.rad + L;
     s.a2 = s.a1 + L;
-    s.wtot = s.a2 + L;
-    s.cnt = reinterpret_cast<uint64_t*>(s.wtot + 4 * kWarps);
+    s.cnt = reinterpret_cast<uint64_t*>(s.a2 + L);
     s.sorted = reinterpret_cast<int*>(s.cnt + L);
     s.pos = s.sorted + L;
     s.i1 = s.pos + L;
     s.i2 = s.i1 + L;
     s.tb = s.i2 + L;
-    s.flag = s.tb + L + 1;
+    s.wtot = wtot;
+    s.flag = flag;
     return s;
 }
 
-size_t smem_bytes(int L) {
-    return static_cast<size_t>(L) * (5 * sizeof(double) + 5 * sizeof(int)) + sizeof(int) +
-           4 * kWarps * sizeof(double) + 8 * sizeof(int);
+}  // namespace
+
+size_t resolve_scratch_bytes(int L) {
+    return static_cast<size_t>(L) * (5 * sizeof(double) + 5 * sizeof(int)) + sizeof(int) + 16;
 }
+
+namespace {
+
+// dynamic shared memory of the single-CTA kernels (0 when the arrays are global)
+size_t smem_bytes(int L) { return L <= kSmemResolveLayers ? resolve_scratch_bytes(L) : 0; }
 
 // One coalesced load of the layer geometry into shared memory; everything the
 // single-CTA phases need per layer is then a shared-memory read.
@@ -369,10 +380,12 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
                                                              const float* __restrict__ X,
                                                              uint64_t ldX) {
     extern __shared__ __align__(16) char smem_raw[];
+    __shared__ double sh_wtot[4 * kWarps];
+    __shared__ int sh_flag[8];
     pdl_wait();
     pdl_trigger();
     const int L = g.L;
-    const Smem s = carve(smem_raw, L);
+    const Smem s = carve(g.rscratch ? g.rscratch : smem_raw, L, sh_wtot, sh_flag);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
     // 0. every block: tree sums of the tile partials per sum item (<= kSumChunk
@@ -508,8 +521,10 @@ __global__ void __launch_bounds__(kResolveThreads) k_resolve(GroupView g, AggPar
 __global__ void __launch_bounds__(kResolveThreads) k_install(GroupView g, const int* order,
                                                              int n_order, uint32_t tag) {
     extern __shared__ __align__(16) char smem_raw[];
+    __shared__ double sh_wtot[4 * kWarps];
+    __shared__ int sh_flag[8];
     const int L = g.L;
-    const Smem s = carve(smem_raw, L);
+    const Smem s = carve(g.rscratch ? g.rscratch : smem_raw, L, sh_wtot, sh_flag);
     stage_geometry(g, s);
     if (threadIdx.x == 0) {
         int k = 0;
@@ -582,9 +597,11 @@ __global__ void k_pgp_exact(const float* __restrict__ P, const float* __restrict
 __global__ void __launch_bounds__(kResolveThreads) k_rank_gib(const double* scores,
                                                               const uint64_t* counts, uint32_t bpe,
                                                               int L, uint64_t budget, int* order,
-                                                              uint8_t* flags) {
+                                                              uint8_t* flags, char* scratch) {
     extern __shared__ __align__(16) char smem_raw[];
-    const Smem s = carve(smem_raw, L);
+    __shared__ double sh_wtot[4 * kWarps];
+    __shared__ int sh_flag[8];
+    const Smem s = carve(scratch ? scratch : smem_raw, L, sh_wtot, sh_flag);
     for (int l = threadIdx.x; l < L; l += blockDim.x) s.key[l] = scores[l];
     __syncthreads();
     rank_layers_block(s, L);
@@ -661,10 +678,19 @@ cudaError_t launch_rank_gib(const double* scores, const uint64_t* counts, uint32
                             uint64_t budget, int* order, uint8_t* flags, cudaStream_t st) {
     if (L < 1) return cudaSuccess;
     const size_t sm = smem_bytes(L);
+    char* scratch = nullptr;
+    if (sm == 0) {  // above kSmemResolveLayers: the per-layer arrays in global memory
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), resolve_scratch_bytes(L), st);
+        if (e != cudaSuccess) return e;
+    }
     cudaError_t e = set_smem(reinterpret_cast<const void*>(k_rank_gib), sm);
-    if (e != cudaSuccess) return e;
-    k_rank_gib<<<1, kResolveThreads, sm, st>>>(scores, counts, bpe, L, budget, order, flags);
-    return cudaGetLastError();
+    if (e == cudaSuccess) {
+        k_rank_gib<<<1, kResolveThreads, sm, st>>>(scores, counts, bpe, L, budget, order, flags,
+                                                   scratch);
+        e = cudaGetLastError();
+    }
+    if (scratch) cudaFreeAsync(scratch, st);
+    return e;
 }
 
 }  // namespace osp

@@ -102,6 +102,9 @@ struct GroupView {
     int n_sum_items;
     const int* layer_items;      // [L+1] first item of each layer
     double* item_sums;           // [n_sum_items]
+    // the single-CTA resolve's per-layer arrays when L > kSmemResolveLayers
+    // (global memory; null: dynamic shared memory)
+    char* rscratch;
 };
 constexpr int kSumChunk = 4096;  // tiles per resolve sum item
 
@@ -126,7 +129,11 @@ constexpr int kSnapHead = 4;
 __host__ __device__ inline int snap_ints(int L, int n_chunks) { return kSnapHead + n_chunks + 1 + 2 * L + 1; }
 
 constexpr int kHist = 4096;
-constexpr int kMaxLayers = 3072;  // single-CTA resolve (resolve.cu: ~60 B shared memory per layer)
+// Layers per partition. The single-CTA resolve keeps ~60 B per layer in shared
+// memory up to kSmemResolveLayers layers and in a global scratch buffer above.
+constexpr int kMaxLayers = 65536;
+constexpr int kSmemResolveLayers = 3072;
+size_t resolve_scratch_bytes(int L);
 constexpr int kStageThreads = 256;
 constexpr uint32_t kDefaultTile = 512;  // elements per warp tile (sweep: profiles/)
 constexpr uint32_t kDefaultTmaTile = 1024;  // TMA-staged kernels (tools/tma_sweep.sh)

@@ -32,6 +32,18 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
 
 
+def test_checked_build_exports_the_same_symbols():
+    """The bounds-checked build (make checked; OSP_LIB_VARIANT=checked) is a
+    drop-in for the product library."""
+    from paper_2306_16926_b200 import _capi
+    path = os.path.join(os.path.dirname(_capi.LIB_PATH), "libosp_b200_checked.so")
+    if not os.path.exists(path):
+        pytest.skip("checked build not built (make checked)")
+    lib = ctypes.CDLL(path)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
 def test_binding_covers_header():
     from paper_2306_16926_b200 import _capi
     assert set(declared_functions()) == set(_capi.EXPORTED)

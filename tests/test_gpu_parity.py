@@ -316,18 +316,37 @@ def test_group_fused_sgd(osp):
     oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 4, 3, seed=19, sgd_lr=0.05, tma=False)
 
 
-@pytest.mark.parametrize("L", [1, 2, 33, 2500, 3072])
+@pytest.mark.parametrize("L", [1, 2, 33, 2500, 3072, 3073, 20000])
 def test_group_many_layers(osp, L):
-    """Layer counts from 1 to the kMaxLayers cap: bitonic rank padding, stage
-    kernels with global layer tables (L > 2048), resolve shared memory at the cap."""
+    """Layer counts from 1 up: bitonic rank padding, stage kernels with global
+    layer tables (L > 2048), the resolve's per-layer arrays in shared memory up to
+    3072 layers and in a global scratch buffer above (3073, 20000)."""
     rng = np.random.default_rng(L)
     counts = rng.integers(1, 400, L)
     oracle_vs_group(osp, counts, 4, [0.25] * 4, 0.5, 3, 2, seed=L)
 
 
+def test_many_layers_free_functions(osp):
+    """rank_and_gib and split_for_sync above the shared-memory layer count."""
+    rng = np.random.default_rng(9)
+    L = 7000
+    counts = rng.integers(1, 50, L).astype(np.uint64)
+    scores = rng.random(L)
+    scores[100:110] = scores[5]  # ties
+    part = osp.Partition(counts)
+    budget = int(counts.sum()) * 2
+    order, flags = osp.rank_and_gib(part, scores, budget)
+    assert np.array_equal(order, oracle.rank(scores))
+    assert np.array_equal(flags, oracle.build_gib(scores, counts, 4, budget))
+    ics_order = order[: int(flags.sum())]
+    rs, chunk_of, used = osp.split_for_sync(part, flags, ics_order, 5)
+    rs_o, chunk_o, used_o = oracle.split(counts, 4, flags, ics_order, 5)
+    assert np.array_equal(rs, rs_o) and np.array_equal(chunk_of, chunk_o) and used == used_o
+
+
 def test_group_too_many_layers(osp):
     with pytest.raises(osp.InvalidArgument):
-        osp.OspGroup(osp.Partition([1] * 3073), 2)
+        osp.OspGroup(osp.Partition([1] * 65537), 2)
 
 
 def test_group_budget_edges(osp):
