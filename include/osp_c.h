@@ -25,8 +25,9 @@ extern "C" {
 #endif
 
 #define OSP_ABI_VERSION 2
-/* Workers per aggregation call / group (kernel-parameter weights table). */
-#define OSP_MAX_WORKERS 64
+/* Workers per aggregation call / group (kernel-parameter weights table; the
+ * kernels' parameter blocks use the > 4 KB parameter space of CUDA 12.1+). */
+#define OSP_MAX_WORKERS 256
 
 /* Status codes, 1:1 with the pslab::Error hierarchy (errors.hpp:11-69). */
 typedef enum osp_status {

@@ -755,10 +755,10 @@ def test_group_errors(osp):
         part.layer(7)
 
 
-@pytest.mark.parametrize("n", [9, 16, 64])
+@pytest.mark.parametrize("n", [9, 16, 64, 200])
 def test_group_many_workers_vs_oracle(osp, n):
     """N > 8 runs the register family with a runtime worker count (dispatch_n's
-    default case) up to OSP_MAX_WORKERS = 64; fixed-order fp64 aggregation over
+    default case) up to OSP_MAX_WORKERS = 256; fixed-order fp64 aggregation over
     all N rows must stay bit-exact with the oracle (protocol.cpp:14-27)."""
     rng = np.random.default_rng(70 + n)
     counts = [int(c) for c in rng.integers(1, 3000, 13)] + [4096]
@@ -770,7 +770,7 @@ def test_group_many_workers_vs_oracle(osp, n):
 def test_group_more_than_max_workers_refused(osp):
     part = osp.Partition([100, 200])
     with pytest.raises(osp.InvalidArgument, match="OSP_MAX_WORKERS"):
-        osp.OspGroup(part, 65, [1.0 / 65] * 65)
+        osp.OspGroup(part, 257, [1.0 / 257] * 257)
 
 
 # ---- the single-launch step of launch-bound layouts (kernels/step_small.cu) -----
