@@ -24,8 +24,9 @@
 //             list / counter / GIB byte the regular kernels keep, so the group
 //             can continue on either path.
 //
-// Latency is the cost here, not bytes: each warp keeps kBatch tiles' loads in
-// flight; block barriers after the table load, stage 1, stage 2 and the layer sums.
+// Latency is the cost here, not bytes: every warp maps its own tiles from the
+// layer table held in registers and keeps kBatch tiles' loads in flight; block
+// barriers after stage 1, stage 2, the layer sums and the certificate.
 // Results are bit-identical to stage1 + stage2_resolve (tests/test_gpu_parity.py).
 
 #include "common.cuh"
@@ -45,7 +46,6 @@ struct SmallSmem {
     int ptb[kSmallMaxLayers + 1];      // PGP tiles of this kernel per layer (prefix)
     int flag[kSmallMaxLayers];         // current GIB
     double part[kSmallMaxTiles];       // PGP tile partials
-    unsigned char tile_layer[kSmallMaxTiles];  // layer of each PGP tile
     double exact[kSmallMaxLayers];     // exact sequential sums of marked layers
     double lsum[kSmallMaxLayers];      // per-layer tree sums of the tile partials
     uint64_t budget, resolved;
@@ -127,31 +127,33 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     pdl_trigger();
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int L = g.L;
+    // every warp: the layer table in registers (lane = layer) and this kernel's
+    // PGP tile prefix by a warp scan, so each warp maps its own tiles and issues
+    // its loads at once; warp 0 also stages the tables and the resolve's scalars
+    // in shared memory (read after the stage-1 barrier)
+    uint64_t off = 0, cnt = 0;
+    int fl = 0;
+    if (lane < L) {
+        off = g.offsets[lane];
+        cnt = g.counts[lane];
+        fl = g.flags[lane];
+    }
+    const int nt = lane < L ? static_cast<int>((cnt + kSmallTile - 1) / kSmallTile) : 0;
+    const int incl = warp_incl_scan<int>(nt, lane);
+    const int n_ptiles = __shfl_sync(0xffffffffu, incl, L - 1);
     if (warp == 0) {
-        // tables, this kernel's PGP tile prefix (warp scan), the scalars the
-        // resolve needs — all loads issued together
-        uint64_t off = 0, cnt = 0;
-        int fl = 0, tb = 0;
-        if (lane < L) {
-            off = g.offsets[lane];
-            cnt = g.counts[lane];
-            fl = g.flags[lane];
-        }
+        int tb = 0;
         if (lane < L) tb = g.tile_base[lane];
         const int tb_end = g.tile_base[L];  // lane L does not exist when L == 32
         const uint64_t budget = g.meta64[META64_BUDGET], resolved = g.meta64[META64_RESOLVED];
-        const int nt = lane < L ? static_cast<int>((cnt + kSmallTile - 1) / kSmallTile) : 0;
-        const int incl = warp_incl_scan<int>(nt, lane);
         const uint64_t end = warp_incl_scan<unsigned long long>(cnt, lane);
         if (lane < L) {
             s.off[lane] = off;
             s.cnt[lane] = cnt;
             s.flag[lane] = fl;
             s.ptb[lane] = incl - nt;
-            for (int t = incl - nt; t < incl && t < kSmallMaxTiles; ++t)
-                s.tile_layer[t] = static_cast<unsigned char>(lane);
+            s.tb[lane] = tb;
         }
-        if (lane < L) s.tb[lane] = tb;
         if (lane == L - 1) {
             s.ptb[L] = incl;
             s.off[L] = end;
@@ -163,10 +165,18 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             s.n_marked = 0;
         }
     }
-    __syncthreads();
-    const int n_ptiles = s.ptb[L];
     OSP_DCHECK(L >= 1 && L <= kSmallMaxLayers && n_ptiles <= kSmallMaxTiles,
                "small step: layout above the single-launch limits");
+    // tile t -> (first element of the lane's element, layer end, deferred?)
+    auto locate = [&](int t, uint64_t& f, uint64_t& end, bool& ics) {
+        const int l = __popc(__ballot_sync(0xffffffffu, lane < L && incl <= t));
+        const uint64_t lo = __shfl_sync(0xffffffffu, off, l);
+        const uint64_t ln = __shfl_sync(0xffffffffu, cnt, l);
+        const int first = __shfl_sync(0xffffffffu, incl - nt, l);
+        ics = __shfl_sync(0xffffffffu, fl, l) != 0;
+        f = lo + static_cast<uint64_t>(t - first) * kSmallTile + lane;
+        end = lo + ln;
+    };
 
     // ---- stage 1: one warp per 32-element PGP tile, kBatch tiles in flight
     constexpr int kBatch = 4;
@@ -187,13 +197,13 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             ok[j] = false;
             fe[j] = 0;
             ics[j] = false;
-            if (t < n_ptiles) {
-                const int l = s.tile_layer[t];
-                const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
-                ok[j] = f < s.off[l] + s.cnt[l];
+            if (t < n_ptiles) {  // warp-uniform
+                uint64_t f, e;
+                bool dfr;
+                locate(t, f, e, dfr);
+                ok[j] = f < e;
                 fe[j] = f;
-                ics[j] = s.flag[l] != 0;
-                OSP_DCHECK(!ok[j] || f < s.off[L], "small step: element outside the partition");
+                ics[j] = dfr;
             }
             if (ok[j]) {
                 go[j] = g.G[fe[j]];
@@ -228,10 +238,11 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
             const int t = t0 + j * kSmallWarps;
             on[j] = false;
             fe[j] = 0;
-            if (t < n_ptiles) {
-                const int l = s.tile_layer[t];
-                const uint64_t f = s.off[l] + static_cast<uint64_t>(t - s.ptb[l]) * kSmallTile + lane;
-                on[j] = s.flag[l] != 0 && f < s.off[l] + s.cnt[l];
+            if (t < n_ptiles) {  // warp-uniform
+                uint64_t f, e;
+                bool dfr;
+                locate(t, f, e, dfr);
+                on[j] = dfr && f < e;
                 fe[j] = f;
             }
             cv[j] = t0 == warp ? gkeep[j] : (on[j] ? g.C[fe[j]] : 0.f);
