@@ -409,12 +409,9 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
         if (g.hist) g.hist[tag % kHist] = tot;
         g.meta64[META64_RESOLVED] = tag;
     }
-    __syncwarp();
-    if (lane == 0) {
-        __threadfence();
-        atomicExch(reinterpret_cast<unsigned long long*>(g.meta64 + META64_RESOLVE_DONE),
-                   static_cast<unsigned long long>(tag));
-    }
+    // the resolve epoch the regular path's overlapped stage 2 joins on; nothing
+    // runs beside this kernel, so kernel completion publishes it (no fence)
+    if (lane == 0) g.meta64[META64_RESOLVE_DONE] = tag;
 }
 
 }  // namespace
