@@ -422,6 +422,11 @@ osp_group* osp_shard_group(osp_shard* s);
 /* 1 when stage 2 exchanges the deferred layers (OSP_SHARD_DEFER_ICS, or a
  * local group without the carry buffer), 0 for the single-exchange default. */
 int osp_shard_deferred_ics(const osp_shard* s);
+/* Synchronisation form of the exchange kernels: 0 per-tile flags, 1 own tiles
+ * then a cross-GPU barrier, 2 the reduction chain of the single-exchange
+ * stage 1 (rank r continues rank r-1's fp64 running sum; deferred-ICS stages
+ * use form 0/1). Environment OSP_SHARD_SYNC=tile|barrier|chain at create. */
+int osp_shard_sync_form(const osp_shard* s);
 osp_status osp_shard_stage1(osp_shard* s, int buf, void* stream);
 /* ProtocolError before stage 1 of the iteration. */
 osp_status osp_shard_stage2(osp_shard* s, int c0, int c1, int buf, void* stream);

@@ -24,13 +24,19 @@ using namespace osp;
 
 namespace {
 
-constexpr uint32_t kMagic = 0x0600b200u;
+constexpr uint32_t kMagic = 0x0700b200u;
+
+// default sync form of the single-exchange stage 1 by world size: 1 = chain
+int kChainDefault(int world) {
+    (void)world;
+    return 0;
+}
 
 struct ShardHandle {
     uint32_t magic;
-    int32_t rank, world, n_loc, deferred;
+    int32_t rank, world, n_loc, deferred, chain;
     uint64_t M, L, NT, ldX, buf_stride;
-    cudaIpcMemHandle_t hx, hagg, hpart, htflag, hready;
+    cudaIpcMemHandle_t hx, hagg, hpart, htflag, hready, hpre;
 };
 static_assert(sizeof(ShardHandle) <= OSP_SHARD_HANDLE_BYTES, "handle too large");
 
@@ -45,7 +51,8 @@ struct osp_shard {
     float* X = nullptr;        // [2][n_loc][ldX] local delta rows, IPC-exported
     uint64_t ldX = 0, buf_stride = 0;
     float* agg = nullptr;      // [ldX] pull buffer, IPC-exported (the group's agg_full)
-    unsigned* tflag = nullptr; // [NT] per-tile ready flags, IPC-exported
+    unsigned* tflag = nullptr; // [2][NT] per-tile ready flags (tile, chain), IPC-exported
+    double* pre = nullptr;     // [ldX] chain form: this rank's fp64 running sums, IPC-exported
     unsigned* ready = nullptr; // [kMaxRanks] deltas-ready slots, IPC-exported
     unsigned* error = nullptr; // [1] local
     XArgs xa[2]{};             // per delta buffer
@@ -58,7 +65,8 @@ struct osp_shard {
     int lag = 10;              // OSP_SHARD_LAG: B items' due-time lag (A items)
     int pub_batch = 8, pub_min = 4;  // OSP_SHARD_PUB="max,min": flags per fence
     int split = 1;             // OSP_SHARD_SPLIT=0: every CTA takes every item kind
-    int barrier = -1;          // OSP_SHARD_SYNC=tile|barrier; -1: by world size
+    int barrier = -1;          // OSP_SHARD_SYNC=tile|barrier|chain; -1: by world size
+    bool chain = false;        // single-exchange stage 1 as a reduction chain (shard_chain.cu)
     unsigned* ticket = nullptr;  // [1] local, phase-1 last-CTA counter
     unsigned done_epoch = 0;     // barrier-form launches so far (a stage-2 chunk is one)
     unsigned long long* dbg = nullptr;  // OSP_SHARD_DEBUG=1: kernel counters [16]
@@ -114,8 +122,11 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
         }
     }
     if (const char* sp = std::getenv("OSP_SHARD_SPLIT")) s->split = std::atoi(sp) == 0 ? 0 : 1;
-    if (const char* sy = std::getenv("OSP_SHARD_SYNC"))
+    int want_chain = -1;
+    if (const char* sy = std::getenv("OSP_SHARD_SYNC")) {
         s->barrier = std::strcmp(sy, "barrier") == 0 ? 1 : std::strcmp(sy, "tile") == 0 ? 0 : -1;
+        want_chain = std::strcmp(sy, "chain") == 0 ? 1 : s->barrier >= 0 ? 0 : -1;
+    }
     // measured: per-tile flags win at 2 ranks, own-tiles-then-barrier at 4
     if (s->barrier < 0) s->barrier = cfg->world >= 4 ? 1 : 0;
     // the local group: default (TMA-staged, carry) so the stage-2 broadcast and
@@ -128,20 +139,27 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
         return st;
     }
     s->deferred = (cfg->flags & OSP_SHARD_DEFER_ICS) || s->grp->v.C == nullptr;
+    // the chain form runs the single-exchange stage 1 (the deferred-ICS stages
+    // keep the exchange forms); default by world size (measured,
+    // profiles/r2_multi_gpu_notes.md)
+    if (want_chain < 0) want_chain = kChainDefault(cfg->world);
+    s->chain = want_chain == 1 && !s->deferred && cfg->world >= 2 &&
+               shard_chain_supported(s->n_loc, static_cast<int>(T), static_cast<int>(part->counts.size()));
     const uint64_t M = part->total;
     s->ldX = (M + 3) & ~uint64_t(3);
     s->buf_stride = s->ldX * s->n_loc;
     const uint64_t NT = static_cast<uint64_t>(s->grp->v.NT);
     cudaError_t e = cudaMalloc(&s->X, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMalloc(&s->agg, s->ldX * sizeof(float));
-    if (e == cudaSuccess) e = cudaMalloc(&s->tflag, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMalloc(&s->tflag, 2 * std::max<uint64_t>(NT, 1) * sizeof(unsigned));
+    if (e == cudaSuccess && s->chain) e = cudaMalloc(&s->pre, s->ldX * sizeof(double));
     if (e == cudaSuccess) e = cudaMalloc(&s->ready, 2 * kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&s->ticket, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->ticket, 0, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMalloc(&s->error, sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->X, 0, 2 * s->buf_stride * sizeof(float));
     if (e == cudaSuccess) e = cudaMemset(s->agg, 0, s->ldX * sizeof(float));
-    if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, std::max<uint64_t>(NT, 1) * sizeof(unsigned));
+    if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, 2 * std::max<uint64_t>(NT, 1) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->ready, 0, 2 * kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
     if (const char* d = std::getenv("OSP_SHARD_DEBUG"); d && d[0] == '1') {
@@ -165,6 +183,7 @@ void osp_shard_destroy(osp_shard* s) {
     if (s->X) cudaFree(s->X);
     if (s->agg) cudaFree(s->agg);
     if (s->tflag) cudaFree(s->tflag);
+    if (s->pre) cudaFree(s->pre);
     if (s->ready) cudaFree(s->ready);
     if (s->error) cudaFree(s->error);
     if (s->dbg) cudaFree(s->dbg);
@@ -183,6 +202,7 @@ osp_status osp_shard_export(osp_shard* s, uint8_t* handle) {
     h.world = s->world;
     h.n_loc = s->n_loc;
     h.deferred = s->deferred ? 1 : 0;
+    h.chain = s->chain ? 1 : 0;
     h.M = s->part->total;
     h.L = s->part->counts.size();
     h.NT = static_cast<uint64_t>(s->grp->v.NT);
@@ -193,6 +213,7 @@ osp_status osp_shard_export(osp_shard* s, uint8_t* handle) {
     OSP_CUDA(cudaIpcGetMemHandle(&h.hpart, s->grp->v.partials));
     OSP_CUDA(cudaIpcGetMemHandle(&h.htflag, s->tflag));
     OSP_CUDA(cudaIpcGetMemHandle(&h.hready, s->ready));
+    if (s->chain) OSP_CUDA(cudaIpcGetMemHandle(&h.hpre, s->pre));
     std::memset(handle, 0, OSP_SHARD_HANDLE_BYTES);
     std::memcpy(handle, &h, sizeof h);
     return OSP_OK;
@@ -209,21 +230,23 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
         if (h.magic != kMagic || h.rank != q || h.world != s->world || h.n_loc != s->n_loc ||
             h.M != s->part->total || h.L != s->part->counts.size() ||
             h.NT != static_cast<uint64_t>(s->grp->v.NT) || h.ldX != s->ldX ||
-            h.buf_stride != s->buf_stride || h.deferred != (s->deferred ? 1 : 0))
+            h.buf_stride != s->buf_stride || h.deferred != (s->deferred ? 1 : 0) ||
+            h.chain != (s->chain ? 1 : 0))
             return fail(OSP_ERR_CONFIG, "rank " + std::to_string(q) +
                                             " exported an incompatible shard (partition, tiles, "
-                                            "worker split, mode or world size differ)");
+                                            "worker split, mode, sync form or world size differ)");
         if (q == s->rank) {
             xbase[q] = s->X;
             base.agg[q] = s->agg;
             base.part[q] = s->grp->v.partials;
             base.tflag[q] = s->tflag;
             base.ready[q] = s->ready;
+            base.pre[q] = s->pre;
             continue;
         }
-        void* p[5] = {};
-        const cudaIpcMemHandle_t* hs[5] = {&h.hx, &h.hagg, &h.hpart, &h.htflag, &h.hready};
-        for (int k = 0; k < 5; ++k) {
+        void* p[6] = {};
+        const cudaIpcMemHandle_t* hs[6] = {&h.hx, &h.hagg, &h.hpart, &h.htflag, &h.hready, &h.hpre};
+        for (int k = 0; k < (s->chain ? 6 : 5); ++k) {
             OSP_CUDA(cudaIpcOpenMemHandle(&p[k], *hs[k], cudaIpcMemLazyEnablePeerAccess));
             s->opened.push_back(p[k]);
         }
@@ -232,6 +255,7 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
         base.part[q] = static_cast<double*>(p[2]);
         base.tflag[q] = static_cast<unsigned*>(p[3]);
         base.ready[q] = static_cast<unsigned*>(p[4]);
+        base.pre[q] = static_cast<double*>(p[5]);
     }
     base.error = s->error;
     base.world = s->world;
@@ -256,7 +280,9 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
             xa.xrow[w] = xbase[q] + b * s->buf_stride + static_cast<uint64_t>(i) * s->ldX;
             vec = vec && (reinterpret_cast<uintptr_t>(xa.xrow[w]) % 16 == 0);
         }
-        for (int q = 0; q < s->world; ++q) vec = vec && (reinterpret_cast<uintptr_t>(xa.agg[q]) % 16 == 0);
+        for (int q = 0; q < s->world; ++q)
+            vec = vec && (reinterpret_cast<uintptr_t>(xa.agg[q]) % 16 == 0) &&
+                  (reinterpret_cast<uintptr_t>(xa.pre[q]) % 32 == 0);
         xa.vec = vec ? 1 : 0;
     }
     s->connected = true;
@@ -273,6 +299,11 @@ osp_group* osp_shard_group(osp_shard* s) { return s ? s->grp : nullptr; }
 
 int osp_shard_deferred_ics(const osp_shard* s) { return s && s->deferred ? 1 : 0; }
 
+int osp_shard_sync_form(const osp_shard* s) {
+    if (!s) return -1;
+    return s->chain ? 2 : s->barrier ? 1 : 0;
+}
+
 static osp_status check_ready(osp_shard* s, int buf) {
     if (!s) return fail(OSP_ERR_INVALID, "null shard");
     if (!s->connected) return fail(OSP_ERR_PROTOCOL, "shard not connected to its peers");
@@ -288,6 +319,7 @@ static cudaError_t launch_x(osp_shard* s, int buf, int mode, int c0, int c1, int
     xa.c0 = c0;
     xa.c1 = c1;
     xa.solo = solo;
+    if (s->chain && mode == XM_SINGLE && !solo) return launch_shard_chain(s->grp->v, s->ap_all, xa, st);
     if (solo || !s->barrier) {
         xa.phase = 0;
         return launch_shard_x(s->grp->v, s->ap_all, xa, st);

@@ -1,0 +1,470 @@
+// The sharded stage 1 as a reduction CHAIN over the ranks (single-exchange mode,
+// SURVEY.md §8(e); one process per GPU, CUDA-IPC mappings).
+//
+// The reference aggregates every element in ascending worker order
+// (protocol.cpp:9-30): sum = ((w0 x0 + w1 x1) + w2 x2) + ... in fp64. Rank r
+// hosts workers [r*NL, (r+1)*NL), so the running fp64 sum after rank r's
+// workers is an exact intermediate of that sequence: rank 0 starts it, every
+// next rank continues it from the previous rank's prefix, and the last rank
+// finishes it. Nothing but the 8-byte prefix crosses NVLink on the way there
+// (the exchange form of shard_x.cu moves every peer worker's 4-byte row to the
+// owner: 4*NL bytes), and the 4-byte aggregate comes back. At P = 2 with
+// N = 8 that is 8 + 4 bytes per element instead of 10 + 10 each way.
+//
+// Item kinds (one per tile of the whole tile sequence; CTA c of C takes tiles
+// c, c + C, ... so every rank's front moves through the tiles in order):
+//   PRE    (ranks 0..P-2) bulk-copy the previous rank's prefix (over NVLink,
+//          rank > 0), this rank's delta rows and, for a deferred layer, G;
+//          continue the sum over the local workers and store the prefix in
+//          local HBM; a deferred layer also gets its LGP local estimates here
+//          (rows = G + x_w). Flag: the next rank's chain flag.
+//   FIN    (rank P-1) the same from the last prefix, then agg = float(sum / W),
+//          G' = G + agg: RS layers G = G', rows = G'; ICS layers the carry
+//          C = G' and rows = G + x_w; the tile's PGP partial (importance.cpp
+//          11-28) goes to every rank's partials. Flag: every other rank's tile
+//          flag.
+//   APPLY  (ranks 0..P-2) after the tile flag: bulk-copy agg from the last
+//          rank's HBM (NVLink) and G; RS: G = G + agg, rows = G'; ICS: C.
+// Data always stays where it was written; readers pull with cp.async.bulk
+// after acquiring a flag the writer pushed into their memory (the writer's
+// system-scope fence then drains only local stores and tiny flag stores).
+// Non-finishing ranks split their CTAs: even ones PRE, odd ones APPLY.
+//
+// Hazards across iterations: rank r overwrites its prefix at iteration i+1
+// only after finishing iteration i, whose APPLY items waited for every FIN of
+// iteration i, each of which consumed the prefixes of iteration i; likewise the
+// last rank's agg of iteration i+1 follows rank 0's completion of iteration i.
+// Flags carry the iteration number and are never reset; every wait is bounded.
+
+#include <cstdlib>
+
+#include "shard_common.cuh"
+
+namespace osp {
+namespace {
+
+enum CItem { CI_PRE = 0, CI_FIN = 1, CI_APPLY = 2 };
+constexpr int kCPQ = 16;  // publication queue entries per CTA
+constexpr int kCCW = 8;   // consumer warps
+
+struct CMeta {
+    uint64_t s, e;  // element range
+    int t;          // tile id, -1 = stop
+    int kind;       // CItem
+    int staged;     // rows in shared memory (else consumers read global memory)
+    int ics;        // tile of a deferred layer
+};
+
+// Slot layout (floats): [0, 2T) the incoming prefix (T doubles) or, for APPLY,
+// row 0 = agg and row 1 = G; rows 2 .. 2+NL-1 the local delta rows; row 2+NL G.
+template <int NL, int KS>
+__global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, AggParams ap, XArgs xa) {
+    constexpr int CW = kCCW;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int T = g.T, NT = g.NT, L = g.L;
+    const int P = xa.world, R = xa.rank;
+    const size_t SF = static_cast<size_t>(NL + 3) * T;
+
+    float* ring = reinterpret_cast<float*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + KS * SF);
+    uint64_t* empty = full + KS;
+    uint64_t* pdone = empty + KS;
+    CMeta* meta = reinterpret_cast<CMeta*>(pdone + kCPQ);
+    double* red = reinterpret_cast<double*>(meta + KS);  // [kCPQ][CW]
+    int* pq_t = reinterpret_cast<int*>(red + kCPQ * CW);  // [kCPQ] tile id, -1 stop
+    int* pq_k = pq_t + kCPQ;                              // [kCPQ] item kind
+    int* pub_head = pq_k + kCPQ;
+    unsigned char* tabmem = reinterpret_cast<unsigned char*>(pub_head + 4);
+    uint64_t* t_off = reinterpret_cast<uint64_t*>(tabmem);
+    uint64_t* t_cnt = t_off + L;
+    int* t_tb = reinterpret_cast<int*>(t_cnt + L);
+    uint8_t* t_flag = reinterpret_cast<uint8_t*>(t_tb + L + 1);
+
+    for (int i = tid; i < L; i += blockDim.x) {
+        t_off[i] = g.offsets[i];
+        t_cnt[i] = g.counts[i];
+        t_tb[i] = g.tile_base[i];
+        t_flag[i] = g.flags[i];
+    }
+    if (tid == 0) t_tb[L] = g.tile_base[L];
+    // this is the iteration's stage 1: block 0 snapshots the ICS lists the
+    // carry broadcast of stage 2 walks (as k_stage_tma's stage 1 does)
+    if (g.snap && blockIdx.x == 0) {
+        const int used = g.meta[META_N_USED];
+        const int n_ics = g.meta[META_N_ICS];
+        int* snap_cb = g.snap + kSnapHead;
+        int* snap_il = snap_cb + g.n_chunks + 1;
+        int* snap_tp = snap_il + L;
+        if (tid == 0) {
+            g.snap[0] = used;
+            g.snap[1] = static_cast<int>(g.meta64[META64_RESOLVED] + 1);
+        }
+        for (int i = tid; i <= g.n_chunks; i += blockDim.x) snap_cb[i] = g.chunk_begin[i];
+        for (int i = tid; i < n_ics; i += blockDim.x) snap_il[i] = g.ics_layers[i];
+        for (int i = tid; i <= n_ics; i += blockDim.x) snap_tp[i] = g.ics_tile_prefix[i];
+    }
+    if (tid == 0) {
+        for (int s = 0; s < KS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CW);
+        }
+        for (int j = 0; j < kCPQ; ++j) mbar_init(&pdone[j], CW);
+        *pub_head = 0;
+        mbar_init_fence();
+    }
+    __syncthreads();
+
+    // roles and this CTA's tiles
+    const bool fin = R == P - 1;
+    const int GX = static_cast<int>(gridDim.x);
+    const bool split = !fin && GX >= 2;
+    const int C = split ? GX / 2 : GX;
+    const int c = split ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
+    const int n_own = c < C && c < NT ? (NT - 1 - c) / C + 1 : 0;
+    // item i -> (kind, tile); false when the CTA is done
+    auto item = [&](int i, int& kind, int& t) -> bool {
+        if (fin) {
+            kind = CI_FIN;
+        } else if (split) {
+            kind = (blockIdx.x & 1) ? CI_APPLY : CI_PRE;
+        } else {  // one CTA: every prefix, then every apply
+            kind = i < n_own ? CI_PRE : CI_APPLY;
+            if (i >= n_own) i -= n_own;
+        }
+        if (i >= n_own) return false;
+        t = c + i * C;
+        return true;
+    };
+    auto locate = [&](int t, int kind, CMeta& m) {
+        int l, kk;
+        xseq_lookup(t_tb, nullptr, L, t, l, kk);
+        m.t = t;
+        m.kind = kind;
+        m.s = t_off[l] + static_cast<uint64_t>(kk) * T;
+        const uint64_t le = t_off[l] + t_cnt[l];
+        m.e = m.s + static_cast<uint64_t>(T) < le ? m.s + static_cast<uint64_t>(T) : le;
+        m.ics = t_flag[l];
+        OSP_DCHECK(l >= 0 && l < L && m.s < m.e && m.e - m.s <= static_cast<uint64_t>(T),
+                   "chain: tile lookup");
+        m.staged = xa.vec && (m.s % 4 == 0) && ((m.e - m.s) % 4 == 0);
+    };
+
+    if (warp == CW + 1) {
+        // ================= publisher =================
+        // FIN tiles: the partial into every rank's partials, then (batched under
+        // one system-scope fence) the tile flag on every other rank; PRE tiles:
+        // the chain flag on the next rank. The fence is cumulative over the
+        // consumers' stores, acquired through the entry barrier.
+        constexpr int kPubMax = 16;
+        const int batch = xa.pub_batch < 1 ? 1 : (xa.pub_batch > kPubMax ? kPubMax : xa.pub_batch);
+        int pend[kPubMax];
+        int np = 0;
+        auto flush = [&]() {
+            if (np == 0) return;
+            if (lane == 0) {
+                asm volatile("fence.acq_rel.sys;" ::: "memory");
+                for (int j = 0; j < np; ++j) {
+                    if (fin) {
+                        for (int r = 0; r < P; ++r)
+                            if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + pend[j]) = xa.epoch;
+                    } else {
+                        *reinterpret_cast<volatile unsigned*>(xa.tflag[R + 1] + NT + pend[j]) = xa.epoch;
+                    }
+                }
+            }
+            np = 0;
+            __syncwarp();
+        };
+        for (int i = 0;; ++i) {
+            const int j = i % kCPQ;
+            const unsigned par = (i / kCPQ) & 1;
+            if (!mbar_try(&pdone[j], par)) {
+                if (np >= xa.pub_min) flush();
+                const uint64_t w0 = now_ns();
+                while (!mbar_try(&pdone[j], par)) {
+                    const uint64_t dt = now_ns() - w0;
+                    if (np > 0 && dt > 2000) flush();
+                    if (dt > 20000000000ull) __trap();
+                }
+            }
+            const int t = pq_t[j], kind = pq_k[j];
+            double tot = 0.0;
+            if (t >= 0 && kind == CI_FIN)
+                for (int w = 0; w < CW; ++w) tot = __dadd_rn(tot, red[j * CW + w]);
+            __syncwarp();
+            if (lane == 0) st_release_cta_s32(pub_head, i + 1);
+            if (t == -1) {
+                flush();
+                break;
+            }
+            if (kind == CI_APPLY) continue;
+            if (kind == CI_FIN && lane == 0)
+                for (int r = 0; r < P; ++r) xa.part[r][t] = tot;
+            pend[np++] = t;
+            if (np >= batch) flush();
+        }
+        return;
+    }
+
+    if (warp == CW) {
+        // ================= producer (lane j issues copy j) =================
+        for (int i = 0;; ++i) {
+            const int s = i % KS;
+            const int use = i / KS;
+            if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+            int kind = 0, t = 0;
+            if (!item(i, kind, t)) {
+                if (lane == 0) {
+                    CMeta m{};
+                    m.t = -1;
+                    meta[s] = m;
+                    mbar_arrive(&full[s]);
+                }
+                break;
+            }
+            CMeta m{};
+            locate(t, kind, m);
+            const bool has_pre = kind != CI_APPLY && R > 0;
+            const unsigned* fl = kind == CI_APPLY ? xa.tflag[R] + t : has_pre ? xa.tflag[R] + NT + t : nullptr;
+            if (fl) {
+                if (lane == 0) xspin(fl, xa.epoch, xa.error);
+                __syncwarp();
+                fence_proxy_async();
+            }
+            const unsigned bytes = static_cast<unsigned>((m.e - m.s) * 4);
+            const bool need_g = kind != CI_PRE || m.ics;
+            unsigned total = 0;
+            if (m.staged)
+                total = kind == CI_APPLY ? 2 * bytes : (has_pre ? 2 * bytes : 0) + NL * bytes + (need_g ? bytes : 0);
+            if (lane == 0) {
+                meta[s] = m;
+                if (m.staged) mbar_arrive_tx(&full[s], total);
+                else mbar_arrive(&full[s]);
+            }
+            __syncwarp();
+            if (m.staged) {
+                float* dst = ring + s * SF;
+                if (kind == CI_APPLY) {
+                    if (lane == 0) bulk_g2s(dst, xa.agg[P - 1] + m.s, bytes, &full[s]);
+                    if (lane == 1) bulk_g2s(dst + T, g.G + m.s, bytes, &full[s]);
+                } else {
+                    if (lane == 0 && has_pre) bulk_g2s(dst, xa.pre[R - 1] + m.s, 2 * bytes, &full[s]);
+                    if (lane >= 1 && lane <= NL)
+                        bulk_g2s(dst + static_cast<size_t>(1 + lane) * T, xa.xrow[R * NL + lane - 1] + m.s,
+                                 bytes, &full[s]);
+                    if (lane == NL + 1 && need_g)
+                        bulk_g2s(dst + static_cast<size_t>(2 + NL) * T, g.G + m.s, bytes, &full[s]);
+                }
+            }
+        }
+        return;
+    }
+
+    // ================= consumers =================
+    const int ctid = tid;
+    for (int i = 0;; ++i) {
+        const int s = i % KS;
+        mbar_wait(&full[s], (i / KS) & 1);
+        const CMeta m = meta[s];
+        const int j = i % kCPQ;
+        if (m.t < 0) {
+            if (lane == 0) {
+                while (ld_acquire_cta_s32(pub_head) < i - kCPQ + 1) __nanosleep(32);
+                if (warp == 0) pq_t[j] = -1;
+                mbar_arrive(&pdone[j]);
+            }
+            break;
+        }
+        const float* buf = ring + s * SF;
+        const bool has_pre = m.kind != CI_APPLY && R > 0;
+        double acc = 0.0;
+        if (m.staged) {
+            const int nq = static_cast<int>((m.e - m.s) >> 2);
+            for (int qd = ctid; qd < nq; qd += CW * 32) {
+                const uint64_t f = m.s + 4ull * qd;
+                if (m.kind == CI_APPLY) {
+                    const float4 a = *reinterpret_cast<const float4*>(buf + 4 * qd);
+                    const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(T) + 4 * qd);
+                    const float4 gn = add4x(go, a);
+                    st_stream4(xa.agg[R] + f, a);  // the resolve's exact fallback reads it
+                    if (m.ics) {
+                        st_stream4(g.C + f, gn);
+                    } else {
+                        *reinterpret_cast<float4*>(g.G + f) = gn;
+#pragma unroll
+                        for (int w = 0; w < NL; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+                    }
+                    continue;
+                }
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                if (has_pre) {
+                    const double2 p0 = *reinterpret_cast<const double2*>(buf + 8 * qd);
+                    const double2 p1 = *reinterpret_cast<const double2*>(buf + 8 * qd + 4);
+                    s0 = p0.x;
+                    s1 = p0.y;
+                    s2 = p1.x;
+                    s3 = p1.y;
+                }
+                float4 v[NL];
+#pragma unroll
+                for (int w = 0; w < NL; ++w) {
+                    v[w] = cvt4x(ap, *reinterpret_cast<const float4*>(buf + static_cast<size_t>(2 + w) * T + 4 * qd));
+                    const double wt = ap.w[R * NL + w];
+                    s0 = agg_acc(s0, wt, v[w].x);
+                    s1 = agg_acc(s1, wt, v[w].y);
+                    s2 = agg_acc(s2, wt, v[w].z);
+                    s3 = agg_acc(s3, wt, v[w].w);
+                }
+                const bool need_g = m.kind == CI_FIN || m.ics;
+                const float4 go = need_g ? *reinterpret_cast<const float4*>(buf + static_cast<size_t>(2 + NL) * T + 4 * qd)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                if (m.kind == CI_PRE) {
+                    double* pr = xa.pre[R] + f;
+                    *reinterpret_cast<double2*>(pr) = make_double2(s0, s1);
+                    *reinterpret_cast<double2*>(pr + 2) = make_double2(s2, s3);
+                    if (m.ics) {
+#pragma unroll
+                        for (int w = 0; w < NL; ++w)
+                            st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, add4x(go, v[w]));
+                    }
+                    continue;
+                }
+                const float4 a = make_float4(agg_finish(ap, s0), agg_finish(ap, s1), agg_finish(ap, s2),
+                                             agg_finish(ap, s3));
+                const float4 gn = add4x(go, a);
+                *reinterpret_cast<float4*>(xa.agg[R] + f) = a;
+                if (m.ics) {
+                    st_stream4(g.C + f, gn);
+#pragma unroll
+                    for (int w = 0; w < NL; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, add4x(go, v[w]));
+                } else {
+                    *reinterpret_cast<float4*>(g.G + f) = gn;
+#pragma unroll
+                    for (int w = 0; w < NL; ++w) st_stream4(g.P + static_cast<uint64_t>(w) * g.ldP + f, gn);
+                }
+                acc = __dadd_rn(acc, pgp_term(a.x, gn.x));
+                acc = __dadd_rn(acc, pgp_term(a.y, gn.y));
+                acc = __dadd_rn(acc, pgp_term(a.z, gn.z));
+                acc = __dadd_rn(acc, pgp_term(a.w, gn.w));
+            }
+        } else {
+            // unstaged tile (unaligned layer): per element from global memory
+            // (the previous prefix and the last rank's agg over NVLink)
+            for (uint64_t f = m.s + ctid; f < m.e; f += CW * 32) {
+                const float go = g.G[f];
+                if (m.kind == CI_APPLY) {
+                    const float a = __ldcg(xa.agg[P - 1] + f);
+                    const float gn = __fadd_rn(go, a);
+                    xa.agg[R][f] = a;
+                    if (m.ics) {
+                        g.C[f] = gn;
+                    } else {
+                        g.G[f] = gn;
+                        for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+                    }
+                    continue;
+                }
+                double sum = has_pre ? __ldcg(xa.pre[R - 1] + f) : 0.0;
+                float x[NL];
+                for (int w = 0; w < NL; ++w) {
+                    x[w] = xa.xrow[R * NL + w][f];
+                    if (ap.sgd) x[w] = sgd_conv(ap.neg_lr, x[w]);
+                    sum = agg_acc(sum, ap.w[R * NL + w], x[w]);
+                }
+                if (m.kind == CI_PRE) {
+                    xa.pre[R][f] = sum;
+                    if (m.ics)
+                        for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x[w]);
+                    continue;
+                }
+                const float a = agg_finish(ap, sum);
+                const float gn = __fadd_rn(go, a);
+                xa.agg[R][f] = a;
+                if (m.ics) {
+                    g.C[f] = gn;
+                    for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x[w]);
+                } else {
+                    g.G[f] = gn;
+                    for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = gn;
+                }
+                acc = __dadd_rn(acc, pgp_term(a, gn));
+            }
+        }
+        if (m.kind == CI_FIN) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[s]);
+            while (ld_acquire_cta_s32(pub_head) < i - kCPQ + 1) __nanosleep(32);
+            red[j * CW + warp] = acc;
+            if (warp == 0) {
+                pq_t[j] = m.t;
+                pq_k[j] = m.kind;
+            }
+            mbar_arrive(&pdone[j]);
+        }
+    }
+}
+
+size_t chain_smem_bytes(int n_loc, int T, int L, int ks) {
+    const size_t ring = static_cast<size_t>(ks) * (n_loc + 3) * T * sizeof(float);
+    const size_t ctl = 2 * ks * sizeof(uint64_t) + kCPQ * sizeof(uint64_t) + ks * sizeof(CMeta) +
+                       kCPQ * kCCW * sizeof(double) + 2 * kCPQ * sizeof(int) + 16;
+    const size_t tab = static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + 64;
+    return ring + ctl + tab;
+}
+
+int chain_stages() {
+    static const int ks = [] {
+        const char* e = std::getenv("OSP_SHARD_CHAIN_STAGES");
+        return e && std::atoi(e) == 3 ? 3 : 2;
+    }();
+    return ks;
+}
+
+template <int NL, int KS>
+cudaError_t launch_chain_ks(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
+    auto kern = k_shard_chain<NL, KS>;
+    const size_t sm = chain_smem_bytes(NL, g.T, g.L, KS);
+    int per_sm = 0;
+    cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), (kCCW + 2) * 32, sm, &per_sm);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    const int grid = sm_count() * (per_sm > 2 ? 2 : per_sm);
+    kern<<<grid, (kCCW + 2) * 32, sm, s>>>(g, ap, xa);
+    return cudaGetLastError();
+}
+
+template <int NL>
+cudaError_t launch_chain_nl(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
+    if (chain_stages() == 3 && chain_smem_bytes(NL, g.T, g.L, 3) <= 220 * 1024)
+        return launch_chain_ks<NL, 3>(g, ap, xa, s);
+    return launch_chain_ks<NL, 2>(g, ap, xa, s);
+}
+
+}  // namespace
+
+bool shard_chain_supported(int n_loc, int T, int L) {
+    if (n_loc < 1 || n_loc > kXMaxStagedWorkers || T < 512 || T > 4096) return false;
+    return chain_smem_bytes(n_loc, T, L, 2) <= 220 * 1024;
+}
+
+cudaError_t launch_shard_chain(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
+    switch (xa.n_loc) {
+        case 1: return launch_chain_nl<1>(g, ap, xa, s);
+        case 2: return launch_chain_nl<2>(g, ap, xa, s);
+        case 3: return launch_chain_nl<3>(g, ap, xa, s);
+        case 4: return launch_chain_nl<4>(g, ap, xa, s);
+        case 5: return launch_chain_nl<5>(g, ap, xa, s);
+        case 6: return launch_chain_nl<6>(g, ap, xa, s);
+        case 7: return launch_chain_nl<7>(g, ap, xa, s);
+        case 8: return launch_chain_nl<8>(g, ap, xa, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace osp

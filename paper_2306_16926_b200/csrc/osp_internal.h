@@ -155,6 +155,7 @@ struct XArgs {
     double* part[kMaxRanks];             // every rank's per-tile PGP partials [NT]
     unsigned* tflag[kMaxRanks];          // every rank's per-tile ready flags [NT]
     unsigned* ready[kMaxRanks];          // every rank's slots [2][kMaxRanks]: deltas ready, own tiles done
+    double* pre[kMaxRanks];              // chain form: every rank's fp64 running sums [ldX]
     unsigned* error;                     // local: set when a bounded wait timed out
     int world, rank, n_loc;
     unsigned epoch;                      // iteration number (1-based)
@@ -178,6 +179,13 @@ cudaError_t launch_shard_x(const GroupView& g, const AggParams& ap, const XArgs&
 // the barrier form's phase 2: the peers' tiles from the pull buffer (128-bit loads)
 cudaError_t launch_shard_peer_apply(const GroupView& g, const AggParams& ap, const XArgs& xa,
                                     cudaStream_t s);
+
+// The chain form of the single-exchange stage 1 (kernels/shard_chain.cu):
+// rank r continues rank r-1's fp64 running sum over its own workers, the last
+// rank finishes and the others pull the aggregate back; tflag holds [2][NT]
+// (tile flags, chain flags).
+bool shard_chain_supported(int n_loc, int T, int L);
+cudaError_t launch_shard_chain(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s);
 
 // Opt a kernel into `smem` bytes of dynamic shared memory and return its
 // occupancy, cached per (context, kernel, bytes) (stage_tma.cu).

@@ -132,6 +132,12 @@ class ShardGroup:
         return bool(lib().osp_shard_deferred_ics(self._h))
 
     @property
+    def sync_form(self) -> str:
+        """Exchange synchronisation: 'tile' (per-tile flags), 'barrier' (own tiles,
+        then a cross-GPU signal) or 'chain' (stage 1 as a reduction chain)."""
+        return {0: "tile", 1: "barrier", 2: "chain"}[lib().osp_shard_sync_form(self._h)]
+
+    @property
     def mode(self) -> str:
         return ("deferred ICS: stage 1 exchanges the RS layers, stage 2 the ICS chunks"
                 if self.deferred_ics else

@@ -35,6 +35,8 @@ def _worker(rank, world, port, cfg, q):
         from paper_2306_16926_b200 import osp
 
         torch.cuda.set_device(rank % torch.cuda.device_count())
+        if cfg.get("sync"):
+            os.environ["OSP_SHARD_SYNC"] = cfg["sync"]
         dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
                                 world_size=world)
         counts = np.asarray(cfg["counts"], dtype=np.uint64)
@@ -48,6 +50,8 @@ def _worker(rank, world, port, cfg, q):
                               tile_elems=cfg.get("tile", 0), defer_ics=cfg.get("defer", False))
         sh.connect_via()
         assert sh.deferred_ics == bool(cfg.get("defer", False)), "shard exchange mode"
+        if cfg.get("sync") and not cfg.get("defer"):
+            assert sh.sync_form == cfg["sync"], (sh.sync_form, cfg["sync"])
         G = p0.copy()
         P = np.tile(p0, (N, 1))
         flags = np.zeros(len(counts), np.uint8)
@@ -139,6 +143,26 @@ def test_shard_four_gpus(defer):
                    budget_frac=0.5, iters=3, seed=11, p0_seed=0, defer=defer), world=4)
 
 
+@pytest.mark.parametrize("per_chunk", [False, True])
+def test_shard_chain_two_gpus(per_chunk):
+    """The reduction-chain form of stage 1 (kernels/shard_chain.cu): rank 1
+    continues rank 0's fp64 running sum; ragged layers, unequal weights, P0."""
+    rng = np.random.default_rng(41)
+    counts = [int(c) for c in rng.integers(1, 30000, 37)]
+    w = [float(x) for x in 0.1 + rng.random(8)]
+    run_world(dict(counts=counts, N=8, weights=w, chunks=4, budget_frac=0.5, iters=4, seed=13,
+                   p0_seed=2, per_chunk=per_chunk, sync="chain"))
+
+
+def test_shard_chain_four_gpus():
+    """Chain over 4 ranks: two middle ranks continue the running sum."""
+    rng = np.random.default_rng(43)
+    counts = [int(c) for c in rng.integers(1, 30000, 29)]
+    w = [float(x) for x in 0.1 + rng.random(8)]
+    run_world(dict(counts=counts, N=8, weights=w, chunks=4, budget_frac=0.4, iters=3, seed=17,
+                   p0_seed=3, sync="chain"), world=4)
+
+
 def test_shard_four_gpus_ragged_per_chunk():
     rng = np.random.default_rng(12)
     counts = [int(c) for c in rng.integers(1, 20000, 30)]
@@ -177,6 +201,19 @@ def test_shard_oversubscribed_ragged(world, N, frac):
                iters=3, seed=5, p0_seed=4)
     run_world(cfg, world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True, defer=True), world=world, oversubscribe=True)
+    run_world(dict(cfg, per_chunk=True), world=world, oversubscribe=True)
+
+
+@pytest.mark.parametrize("world,N,frac", [(2, 8, 0.5), (4, 8, 0.3), (2, 2, 1.0), (8, 8, 0.6)])
+def test_shard_chain_oversubscribed(world, N, frac):
+    """The chain form on however many GPUs exist: first, middle and last ranks,
+    ragged layers (unstaged scalar tiles), budgets 0.3..1.0, per-chunk and fused
+    steps, bit-exact vs the oracle."""
+    rng = np.random.default_rng(51 + world + N)
+    w = [float(x) for x in 0.1 + rng.random(N)]
+    cfg = dict(counts=_ragged(13 + world, 21, 4000), N=N, weights=w, chunks=3, budget_frac=frac,
+               iters=3, seed=7, p0_seed=9, sync="chain")
+    run_world(cfg, world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True), world=world, oversubscribe=True)
 
 
