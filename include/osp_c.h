@@ -449,6 +449,11 @@ osp_status osp_shard_check(osp_shard* s, void* stream);
  * cycles in total, [5] blocking B waits, [6..8] A / B / L items, [9] flag
  * batches. Returns 1 when filled, 0 when disabled. */
 int osp_shard_debug_counters(osp_shard* s, unsigned long long* out16);
+/* OSP_SHARD_DEBUG=2 (chain form): the last stage-1 launch's per-tile timeline,
+ * [8][NT] globaltimer ns (0 PRE issued, 2 PRE flag published, 3 FIN flag
+ * acquired, 4 FIN published, 5 APPLY flag acquired, 6 APPLY done). out null:
+ * returns the entry count; else copies min(n, count) entries and returns it. */
+uint64_t osp_shard_debug_trace(osp_shard* s, unsigned long long* out, uint64_t n);
 /* Synthetic deltas of workers [worker0, worker0+n_workers) into [n_workers][ld]. */
 osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
                                   uint64_t n, float* out, uint64_t ld, void* stream);

@@ -149,6 +149,7 @@ _SIGS = {
     "osp_shard_deferred_ics": (c_int, [c_void_p]),
     "osp_shard_sync_form": (c_int, [c_void_p]),
     "osp_shard_debug_counters": (c_int, [c_void_p, P(c_u64)]),
+    "osp_shard_debug_trace": (c_u64, [c_void_p, P(c_u64), c_u64]),
     "osp_shard_profile": (c_int, [c_void_p, c_int, P(ctypes.c_float), c_void_p]),
     "osp_shard_solo_agg": (c_int, [c_void_p, c_int, c_int, c_void_p]),
     "osp_synth_deltas_range": (c_int, [c_u64, c_int, c_int, c_u64, c_u64, c_void_p, c_u64,

@@ -67,9 +67,11 @@ struct osp_shard {
     int split = 1;             // OSP_SHARD_SPLIT=0: every CTA takes every item kind
     int barrier = -1;          // OSP_SHARD_SYNC=tile|barrier|chain; -1: by world size
     bool chain = false;        // single-exchange stage 1 as a reduction chain (shard_chain.cu)
+    bool chain_fence_gpu = false;  // OSP_SHARD_CHAIN_FENCE=gpu: diagnostics only (not a valid order)
     unsigned* ticket = nullptr;  // [1] local, phase-1 last-CTA counter
     unsigned done_epoch = 0;     // barrier-form launches so far (a stage-2 chunk is one)
     unsigned long long* dbg = nullptr;  // OSP_SHARD_DEBUG=1: kernel counters [16]
+    uint64_t n_trace = 0;               // OSP_SHARD_DEBUG=2: chain timeline entries after them
 };
 
 extern "C" {
@@ -143,6 +145,7 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     // keep the exchange forms); default by world size (measured,
     // profiles/r2_multi_gpu_notes.md)
     if (want_chain < 0) want_chain = kChainDefault(cfg->world);
+    if (const char* cf = std::getenv("OSP_SHARD_CHAIN_FENCE")) s->chain_fence_gpu = std::strcmp(cf, "gpu") == 0;
     s->chain = want_chain == 1 && !s->deferred && cfg->world >= 2 &&
                shard_chain_supported(s->n_loc, static_cast<int>(T), static_cast<int>(part->counts.size()));
     const uint64_t M = part->total;
@@ -162,9 +165,12 @@ osp_status osp_shard_create(const osp_partition* part, const osp_shard_config* c
     if (e == cudaSuccess) e = cudaMemset(s->tflag, 0, 2 * std::max<uint64_t>(NT, 1) * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->ready, 0, 2 * kMaxRanks * sizeof(unsigned));
     if (e == cudaSuccess) e = cudaMemset(s->error, 0, sizeof(unsigned));
-    if (const char* d = std::getenv("OSP_SHARD_DEBUG"); d && d[0] == '1') {
-        if (e == cudaSuccess) e = cudaMalloc(&s->dbg, 16 * sizeof(unsigned long long));
-        if (e == cudaSuccess) e = cudaMemset(s->dbg, 0, 16 * sizeof(unsigned long long));
+    if (const char* d = std::getenv("OSP_SHARD_DEBUG"); d && (d[0] == '1' || d[0] == '2')) {
+        // '2' adds the chain form's per-tile timeline [8][NT] after the counters
+        s->n_trace = d[0] == '2' ? 8 * NT : 0;
+        const size_t n = 16 + s->n_trace;
+        if (e == cudaSuccess) e = cudaMalloc(&s->dbg, n * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMemset(s->dbg, 0, n * sizeof(unsigned long long));
     }
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
@@ -266,8 +272,13 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.pub_batch = s->pub_batch;
     base.pub_min = s->pub_min;
     base.split = s->split;
+    base.chain_pre = 0;  // mixed CTAs
+    base.chain_lead = 4;
+    if (const char* cp = std::getenv("OSP_SHARD_CHAIN_PRE")) base.chain_pre = std::max(0, std::min(3, std::atoi(cp)));
+    if (const char* cl = std::getenv("OSP_SHARD_CHAIN_LEAD")) base.chain_lead = std::max(0, std::atoi(cl));
     base.ticket = s->ticket;
     base.dbg = s->dbg;
+    base.trace = s->n_trace ? s->dbg + 16 : nullptr;
     for (int b = 0; b < 2; ++b) {
         XArgs& xa = s->xa[b];
         xa = base;
@@ -285,6 +296,9 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
                   (reinterpret_cast<uintptr_t>(xa.pre[q]) % 32 == 0);
         xa.vec = vec ? 1 : 0;
     }
+    // chain form: the aggregate lives on the last rank only (the others' APPLY
+    // items read it there), so their resolve's exact fallback reads it there
+    if (s->chain && s->rank != s->world - 1) s->grp->v.agg_full = base.agg[s->world - 1];
     s->connected = true;
     return OSP_OK;
 }
@@ -311,6 +325,13 @@ static osp_status check_ready(osp_shard* s, int buf) {
     return OSP_OK;
 }
 
+// diagnostics: OSP_SHARD_SOLO=apply makes osp_shard_solo_agg time the chain
+// form's APPLY items alone (else its PRE / FIN items alone)
+static bool stage1_solo_apply() {
+    const char* e = std::getenv("OSP_SHARD_SOLO");
+    return e && std::strcmp(e, "apply") == 0;
+}
+
 static cudaError_t launch_x(osp_shard* s, int buf, int mode, int c0, int c1, int solo,
                             cudaStream_t st) {
     XArgs xa = s->xa[buf];
@@ -319,7 +340,11 @@ static cudaError_t launch_x(osp_shard* s, int buf, int mode, int c0, int c1, int
     xa.c0 = c0;
     xa.c1 = c1;
     xa.solo = solo;
-    if (s->chain && mode == XM_SINGLE && !solo) return launch_shard_chain(s->grp->v, s->ap_all, xa, st);
+    if (s->chain && mode == XM_SINGLE) {
+        if (!solo && s->chain_fence_gpu) xa.solo = 2;
+        if (solo && stage1_solo_apply()) xa.solo = 3;
+        return launch_shard_chain(s->grp->v, s->ap_all, xa, st);
+    }
     if (solo || !s->barrier) {
         xa.phase = 0;
         return launch_shard_x(s->grp->v, s->ap_all, xa, st);
@@ -453,6 +478,15 @@ int osp_shard_debug_counters(osp_shard* s, unsigned long long* out16) {
         return 0;
     cudaMemset(s->dbg, 0, 16 * sizeof(unsigned long long));
     return 1;
+}
+
+uint64_t osp_shard_debug_trace(osp_shard* s, unsigned long long* out, uint64_t n) {
+    if (!s || !s->n_trace) return 0;
+    if (!out) return s->n_trace;
+    const uint64_t k = std::min(n, s->n_trace);
+    if (cudaMemcpy(out, s->dbg + 16, k * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+        return 0;
+    return k;
 }
 
 osp_status osp_shard_check(osp_shard* s, void* stream) {

@@ -25,10 +25,19 @@
 //          flag.
 //   APPLY  (ranks 0..P-2) after the tile flag: bulk-copy agg from the last
 //          rank's HBM (NVLink) and G; RS: G = G + agg, rows = G'; ICS: C.
+//          (No local copy of agg: these ranks' resolve reads the last rank's
+//          for its exact fallback, osp_shard.cu.)
 // Data always stays where it was written; readers pull with cp.async.bulk
 // after acquiring a flag the writer pushed into their memory (the writer's
 // system-scope fence then drains only local stores and tiny flag stores).
-// Non-finishing ranks split their CTAs: even ones PRE, odd ones APPLY.
+// Non-finishing ranks split their CTAs between PRE and APPLY items
+// (OSP_SHARD_CHAIN_PRE of every 4 CTAs take PRE; default 2).
+//
+// Diagnostics (xa.solo): 1 = every rank's PRE / FIN items alone, no flags,
+// no APPLY (throughput of each role without the chain; results meaningless);
+// 3 = the APPLY items alone, no flags;
+// 2 = flags released with a GPU-scope fence (timing of the fence only; not a
+// valid ordering for a peer reader).
 //
 // Hazards across iterations: rank r overwrites its prefix at iteration i+1
 // only after finishing iteration i, whose APPLY items waited for every FIN of
@@ -55,9 +64,16 @@ struct CMeta {
     int ics;        // tile of a deferred layer
 };
 
-// Slot layout (floats): [0, 2T) the incoming prefix (T doubles) or, for APPLY,
-// row 0 = agg and row 1 = G; rows 2 .. 2+NL-1 the local delta rows; row 2+NL G.
-template <int NL, int KS>
+// The ring is an arena of xa.chain_arena floats cut into as many slots as the
+// CTA's item kind needs (at most kCMaxSlots): the bytes in flight per SM, not
+// the slot count, set an HBM-bound role's rate, so a PRE slot of rank 0 (rows
+// and G only), an APPLY slot (agg and G) and a FIN slot (prefix, rows, G) each
+// fill the same shared memory. Slot layout (floats): PRE / FIN: [0, 2X) the
+// incoming prefix (X = T when the rank has a predecessor, else 0), then the NL
+// local delta rows, then G; APPLY: row 0 = agg, row 1 = G.
+constexpr int kCMaxSlots = 16;
+
+template <int NL>
 __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, AggParams ap, XArgs xa) {
     constexpr int CW = kCCW;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -65,14 +81,13 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
     const int warp = tid >> 5, lane = tid & 31;
     const int T = g.T, NT = g.NT, L = g.L;
     const int P = xa.world, R = xa.rank;
-    const size_t SF = static_cast<size_t>(NL + 3) * T;
 
     float* ring = reinterpret_cast<float*>(smem);
-    uint64_t* full = reinterpret_cast<uint64_t*>(ring + KS * SF);
-    uint64_t* empty = full + KS;
-    uint64_t* pdone = empty + KS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + xa.chain_arena);
+    uint64_t* empty = full + kCMaxSlots;
+    uint64_t* pdone = empty + kCMaxSlots;
     CMeta* meta = reinterpret_cast<CMeta*>(pdone + kCPQ);
-    double* red = reinterpret_cast<double*>(meta + KS);  // [kCPQ][CW]
+    double* red = reinterpret_cast<double*>(meta + kCMaxSlots);  // [kCPQ][CW]
     int* pq_t = reinterpret_cast<int*>(red + kCPQ * CW);  // [kCPQ] tile id, -1 stop
     int* pq_k = pq_t + kCPQ;                              // [kCPQ] item kind
     int* pub_head = pq_k + kCPQ;
@@ -105,6 +120,25 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
         for (int i = tid; i < n_ics; i += blockDim.x) snap_il[i] = g.ics_layers[i];
         for (int i = tid; i <= n_ics; i += blockDim.x) snap_tp[i] = g.ics_tile_prefix[i];
     }
+    // roles and this CTA's tiles (non-finishing ranks: every CTA both kinds, or
+    // with xa.chain_pre = 1..3 and a grid multiple of 4, that many of every 4
+    // CTAs PRE items only and the rest APPLY items only)
+    const bool fin = R == P - 1;
+    const int GX = static_cast<int>(gridDim.x);
+    const int pre4 = xa.chain_pre;
+    const bool split = !fin && GX >= 4 && GX % 4 == 0 && pre4 >= 1 && pre4 <= 3 && xa.solo == 0;
+    const int b4 = static_cast<int>(blockIdx.x) & 3, q4 = static_cast<int>(blockIdx.x) >> 2;
+    const bool is_pre = b4 < pre4;
+    const int C = split ? (GX / 4) * (is_pre ? pre4 : 4 - pre4) : GX;
+    const int c = split ? q4 * (is_pre ? pre4 : 4 - pre4) + (is_pre ? b4 : b4 - pre4)
+                        : static_cast<int>(blockIdx.x);
+    const int n_own = c < C && c < NT ? (NT - 1 - c) / C + 1 : 0;
+    // slot size and count for this CTA's item kinds
+    const int xoff = R > 0 ? 2 : 0;  // rows of the incoming prefix in a PRE / FIN slot
+    const int slot_pf = (xoff + NL + 1) * T, slot_ap = 2 * T;
+    const int SF = fin ? slot_pf : split ? (is_pre ? slot_pf : slot_ap) : max(slot_pf, slot_ap);
+    const int KS = min(kCMaxSlots, xa.chain_arena / SF);
+    OSP_DCHECK(KS >= 2, "chain: arena holds fewer than two slots");
     if (tid == 0) {
         for (int s = 0; s < KS; ++s) {
             mbar_init(&full[s], 1);
@@ -116,26 +150,76 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
     }
     __syncthreads();
 
-    // roles and this CTA's tiles
-    const bool fin = R == P - 1;
-    const int GX = static_cast<int>(gridDim.x);
-    const bool split = !fin && GX >= 2;
-    const int C = split ? GX / 2 : GX;
-    const int c = split ? static_cast<int>(blockIdx.x) / 2 : static_cast<int>(blockIdx.x);
-    const int n_own = c < C && c < NT ? (NT - 1 - c) / C + 1 : 0;
-    // item i -> (kind, tile); false when the CTA is done
-    auto item = [&](int i, int& kind, int& t) -> bool {
-        if (fin) {
-            kind = CI_FIN;
-        } else if (split) {
-            kind = (blockIdx.x & 1) ? CI_APPLY : CI_PRE;
-        } else {  // one CTA: every prefix, then every apply
-            kind = i < n_own ? CI_PRE : CI_APPLY;
-            if (i >= n_own) i -= n_own;
+    // Next item (kind, tile) of this CTA; false when done. FIN ranks and split
+    // CTAs have one kind. Mixed CTAs (xa.chain_pre == 0: every CTA of a
+    // non-finishing rank takes both kinds of its tiles) choose by readiness: an
+    // APPLY item whose flag has landed goes first once the PRE front is
+    // xa.chain_lead items ahead, else a PRE item; so PRE items lead the chain
+    // and the APPLY items follow the last rank without a tail of idle PRE CTAs.
+    // Readiness comes from relaxed loads issued one iteration ahead (lane k:
+    // the k-th next item's flag; their latency hides behind the copy issue),
+    // and an item is issued only after an acquire: lanes 0..kProbe-1 acquire
+    // the next kProbe flags at once and the ready prefix is cached (a flag only
+    // goes from not-ready to ready within a launch). The acquiring lanes'
+    // order reaches the copy-issuing lanes through __syncwarp.
+    constexpr int kProbe = 8;
+    int ip = 0, ia = 0;              // next PRE / APPLY index of this CTA's tiles
+    int pre_upto = 0, app_upto = 0;  // items whose flags were acquired lie below these
+    unsigned rp_pre = 0, rp_app = 0; // this lane's relaxed probe of item ip / ia + lane
+    const bool do_pre = !fin && (!split || is_pre) && xa.solo != 3;
+    const bool do_app = !fin && (!split || !is_pre) && xa.solo != 1;
+    const bool pre_flags = R > 0 && xa.solo != 1 && xa.solo != 3;  // PRE / FIN wait for a prefix
+    const bool app_flags = xa.solo != 3;
+    const int n_pf = (fin && xa.solo != 3) || do_pre ? n_own : 0;  // PRE or FIN items
+    const unsigned* pflag = xa.tflag[R] + NT;  // chain flags (from rank R-1)
+    const unsigned* aflag = xa.tflag[R];       // tile flags (from the last rank)
+    auto issue_probes = [&]() {
+        if (lane < kProbe) {
+            if (pre_flags && ip + lane < n_pf) rp_pre = ld_relaxed_sys(pflag + c + (ip + lane) * C);
+            if (do_app && app_flags && ia + lane < n_own) rp_app = ld_relaxed_sys(aflag + c + (ia + lane) * C);
         }
-        if (i >= n_own) return false;
-        t = c + i * C;
+    };
+    // ready prefix of items [from, from + kProbe), acquired
+    auto acquire = [&](const unsigned* base, int from, int n) -> int {
+        int ok = 0;
+        if (lane < kProbe && from + lane < n)
+            ok = static_cast<int>(ld_acquire_sys(base + c + (from + lane) * C) - xa.epoch) >= 0;
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        return from + __ffs(~m) - 1;
+    };
+    auto next_item = [&](int& kind, int& t) -> bool {
+        const bool pre_left = ip < n_pf, app_left = do_app && ia < n_own;
+        if (!pre_left && !app_left) return false;
+        // the relaxed probes of the head items (issued last iteration)
+        const bool pr = pre_left && (!pre_flags || ip < pre_upto ||
+                                     __shfl_sync(0xffffffffu, static_cast<int>(rp_pre - xa.epoch) >= 0, 0));
+        const bool ar = app_left && (!app_flags || ia < app_upto ||
+                                     __shfl_sync(0xffffffffu, static_cast<int>(rp_app - xa.epoch) >= 0, 0));
+        const bool ahead = ip - ia >= xa.chain_lead;
+        int choice;
+        if (!pre_left) choice = CI_APPLY;
+        else if (!app_left) choice = fin ? CI_FIN : CI_PRE;
+        else if (ar && (ahead || !pr)) choice = CI_APPLY;
+        else if (pr || !ahead) choice = CI_PRE;
+        else choice = CI_APPLY;
+        // acquire the chosen item's flag (and its successors') when it looked ready
+        if (choice == CI_APPLY && app_flags && ia >= app_upto && ar) app_upto = acquire(aflag, ia, n_own);
+        if (choice != CI_APPLY && pre_flags && ip >= pre_upto && pr) pre_upto = acquire(pflag, ip, n_pf);
+        kind = choice;
+        t = c + (choice == CI_APPLY ? ia++ : ip++) * C;
         return true;
+    };
+    // blocking wait for an item whose flag was not seen ready (lane 0)
+    auto ensure = [&](int kind, int idx, int t, long long& t_flag, long long& n_block) {
+        const bool flagged = kind == CI_APPLY ? app_flags : pre_flags;
+        const int upto = kind == CI_APPLY ? app_upto : pre_upto;
+        if (!flagged || idx < upto) return;
+        const long long b0 = clock64();
+        const unsigned* fl = kind == CI_APPLY ? xa.tflag[R] + t : xa.tflag[R] + NT + t;
+        if (lane == 0) xspin(fl, xa.epoch, xa.error);
+        __syncwarp();
+        ++n_block;
+        t_flag += clock64() - b0;
     };
     auto locate = [&](int t, int kind, CMeta& m) {
         int l, kk;
@@ -160,12 +244,20 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
         constexpr int kPubMax = 16;
         const int batch = xa.pub_batch < 1 ? 1 : (xa.pub_batch > kPubMax ? kPubMax : xa.pub_batch);
         int pend[kPubMax];
-        int np = 0;
+        int np = 0, nf = 0;  // pending flags, flushes so far (warp-uniform)
+        long long t_fence = 0, n_flush = 0;
         auto flush = [&]() {
             if (np == 0) return;
-            if (lane == 0) {
-                asm volatile("fence.acq_rel.sys;" ::: "memory");
+            ++nf;
+            if (lane == 0 && xa.solo != 1 && xa.solo != 3) {
+                const long long f0 = clock64();
+                if (xa.solo == 2) asm volatile("fence.acq_rel.gpu;" ::: "memory");  // diagnostics only
+                else asm volatile("fence.acq_rel.sys;" ::: "memory");
+                t_fence -= f0 - clock64();
+                ++n_flush;
+                const unsigned long long now = xa.trace ? now_ns() : 0;
                 for (int j = 0; j < np; ++j) {
+                    if (xa.trace) xa.trace[static_cast<size_t>(fin ? 4 : 2) * NT + pend[j]] = now;
                     if (fin) {
                         for (int r = 0; r < P; ++r)
                             if (r != R) *reinterpret_cast<volatile unsigned*>(xa.tflag[r] + pend[j]) = xa.epoch;
@@ -200,22 +292,36 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 break;
             }
             if (kind == CI_APPLY) continue;
-            if (kind == CI_FIN && lane == 0)
+            if (kind == CI_FIN && lane == 0 && xa.solo != 1 && xa.solo != 3)
                 for (int r = 0; r < P; ++r) xa.part[r][t] = tot;
             pend[np++] = t;
-            if (np >= batch) flush();
+            // the first flushes carry 1, 2, 4, ... flags: the next rank's first
+            // tiles are released at once, later ones in full batches
+            if (np >= min(batch, 1 << min(nf, 4))) flush();
+        }
+        if (xa.dbg && lane == 0) {
+            atomicAdd(xa.dbg + 3, static_cast<unsigned long long>(t_fence));
+            atomicAdd(xa.dbg + 9, static_cast<unsigned long long>(n_flush));
         }
         return;
     }
 
     if (warp == CW) {
         // ================= producer (lane j issues copy j) =================
+        long long t_flag = 0, t_empty = 0, n_block = 0, n_it[3] = {0, 0, 0};
+        const long long t_start = clock64();
+        const uint64_t ns0 = now_ns();
+        issue_probes();
         for (int i = 0;; ++i) {
             const int s = i % KS;
             const int use = i / KS;
-            if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
+            if (use > 0) {
+                const long long e0 = clock64();
+                mbar_wait(&empty[s], (use - 1) & 1);
+                t_empty += clock64() - e0;
+            }
             int kind = 0, t = 0;
-            if (!item(i, kind, t)) {
+            if (!next_item(kind, t)) {
                 if (lane == 0) {
                     CMeta m{};
                     m.t = -1;
@@ -227,12 +333,13 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
             CMeta m{};
             locate(t, kind, m);
             const bool has_pre = kind != CI_APPLY && R > 0;
-            const unsigned* fl = kind == CI_APPLY ? xa.tflag[R] + t : has_pre ? xa.tflag[R] + NT + t : nullptr;
-            if (fl) {
-                if (lane == 0) xspin(fl, xa.epoch, xa.error);
-                __syncwarp();
-                fence_proxy_async();
-            }
+            ++n_it[kind];
+            if (xa.trace && lane == 0 && kind == CI_PRE) xa.trace[t] = now_ns();
+            ensure(kind, kind == CI_APPLY ? ia - 1 : ip - 1, t, t_flag, n_block);
+            fence_proxy_async();  // the acquired flags before this item's bulk reads
+            issue_probes();       // readiness for the next choice, in flight meanwhile
+            if (xa.trace && lane == 0 && (kind == CI_APPLY || has_pre))
+                xa.trace[static_cast<size_t>(kind == CI_APPLY ? 5 : 3) * NT + t] = now_ns();
             const unsigned bytes = static_cast<unsigned>((m.e - m.s) * 4);
             const bool need_g = kind != CI_PRE || m.ics;
             unsigned total = 0;
@@ -252,21 +359,34 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 } else {
                     if (lane == 0 && has_pre) bulk_g2s(dst, xa.pre[R - 1] + m.s, 2 * bytes, &full[s]);
                     if (lane >= 1 && lane <= NL)
-                        bulk_g2s(dst + static_cast<size_t>(1 + lane) * T, xa.xrow[R * NL + lane - 1] + m.s,
+                        bulk_g2s(dst + static_cast<size_t>(xoff + lane - 1) * T, xa.xrow[R * NL + lane - 1] + m.s,
                                  bytes, &full[s]);
                     if (lane == NL + 1 && need_g)
-                        bulk_g2s(dst + static_cast<size_t>(2 + NL) * T, g.G + m.s, bytes, &full[s]);
+                        bulk_g2s(dst + static_cast<size_t>(xoff + NL) * T, g.G + m.s, bytes, &full[s]);
                 }
             }
+        }
+        if (xa.dbg && lane == 0) {
+            atomicAdd(xa.dbg + 0, static_cast<unsigned long long>(t_flag));
+            atomicAdd(xa.dbg + 1, static_cast<unsigned long long>(t_empty));
+            atomicAdd(xa.dbg + 4, static_cast<unsigned long long>(clock64() - t_start));
+            atomicAdd(xa.dbg + 5, static_cast<unsigned long long>(n_block));
+            atomicAdd(xa.dbg + 6, static_cast<unsigned long long>(n_it[CI_PRE]));
+            atomicAdd(xa.dbg + 7, static_cast<unsigned long long>(n_it[CI_APPLY]));
+            atomicAdd(xa.dbg + 8, static_cast<unsigned long long>(n_it[CI_FIN]));
+            atomicMax(xa.dbg + 10, static_cast<unsigned long long>(now_ns() - ns0));
         }
         return;
     }
 
     // ================= consumers =================
     const int ctid = tid;
+    long long t_full = 0;
     for (int i = 0;; ++i) {
         const int s = i % KS;
+        const long long f0 = clock64();
         mbar_wait(&full[s], (i / KS) & 1);
+        t_full += clock64() - f0;
         const CMeta m = meta[s];
         const int j = i % kCPQ;
         if (m.t < 0) {
@@ -288,7 +408,6 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                     const float4 a = *reinterpret_cast<const float4*>(buf + 4 * qd);
                     const float4 go = *reinterpret_cast<const float4*>(buf + static_cast<size_t>(T) + 4 * qd);
                     const float4 gn = add4x(go, a);
-                    st_stream4(xa.agg[R] + f, a);  // the resolve's exact fallback reads it
                     if (m.ics) {
                         st_stream4(g.C + f, gn);
                     } else {
@@ -310,7 +429,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 float4 v[NL];
 #pragma unroll
                 for (int w = 0; w < NL; ++w) {
-                    v[w] = cvt4x(ap, *reinterpret_cast<const float4*>(buf + static_cast<size_t>(2 + w) * T + 4 * qd));
+                    v[w] = cvt4x(ap, *reinterpret_cast<const float4*>(buf + static_cast<size_t>(xoff + w) * T + 4 * qd));
                     const double wt = ap.w[R * NL + w];
                     s0 = agg_acc(s0, wt, v[w].x);
                     s1 = agg_acc(s1, wt, v[w].y);
@@ -318,7 +437,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                     s3 = agg_acc(s3, wt, v[w].w);
                 }
                 const bool need_g = m.kind == CI_FIN || m.ics;
-                const float4 go = need_g ? *reinterpret_cast<const float4*>(buf + static_cast<size_t>(2 + NL) * T + 4 * qd)
+                const float4 go = need_g ? *reinterpret_cast<const float4*>(buf + static_cast<size_t>(xoff + NL) * T + 4 * qd)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
                 if (m.kind == CI_PRE) {
                     double* pr = xa.pre[R] + f;
@@ -357,7 +476,6 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 if (m.kind == CI_APPLY) {
                     const float a = __ldcg(xa.agg[P - 1] + f);
                     const float gn = __fadd_rn(go, a);
-                    xa.agg[R][f] = a;
                     if (m.ics) {
                         g.C[f] = gn;
                     } else {
@@ -397,6 +515,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
             for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_down_sync(0xffffffffu, acc, o));
         }
         __syncwarp();
+        if (xa.trace && warp == 0 && lane == 0 && m.kind == CI_APPLY) xa.trace[6ull * NT + m.t] = now_ns();
         if (lane == 0) {
             mbar_arrive(&empty[s]);
             while (ld_acquire_cta_s32(pub_head) < i - kCPQ + 1) __nanosleep(32);
@@ -408,28 +527,35 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
             mbar_arrive(&pdone[j]);
         }
     }
+    if (xa.dbg && tid == 0) atomicAdd(xa.dbg + 2, static_cast<unsigned long long>(t_full));
 }
 
-size_t chain_smem_bytes(int n_loc, int T, int L, int ks) {
-    const size_t ring = static_cast<size_t>(ks) * (n_loc + 3) * T * sizeof(float);
-    const size_t ctl = 2 * ks * sizeof(uint64_t) + kCPQ * sizeof(uint64_t) + ks * sizeof(CMeta) +
-                       kCPQ * kCCW * sizeof(double) + 2 * kCPQ * sizeof(int) + 16;
+size_t chain_ctl_bytes(int L) {
+    const size_t ctl = 2 * kCMaxSlots * sizeof(uint64_t) + kCPQ * sizeof(uint64_t) +
+                       kCMaxSlots * sizeof(CMeta) + kCPQ * kCCW * sizeof(double) + 2 * kCPQ * sizeof(int) + 16;
     const size_t tab = static_cast<size_t>(L) * 16 + (L + 1) * 4 + ((L + 15) & ~15) + 64;
-    return ring + ctl + tab;
+    return ctl + tab;
 }
 
-int chain_stages() {
-    static const int ks = [] {
-        const char* e = std::getenv("OSP_SHARD_CHAIN_STAGES");
-        return e && std::atoi(e) == 3 ? 3 : 2;
+// the ring arena in floats: OSP_SHARD_CHAIN_ARENA_KB (default 200), at least
+// two FIN slots, and the whole CTA within 227 KB
+int chain_arena_floats(int n_loc, int T, int L) {
+    static const int kb = [] {
+        const char* e = std::getenv("OSP_SHARD_CHAIN_ARENA_KB");
+        const int v = e ? std::atoi(e) : 200;
+        return v >= 32 && v <= 224 ? v : 200;
     }();
-    return ks;
+    const size_t cap = 227 * 1024 - chain_ctl_bytes(L);
+    size_t bytes = std::min<size_t>(static_cast<size_t>(kb) * 1024, cap);
+    bytes = std::max<size_t>(bytes, 2ull * (n_loc + 3) * T * sizeof(float));
+    return static_cast<int>(bytes / sizeof(float)) & ~31;
 }
 
-template <int NL, int KS>
-cudaError_t launch_chain_ks(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
-    auto kern = k_shard_chain<NL, KS>;
-    const size_t sm = chain_smem_bytes(NL, g.T, g.L, KS);
+template <int NL>
+cudaError_t launch_chain_nl(const GroupView& g, const AggParams& ap, XArgs xa, cudaStream_t s) {
+    auto kern = k_shard_chain<NL>;
+    xa.chain_arena = chain_arena_floats(NL, g.T, g.L);
+    const size_t sm = static_cast<size_t>(xa.chain_arena) * sizeof(float) + chain_ctl_bytes(g.L);
     int per_sm = 0;
     cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), (kCCW + 2) * 32, sm, &per_sm);
     if (e != cudaSuccess) return e;
@@ -439,18 +565,11 @@ cudaError_t launch_chain_ks(const GroupView& g, const AggParams& ap, const XArgs
     return cudaGetLastError();
 }
 
-template <int NL>
-cudaError_t launch_chain_nl(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {
-    if (chain_stages() == 3 && chain_smem_bytes(NL, g.T, g.L, 3) <= 220 * 1024)
-        return launch_chain_ks<NL, 3>(g, ap, xa, s);
-    return launch_chain_ks<NL, 2>(g, ap, xa, s);
-}
-
 }  // namespace
 
 bool shard_chain_supported(int n_loc, int T, int L) {
     if (n_loc < 1 || n_loc > kXMaxStagedWorkers || T < 512 || T > 4096) return false;
-    return chain_smem_bytes(n_loc, T, L, 2) <= 220 * 1024;
+    return 2ull * (n_loc + 3) * T * sizeof(float) + chain_ctl_bytes(L) <= 227 * 1024;
 }
 
 cudaError_t launch_shard_chain(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s) {

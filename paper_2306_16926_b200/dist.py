@@ -123,8 +123,19 @@ class ShardGroup:
         if not lib().osp_shard_debug_counters(self._h, out):
             return None
         names = ["b_block_cycles", "empty_wait_cycles", "full_wait_cycles", "fence_cycles",
-                 "producer_cycles", "b_blocks", "a_items", "b_items", "l_items", "flushes"]
+                 "producer_cycles", "b_blocks", "a_items", "b_items", "l_items", "flushes",
+                 "max_cta_ns"]
         return {n: int(v) for n, v in zip(names, out)}
+
+    def debug_trace(self):
+        """OSP_SHARD_DEBUG=2, chain form: [8, NT] globaltimer stamps of the last
+        stage-1 launch (see osp_shard_debug_trace), or None."""
+        n = int(lib().osp_shard_debug_trace(self._h, None, 0))
+        if not n:
+            return None
+        out = np.zeros(n, dtype=np.uint64)
+        lib().osp_shard_debug_trace(self._h, out.ctypes.data_as(P(c_u64)), n)
+        return out.reshape(8, n // 8)
 
     @property
     def deferred_ics(self) -> bool:

@@ -60,6 +60,10 @@ def _worker(rank, world, port, cfg, q):
             buf = it % 2
             sh.fill_synth(cfg["seed"], it, buf)
             deltas = np.stack([oracle.synth_delta(cfg["seed"], k, it, M) for k in range(N)])
+            for (dst, src, n) in cfg.get("copy_layers", []):  # identical layers: exact PGP ties
+                x = sh.deltas(buf)
+                x[:, dst:dst + n] = x[:, src:src + n]
+                deltas[:, dst:dst + n] = deltas[:, src:src + n]
             r = oracle.step(counts, 4, w, deltas, G, P, flags, order, nc, budget)
             sh.set_budget(budget)
             if cfg.get("per_chunk"):
@@ -85,6 +89,8 @@ def _worker(rank, world, port, cfg, q):
             assert np.array_equal(nxt["flags"], r["flags_out"]), f"flags rank {rank} it {it}"
             assert np.array_equal(nxt["order"], r["order_out"]), f"order rank {rank} it {it}"
             flags, order = r["flags_out"], r["order_out"]
+        if cfg.get("copy_layers"):
+            assert sh.local.stats()["fallback_layers"] > 0, "ties must take the exact fallback"
         dist.barrier()
         sh.close()
         dist.destroy_process_group()
@@ -202,6 +208,18 @@ def test_shard_oversubscribed_ragged(world, N, frac):
     run_world(cfg, world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True, defer=True), world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True), world=world, oversubscribe=True)
+
+
+@pytest.mark.parametrize("sync", ["chain", "tile"])
+def test_shard_exact_ties_oversubscribed(sync):
+    """Identical layers tie exactly: every rank's resolve must take the exact
+    sequential fallback, which reads the applied aggregate (in the chain form
+    the last rank's, over NVLink) and reproduce the reference's stable order."""
+    h = 30_000
+    cfg = dict(counts=[h, h, 1000, h], N=8, weights=[0.125] * 8, chunks=2, budget_frac=0.6,
+               iters=3, seed=7, p0_seed=0, sync=sync,
+               copy_layers=[(h, 0, h), (2 * h + 1000, 0, h)])
+    run_world(cfg, world=2, oversubscribe=True)
 
 
 @pytest.mark.parametrize("world,N,frac", [(2, 8, 0.5), (4, 8, 0.3), (2, 2, 1.0), (8, 8, 0.6)])

@@ -65,6 +65,12 @@ def main():
     sh.debug_counters()
     t = torch.tensor([step_ms, solo_ms] + [ph[k] for k in ph], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # every rank's counters (the chain form's ranks play different roles)
+    keys = sorted(dbg) if dbg else []
+    dv = torch.tensor([dbg[k] for k in keys] if dbg else [0.0], dtype=torch.float64, device="cuda")
+    allv = [torch.zeros_like(dv) for _ in range(world)]
+    dist.all_gather(allv, dv)
+    dbg_all = [dict(zip(keys, v.tolist())) for v in allv] if dbg else None
     if rank == 0:
         n_loc = 8 // world
         nvl = 4.0 * M * ((8 - n_loc) / world + (world - 1) / world)
@@ -75,7 +81,8 @@ def main():
                           "world": world, "step_ms": vals[0], "solo_exchange_ms": vals[1],
                           "phases_ms": dict(zip(ph, vals[2:])),
                           "nvlink_GBps_step": nvl / (vals[0] * 1e-3) / 1e9,
-                          "debug_per_step_rank0": dbg}), flush=True)
+                          "sync": sh.sync_form,
+                          "debug_per_step": dbg_all}), flush=True)
     sh.close()
     dist.destroy_process_group()
 
