@@ -26,11 +26,11 @@ namespace {
 
 constexpr uint32_t kMagic = 0x0700b200u;
 
-// default sync form of the single-exchange stage 1 by world size: 1 = chain
-int kChainDefault(int world) {
-    (void)world;
-    return 0;
-}
+// default sync form of the single-exchange stage 1 by world size: the chain
+// at 2 ranks (ResNet-50 0.45-0.49 vs 0.54 ms, VGG-16 2.09-2.18 vs 2.47 ms with
+// per-tile flags); at 4 ranks the last rank's 3-way aggregate fan-out makes it
+// slower than the barrier form (0.73 vs 0.55 ms; profiles/r2_multi_gpu_notes.md)
+int kChainDefault(int world) { return world == 2 ? 1 : 0; }
 
 struct ShardHandle {
     uint32_t magic;
@@ -272,9 +272,7 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.pub_batch = s->pub_batch;
     base.pub_min = s->pub_min;
     base.split = s->split;
-    base.chain_pre = 0;  // mixed CTAs
     base.chain_lead = 4;
-    if (const char* cp = std::getenv("OSP_SHARD_CHAIN_PRE")) base.chain_pre = std::max(0, std::min(3, std::atoi(cp)));
     if (const char* cl = std::getenv("OSP_SHARD_CHAIN_LEAD")) base.chain_lead = std::max(0, std::atoi(cl));
     base.ticket = s->ticket;
     base.dbg = s->dbg;

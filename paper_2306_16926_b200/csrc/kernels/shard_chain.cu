@@ -30,8 +30,8 @@
 // Data always stays where it was written; readers pull with cp.async.bulk
 // after acquiring a flag the writer pushed into their memory (the writer's
 // system-scope fence then drains only local stores and tiny flag stores).
-// Non-finishing ranks split their CTAs between PRE and APPLY items
-// (OSP_SHARD_CHAIN_PRE of every 4 CTAs take PRE; default 2).
+// Every CTA of a non-finishing rank takes both PRE and APPLY items of its
+// tiles, PRE items leading (see next_item).
 //
 // Diagnostics (xa.solo): 1 = every rank's PRE / FIN items alone, no flags,
 // no APPLY (throughput of each role without the chain; results meaningless);
@@ -120,23 +120,22 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
         for (int i = tid; i < n_ics; i += blockDim.x) snap_il[i] = g.ics_layers[i];
         for (int i = tid; i <= n_ics; i += blockDim.x) snap_tp[i] = g.ics_tile_prefix[i];
     }
-    // roles and this CTA's tiles (non-finishing ranks: every CTA both kinds, or
-    // with xa.chain_pre = 1..3 and a grid multiple of 4, that many of every 4
-    // CTAs PRE items only and the rest APPLY items only)
+    // roles and this CTA's tiles: the last rank's CTAs take FIN items, every
+    // other rank's CTAs both PRE and APPLY items of their tiles (splitting the
+    // CTAs between the two kinds measured slower: 0.48-0.53 vs 0.45-0.47 ms)
     const bool fin = R == P - 1;
-    const int GX = static_cast<int>(gridDim.x);
-    const int pre4 = xa.chain_pre;
-    const bool split = !fin && GX >= 4 && GX % 4 == 0 && pre4 >= 1 && pre4 <= 3 && xa.solo == 0;
-    const int b4 = static_cast<int>(blockIdx.x) & 3, q4 = static_cast<int>(blockIdx.x) >> 2;
-    const bool is_pre = b4 < pre4;
-    const int C = split ? (GX / 4) * (is_pre ? pre4 : 4 - pre4) : GX;
-    const int c = split ? q4 * (is_pre ? pre4 : 4 - pre4) + (is_pre ? b4 : b4 - pre4)
-                        : static_cast<int>(blockIdx.x);
+    const int C = static_cast<int>(gridDim.x);
+    const int c = static_cast<int>(blockIdx.x);
     const int n_own = c < C && c < NT ? (NT - 1 - c) / C + 1 : 0;
     // slot size and count for this CTA's item kinds
     const int xoff = R > 0 ? 2 : 0;  // rows of the incoming prefix in a PRE / FIN slot
+    // the running sums: pulled from the previous rank's buffer, ours kept in our
+    // own (pushing them into the next rank with NVLink stores measured slower:
+    // 0.57 vs 0.49 ms, profiles/r2_multi_gpu_notes.md)
+    const double* pre_in = R == 0 ? nullptr : xa.pre[R - 1];
+    double* pre_out = R == P - 1 ? nullptr : xa.pre[R];
     const int slot_pf = (xoff + NL + 1) * T, slot_ap = 2 * T;
-    const int SF = fin ? slot_pf : split ? (is_pre ? slot_pf : slot_ap) : max(slot_pf, slot_ap);
+    const int SF = fin ? slot_pf : max(slot_pf, slot_ap);
     const int KS = min(kCMaxSlots, xa.chain_arena / SF);
     OSP_DCHECK(KS >= 2, "chain: arena holds fewer than two slots");
     if (tid == 0) {
@@ -150,9 +149,8 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
     }
     __syncthreads();
 
-    // Next item (kind, tile) of this CTA; false when done. FIN ranks and split
-    // CTAs have one kind. Mixed CTAs (xa.chain_pre == 0: every CTA of a
-    // non-finishing rank takes both kinds of its tiles) choose by readiness: an
+    // Next item (kind, tile) of this CTA; false when done. FIN CTAs have one
+    // kind; the others choose by readiness: an
     // APPLY item whose flag has landed goes first once the PRE front is
     // xa.chain_lead items ahead, else a PRE item; so PRE items lead the chain
     // and the APPLY items follow the last rank without a tail of idle PRE CTAs.
@@ -166,8 +164,8 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
     int ip = 0, ia = 0;              // next PRE / APPLY index of this CTA's tiles
     int pre_upto = 0, app_upto = 0;  // items whose flags were acquired lie below these
     unsigned rp_pre = 0, rp_app = 0; // this lane's relaxed probe of item ip / ia + lane
-    const bool do_pre = !fin && (!split || is_pre) && xa.solo != 3;
-    const bool do_app = !fin && (!split || !is_pre) && xa.solo != 1;
+    const bool do_pre = !fin && xa.solo != 3;
+    const bool do_app = !fin && xa.solo != 1;
     const bool pre_flags = R > 0 && xa.solo != 1 && xa.solo != 3;  // PRE / FIN wait for a prefix
     const bool app_flags = xa.solo != 3;
     const int n_pf = (fin && xa.solo != 3) || do_pre ? n_own : 0;  // PRE or FIN items
@@ -307,8 +305,8 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
     }
 
     if (warp == CW) {
-        // ================= producer (lane j issues copy j) =================
-        long long t_flag = 0, t_empty = 0, n_block = 0, n_it[3] = {0, 0, 0};
+        // ================= producer (whole warp: probes; lane 0 issues the copies) =================
+        long long t_flag = 0, t_empty = 0, n_block = 0, n_it[3] = {0, 0, 0}, t_next = 0, t_issue = 0;
         const long long t_start = clock64();
         const uint64_t ns0 = now_ns();
         issue_probes();
@@ -321,7 +319,10 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 t_empty += clock64() - e0;
             }
             int kind = 0, t = 0;
-            if (!next_item(kind, t)) {
+            const long long n0 = clock64();
+            const bool more = next_item(kind, t);
+            t_next += clock64() - n0;
+            if (!more) {
                 if (lane == 0) {
                     CMeta m{};
                     m.t = -1;
@@ -330,13 +331,15 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 }
                 break;
             }
+            const long long i0 = clock64();
             CMeta m{};
             locate(t, kind, m);
             const bool has_pre = kind != CI_APPLY && R > 0;
             ++n_it[kind];
             if (xa.trace && lane == 0 && kind == CI_PRE) xa.trace[t] = now_ns();
             ensure(kind, kind == CI_APPLY ? ia - 1 : ip - 1, t, t_flag, n_block);
-            fence_proxy_async();  // the acquired flags before this item's bulk reads
+            if (kind == CI_APPLY ? app_flags : pre_flags)
+                fence_proxy_async();  // the acquired flags before this item's bulk reads
             issue_probes();       // readiness for the next choice, in flight meanwhile
             if (xa.trace && lane == 0 && (kind == CI_APPLY || has_pre))
                 xa.trace[static_cast<size_t>(kind == CI_APPLY ? 5 : 3) * NT + t] = now_ns();
@@ -351,20 +354,20 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 else mbar_arrive(&full[s]);
             }
             __syncwarp();
-            if (m.staged) {
+            if (m.staged && lane == 0) {  // one thread issues the item's copies (as k_stage_tma)
                 float* dst = ring + s * SF;
                 if (kind == CI_APPLY) {
-                    if (lane == 0) bulk_g2s(dst, xa.agg[P - 1] + m.s, bytes, &full[s]);
-                    if (lane == 1) bulk_g2s(dst + T, g.G + m.s, bytes, &full[s]);
+                    bulk_g2s(dst, xa.agg[P - 1] + m.s, bytes, &full[s]);
+                    bulk_g2s(dst + T, g.G + m.s, bytes, &full[s]);
                 } else {
-                    if (lane == 0 && has_pre) bulk_g2s(dst, xa.pre[R - 1] + m.s, 2 * bytes, &full[s]);
-                    if (lane >= 1 && lane <= NL)
-                        bulk_g2s(dst + static_cast<size_t>(xoff + lane - 1) * T, xa.xrow[R * NL + lane - 1] + m.s,
-                                 bytes, &full[s]);
-                    if (lane == NL + 1 && need_g)
-                        bulk_g2s(dst + static_cast<size_t>(xoff + NL) * T, g.G + m.s, bytes, &full[s]);
+                    if (has_pre) bulk_g2s(dst, pre_in + m.s, 2 * bytes, &full[s]);
+#pragma unroll
+                    for (int w = 0; w < NL; ++w)
+                        bulk_g2s(dst + static_cast<size_t>(xoff + w) * T, xa.xrow[R * NL + w] + m.s, bytes, &full[s]);
+                    if (need_g) bulk_g2s(dst + static_cast<size_t>(xoff + NL) * T, g.G + m.s, bytes, &full[s]);
                 }
             }
+            t_issue += clock64() - i0;
         }
         if (xa.dbg && lane == 0) {
             atomicAdd(xa.dbg + 0, static_cast<unsigned long long>(t_flag));
@@ -375,6 +378,8 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
             atomicAdd(xa.dbg + 7, static_cast<unsigned long long>(n_it[CI_APPLY]));
             atomicAdd(xa.dbg + 8, static_cast<unsigned long long>(n_it[CI_FIN]));
             atomicMax(xa.dbg + 10, static_cast<unsigned long long>(now_ns() - ns0));
+            atomicAdd(xa.dbg + 11, static_cast<unsigned long long>(t_next));
+            atomicAdd(xa.dbg + 12, static_cast<unsigned long long>(t_issue));
         }
         return;
     }
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 const float4 go = need_g ? *reinterpret_cast<const float4*>(buf + static_cast<size_t>(xoff + NL) * T + 4 * qd)
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
                 if (m.kind == CI_PRE) {
-                    double* pr = xa.pre[R] + f;
+                    double* pr = pre_out + f;
                     *reinterpret_cast<double2*>(pr) = make_double2(s0, s1);
                     *reinterpret_cast<double2*>(pr + 2) = make_double2(s2, s3);
                     if (m.ics) {
@@ -484,7 +489,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                     }
                     continue;
                 }
-                double sum = has_pre ? __ldcg(xa.pre[R - 1] + f) : 0.0;
+                double sum = has_pre ? __ldcg(pre_in + f) : 0.0;
                 float x[NL];
                 for (int w = 0; w < NL; ++w) {
                     x[w] = xa.xrow[R * NL + w][f];
@@ -492,7 +497,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                     sum = agg_acc(sum, ap.w[R * NL + w], x[w]);
                 }
                 if (m.kind == CI_PRE) {
-                    xa.pre[R][f] = sum;
+                    pre_out[f] = sum;
                     if (m.ics)
                         for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x[w]);
                     continue;

@@ -156,7 +156,6 @@ struct XArgs {
     unsigned* tflag[kMaxRanks];          // every rank's per-tile ready flags [NT]
     unsigned* ready[kMaxRanks];          // every rank's slots [2][kMaxRanks]: deltas ready, own tiles done
     double* pre[kMaxRanks];              // chain form: every rank's fp64 running sums [ldX]
-    int chain_pre;                       // chain form: PRE CTAs of every 4 (the rest APPLY); 0 = mixed
     int chain_lead;                      // chain form, mixed CTAs: PRE items kept ahead of APPLY
     int chain_arena;                     // chain form: ring arena in floats (set at launch)
     unsigned long long* trace;           // chain form diagnostics: [8][NT] globaltimer stamps or null

@@ -124,7 +124,7 @@ class ShardGroup:
             return None
         names = ["b_block_cycles", "empty_wait_cycles", "full_wait_cycles", "fence_cycles",
                  "producer_cycles", "b_blocks", "a_items", "b_items", "l_items", "flushes",
-                 "max_cta_ns"]
+                 "max_cta_ns", "next_item_cycles", "issue_cycles"]
         return {n: int(v) for n, v in zip(names, out)}
 
     def debug_trace(self):

@@ -98,16 +98,29 @@ def run(args, metric: str, unit: str):
     ms_step = total_ms / K
     u = sh.local.deferred_history(tag0, K).astype(np.float64) / model_bytes
     u_mean = float(u.mean())
-    # per-GPU NVLink bytes per step, each direction: the peers' delta rows this
-    # rank's shard reads + its aggregate stored into the other ranks
-    nvl_bytes = 4.0 * M * ((N - n_loc) / world + (world - 1) / world)
-    # per-GPU algorithmic HBM bytes per step (single exchange): local rows read
-    # once (by this rank or a peer) and written once, G read, the pull buffer
-    # written everywhere and read back on the peers' tiles, G (RS) / carry (ICS)
-    # written, the local rows re-read for the peers' deferred tiles, and the
-    # stage-2 broadcast (carry read, G + local rows written)
-    hbm_bytes = 4.0 * M * (2 * n_loc + 1 + 1 + (world - 1) / world + 1
-                           + u_mean * (n_loc * (world - 1) / world + 2 + n_loc))
+    sync = sh.sync_form
+    if sync == "chain":
+        # the chain (kernels/shard_chain.cu): every link r -> r+1 carries the fp64
+        # running sums (8 B per element) and the last rank serves its 4-byte
+        # aggregate to the P-1 others: the busiest direction of any GPU
+        nvl_bytes = max(8.0 * M, 4.0 * M * (world - 1))
+        # rank 0's HBM bytes (the busier rank): its rows read (4 NL), the running
+        # sums written and read by the next rank (16), G read for the deferred
+        # tiles' local estimates and for the apply (u + 1), rows written (4 NL:
+        # local estimates on deferred tiles, G' on the others), G or C written
+        # (1), and the stage-2 broadcast (carry read, G + rows written)
+        hbm_bytes = 4.0 * M * (2 * n_loc + 4 + u_mean + 1 + 1 + u_mean * (2 + n_loc))
+    else:
+        # per-GPU NVLink bytes per step, each direction: the peers' delta rows
+        # this rank's shard reads + its aggregate stored into the other ranks
+        nvl_bytes = 4.0 * M * ((N - n_loc) / world + (world - 1) / world)
+        # per-GPU algorithmic HBM bytes per step (single exchange): local rows
+        # read once (by this rank or a peer) and written once, G read, the pull
+        # buffer written everywhere and read back on the peers' tiles, G (RS) /
+        # carry (ICS) written, the local rows re-read for the peers' deferred
+        # tiles, and the stage-2 broadcast (carry read, G + local rows written)
+        hbm_bytes = 4.0 * M * (2 * n_loc + 1 + 1 + (world - 1) / world + 1
+                               + u_mean * (n_loc * (world - 1) / world + 2 + n_loc))
 
     # ---- per-phase breakdown (events between kernels, 5 profiled steps, max over ranks)
     prof = [sh.profile(k % 2) for k in range(5)]
@@ -197,14 +210,16 @@ def run(args, metric: str, unit: str):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32+f64acc", "data": "synthetic",
             "config": workload_config(args, counts),
             "arm": {"parallelism": f"ps-shard{world}", "workers_per_gpu": n_loc,
-                    "shard_mode": mode, "tile_elems": geometry["tile_elems"],
+                    "shard_mode": mode, "sync_form": sync, "tile_elems": geometry["tile_elems"],
                     "deltas": "2 device-resident sets (iterations 0 and 1) alternating",
                     "per_chunk": bool(args.per_chunk)},
             "roofline": {"bound": "nvlink" if nvl_bytes / nvl_peak > hbm_bytes / hbm_peak else "hbm",
-                         "kernel": "k_shard_x (exchange + apply, one launch per step)",
+                         "kernel": ("k_shard_chain (fp64 running-sum chain + pull of the aggregate, "
+                                    "one launch per step)" if sync == "chain" else
+                                    "k_shard_x (exchange + apply, one launch per step)"),
                          "achieved": nvl_gbs, "peak": nvl_peak, "unit": "GB/s",
                          "frac": nvl_gbs / nvl_peak, "traffic": None,
-                         "note": "per-GPU NVLink bytes each direction / step time; peak = measured "
+                         "note": "per-GPU NVLink bytes of the busiest direction / step time; peak = measured "
                                  "one-way peer copy 770 GB/s (B200_PROFILING.md); both directions "
                                  "load at once, where the measured ceiling is 667 GB/s",
                          "nvlink_bytes_per_gpu_per_direction": nvl_bytes,

@@ -116,11 +116,14 @@ def run_world(cfg, world=2, oversubscribe=False):
     assert not bad, bad
 
 
-@pytest.mark.parametrize("defer", [False, True])
-def test_shard_two_gpus_resnet_like(defer):
+@pytest.mark.parametrize("defer,sync", [(False, None), (True, None), (False, "tile"),
+                                        (False, "barrier")])
+def test_shard_two_gpus_resnet_like(defer, sync):
+    """Default form at 2 ranks (the chain for the single exchange), the
+    deferred-ICS mode, and the single exchange in the other two forms."""
     from paper_2306_16926_b200 import layouts
     run_world(dict(counts=layouts.resnet50()[:60], N=8, weights=[0.125] * 8, chunks=4,
-                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, defer=defer))
+                   budget_frac=0.5, iters=3, seed=11, p0_seed=0, defer=defer, sync=sync))
 
 
 @pytest.mark.parametrize("defer", [False, True])

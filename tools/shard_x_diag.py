@@ -62,7 +62,16 @@ def main():
     e.record()
     torch.cuda.synchronize()
     solo_ms = s.elapsed_time(e) / 20
-    sh.debug_counters()
+    solo_dbg = sh.debug_counters()
+    solo_t = torch.tensor([solo_ms], dtype=torch.float64, device="cuda")
+    solo_all = [torch.zeros_like(solo_t) for _ in range(world)]
+    dist.all_gather(solo_all, solo_t)
+    solo_per_rank = [float(x.item()) for x in solo_all]
+    sk = sorted(solo_dbg) if solo_dbg else []
+    sv = torch.tensor([solo_dbg[k] / 20 for k in sk] if solo_dbg else [0.0], dtype=torch.float64, device="cuda")
+    sva = [torch.zeros_like(sv) for _ in range(world)]
+    dist.all_gather(sva, sv)
+    solo_dbg_all = [dict(zip(sk, v.tolist())) for v in sva] if solo_dbg else None
     t = torch.tensor([step_ms, solo_ms] + [ph[k] for k in ph], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     # every rank's counters (the chain form's ranks play different roles)
@@ -81,7 +90,8 @@ def main():
                           "world": world, "step_ms": vals[0], "solo_exchange_ms": vals[1],
                           "phases_ms": dict(zip(ph, vals[2:])),
                           "nvlink_GBps_step": nvl / (vals[0] * 1e-3) / 1e9,
-                          "sync": sh.sync_form,
+                          "sync": sh.sync_form, "solo_ms_per_rank": solo_per_rank,
+                          "solo_debug_per_step": solo_dbg_all,
                           "debug_per_step": dbg_all}), flush=True)
     sh.close()
     dist.destroy_process_group()
