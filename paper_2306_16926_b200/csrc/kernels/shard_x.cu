@@ -31,7 +31,7 @@
 //
 // Ordering across GPUs: at launch every CTA signals "this iteration's delta rows
 // are ready" (epoch) into every peer's ready slots and waits for every peer's
-// before its first A item; a rank at iteration i has finished iteration i-1's
+// before its first A item (or, with none, before it ends); a rank at iteration i has finished iteration i-1's
 // kernels, so the pull buffer, partials and flags need no double buffering.
 // Tile flags carry the iteration number (each tile is exchanged once per
 // iteration) and are never reset. Every wait is bounded (20 s) and records an
@@ -387,6 +387,19 @@ __global__ void __launch_bounds__((CW + 2) * 32) k_shard_x(GroupView g, AggParam
             sc.next(ready != 0, kind, q, k);  // every lane, same result
             XMeta m{};
             if (kind < 0) {
+                // A CTA that exchanged nothing still waits for every peer's
+                // deltas-ready epoch before it ends: the stage-2 (ICS) launch of
+                // the same iteration reads the peers' rows on the strength of
+                // this launch's wait (a budget of the whole model leaves stage 1
+                // without barrier tiles), and a rank must not run ahead into the
+                // next iteration's rows while a peer still reads this one's.
+                if (!peers_ready && do_a) {
+                    if (lane == 0)
+                        for (int p = 0; p < P; ++p)
+                            if (p != R) xspin(xa.ready[R] + p, xa.epoch, xa.error);
+                    __syncwarp();
+                    peers_ready = true;
+                }
                 if (lane == 0) {
                     m.t = -1;
                     meta[s] = m;

@@ -58,6 +58,10 @@ def _worker(rank, world, port, cfg, q):
         order = np.zeros(0, np.int32)
         for it in range(cfg["iters"]):
             buf = it % 2
+            if rank == cfg.get("lag_rank", -1):  # this rank's host falls behind its peers
+                import time
+                torch.cuda.synchronize()
+                time.sleep(0.3)
             sh.fill_synth(cfg["seed"], it, buf)
             deltas = np.stack([oracle.synth_delta(cfg["seed"], k, it, M) for k in range(N)])
             for (dst, src, n) in cfg.get("copy_layers", []):  # identical layers: exact PGP ties
@@ -211,6 +215,19 @@ def test_shard_oversubscribed_ragged(world, N, frac):
     run_world(cfg, world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True, defer=True), world=world, oversubscribe=True)
     run_world(dict(cfg, per_chunk=True), world=world, oversubscribe=True)
+
+
+@pytest.mark.parametrize("per_chunk", [False, True])
+def test_shard_deferred_all_ics_lagging_rank(per_chunk):
+    """Budget = the whole model in the deferred-ICS mode: from iteration 1 stage 1
+    exchanges no barrier tile, so its launch must still establish that every
+    peer's deltas of the iteration are in place before stage 2 reads them; rank 1's
+    host lags every iteration to expose a missing wait."""
+    rng = np.random.default_rng(61)
+    w = [float(x) for x in 0.1 + rng.random(4)]
+    cfg = dict(counts=_ragged(17, 15, 6000), N=4, weights=w, chunks=3, budget_frac=1.0,
+               iters=4, seed=3, p0_seed=2, defer=True, per_chunk=per_chunk, lag_rank=1)
+    run_world(cfg, world=2, oversubscribe=True)
 
 
 @pytest.mark.parametrize("sync", ["chain", "tile"])

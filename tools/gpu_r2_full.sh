@@ -11,3 +11,5 @@ python -c "
 import json
 d=json.loads(open('gpurun_out/r2_bench_default.json').read().strip().splitlines()[-1]); o=d['overlap']; cl=o.pop('closed_loop')
 print(d['ms_per_step'], d['roofline']['frac'], d['roofline']['step_frac'], d['e2e']['ms_per_step'], o, cl['epoch_budgets'], d['cpu_baseline']['value'])"
+timeout 900 python bench.py --impl reference --steps 20 --warmup 5 > gpurun_out/r2_bench_reference.json 2> gpurun_out/r2_bench_reference.err
+tail -1 gpurun_out/r2_bench_reference.json | cut -c1-400
