@@ -15,7 +15,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo --fmad=false -std=c++17 -Xcompiler -fPIC -Xcomp
            -Iinclude -I$(CSRC) --expt-relaxed-constexpr -Xptxas -warn-spills
 
 CU_SRCS := $(CSRC)/kernels/stage.cu $(CSRC)/kernels/resolve.cu $(CSRC)/kernels/elementwise.cu \
-           $(CSRC)/kernels/codec.cu $(CSRC)/kernels/stage_tma.cu $(CSRC)/kernels/step_small.cu $(CSRC)/kernels/shard_x.cu $(CSRC)/kernels/shard_chain.cu $(CSRC)/capi/osp_capi.cu $(CSRC)/capi/osp_shard.cu \
+           $(CSRC)/kernels/codec.cu $(CSRC)/kernels/stage_tma.cu $(CSRC)/kernels/step_small.cu $(CSRC)/kernels/shard_x.cu $(CSRC)/kernels/shard_chain.cu $(CSRC)/kernels/learner.cu $(CSRC)/capi/osp_capi.cu $(CSRC)/capi/osp_shard.cu $(CSRC)/capi/osp_learner.cu \
            $(CSRC)/capi/osp_codec.cu
 CU_OBJS := $(patsubst $(CSRC)/%.cu,build/%.o,$(CU_SRCS))
 HDRS := include/osp_c.h $(CSRC)/osp_internal.h $(CSRC)/kernels/common.cuh $(CSRC)/kernels/tma.cuh $(CSRC)/kernels/shard_common.cuh $(CSRC)/capi/handles.h

@@ -458,6 +458,39 @@ uint64_t osp_shard_debug_trace(osp_shard* s, unsigned long long* out, uint64_t n
 osp_status osp_synth_deltas_range(uint64_t seed, int worker0, int n_workers, uint64_t iteration,
                                   uint64_t n, float* out, uint64_t ld, void* stream);
 
+/* ------------------------------------------------------------------------
+ * Learner: the gradient producer on the other side of the sync path — the
+ * reference learner's MLP forward_backward (learner.hpp:63-64,
+ * learner.cpp:299-367) for N workers at once over a device-resident dataset
+ * (Dataset, learner.hpp:23-31: features [n][widths[0]] row-major, labels [n]).
+ * Parameters are the partition-ordered vector W0, b0, W1, b1, ... of
+ * mlp_partition (learner.hpp:51-53), one row per worker (e.g. the group's
+ * worker rows); gradients come out as float rows, ready for an OSP group
+ * created with sgd_lr > 0 (the step applies sgd_delta, learner.cpp:391-398).
+ * fp64 arithmetic in the reference's order: relu+MSE is bit-exact; tanh and
+ * the softmax's exp/log use CUDA's libm (tolerance, tests/test_gpu_learner.py).
+ * ---------------------------------------------------------------------- */
+typedef struct osp_mlp osp_mlp;
+#define OSP_ACT_RELU 0
+#define OSP_ACT_TANH 1
+#define OSP_LOSS_CE 0  /* Loss::softmax_cross_entropy */
+#define OSP_LOSS_MSE 1 /* Loss::mse */
+/* ConfigError for the MlpSpec::validate cases (learner.cpp:15-20); the dataset
+ * pointers are borrowed (device memory, must outlive the handle). */
+osp_status osp_mlp_create(const int32_t* widths, int n_widths, int activation, int loss,
+                          const float* features, const int32_t* labels, uint64_t n_rows,
+                          osp_mlp** out);
+void osp_mlp_destroy(osp_mlp* m);
+uint64_t osp_mlp_num_params(const osp_mlp* m);
+/* Asynchronous: batch is [n_workers][batch_size] device row indices; grad_out
+ * [n_workers][ld_out] floats; loss_out (device, may be NULL) [n_workers] mean
+ * batch losses. Row / label range and finiteness are flagged on the device and
+ * reported by osp_mlp_check (ShapeError / NumericError, as the reference throws). */
+osp_status osp_mlp_grad(osp_mlp* m, const float* params, uint64_t ld_params, int n_workers,
+                        const int32_t* batch, int batch_size, float* grad_out, uint64_t ld_out,
+                        double* loss_out, void* stream);
+osp_status osp_mlp_check(osp_mlp* m, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -75,6 +75,13 @@ _SIGS = {
                                            c_void_p]),
     "osp_apply_delta": (c_int, [c_void_p, c_void_p, c_u64, c_float, c_void_p]),
     "osp_sgd_delta": (c_int, [c_void_p, c_u64, c_dbl, c_void_p, c_void_p]),
+    "osp_mlp_create": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_u64,
+                               P(c_void_p)]),
+    "osp_mlp_destroy": (None, [c_void_p]),
+    "osp_mlp_num_params": (c_u64, [c_void_p]),
+    "osp_mlp_grad": (c_int, [c_void_p, c_void_p, c_u64, c_int, c_void_p, c_int, c_void_p, c_u64,
+                             c_void_p, c_void_p]),
+    "osp_mlp_check": (c_int, [c_void_p, c_void_p]),
     "osp_synth_delta": (c_int, [c_u64, c_u64, c_u64, c_u64, c_u64, c_void_p, c_void_p]),
     "osp_synth_deltas": (c_int, [c_u64, c_int, c_u64, c_u64, c_void_p, c_u64, c_void_p]),
     "osp_lgp_partial": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(ctypes.c_uint8),

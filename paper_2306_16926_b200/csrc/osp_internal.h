@@ -190,6 +190,29 @@ cudaError_t launch_shard_peer_apply(const GroupView& g, const AggParams& ap, con
 bool shard_chain_supported(int n_loc, int T, int L);
 cudaError_t launch_shard_chain(const GroupView& g, const AggParams& ap, const XArgs& xa, cudaStream_t s);
 
+// ---- gradient producer: the reference learner's MLP forward/backward (kernels/learner.cu)
+constexpr int kMlpMaxDepth = 8;  // linear layers
+struct MlpArgs {
+    int depth;                       // linear layers
+    int widths[kMlpMaxDepth + 1];    // input, hidden..., output
+    int act;                         // 0 relu, 1 tanh
+    int loss;                        // 0 softmax cross-entropy, 1 MSE
+    int maxw;                        // largest width
+    int B;                           // batch rows per worker
+    const float* P;                  // [N][ldP] worker parameter rows
+    uint64_t ldP;
+    const float* feats;              // [n][widths[0]] dataset rows
+    uint64_t n_rows;                 // n
+    const int* labels;               // [n]
+    const int* batch;                // [N][B] row indices
+    float* out;                      // [N][ldo] float gradients
+    uint64_t ldo;
+    double* loss_out;                // [N] mean batch loss, or null
+    unsigned* error;                 // 1 non-finite (NumericError), 2 label out of range (ShapeError)
+};
+size_t mlp_grad_smem(const MlpArgs& a);
+cudaError_t launch_mlp_grad(const MlpArgs& a, int n_workers, cudaStream_t s);
+
 // Opt a kernel into `smem` bytes of dynamic shared memory and return its
 // occupancy, cached per (context, kernel, bytes) (stage_tma.cu).
 cudaError_t tma_blocks_per_sm(const void* kern, int threads, size_t smem, int* per_sm);
