@@ -91,12 +91,14 @@ def test_errors_as_the_reference_throws(mods):
     labels[3] = 5
     with pytest.raises(osp.ShapeError):  # label exceeds output width
         mlp.grad(P, torch.tensor([[3]], dtype=torch.int32, device="cuda"))
-    P[0, 0] = float("nan")
-    feats[1, 0] = 1.0
+    # a NaN output bias (W0 12, b0 4, W1 8, then b1): the loss is not finite
+    # (a NaN in a hidden pre-activation would not be: relu maps it to 0, as in
+    # the reference's z > 0 ? z : 0.0)
+    P[0, 24] = float("nan")
     with pytest.raises(osp.NumericError):
         mlp.grad(P, torch.tensor([[1]], dtype=torch.int32, device="cuda"))
     # the flag is cleared once reported
-    P[0, 0] = 0.0
+    P[0, 24] = 0.0
     mlp.grad(P, torch.tensor([[1]], dtype=torch.int32, device="cuda"))
 
 
