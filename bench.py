@@ -287,6 +287,92 @@ def reference_arm(args, rank: int):
 
 # ---- the B200 arm ---------------------------------------------------------------
 
+MLP_WIDTHS = {"mlp": [8, 32, 4], "mlp_acc": [16, 64, 64, 4]}
+
+
+def training_pass(args, N: int, K: int):
+    """Config #1's whole training iteration on the device (MLP layouts): every
+    worker's gradient from its own parameter row (the reference learner's
+    forward_backward, kernels/learner.cu; config.hpp:30-41's default spec, relu +
+    softmax CE, batch 32) and the OSP step with the fused sgd_delta, G iterations
+    per CUDA graph, two batch sets alternating. Synthetic Gaussian-blob dataset
+    (the shape of pslab::synth_dataset: n 1024, classes = output width)."""
+    import torch
+
+    from paper_2306_16926_b200 import layouts, learner, osp
+    widths = MLP_WIDTHS[args.layout]
+    counts = layouts.get(args.layout)
+    M = sum(counts)
+    n, d, k, B = 1024, widths[0], widths[-1], 32
+    gen = torch.Generator(device="cpu").manual_seed(args.seed)
+    labels = torch.arange(n, dtype=torch.int32) % k
+    feats = torch.randn((n, d), generator=gen, dtype=torch.float32)
+    feats[:, 0] += 6.0 * labels.float()
+    feats, labels = feats.cuda(), labels.cuda()
+    batches = [torch.randint(0, n, (N, B), generator=gen, dtype=torch.int32).cuda() for _ in range(2)]
+    mlp = learner.Mlp(widths, feats, labels, "relu", "ce")
+    p0 = (torch.rand(M, generator=gen) * 0.2 - 0.1).cuda()
+    grp = osp.OspGroup(osp.Partition(counts), N, [1.0 / N] * N, n_chunks=args.chunks,
+                       init_params=p0, sgd_lr=0.05)
+    grp.set_budget(int(args.budget_frac * M * 4))
+    grads = torch.empty((N, M), dtype=torch.float32, device="cuda")
+    losses = torch.empty(N, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def it(j, producer_only=False):
+        mlp.grad(grp.worker_params, batches[j % 2], out=grads, losses=losses, check=False)
+        if not producer_only:
+            grp.step(grads)
+
+    def timed(producer_only):
+        G = max(2, args.graph_steps + args.graph_steps % 2)
+        reps = max(1, K // G)
+        for j in range(4):
+            it(j, producer_only)
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(stream)
+        with torch.cuda.graph(g, stream=cs, capture_error_mode="thread_local"):
+            for j in range(G):
+                it(j, producer_only)
+        torch.cuda.synchronize()
+        g.replay()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(reps):
+            g.replay()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / (reps * G), reps * G
+
+    ms_it, n_it = timed(False)
+    ms_prod, _ = timed(True)
+    mlp.check()
+    out = {"ms_per_iteration": ms_it, "us_per_iteration": ms_it * 1e3,
+           "producer_us": ms_prod * 1e3, "iterations": n_it,
+           "spec": {"widths": widths, "activation": "relu", "loss": "softmax_cross_entropy",
+                    "batch": B, "workers": N, "sgd_lr": 0.05},
+           "launches_per_iteration": 1 + (1 if grp.single_launch else 3),
+           "data": "synthetic Gaussian blobs on the device (n 1024), random batches",
+           "note": "osp_mlp_grad (every worker's forward_backward, learner.cpp:299-367) + "
+                   "osp_group_step with the fused sgd_delta, from a CUDA graph"}
+    grp.close()
+    return out
+
+
+def reference_learner_us(widths, N: int):
+    """The reference learner's forward_backward for N workers, one host thread
+    (oracle/_ref/ref_fb --bench; cpu_baseline leg only)."""
+    drv = os.path.join(REPO, "oracle", "_ref", "ref_fb")
+    if not os.path.exists(drv):
+        return None
+    r = subprocess.run([drv, "--bench", ",".join(str(w) for w in widths), "relu", "ce", "32",
+                        str(N), "2000" if widths[-1] <= 4 and len(widths) == 3 else "200"],
+                       capture_output=True, text=True, timeout=300)
+    return json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else None
+
+
 def b200_single(args):
     import numpy as np
     import torch
@@ -557,6 +643,8 @@ def b200_single(args):
         "clocks": clk,
         "overlap": ovl,
     }
+    if args.layout in MLP_WIDTHS:
+        line["training"] = training_pass(args, N, K)
     if not args.no_cpu_baseline:
         try:
             cb = run_reference_cpu(args.layout, N, args.budget_frac, args.chunks, args.seed,
@@ -565,6 +653,19 @@ def b200_single(args):
             line["cpu_baseline"].update(host_cpu())
         except Exception as e:  # reported, not fatal
             line["cpu_baseline"] = {"error": str(e)[:200]}
+        if args.layout in MLP_WIDTHS:
+            try:
+                rl = reference_learner_us(MLP_WIDTHS[args.layout], N)
+                if rl and "training" in line:
+                    sync_us = (M / cb["value"]) * 1e6 if "value" in line["cpu_baseline"] else None
+                    line["training"]["reference_cpu"] = {
+                        "learner_us": rl["us_per_iteration"], "sync_us": sync_us,
+                        "us_per_iteration": rl["us_per_iteration"] + (sync_us or 0.0),
+                        "kind": "reference", "cores": 1,
+                        "sample": f"{rl['reps']} iterations of {N} workers' forward_backward "
+                                  "(oracle/_ref/ref_fb --bench) + the sync step above"}
+            except Exception as e:
+                line["training"]["reference_cpu"] = {"error": str(e)[:200]}
     print(json.dumps(line), flush=True)
 
 

@@ -4,12 +4,14 @@
 // gen_learner_golden.py). Test infrastructure only; built by `make -C oracle
 // ref` into oracle/_ref/ against the reference sources.
 //
-// Usage: ref_fb <out_dir>
+// Usage: ref_fb <out_dir>   |   ref_fb --bench <widths> <act> <loss> <batch> <workers> <reps>
 // For every case: <out>/<name>.meta (text: widths, activation, loss, n, d,
 // workers, batch) and <name>.{feat.f32, label.i32, param.f32, batch.i32,
 // grad.f32, loss.f64}.
 
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <fstream>
 #include <string>
 #include <vector>
@@ -79,9 +81,46 @@ void run(const std::string& out, const Case& c) {
 
 }  // namespace
 
+// bench mode: the reference learner's cost per training iteration of config
+// #1's shape: forward_backward of every worker's batch, one host thread
+// (the reference harness runs the workers' learners one after the other).
+int bench(int argc, char** argv) {
+    // ref_fb --bench <w0,w1,...> <relu|tanh> <ce|mse> <batch> <workers> <reps>
+    if (argc < 8) return 2;
+    MlpSpec spec;
+    for (const char* p = argv[2]; *p;) {
+        spec.widths.push_back(std::atoi(p));
+        while (*p && *p != ',') ++p;
+        if (*p) ++p;
+    }
+    spec.activation = std::string(argv[3]) == "tanh" ? Activation::tanh : Activation::relu;
+    spec.loss = std::string(argv[4]) == "mse" ? Loss::mse : Loss::softmax_cross_entropy;
+    const size_t B = std::strtoul(argv[5], nullptr, 10);
+    const int N = std::atoi(argv[6]), reps = std::atoi(argv[7]);
+    Dataset ds = synth_dataset(7, 1024, static_cast<size_t>(spec.widths.front()),
+                               static_cast<size_t>(spec.widths.back()), 6.0);
+    std::vector<ParamVector> ps;
+    std::vector<Batch> bs;
+    for (int w = 0; w < N; ++w) {
+        ps.push_back(init_params(spec, 100 + static_cast<uint64_t>(w)));
+        std::vector<size_t> perm = shuffle_epoch(ds.n, 7, 1, static_cast<uint64_t>(w));
+        bs.emplace_back(perm.begin(), perm.begin() + static_cast<long>(B));
+    }
+    double sink = 0.0;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r)
+        for (int w = 0; w < N; ++w) sink += forward_backward(spec, ps[w], ds, bs[w]).loss;
+    auto t1 = std::chrono::steady_clock::now();
+    const double us = std::chrono::duration<double, std::micro>(t1 - t0).count() / reps;
+    std::printf("{\"us_per_iteration\": %.4f, \"workers\": %d, \"batch\": %zu, \"reps\": %d, "
+                "\"sink\": %.3f}\n", us, N, B, reps, sink);
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc >= 2 && std::string(argv[1]) == "--bench") return bench(argc, argv);
     if (argc < 2) {
-        std::fprintf(stderr, "usage: ref_fb <out_dir>\n");
+        std::fprintf(stderr, "usage: ref_fb <out_dir> | ref_fb --bench ...\n");
         return 2;
     }
     const std::string out = argv[1];

@@ -45,6 +45,7 @@ osp_status osp_mlp_create(const int32_t* widths, int n_widths, int activation, i
     }
     a.act = activation == OSP_ACT_TANH ? 1 : 0;
     a.loss = loss == OSP_LOSS_MSE ? 1 : 0;
+    a.n_params = m->n_params;
     a.feats = features;
     a.labels = labels;
     a.n_rows = n_rows;

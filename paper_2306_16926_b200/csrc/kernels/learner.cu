@@ -18,14 +18,15 @@
 // (tests/test_gpu_learner.py).
 //
 // Shared memory per CTA: pre-activations and activations of every sample and
-// layer, and two delta buffers (B x max width), all fp64.
+// layer, two delta buffers (B x max width) and the worker's parameters, all
+// fp64.
 
 #include "common.cuh"
 
 namespace osp {
 namespace {
 
-constexpr int kLearnThreads = 256;
+constexpr int kLearnThreads = 512;
 
 __device__ __forceinline__ double act_fwd(int act, double z) {
     return act == 0 ? (z > 0.0 ? z : 0.0) : tanh(z);
@@ -35,6 +36,7 @@ __device__ __forceinline__ double act_bwd(int act, double z, double a) {
     return act == 0 ? (z > 0.0 ? 1.0 : 0.0) : __dsub_rn(1.0, __dmul_rn(a, a));
 }
 
+template <bool SW>  // SW: the worker's parameters staged in shared memory as doubles
 __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
     extern __shared__ __align__(16) double lsm[];
     const int w = blockIdx.x;
@@ -45,13 +47,21 @@ __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
     int off[kMlpMaxDepth + 2];
     off[0] = 0;
     for (int l = 0; l <= depth; ++l) off[l + 1] = off[l] + a.widths[l];
-    const int S = off[depth + 1];
+    // rows of an odd number of doubles: a warp walking samples (one row each)
+    // touches 16 distinct 8-byte banks per half-warp
+    const int S = off[depth + 1] | 1;
     double* act = lsm;
     double* pre = act + static_cast<size_t>(B) * S;
     double* dzA = pre + static_cast<size_t>(B) * S;
     double* dzB = dzA + static_cast<size_t>(B) * a.maxw;
     double* sloss = dzB + static_cast<size_t>(B) * a.maxw;
-    const float* P = a.P + static_cast<uint64_t>(w) * a.ldP;
+    // this worker's parameters as doubles in shared memory (every forward and
+    // backward inner loop reads them; exact conversion)
+    double* Pd = sloss + B;
+    const float* Pg = a.P + static_cast<uint64_t>(w) * a.ldP;
+    if (SW)
+        for (uint64_t k = tid; k < a.n_params; k += blockDim.x) Pd[k] = static_cast<double>(Pg[k]);
+    auto wv = [&](uint64_t k) -> double { return SW ? Pd[k] : static_cast<double>(Pg[k]); };
     const int* batch = a.batch + static_cast<size_t>(w) * B;
     float* out = a.out + static_cast<uint64_t>(w) * a.ldo;
 
@@ -72,14 +82,13 @@ __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
     uint64_t at = 0;  // parameter offset of layer l (W then b)
     for (int l = 0; l < depth; ++l) {
         const int in = a.widths[l], outw = a.widths[l + 1];
-        const float* W = P + at;
-        const float* bias = W + static_cast<uint64_t>(in) * outw;
+        const uint64_t bias = at + static_cast<uint64_t>(in) * outw;
         for (int k = tid; k < B * outw; k += blockDim.x) {
-            const int s = k / outw, o = k % outw;
+            const int s = k % B, o = k / B;  // lanes walk samples: the W row is a broadcast
             const double* ain = act + static_cast<size_t>(s) * S + off[l];
-            double z = static_cast<double>(bias[o]);
-            const float* wr = W + static_cast<uint64_t>(o) * in;
-            for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(static_cast<double>(wr[i]), ain[i]));
+            double z = wv(bias + o);
+            const uint64_t wr = at + static_cast<uint64_t>(o) * in;
+            for (int i = 0; i < in; ++i) z = __dadd_rn(z, __dmul_rn(wv(wr + i), ain[i]));
             pre[static_cast<size_t>(s) * S + off[l + 1] + o] = z;
             act[static_cast<size_t>(s) * S + off[l + 1] + o] = l + 1 < depth ? act_fwd(a.act, z) : z;
         }
@@ -131,7 +140,6 @@ __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
     for (int l = depth - 1; l >= 0; --l) {
         const int in = a.widths[l], outw = a.widths[l + 1];
         at -= static_cast<uint64_t>(in) * outw + outw;
-        const float* W = P + at;
         // weight and bias gradients: per-sample terms summed in batch order
         for (int k = tid; k < in * outw + outw; k += blockDim.x) {
             double acc = 0.0;
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
                 double v = 0.0;
                 for (int o = 0; o < outw; ++o)
                     v = __dadd_rn(v, __dmul_rn(dz[static_cast<size_t>(s) * a.maxw + o],
-                                               static_cast<double>(W[static_cast<uint64_t>(o) * in + i])));
+                                               wv(at + static_cast<uint64_t>(o) * in + i)));
                 const size_t q = static_cast<size_t>(s) * S + off[l] + i;
                 dn[static_cast<size_t>(s) * a.maxw + i] = __dmul_rn(v, act_bwd(a.act, pre[q], act[q]));
             }
@@ -168,18 +176,26 @@ __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
 
 }  // namespace
 
-size_t mlp_grad_smem(const MlpArgs& a) {
+size_t mlp_smem_bytes(const MlpArgs& a, bool stage_w) {
     int S = 0;
     for (int l = 0; l <= a.depth; ++l) S += a.widths[l];
-    return (2ull * a.B * S + 2ull * a.B * a.maxw + a.B) * sizeof(double);
+    S |= 1;
+    return (2ull * a.B * S + 2ull * a.B * a.maxw + a.B + (stage_w ? a.n_params : 0)) * sizeof(double);
 }
 
+// parameters staged in shared memory when the whole CTA still fits
+bool mlp_stage_w(const MlpArgs& a) { return mlp_smem_bytes(a, true) <= 200 * 1024; }
+
+size_t mlp_grad_smem(const MlpArgs& a) { return mlp_smem_bytes(a, mlp_stage_w(a)); }
+
 cudaError_t launch_mlp_grad(const MlpArgs& a, int n_workers, cudaStream_t s) {
-    const size_t sm = mlp_grad_smem(a);
+    const bool sw = mlp_stage_w(a);
+    const size_t sm = mlp_smem_bytes(a, sw);
+    void (*kern)(MlpArgs) = sw ? k_mlp_grad<true> : k_mlp_grad<false>;
     int per_sm = 0;  // opts the kernel into `sm` bytes (cached per context)
-    cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(k_mlp_grad), kLearnThreads, sm, &per_sm);
+    cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), kLearnThreads, sm, &per_sm);
     if (e != cudaSuccess) return e;
-    k_mlp_grad<<<n_workers, kLearnThreads, sm, s>>>(a);
+    kern<<<n_workers, kLearnThreads, sm, s>>>(a);
     return cudaGetLastError();
 }
 

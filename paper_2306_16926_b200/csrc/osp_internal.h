@@ -199,6 +199,7 @@ struct MlpArgs {
     int loss;                        // 0 softmax cross-entropy, 1 MSE
     int maxw;                        // largest width
     int B;                           // batch rows per worker
+    uint64_t n_params;               // mlp_partition total
     const float* P;                  // [N][ldP] worker parameter rows
     uint64_t ldP;
     const float* feats;              // [n][widths[0]] dataset rows
