@@ -329,6 +329,15 @@ osp_status osp_group_step(osp_group* g, const float* deltas, uint64_t ld, void* 
  * (protocol.hpp). Synchronous. */
 osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t host_ld,
                                uint8_t* gib_out, float* params_out, void* stream);
+/* Pipelined osp_group_step_host: returns once issued. Call k's H2D (its own
+ * copy stream, one of two staging buffers) overlaps call k-1's step and D2H;
+ * the step runs on `stream`. gib_out / params_out are written when
+ * osp_group_host_wait returns (or when a later call's step has started); host
+ * buffers should be pinned, and host_deltas must stay unchanged until the
+ * next-but-one call or the wait. */
+osp_status osp_group_step_host_async(osp_group* g, const float* host_deltas, uint64_t host_ld,
+                                     uint8_t* gib_out, float* params_out, void* stream);
+osp_status osp_group_host_wait(osp_group* g);
 
 /* Device pointers into the group state (valid until destroy). */
 float* osp_group_global(osp_group* g);

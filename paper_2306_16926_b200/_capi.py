@@ -131,6 +131,9 @@ _SIGS = {
     "osp_group_set_momentum": (c_int, [c_void_p, c_dbl, c_void_p]),
     "osp_group_step_host": (c_int, [c_void_p, c_void_p, c_u64, P(ctypes.c_uint8), c_void_p,
                                     c_void_p]),
+    "osp_group_step_host_async": (c_int, [c_void_p, c_void_p, c_u64, c_void_p, c_void_p,
+                                          c_void_p]),
+    "osp_group_host_wait": (c_int, [c_void_p]),
     "osp_group_global": (c_void_p, [c_void_p]),
     "osp_group_worker_params": (c_void_p, [c_void_p, P(c_u64)]),
     "osp_group_scores": (c_void_p, [c_void_p]),

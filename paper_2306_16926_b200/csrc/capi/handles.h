@@ -40,6 +40,11 @@ struct osp_group {
     std::vector<void*> owned;
     int* d_order_tmp = nullptr;
     float* d_staging = nullptr;
+    // osp_group_step_host_async: two staging buffers, copy streams, events
+    float* d_stage2[2] = {nullptr, nullptr};
+    cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr}, ev_d2h = nullptr;
+    unsigned long long n_async = 0;
 };
 
 // NVTX range over a C-ABI call (header-only NVTX3: a no-op unless a tool such as

@@ -893,6 +893,14 @@ void osp_group_destroy(osp_group* g) {
     cudaDeviceSynchronize();
     for (void* p : g->owned) cudaFree(p);
     if (g->d_staging) cudaFree(g->d_staging);
+    for (int b = 0; b < 2; ++b) {
+        if (g->d_stage2[b]) cudaFree(g->d_stage2[b]);
+        if (g->ev_h2d[b]) cudaEventDestroy(g->ev_h2d[b]);
+        if (g->ev_used[b]) cudaEventDestroy(g->ev_used[b]);
+    }
+    if (g->ev_d2h) cudaEventDestroy(g->ev_d2h);
+    if (g->s_h2d) cudaStreamDestroy(g->s_h2d);
+    if (g->s_d2h) cudaStreamDestroy(g->s_d2h);
     delete g;
 }
 
@@ -1051,6 +1059,54 @@ osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t 
     if (params_out)
         OSP_CUDA(cudaMemcpyAsync(params_out, g->v.G, M * 4, cudaMemcpyDeviceToHost, s));
     OSP_CUDA(cudaStreamSynchronize(s));
+    return OSP_OK;
+}
+
+// Pipelined host step: call k's H2D (copy stream, staging buffer k % 2) runs
+// beside call k-1's step and D2H; the step waits for its rows and for the
+// previous D2H of the global vector (which it is about to update); the D2H of
+// its GIB and global vector runs on a third stream.
+osp_status osp_group_step_host_async(osp_group* g, const float* host_deltas, uint64_t host_ld,
+                                     uint8_t* gib_out, float* params_out, void* stream) {
+    OSP_RANGE("osp_group_step_host_async");
+    if (!g || !host_deltas) return fail(OSP_ERR_INVALID, "null argument");
+    const uint64_t M = g->part->total;
+    if (host_ld < M) return fail(OSP_ERR_SHAPE, "delta rows shorter than the partition");
+    cudaStream_t s = as_stream(stream);
+    if (!g->s_h2d) {
+        OSP_CUDA(cudaStreamCreateWithFlags(&g->s_h2d, cudaStreamNonBlocking));
+        OSP_CUDA(cudaStreamCreateWithFlags(&g->s_d2h, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            OSP_CUDA(cudaMalloc(&g->d_stage2[b], g->v.ldP * g->N * 4));
+            OSP_CUDA(cudaEventCreateWithFlags(&g->ev_h2d[b], cudaEventDisableTiming));
+            OSP_CUDA(cudaEventCreateWithFlags(&g->ev_used[b], cudaEventDisableTiming));
+        }
+        OSP_CUDA(cudaEventCreateWithFlags(&g->ev_d2h, cudaEventDisableTiming));
+    }
+    const int b = static_cast<int>(g->n_async & 1);
+    if (g->n_async >= 2) OSP_CUDA(cudaStreamWaitEvent(g->s_h2d, g->ev_used[b], 0));  // step k-2 read it
+    OSP_CUDA(cudaMemcpy2DAsync(g->d_stage2[b], g->v.ldP * 4, host_deltas, host_ld * 4, M * 4, g->N,
+                               cudaMemcpyHostToDevice, g->s_h2d));
+    OSP_CUDA(cudaEventRecord(g->ev_h2d[b], g->s_h2d));
+    OSP_CUDA(cudaStreamWaitEvent(s, g->ev_h2d[b], 0));
+    if (g->n_async >= 1) OSP_CUDA(cudaStreamWaitEvent(s, g->ev_d2h, 0));
+    OSP_TRY(osp_group_step(g, g->d_stage2[b], g->v.ldP, stream));
+    OSP_CUDA(cudaEventRecord(g->ev_used[b], s));
+    OSP_CUDA(cudaStreamWaitEvent(g->s_d2h, g->ev_used[b], 0));
+    if (gib_out)
+        OSP_CUDA(cudaMemcpyAsync(gib_out, g->v.gib_bytes, osp_gib_encoded_size(g->v.L),
+                                 cudaMemcpyDeviceToHost, g->s_d2h));
+    if (params_out)
+        OSP_CUDA(cudaMemcpyAsync(params_out, g->v.G, M * 4, cudaMemcpyDeviceToHost, g->s_d2h));
+    OSP_CUDA(cudaEventRecord(g->ev_d2h, g->s_d2h));
+    g->n_async += 1;
+    return OSP_OK;
+}
+
+osp_status osp_group_host_wait(osp_group* g) {
+    if (!g) return fail(OSP_ERR_INVALID, "null group");
+    if (g->s_d2h) OSP_CUDA(cudaStreamSynchronize(g->s_d2h));
+    if (g->s_h2d) OSP_CUDA(cudaStreamSynchronize(g->s_h2d));
     return OSP_OK;
 }
 

@@ -599,6 +599,38 @@ class OspGroup:
         p, ld = self._deltas(deltas)
         _check(lib().osp_group_step(self._h, p, ld, _stream(stream)))
 
+    def _host_args(self, host_deltas, params_out):
+        if isinstance(host_deltas, torch.Tensor):
+            if host_deltas.device.type != "cpu" or host_deltas.dtype != torch.float32:
+                raise InvalidArgument("host deltas must be a float32 CPU tensor")
+            if host_deltas.dim() != 2 or host_deltas.stride(1) != 1:
+                raise ShapeError("host deltas must be [N, >=M] with unit inner stride")
+            shape, ptr, ld = tuple(host_deltas.shape), host_deltas.data_ptr(), host_deltas.stride(0)
+        else:
+            raise InvalidArgument("the pipelined host step takes pinned torch CPU tensors")
+        if shape[0] != self.N or shape[1] < self.M:
+            raise ShapeError(f"host deltas are {list(shape)}, need [{self.N}, >={self.M}]")
+        pout = None
+        if params_out is not None:
+            if not (isinstance(params_out, torch.Tensor) and params_out.device.type == "cpu"
+                    and params_out.dtype == torch.float32 and params_out.is_contiguous()
+                    and params_out.numel() == self.M):
+                raise ShapeError("params_out must be a contiguous float32 CPU tensor of M")
+            pout = params_out.data_ptr()
+        return ptr, ld, pout
+
+    def step_host_async(self, host_deltas: torch.Tensor, params_out: Optional[torch.Tensor] = None,
+                        gib_out: Optional[torch.Tensor] = None, stream=None):
+        """Pipelined step_host (osp_group_step_host_async): returns once issued;
+        this call's H2D overlaps the previous call's step and D2H. Outputs are
+        valid after host_wait()."""
+        ptr, ld, pout = self._host_args(host_deltas, params_out)
+        gout = gib_out.data_ptr() if gib_out is not None else None
+        _check(lib().osp_group_step_host_async(self._h, ptr, ld, gout, pout, _stream(stream)))
+
+    def host_wait(self):
+        _check(lib().osp_group_host_wait(self._h))
+
     def step_host(self, host_deltas, stream=None, params_out=None) -> bytes:
         """End-to-end step from host memory: H2D copy of the N delta rows, the
         step, and D2H of the next GIB and of the updated global vector (every

@@ -591,6 +591,34 @@ def test_gib_wire_installs_like_set_gib(osp):
         osp.OspGroup(osp.Partition(counts[:5]), N).set_gib_wire(w)
 
 
+def test_step_host_async_pipelined(osp):
+    """osp_group_step_host_async: five pipelined calls (each call's H2D beside
+    the previous step and D2H), then the wait: every call's updated global
+    vector and GIB bytes equal the device step's, iteration by iteration."""
+    from paper_2306_16926_b200 import layouts
+    counts = layouts.resnet50()[:30]
+    M, N, K = sum(counts), 8, 5
+    part = osp.Partition(counts)
+    a = osp.OspGroup(part, N, [0.125] * N, n_chunks=4)
+    b = osp.OspGroup(part, N, [0.125] * N, n_chunks=4)
+    a.set_budget(M * 2)
+    b.set_budget(M * 2)
+    hosts = [osp.synth_deltas(11, N, it, M).cpu().pin_memory() for it in range(K)]
+    outs = [torch.empty(M, dtype=torch.float32).pin_memory() for _ in range(K)]
+    gibs = [torch.empty(int(osp.lib().osp_gib_encoded_size(len(counts))), dtype=torch.uint8).pin_memory()
+            for _ in range(K)]
+    for it in range(K):
+        b.step_host_async(hosts[it], params_out=outs[it], gib_out=gibs[it])
+    b.host_wait()
+    for it in range(K):
+        a.step(hosts[it].cuda())
+        assert np.array_equal(outs[it].numpy().view(np.uint32),
+                              a.global_params.cpu().numpy().view(np.uint32)), f"params, it {it}"
+        ra = a.read_gib()
+        assert bytes(gibs[it].numpy()) == oracle.gib_encode(ra["tag"], ra["flags"]), f"gib, it {it}"
+    assert np.array_equal(bits(a.worker_params), bits(b.worker_params))
+
+
 def test_step_host_matches_device_step(osp):
     from paper_2306_16926_b200 import layouts
     counts = layouts.resnet50()[:40]
