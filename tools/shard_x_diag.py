@@ -86,7 +86,6 @@ def main():
         vals = t.tolist()
         print(json.dumps({"layout": layout, "tile": sh.local.geometry()["tile_elems"],
                           "lag": os.environ.get("OSP_SHARD_LAG", "2"),
-                          "stages": os.environ.get("OSP_SHARD_STAGES", "2"),
                           "world": world, "step_ms": vals[0], "solo_exchange_ms": vals[1],
                           "phases_ms": dict(zip(ph, vals[2:])),
                           "nvlink_GBps_step": nvl / (vals[0] * 1e-3) / 1e9,
