@@ -144,6 +144,43 @@ def run(args, metric: str, unit: str):
         if k > 0:
             e2e.append((t1 - t0) * 1e3)
     e2e_ms, = _max([statistics.median(e2e)], dev)
+    # the same pipelined over consecutive steps: step k+1's rows go H2D on a
+    # copy stream into the other delta buffer while step k runs and rank 0's
+    # D2H of its global vector runs on a third stream; wall clock from the
+    # first copy to the last read-back, max over ranks
+    h2d, d2h = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_step = [torch.cuda.Event() for _ in range(2)]
+    ev_out = torch.cuda.Event()
+    E = max(10, args.e2e_steps)
+
+    def pipelined(n):
+        for k in range(n):
+            b = k % 2
+            if k >= 2:
+                h2d.wait_event(ev_step[b])  # step k-2 has read this buffer
+            with torch.cuda.stream(h2d):
+                sh.deltas(b).copy_(host[b], non_blocking=True)
+                ev_in[b].record(h2d)
+            stream.wait_event(ev_in[b])
+            if k >= 1:
+                stream.wait_event(ev_out)  # the previous read-back of G is done
+            step(k)
+            ev_step[b].record(stream)
+            if rank == 0:
+                d2h.wait_event(ev_step[b])
+                with torch.cuda.stream(d2h):
+                    params_host.copy_(sh.global_params, non_blocking=True)
+            ev_out.record(d2h)
+        torch.cuda.synchronize()
+
+    pipelined(2)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pipelined(E)
+    e2e_pipe, = _max([(time.perf_counter() - t0) * 1e3 / E], dev)
+    sh.check()
     geometry = sh.local.geometry()
     mode = sh.mode
     sh.close()
@@ -230,11 +267,17 @@ def run(args, metric: str, unit: str):
             "phase_ms": phases,
             "overlap": ovl,
             "u_mean": u_mean,
-            "e2e": {"value": M / (e2e_ms * 1e-3), "unit": unit, "ms_per_step": e2e_ms,
+            "e2e": {"value": M / (e2e_pipe * 1e-3), "unit": unit, "ms_per_step": e2e_pipe,
+                    "pipelined": True, "steps": E,
+                    "sync_steps": {"ms_per_step": e2e_ms, "value": M / (e2e_ms * 1e-3),
+                                   "path": "the same, one step at a time (H2D, step, GIB read "
+                                           "on every rank, global vector on rank 0), median"},
                     "h2d_bytes_per_step": n_loc * M * 4 * world,
-                    "d2h_bytes_per_step": (8 + (L + 7) // 8) * world + 4 * M,
-                    "path": "pinned host rows -> osp_shard_deltas, osp_shard_* step, GIB read on "
-                            "every rank, updated global vector read on rank 0"},
+                    "d2h_bytes_per_step": 4 * M,
+                    "path": "every rank: pinned host rows -> osp_shard_deltas on a copy stream "
+                            "(one buffer ahead), osp_shard_step; rank 0: the updated global "
+                            "vector (= every worker's params) read back on a third stream, every "
+                            "step; wall clock over the pipelined steps, max over ranks"},
             # per step: the exchange kernel, the resolve, the stage-2 broadcast
             # (per chunk: one broadcast launch per chunk)
             "gpu_launches": K * (2 + (args.chunks if args.per_chunk else 1)),
