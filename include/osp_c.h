@@ -334,7 +334,9 @@ osp_status osp_group_step_host(osp_group* g, const float* host_deltas, uint64_t 
  * the step runs on `stream`. gib_out / params_out are written when
  * osp_group_host_wait returns (or when a later call's step has started); host
  * buffers should be pinned, and host_deltas must stay unchanged until the
- * next-but-one call or the wait. */
+ * next-but-one call or the wait. Do not issue other steps or GIB installs on
+ * the group between the first asynchronous call and osp_group_host_wait (the
+ * read-back of the global vector runs on its own stream). */
 osp_status osp_group_step_host_async(osp_group* g, const float* host_deltas, uint64_t host_ld,
                                      uint8_t* gib_out, float* params_out, void* stream);
 osp_status osp_group_host_wait(osp_group* g);
