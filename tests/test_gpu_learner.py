@@ -138,3 +138,32 @@ def test_training_iterations_end_to_end(mods):
         nxt = grp.read_gib()
         assert np.array_equal(nxt["flags"], r["flags_out"]) and np.array_equal(nxt["order"], r["order_out"])
         flags, order = r["flags_out"], r["order_out"]
+
+
+@pytest.mark.parametrize("widths,act,loss,B", [([5, 3], "relu", "mse", 1), ([5, 3], "tanh", "ce", 7),
+                                               ([6, 9, 1], "relu", "mse", 13),
+                                               ([4, 7, 5, 3], "tanh", "mse", 33),
+                                               ([3, 40, 2], "relu", "ce", 64)])
+def test_grad_random_specs_vs_restatement(mods, widths, act, loss, B):
+    """Depth 1 (no hidden layer) to 3, batches from 1 to 64 with repeated rows,
+    against the reference-pinned restatement (oracle/learner_oracle.py)."""
+    learner, _ = mods
+    rng = np.random.default_rng(sum(widths) * 7 + B)
+    n, k = 50, widths[-1]
+    feats = rng.normal(size=(n, widths[0])).astype(np.float32)
+    labels = rng.integers(0, max(k, 2) if k > 1 else 3, n).astype(np.int32)
+    M = sum(widths[l] * widths[l + 1] + widths[l + 1] for l in range(len(widths) - 1))
+    N = 3
+    params = (rng.normal(size=(N, M)) * 0.5).astype(np.float32)
+    batch = rng.integers(0, n, (N, B)).astype(np.int32)
+    mlp = learner.Mlp(widths, torch.as_tensor(feats).cuda(), torch.as_tensor(labels).cuda(), act, loss)
+    g, lv = mlp.grad(torch.as_tensor(params).cuda(), torch.as_tensor(batch).cuda())
+    g, lv = g.cpu().numpy(), lv.cpu().numpy()
+    for w in range(N):
+        go, lo_ = lo.forward_backward(widths, act, loss, feats, labels, params[w], list(batch[w]))
+        if act == "relu" and loss == "mse":
+            assert np.array_equal(g[w].view(np.uint32), go.view(np.uint32)), f"worker {w}"
+            assert lv[w] == lo_
+        else:
+            assert ulp_diff(g[w], go).max() <= 1, f"worker {w}"
+            np.testing.assert_allclose(lv[w], lo_, rtol=1e-13, atol=0)
