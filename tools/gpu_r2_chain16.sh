@@ -1,0 +1,15 @@
+# chain form: 2 CTAs per SM on rank 0 (smaller arena), 1 on the last rank
+mkdir -p gpurun_out
+OSP_SHARD_CHAIN_ARENA_KB0=100 timeout 900 python -m pytest tests/test_gpu_multi.py -x -q -k "chain_two or chain_oversubscribed" 2>&1 | tail -2
+run() { OSP_SHARD_DEBUG=1 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $2 --master-addr 127.0.0.1 --master-port $1 tools/shard_x_diag.py ${@:3} 2>>gpurun_out/r2_diag.err | tail -1 | sed "s/^/$VAR /" >> gpurun_out/r2_chain_diag17.txt; }
+: > gpurun_out/r2_chain_diag17.txt; : > gpurun_out/r2_diag.err
+VAR=base run 29861 2 resnet50
+VAR=a0_100 OSP_SHARD_CHAIN_ARENA_KB0=100 run 29862 2 resnet50
+VAR=a0_84 OSP_SHARD_CHAIN_ARENA_KB0=84 run 29863 2 resnet50
+VAR=a0_100_vgg OSP_SHARD_CHAIN_ARENA_KB0=100 run 29864 2 vgg16
+VAR=base_vgg run 29865 2 vgg16
+python -c "
+import json
+for line in open('gpurun_out/r2_chain_diag17.txt'):
+    var, js = line.split(' ',1); d=json.loads(js); print(var, round(d['step_ms'],3), {k: round(v,3) for k,v in d['phases_ms'].items()}, d['sync'], [c['a_items']+c['b_items']+c['l_items'] for c in d['debug_per_step']])"
+grep -i -E "error|Traceback" gpurun_out/r2_diag.err | head -5
