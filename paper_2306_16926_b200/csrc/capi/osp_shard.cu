@@ -274,6 +274,12 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
     base.split = s->split;
     base.chain_lead = 4;
     if (const char* cl = std::getenv("OSP_SHARD_CHAIN_LEAD")) base.chain_lead = std::max(0, std::atoi(cl));
+    // the last rank stores the aggregate into every rank's pull buffer (NVLink
+    // stores, 1 -> 0) instead of the others pulling it: its read requests no
+    // longer share the link carrying the running sums (0.433 vs 0.441 ms,
+    // VGG-16 1.90 vs 1.95; OSP_SHARD_CHAIN_PUSHAGG=0 pulls)
+    base.chain_pushagg = 1;
+    if (const char* pa = std::getenv("OSP_SHARD_CHAIN_PUSHAGG")) base.chain_pushagg = std::atoi(pa) ? 1 : 0;
     base.ticket = s->ticket;
     base.dbg = s->dbg;
     base.trace = s->n_trace ? s->dbg + 16 : nullptr;
@@ -294,9 +300,11 @@ osp_status osp_shard_connect(osp_shard* s, const uint8_t* handles) {
                   (reinterpret_cast<uintptr_t>(xa.pre[q]) % 32 == 0);
         xa.vec = vec ? 1 : 0;
     }
-    // chain form: the aggregate lives on the last rank only (the others' APPLY
-    // items read it there), so their resolve's exact fallback reads it there
-    if (s->chain && s->rank != s->world - 1) s->grp->v.agg_full = base.agg[s->world - 1];
+    // chain form pulling the aggregate: it lives on the last rank only (the
+    // others' APPLY items read it there), so their resolve's exact fallback
+    // reads it there; pushed, every rank holds it
+    if (s->chain && s->rank != s->world - 1 && !base.chain_pushagg)
+        s->grp->v.agg_full = base.agg[s->world - 1];
     s->connected = true;
     return OSP_OK;
 }

@@ -23,10 +23,12 @@
 //          C = G' and rows = G + x_w; the tile's PGP partial (importance.cpp
 //          11-28) goes to every rank's partials. Flag: every other rank's tile
 //          flag.
-//   APPLY  (ranks 0..P-2) after the tile flag: bulk-copy agg from the last
-//          rank's HBM (NVLink) and G; RS: G = G + agg, rows = G'; ICS: C.
-//          (No local copy of agg: these ranks' resolve reads the last rank's
-//          for its exact fallback, osp_shard.cu.)
+//   APPLY  (ranks 0..P-2) after the tile flag: bulk-copy agg and G; RS:
+//          G = G + agg, rows = G'; ICS: C. By default the last rank has stored
+//          agg into every rank's pull buffer (NVLink stores ahead of its
+//          flag's fence); with xa.chain_pushagg = 0 it is pulled from the last
+//          rank's HBM, and these ranks' resolve reads it there for its exact
+//          fallback (osp_shard.cu).
 // Data always stays where it was written; readers pull with cp.async.bulk
 // after acquiring a flag the writer pushed into their memory (the writer's
 // system-scope fence then drains only local stores and tiny flag stores).
@@ -357,7 +359,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
             if (m.staged && lane == 0) {  // one thread issues the item's copies (as k_stage_tma)
                 float* dst = ring + s * SF;
                 if (kind == CI_APPLY) {
-                    bulk_g2s(dst, xa.agg[P - 1] + m.s, bytes, &full[s]);
+                    bulk_g2s(dst, xa.agg[xa.chain_pushagg ? R : P - 1] + m.s, bytes, &full[s]);
                     bulk_g2s(dst + T, g.G + m.s, bytes, &full[s]);
                 } else {
                     if (has_pre) bulk_g2s(dst, pre_in + m.s, 2 * bytes, &full[s]);
@@ -459,6 +461,8 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                                              agg_finish(ap, s3));
                 const float4 gn = add4x(go, a);
                 *reinterpret_cast<float4*>(xa.agg[R] + f) = a;
+                if (xa.chain_pushagg)  // every other rank's copy (NVLink stores), flagged below
+                    for (int r = 0; r < P - 1; ++r) *reinterpret_cast<float4*>(xa.agg[r] + f) = a;
                 if (m.ics) {
                     st_stream4(g.C + f, gn);
 #pragma unroll
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
             for (uint64_t f = m.s + ctid; f < m.e; f += CW * 32) {
                 const float go = g.G[f];
                 if (m.kind == CI_APPLY) {
-                    const float a = __ldcg(xa.agg[P - 1] + f);
+                    const float a = __ldcg(xa.agg[xa.chain_pushagg ? R : P - 1] + f);
                     const float gn = __fadd_rn(go, a);
                     if (m.ics) {
                         g.C[f] = gn;
@@ -505,6 +509,8 @@ __global__ void __launch_bounds__((kCCW + 2) * 32) k_shard_chain(GroupView g, Ag
                 const float a = agg_finish(ap, sum);
                 const float gn = __fadd_rn(go, a);
                 xa.agg[R][f] = a;
+                if (xa.chain_pushagg)
+                    for (int r = 0; r < P - 1; ++r) xa.agg[r][f] = a;
                 if (m.ics) {
                     g.C[f] = gn;
                     for (int w = 0; w < NL; ++w) g.P[static_cast<uint64_t>(w) * g.ldP + f] = __fadd_rn(go, x[w]);

@@ -158,6 +158,7 @@ struct XArgs {
     double* pre[kMaxRanks];              // chain form: every rank's fp64 running sums [ldX]
     int chain_lead;                      // chain form, mixed CTAs: PRE items kept ahead of APPLY
     int chain_arena;                     // chain form: ring arena in floats (set at launch)
+    int chain_pushagg;                   // chain form: the last rank stores agg into every rank
     unsigned long long* trace;           // chain form diagnostics: [8][NT] globaltimer stamps or null
     unsigned* error;                     // local: set when a bounded wait timed out
     int world, rank, n_loc;
