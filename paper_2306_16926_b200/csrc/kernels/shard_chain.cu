@@ -29,9 +29,11 @@
 //          flag's fence); with xa.chain_pushagg = 0 it is pulled from the last
 //          rank's HBM, and these ranks' resolve reads it there for its exact
 //          fallback (osp_shard.cu).
-// Data always stays where it was written; readers pull with cp.async.bulk
-// after acquiring a flag the writer pushed into their memory (the writer's
-// system-scope fence then drains only local stores and tiny flag stores).
+// The running sums stay where they were written and the next rank pulls them
+// with cp.async.bulk after acquiring a flag the writer pushed into its memory
+// (the writer's system-scope fence then drains only local stores and tiny flag
+// stores); the aggregate goes the other way as NVLink stores, so no read
+// request shares the link that carries the running sums.
 // Every CTA of a non-finishing rank takes both PRE and APPLY items of its
 // tiles, PRE items leading (see next_item).
 //
