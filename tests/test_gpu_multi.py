@@ -47,7 +47,8 @@ def _worker(rank, world, port, cfg, q):
         p0 = rng.uniform(-1, 1, M).astype(np.float32) if cfg["p0_seed"] else np.zeros(M, np.float32)
         part = osp.Partition(counts)
         sh = odist.ShardGroup(part, N, w, n_chunks=nc, init_params=torch.as_tensor(p0, device="cuda"),
-                              tile_elems=cfg.get("tile", 0), defer_ics=cfg.get("defer", False))
+                              tile_elems=cfg.get("tile", 0), defer_ics=cfg.get("defer", False),
+                              sgd_lr=cfg.get("sgd_lr", 0.0))
         sh.connect_via()
         assert sh.deferred_ics == bool(cfg.get("defer", False)), "shard exchange mode"
         if cfg.get("sync") and not cfg.get("defer"):
@@ -68,6 +69,11 @@ def _worker(rank, world, port, cfg, q):
                 x = sh.deltas(buf)
                 x[:, dst:dst + n] = x[:, src:src + n]
                 deltas[:, dst:dst + n] = deltas[:, src:src + n]
+            if cfg.get("sgd_lr"):  # the rows are gradients: the step applies sgd_delta
+                x = sh.deltas(buf)
+                x.mul_(37.0)
+                raw = deltas * np.float32(37.0)
+                deltas = np.stack([oracle.sgd_delta(raw[k], cfg["sgd_lr"]) for k in range(N)])
             r = oracle.step(counts, 4, w, deltas, G, P, flags, order, nc, budget)
             sh.set_budget(budget)
             if cfg.get("per_chunk"):
@@ -228,6 +234,19 @@ def test_shard_deferred_all_ics_lagging_rank(per_chunk):
     cfg = dict(counts=_ragged(17, 15, 6000), N=4, weights=w, chunks=3, budget_frac=1.0,
                iters=4, seed=3, p0_seed=2, defer=True, per_chunk=per_chunk, lag_rank=1)
     run_world(cfg, world=2, oversubscribe=True)
+
+
+@pytest.mark.parametrize("world,sync,defer", [(2, "chain", False), (2, "tile", False), (4, None, False),
+                                              (2, None, True)])
+def test_shard_fused_sgd_oversubscribed(world, sync, defer):
+    """Gradients as the rows, sgd_delta fused into the exchange (learner.cpp:
+    391-398): every form (chain, per-tile flags, the barrier form at 4 ranks,
+    the deferred mode), bit-exact vs the oracle fed with the CPU sgd_delta."""
+    rng = np.random.default_rng(91 + world)
+    w = [float(x) for x in 0.1 + rng.random(8)]
+    cfg = dict(counts=_ragged(29 + world, 19, 5000), N=8, weights=w, chunks=3, budget_frac=0.5,
+               iters=3, seed=13, p0_seed=6, sgd_lr=0.05, sync=sync, defer=defer)
+    run_world(cfg, world=world, oversubscribe=True)
 
 
 @pytest.mark.parametrize("sync", ["chain", "tile"])
