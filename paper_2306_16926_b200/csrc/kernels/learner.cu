@@ -39,6 +39,11 @@ __device__ __forceinline__ double act_bwd(int act, double z, double a) {
 template <bool SW>  // SW: the worker's parameters staged in shared memory as doubles
 __global__ void __launch_bounds__(kLearnThreads) k_mlp_grad(MlpArgs a) {
     extern __shared__ __align__(16) double lsm[];
+    // programmatic dependent launch: the parameter rows are the previous step's
+    // output (wait for it), and the step consuming these gradients may get
+    // resident meanwhile (it waits for this grid before reading them)
+    pdl_wait();
+    pdl_trigger();
     const int w = blockIdx.x;
     const int tid = threadIdx.x;
     const int B = a.B, depth = a.depth;
@@ -195,8 +200,7 @@ cudaError_t launch_mlp_grad(const MlpArgs& a, int n_workers, cudaStream_t s) {
     int per_sm = 0;  // opts the kernel into `sm` bytes (cached per context)
     cudaError_t e = tma_blocks_per_sm(reinterpret_cast<const void*>(kern), kLearnThreads, sm, &per_sm);
     if (e != cudaSuccess) return e;
-    kern<<<n_workers, kLearnThreads, sm, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(n_workers), dim3(kLearnThreads), sm, s, a);
 }
 
 }  // namespace osp
