@@ -53,6 +53,8 @@ def _worker(rank, world, port, cfg, q):
         assert sh.deferred_ics == bool(cfg.get("defer", False)), "shard exchange mode"
         if cfg.get("sync") and not cfg.get("defer"):
             assert sh.sync_form == cfg["sync"], (sh.sync_form, cfg["sync"])
+        if cfg.get("expect_sync"):
+            assert sh.sync_form == cfg["expect_sync"], (sh.sync_form, cfg["expect_sync"])
         G = p0.copy()
         P = np.tile(p0, (N, 1))
         flags = np.zeros(len(counts), np.uint8)
@@ -247,6 +249,18 @@ def test_shard_fused_sgd_oversubscribed(world, sync, defer):
     cfg = dict(counts=_ragged(29 + world, 19, 5000), N=8, weights=w, chunks=3, budget_frac=0.5,
                iters=3, seed=13, p0_seed=6, sgd_lr=0.05, sync=sync, defer=defer)
     run_world(cfg, world=world, oversubscribe=True)
+
+
+def test_shard_chain_falls_back_above_eight_local_workers():
+    """32 workers on 2 ranks (16 per rank): more local rows than the TMA stage
+    family holds, so the local group has no carry buffer and the shard runs
+    the deferred-ICS mode with per-tile flags (unstaged rows), not the chain —
+    still bit-exact."""
+    rng = np.random.default_rng(5)
+    w = [float(x) for x in 0.1 + rng.random(32)]
+    run_world(dict(counts=_ragged(41, 9, 1500), N=32, weights=w, chunks=2, budget_frac=0.5,
+                   iters=2, seed=21, p0_seed=3, defer=True, expect_sync="tile"), world=2,
+              oversubscribe=True)
 
 
 @pytest.mark.parametrize("sync", ["chain", "tile"])
